@@ -1,0 +1,357 @@
+"""Benchmark: MINRES + IC(0) block-preconditioned Stokes solve on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 2D unit-square Stokes, k'=2
+divergence-conforming B-splines on 64x64 elements, psi-MMS forcing, solved
+with IC0-PCG(A,Q) (RCM + IC(0) preconditioned inner CG on A and on Q_nu) at
+outer tolerance 1e-8, once with relaxed inner CG (1e-1) and once with
+exact-ish inner CG (1e-8). One bench step = both solves.
+
+metric  : MINRES outer iterations per second (whole job, all ranks)
+value   : device-resident solves (inputs already in HBM), CUDA-event time of
+          the solve kernels
+e2e     : the same solves through the C-ABI with HOST buffers (H2D of f and
+          D2H of u, p inside the timed region), wall clock
+roofline: dominant kernel = the persistent MINRES kernel; algorithmic bytes
+          per SURVEY.md §8(d) with the counted inner iterations
+--impl reference: the unmodified reference (oracle/_ref, built from
+          /root/reference/proj/src) on the host CPU, same workload.
+Multi-GPU (--gpus N under torchrun): the C2 solve does not shard usefully
+(replicated triangular sweeps); each rank runs an
+independent replica ("replicas only", weak scaling), max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c2": dict(case="psi-mms", k=2, n=64, dim=2, seed=0, strategy="IC0-PCG(A,Q)",
+               outer=1e-8, inners=(1e-1, 1e-8),
+               label="C2: 2D k'=2 64x64 psi-MMS, IC0-PCG(A,Q), outer 1e-8, inner {1e-1, 1e-8}"),
+    "c1": dict(case="psi-mms", k=2, n=16, dim=2, seed=0, strategy="IC0-PCG(A)+Diag(Q)",
+               outer=1e-8, inners=(1e-1,),
+               label="C1: 2D k'=2 16x16 psi-MMS, IC0-PCG(A)+Diag(Q), outer 1e-8, inner 1e-1"),
+}
+METRIC = "MINRES outer iterations/s (time-to-solution of the BASELINE C2 solve pair)"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+            sm = [float(r[0]) for r in rows]
+            mx = max(float(r[1]) for r in rows)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = sorted({names[i] for r in rows for i in range(4)
+                              if r[2 + i].strip().lower() in ("active", "1")})
+            loaded = [s for s in sm if s > 0.5 * mx] or sm
+            return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                    "samples": len(sm)}
+        except Exception as e:  # no nvidia-smi
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)[:80]}
+
+
+def algorithmic_bytes(info: dict, rep, outer_iters: int) -> float:
+    """SURVEY.md §8(d) algorithmic bytes of one solve with the counted work:
+    outer_iters saddle SpMVs + MINRES vector passes, and for each block
+    apps x (IC apply + PCG init) + inner x (block SpMV + IC apply + PCG vectors)."""
+    n_u, n_p = info["n_u"], info["n_p"]
+    n = n_u + n_p
+    S_K = 12 * info["nnz_K"] + 4 * n + 16 * n
+    S_A = 12 * info["nnz_A"] + 20 * n_u
+    S_ICA = 24 * info["nnz_L_A"] + 40 * n_u
+    S_ICQ = 24 * info["nnz_L_Q"] + 40 * n_p
+    S_Q = 12 * info["nnz_Q"] + 20 * n_p
+    return (outer_iters * (S_K + 160 * n)
+            + rep.apps_top * (S_ICA + 48 * n_u) + rep.inner_top * (S_A + S_ICA + 72 * n_u)
+            + rep.apps_bottom * (S_ICQ + 48 * n_p) + rep.inner_bottom * (S_Q + S_ICQ + 72 * n_p))
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_1309_5048_b200 import host, solver
+
+    W = WORKLOADS[args.workload]
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
+    t0 = time.perf_counter()
+    g = solver.GpuStokesSolver(s, W["strategy"], device=local)
+    setup_s = time.perf_counter() - t0
+    info = g.info()
+    opts = [solver.SolverOptions(outer_tol=W["outer"], inner_tol=t) for t in W["inners"]]
+    dev = torch.device("cuda", local)
+    d_f = torch.from_numpy(s.f).to(dev)
+    d_u = torch.empty(s.n_u, dtype=torch.float64, device=dev)
+    d_p = torch.empty(s.n_p, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step_device():
+        reps = []
+        for o in opts:
+            reps.append(g.solve_device(d_f.data_ptr(), d_u.data_ptr(), d_p.data_ptr(), o))
+        return reps
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    dev_ms = 0.0
+    iters = 0
+    launches = 0
+    last = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # L2 flush between steps (256 MiB > 126 MB L2)
+            torch.cuda.synchronize()
+            reps = step_device()
+            torch.cuda.synchronize()
+            dev_ms += sum(r.wall_seconds for r in reps) * 1e3
+            iters += sum(r.iterations for r in reps)
+            launches += sum(r.gpu_launches for r in reps)
+            last = reps
+    if dist:
+        t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = dev_ms / args.steps
+    value = world * iters / (dev_ms * 1e-3)
+
+    # ---- e2e: host buffers through the C ABI (pinned), wall clock ---------
+    f_pin = torch.from_numpy(s.f.copy()).pin_memory()
+    f_np = f_pin.numpy()
+    e2e_s = 0.0
+    e2e_iters = 0
+    if dist:
+        dist.barrier()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for o in opts:
+            sol = g.solve(f_np, o, history=False)
+            e2e_iters += sol.report.iterations
+        torch.cuda.synchronize()
+        e2e_s += time.perf_counter() - t1
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * e2e_iters / e2e_s
+
+    # ---- roofline of the dominant kernel (the persistent MINRES kernel) ----
+    peak, peak_kind = measured_peak()
+    bytes_step = 0.0
+    kern_ms = 0.0
+    for r in last:
+        bytes_step += algorithmic_bytes(info, r, r.iterations)
+        kern_ms += r.wall_seconds * 1e3
+    achieved = bytes_step / (kern_ms * 1e-3) / 1e9
+    # per-kernel microbenchmarks on device-resident data (same launch path)
+    kernels = {}
+    try:
+        spmv_ms = g.time_kernel(0, 50)
+        ic_ms = g.time_kernel(1, 5)
+        n = info["n_u"] + info["n_p"]
+        kernels = {
+            "saddle_spmv": {"ms": spmv_ms, "GB/s": (12 * info["nnz_K"] + 20 * n) / (spmv_ms * 1e-3) / 1e9},
+            "ic0_apply_A": {"ms": ic_ms, "GB/s": (24 * info["nnz_L_A"] + 40 * info["n_u"]) / (ic_ms * 1e-3) / 1e9,
+                            "levels": info["levels_fwd_A"] + info["levels_bwd_A"],
+                            "us_per_level": ic_ms * 1e3 / (info["levels_fwd_A"] + info["levels_bwd_A"])},
+        }
+    except Exception as e:
+        kernels = {"error": str(e)[:100]}
+
+    result = None
+    if rank == 0:
+        cpu = cpu_baseline(args, W) if (world == 1 and not args.no_cpu_baseline) else None
+        result = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "iter/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (BASELINE psi-MMS forcing, native assembly bit-identical to the reference)",
+            "config": {"workload": W["label"], "n_u": info["n_u"], "n_p": info["n_p"],
+                       "nnz_K": info["nnz_K"], "nnz_L_A": info["nnz_L_A"],
+                       "outer_iterations_per_step": iters // args.steps,
+                       "mean_inner_A": [round(r.mean_inner_top, 3) for r in last],
+                       "mean_inner_Q": [round(r.mean_inner_bottom, 3) for r in last],
+                       "time_to_solution_ms": [round(r.wall_seconds * 1e3, 3) for r in last],
+                       "setup_s": round(setup_s, 3), "grid_ctas": info["grid_ctas"],
+                       "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"replicas x{world}"},
+            "e2e": {"value": e2e_value, "unit": "iter/s",
+                    "h2d_bytes_per_step": 8 * s.n_u * len(opts),
+                    "d2h_bytes_per_step": 8 * (s.n_u + s.n_p) * len(opts)},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_kind": peak_kind, "kernel": "minres_kernel (persistent, cooperative)",
+                         "algorithmic_bytes_per_step": bytes_step},
+            "kernels": kernels,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(result), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def cpu_baseline(args, W):
+    """The reference (oracle/_ref) on this host's cores, bounded sample."""
+    try:
+        from oracle import RefLib, ref_available
+        if not ref_available():
+            from oracle import CSR, PortLib
+            from paper_1309_5048_b200 import host
+            P = PortLib()
+            s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
+            c = lambda m: CSR(m.n_rows, m.n_cols, m.row_ptr, m.cols, m.vals)  # noqa: E731
+            kind = "port"
+            run = lambda t: P.solve_stokes(c(s.A), c(s.B), c(s.Bt), c(s.Q_nu), s.f, W["strategy"],  # noqa: E731
+                                           W["outer"], t, Q_filter=c(s.Q))
+        else:
+            R = RefLib()
+            rs = R.assemble(W["case"], W["k"], W["n"], seed=W["seed"])
+            kind = "reference"
+            run = lambda t: rs.solve(W["strategy"], W["outer"], t)  # noqa: E731
+        iters, secs, reps = 0, 0.0, 0
+        t_start = time.perf_counter()
+        while reps < 3 and time.perf_counter() - t_start < args.cpu_budget_s:
+            for t in W["inners"]:
+                r = run(t)
+                iters += r["iterations"]
+                secs += r["wall_seconds"]
+            reps += 1
+        return {"value": iters / secs, "unit": "iter/s", "cores": 1, "kind": kind,
+                "sample": f"{reps} x the {len(W['inners'])}-solve step (MINRES time only, "
+                          "setup excluded; the reference solver is single-threaded)"}
+    except Exception as e:
+        return {"value": None, "unit": "iter/s", "cores": 1, "kind": "reference",
+                "sample": f"unavailable: {str(e)[:100]}"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return None
+    W = WORKLOADS[args.workload]
+    from oracle import RefLib, ref_available
+    if ref_available():
+        R = RefLib()
+        rs = R.assemble(W["case"], W["k"], W["n"], seed=W["seed"])
+        run = lambda t: rs.solve(W["strategy"], W["outer"], t)  # noqa: E731
+        kind = "reference"
+    else:
+        from oracle import CSR, PortLib
+        from paper_1309_5048_b200 import host
+        P = PortLib()
+        s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
+        c = lambda m: CSR(m.n_rows, m.n_cols, m.row_ptr, m.cols, m.vals)  # noqa: E731
+        run = lambda t: P.solve_stokes(c(s.A), c(s.B), c(s.Bt), c(s.Q_nu), s.f, W["strategy"],  # noqa: E731
+                                       W["outer"], t, Q_filter=c(s.Q))
+        kind = "port"
+    for _ in range(args.warmup):
+        for t in W["inners"][:1]:
+            run(t)
+    iters, secs = 0, 0.0
+    for _ in range(args.steps):
+        for t in W["inners"]:
+            r = run(t)
+            iters += r["iterations"]
+            secs += r["wall_seconds"]
+    value = iters / secs
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iter/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": W["label"], "parallelism": "1 host core (serial reference)"},
+           "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": kind,
+                            "sample": f"{args.steps} steps of the full workload (MINRES time)"},
+           "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

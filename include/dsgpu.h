@@ -1,0 +1,143 @@
+/* dsgpu — C ABI of the B200 (sm_100a) MINRES + IC(0) block-preconditioned
+ * Stokes solve. Drop-in for the reference's solve call:
+ *
+ *   StokesSolution solve_stokes(const StokesSystem&, BlockDiagPreconditioner&,
+ *                               const SolverOptions&)        proj/src/precond.cpp:245-293
+ *   (strategy menu make_strategy, proj/src/precond.cpp:161-193)
+ *
+ * The reference's host code keeps assembling the system and building the
+ * preconditioner factor exactly as PcgBlock does (rcm_permutation ->
+ * permute_symmetric -> ic0, proj/src/precond.cpp:61-64) and hands the
+ * resulting CSR arrays to dsgpu_setup; dsgpu_solve then runs the whole
+ * MINRES loop (proj/src/solvers.cpp:24-123) with its inner PCG
+ * (proj/src/solvers.cpp:125-159) and IC(0) applies (proj/src/cholesky.cpp:
+ * 136-152) on the device — one cooperative persistent kernel, no host round
+ * trip per iteration. See INTEGRATION.md for the reference-side shim.
+ *
+ * Layout: every CSR is the reference CsrMatrix layout (proj/include/divstokes/
+ * csr.hpp:12-16): int64 row_ptr[n_rows+1], int32 cols (sorted, unique), f64
+ * vals. All host arrays are borrowed for the duration of the call only.
+ *
+ * Errors mirror the reference's exception taxonomy (precond.cpp:141-147,
+ * solvers.cpp:46,74-75,133,142,148): non-convergence is NOT an error
+ * (report.converged = 0). A handle is not thread-safe (like BlockSolver);
+ * distinct handles may be used concurrently.
+ */
+#ifndef DSGPU_H
+#define DSGPU_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DSGPU_OK = 0,
+  DSGPU_E_INDEFINITE_PRECOND = 1, /* <z,r> < 0 (block in report.failed_block) */
+  DSGPU_E_NEG_CURVATURE = 2,      /* inner PCG: <p,Ap> <= 0 */
+  DSGPU_E_BAD_INPUT = 3,          /* std::invalid_argument */
+  DSGPU_E_CUDA = 4,               /* CUDA failure: dsgpu_last_error() */
+  DSGPU_E_NONPOS_DIAG = 5,        /* Jacobi block: nonpositive diagonal (std::domain_error) */
+  DSGPU_E_UNSUPPORTED = 7         /* size beyond this build's limits */
+};
+
+/* preconditioner block kinds (precond.cpp:14-118) */
+enum {
+  DSGPU_BLOCK_JACOBI = 0,     /* JacobiBlock: z = r / diag */
+  DSGPU_BLOCK_PCG_JACOBI = 1, /* PcgBlock(Inner::jacobi) */
+  DSGPU_BLOCK_PCG_IC0 = 2     /* PcgBlock(Inner::ic0): RCM + IC(0) preconditioned CG */
+};
+
+enum { DSGPU_STOP_PRECONDITIONED = 0, DSGPU_STOP_EUCLIDEAN = 1 }; /* MinresStop */
+
+typedef struct {
+  int32_t n_rows, n_cols;
+  const int64_t* row_ptr;
+  const int32_t* cols;
+  const double* vals;
+} dsgpu_csr;
+
+/* SolverOptions (precond.hpp:52-59) + the inner cap make_strategy uses */
+typedef struct {
+  double outer_tol;  /* default 1e-12 */
+  double inner_tol;  /* PCG tolerance; must match the factor's strategy */
+  int32_t max_iter;  /* default 20000 */
+  int32_t stop;      /* DSGPU_STOP_*; reference solve_stokes default: EUCLIDEAN */
+  int32_t inner_cap; /* default 100000 (precond.cpp:167) */
+} dsgpu_opts;
+
+/* SolveReport (solvers.hpp:15-23) plus diagnostics */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  int32_t status;       /* DSGPU_* */
+  int32_t failed_block; /* 0 velocity, 1 pressure, -1 none */
+  double wall_seconds;  /* MINRES kernel time (CUDA events), excl. H2D/D2H */
+  double mean_inner_top, mean_inner_bottom;
+  double relres_m, relres_e; /* final M^-1-norm and Euclidean relative residuals */
+  int64_t inner_top, apps_top, inner_bottom, apps_bottom;
+  int32_t hist_len;     /* entries written to the history buffers */
+  int32_t gpu_launches; /* kernels launched by this solve */
+} dsgpu_report;
+
+typedef struct dsgpu_handle dsgpu_handle;
+
+const char* dsgpu_last_error(const dsgpu_handle* h); /* h may be NULL */
+void dsgpu_default_opts(dsgpu_opts* o);
+
+int dsgpu_create(int device, dsgpu_handle** out);
+void dsgpu_destroy(dsgpu_handle* h);
+
+/* Upload the saddle system and the two preconditioner blocks.
+ *   A (n_u x n_u), B (n_p x n_u), Bt (n_u x n_p), Q_nu (n_p x n_p): the
+ *     StokesSystem blocks (assembly.hpp:31-49), original DOF order.
+ *   top_kind / bottom_kind: DSGPU_BLOCK_*.
+ *   perm_A, L_A: for PCG_IC0 tops, the RCM permutation of A and the IC(0)
+ *     factor of permute_symmetric(A, perm_A) (Ic0Factor::lower: lower
+ *     triangle incl. diagonal). NULL otherwise. Same for perm_Q, L_Q.
+ *   Q_filter: the unscaled pressure mass Q when the constant pressure spans
+ *     Ker(B^T) and solve_stokes's zero-mean filter applies (precond.cpp:
+ *     266-284, kernel = all ones on the identity map); NULL disables it.
+ * Everything is kept on the device in the RCM basis diag(P_A, P_Q), so the
+ * inner PCG needs no per-apply gather/scatter. */
+int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu_csr* Bt,
+                const dsgpu_csr* Q_nu, int top_kind, const int32_t* perm_A, const dsgpu_csr* L_A,
+                int bottom_kind, const int32_t* perm_Q, const dsgpu_csr* L_Q,
+                const dsgpu_csr* Q_filter);
+
+/* solve_stokes: b = [f; 0], x0 = 0, MINRES, zero-mean filter. HOST buffers
+ * (f: n_u; u_out: n_u; p_out: n_p; histories nullable, capacity hist_cap:
+ * residual_history / euclid_history as in SolveReport). */
+int dsgpu_solve(dsgpu_handle* h, const double* f, const dsgpu_opts* opts, double* u_out,
+                double* p_out, dsgpu_report* rep, double* hist_m, double* hist_e,
+                int32_t hist_cap);
+
+/* Same, DEVICE buffers (cudaMalloc'd by the caller), on the handle's stream;
+ * histories stay device-side and are not returned. Synchronizes at the end. */
+int dsgpu_solve_device(dsgpu_handle* h, const double* d_f, const dsgpu_opts* opts,
+                       double* d_u_out, double* d_p_out, dsgpu_report* rep);
+
+/* ---- kernel-level entry points (parity tests, benchmarks) -------------- */
+/* y = [A Bt; B 0] x in the ORIGINAL ordering (StokesSystem::apply,
+ * assembly.cpp:363-372); host buffers of length n_u + n_p. */
+int dsgpu_apply_saddle(dsgpu_handle* h, const double* x, double* y);
+/* z = (L L^T)^{-1} r for block 0 (top) / 1 (bottom), in the block's RCM
+ * ordering (Ic0Factor::solve, cholesky.cpp:136-152). Bit-identical to the
+ * reference by construction (same per-row operation order, no FMA). */
+int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z);
+/* y = M x with M = permuted A (block 0) or permuted Q_nu (block 1). */
+int dsgpu_apply_block_matrix(dsgpu_handle* h, int block, const double* x, double* y);
+/* Time `reps` back-to-back launches of one kernel on device-resident data:
+ * which = 0 saddle SpMV, 1 IC(0) apply (top), 2 IC(0) apply (bottom),
+ * 3 block-0 SpMV. Returns mean ms per launch in *ms. */
+int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms);
+
+/* Sizes of the device-resident problem (for roofline accounting):
+ * info[0..11] = n_u, n_p, nnz_K, nnz_Aperm, nnz_L_A, nnz_L_Q, nnz_Qperm,
+ * levels_fwd_A, levels_bwd_A, levels_fwd_Q, levels_bwd_Q, grid_ctas. */
+int dsgpu_info(const dsgpu_handle* h, int64_t* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,73 @@
+// Internal plan shared by the host-side setup (setup.cpp) and the device
+// solver (solver.cu). Everything lives in the RCM basis diag(P_A, P_Q).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "dsgpu.h"
+
+namespace dsgpu {
+
+constexpr int kLanes = 32;  // rows per triangular-solve group (one warp)
+
+// One triangular sweep, level-scheduled and sync-free:
+//   * rows are grouped by dependency level (level(i) = 1 + max level of the
+//     rows it reads); each level is cut into groups of <= 32 rows;
+//   * groups are ordered by level and dealt round-robin to the warps of ONE
+//     CTA; a warp spins (shared memory) only on rows of earlier levels, so no
+//     CTA- or grid-wide barrier is needed between levels;
+//   * group entries are stored lane-interleaved (SELL-32): entry k of lane l
+//     at ptr[g] + 32 k + l, so a warp's loads are coalesced; padding cols = -1.
+// The forward sweep walks L's rows with columns ascending; the backward sweep
+// walks U = L^T's rows (L's columns) with the contributing rows DESCENDING,
+// which is exactly the order in which the reference's column-oriented
+// backward scatter subtracts them (proj/src/cholesky.cpp:145-151) -- so with
+// separate mul/sub roundings the device result is bit-identical.
+struct HostSweep {
+  int n = 0;
+  int n_groups = 0, n_levels = 0;
+  std::vector<int64_t> gptr;   // n_groups + 1 (entries)
+  std::vector<int32_t> gwidth; // n_groups
+  std::vector<int32_t> grows;  // n_groups * 32, -1 = idle lane
+  std::vector<int32_t> cols;   // SELL entries
+  std::vector<double> vals;
+  std::vector<double> diag;    // n
+};
+
+struct HostBlock {
+  int kind = DSGPU_BLOCK_JACOBI;
+  int n = 0, off = 0;
+  std::vector<int32_t> perm;     // block ordering -> original index (empty = identity)
+  // operator in block ordering (bottom block; the top block reads K's A part)
+  std::vector<int64_t> rp;
+  std::vector<int32_t> ci;
+  std::vector<double> v;
+  std::vector<double> dinv;      // Jacobi / Jacobi-PCG
+  HostSweep fwd, bwd;            // IC0-PCG
+};
+
+struct HostPlan {
+  int n_u = 0, n_p = 0, n = 0;
+  // K' = diag(P_A,P_Q) K diag(P_A,P_Q)^T: velocity rows = [A' | Bt'] (A'
+  // entries first, k_na per row), pressure rows = [B'].
+  std::vector<int64_t> k_rp;
+  std::vector<int32_t> k_ci;
+  std::vector<double> k_v;
+  std::vector<int32_t> k_na;
+  HostBlock blk[2];
+  bool filter = false;
+  std::vector<double> qk;  // Q 1 in the pressure block ordering
+  double filter_den = 0.0;
+};
+
+// Throws std::invalid_argument / std::domain_error on bad input.
+void build_plan(HostPlan& plan, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu_csr* Bt,
+                const dsgpu_csr* Q_nu, int top_kind, const int32_t* perm_A, const dsgpu_csr* L_A,
+                int bottom_kind, const int32_t* perm_Q, const dsgpu_csr* L_Q,
+                const dsgpu_csr* Q_filter);
+
+void build_sweeps(const dsgpu_csr& L, HostSweep& fwd, HostSweep& bwd);
+
+}  // namespace dsgpu

@@ -1,0 +1,123 @@
+// Device building blocks for the B200 MINRES + IC(0) solve (sm_100a, fp64).
+//
+// Arithmetic convention: every element-wise update uses explicitly rounded
+// mul/add/sub/div (__dmul_rn etc.), i.e. no FMA contraction, so each update
+// rounds exactly like the reference's scalar C++ (x86-64 baseline, no FMA).
+// Reductions (dot products, SpMV row sums) use a fixed warp-shuffle tree and a
+// fixed CTA/grid order: deterministic run to run, different summation order
+// from the reference (round-off level).
+#pragma once
+
+#include <cstdint>
+
+namespace dsgpu {
+namespace dev {
+
+constexpr unsigned long long kSentinel = 0xFFF4A11C0DEDBEEFull;  // "not yet computed" (a NaN payload)
+constexpr unsigned long long kCanonNaN = 0x7FF8000000000000ull;
+constexpr long long kSpinTimeoutCycles = 8000000000ll;  // ~4 s at 1.9 GHz: abort instead of hanging
+
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic CTA sum; result valid in every thread of warp 0.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident).
+// Fences on both sides make every write before the barrier visible to every
+// read after it (and invalidate this SM's L1 on the way out). Returns false
+// on timeout (abort flag set) instead of hanging the GPU.
+__device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, unsigned* abort_flag) {
+  __shared__ int ok_sh;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    const unsigned g = ld_acquire(gen);
+    __threadfence();
+    const unsigned prev = atomicAdd(count, 1u);
+    if (prev == gridDim.x - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      st_release(gen, g + 1);
+    } else {
+      const long long t0 = clock64();
+      while (ld_acquire(gen) == g) {
+        if (*reinterpret_cast<volatile unsigned*>(abort_flag)) {
+          ok = 0;
+          break;
+        }
+        if (clock64() - t0 > kSpinTimeoutCycles) {
+          atomicExch(abort_flag, 1u);
+          ok = 0;
+          break;
+        }
+      }
+    }
+    __threadfence();
+    ok_sh = ok;
+  }
+  __syncthreads();
+  return ok_sh != 0;
+}
+
+// ---- shared-memory dataflow slots for the triangular sweeps --------------
+__device__ __forceinline__ void slot_reset(double* xs, int i) {
+  reinterpret_cast<volatile unsigned long long*>(xs)[i] = kSentinel;
+}
+__device__ __forceinline__ void slot_publish(double* xs, int i, double v) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  if (b == kSentinel) b = kCanonNaN;
+  reinterpret_cast<volatile unsigned long long*>(xs)[i] = b;
+}
+// Spin until slot c holds a value. On timeout sets *abort_flag and returns NaN.
+__device__ __forceinline__ double slot_wait(const double* xs, int c, unsigned* abort_flag) {
+  const volatile unsigned long long* p = reinterpret_cast<const volatile unsigned long long*>(xs);
+  unsigned long long b = p[c];
+  if (b != kSentinel) return __longlong_as_double(static_cast<long long>(b));
+  const long long t0 = clock64();
+  do {
+    b = p[c];
+    const long long dt = clock64() - t0;
+    // slow path only after ~0.5 ms of waiting: a global abort-flag load costs
+    // an L2 round trip and must stay off the per-level critical path
+    if (dt > (1ll << 20) &&
+        (dt > kSpinTimeoutCycles || *reinterpret_cast<volatile unsigned*>(abort_flag))) {
+      atomicExch(abort_flag, 1u);
+      return __longlong_as_double(static_cast<long long>(kCanonNaN));
+    }
+  } while (b == kSentinel);
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+}  // namespace dev
+}  // namespace dsgpu

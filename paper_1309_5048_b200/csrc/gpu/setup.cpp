@@ -1,0 +1,298 @@
+// Host-side preprocessing for dsgpu_setup: builds the RCM-basis saddle
+// operator, the block operators and the level-grouped triangular sweeps.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "dsgpu_internal.hpp"
+
+namespace dsgpu {
+namespace {
+
+void check_csr(const dsgpu_csr* m, int rows, int cols, const char* name) {
+  if (!m || !m->row_ptr || m->n_rows != rows || m->n_cols != cols)
+    throw std::invalid_argument(std::string("dsgpu_setup: bad dimensions for ") + name);
+  if (m->row_ptr[0] != 0) throw std::invalid_argument(std::string(name) + ": row_ptr[0] != 0");
+  for (int i = 0; i < rows; ++i)
+    if (m->row_ptr[i + 1] < m->row_ptr[i])
+      throw std::invalid_argument(std::string(name) + ": row_ptr not monotone");
+  const int64_t nnz = m->row_ptr[rows];
+  if (nnz > 0 && (!m->cols || !m->vals))
+    throw std::invalid_argument(std::string(name) + ": null cols/vals");
+  for (int64_t k = 0; k < nnz; ++k)
+    if (m->cols[k] < 0 || m->cols[k] >= cols)
+      throw std::invalid_argument(std::string(name) + ": column index out of range");
+}
+
+std::vector<int32_t> inverse(const std::vector<int32_t>& perm, int n, const char* name) {
+  std::vector<int32_t> inv(n, -1);
+  for (int i = 0; i < n; ++i) {
+    const int p = perm[i];
+    if (p < 0 || p >= n || inv[p] >= 0)
+      throw std::invalid_argument(std::string(name) + ": not a permutation");
+    inv[p] = i;
+  }
+  return inv;
+}
+
+double diag_at(const dsgpu_csr* m, int i) {
+  // CsrMatrix::at (proj/src/csr.cpp:13-18): zero outside the pattern
+  const int32_t* b = m->cols + m->row_ptr[i];
+  const int32_t* e = m->cols + m->row_ptr[i + 1];
+  const int32_t* it = std::lower_bound(b, e, i);
+  return (it == e || *it != i) ? 0.0 : m->vals[it - m->cols];
+}
+
+}  // namespace
+
+void build_sweeps(const dsgpu_csr& L, HostSweep& fwd, HostSweep& bwd) {
+  const int n = L.n_rows;
+  // validate: lower triangular, diagonal stored last and nonzero
+  for (int i = 0; i < n; ++i) {
+    const int64_t b = L.row_ptr[i], e = L.row_ptr[i + 1];
+    if (e == b || L.cols[e - 1] != i)
+      throw std::invalid_argument("IC(0) factor: missing diagonal at row " + std::to_string(i));
+    for (int64_t k = b; k < e - 1; ++k)
+      if (L.cols[k] >= i || (k > b && L.cols[k] <= L.cols[k - 1]))
+        throw std::invalid_argument("IC(0) factor: not strictly lower/sorted at row " +
+                                    std::to_string(i));
+  }
+  // backward rows: U row c = {(k, L_kc) : k > c}, k descending
+  std::vector<int64_t> urp(n + 1, 0);
+  for (int i = 0; i < n; ++i)
+    for (int64_t k = L.row_ptr[i]; k < L.row_ptr[i + 1] - 1; ++k) ++urp[L.cols[k] + 1];
+  for (int i = 0; i < n; ++i) urp[i + 1] += urp[i];
+  std::vector<int32_t> uci(urp[n]);
+  std::vector<double> uv(urp[n]);
+  {
+    std::vector<int64_t> next(urp.begin(), urp.end() - 1);
+    for (int i = n - 1; i >= 0; --i)  // descending source row
+      for (int64_t k = L.row_ptr[i]; k < L.row_ptr[i + 1] - 1; ++k) {
+        const int c = L.cols[k];
+        uci[next[c]] = i;
+        uv[next[c]] = L.vals[k];
+        ++next[c];
+      }
+  }
+
+  auto build = [n](HostSweep& s, const std::vector<int64_t>& rp, const int32_t* ci,
+                   const double* v, const std::vector<double>& diag, bool reverse) {
+    s.n = n;
+    s.diag = diag;
+    std::vector<int> level(n, 0);
+    int max_level = -1;
+    for (int t = 0; t < n; ++t) {
+      const int i = reverse ? n - 1 - t : t;
+      int lv = 0;
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) lv = std::max(lv, level[ci[k]] + 1);
+      level[i] = lv;
+      max_level = std::max(max_level, lv);
+    }
+    s.n_levels = max_level + 1;
+    // bucket rows by level (ascending row index inside a level)
+    std::vector<int> cnt(s.n_levels + 1, 0);
+    for (int i = 0; i < n; ++i) ++cnt[level[i] + 1];
+    for (int l = 0; l < s.n_levels; ++l) cnt[l + 1] += cnt[l];
+    std::vector<int> order(n);
+    {
+      std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+      for (int i = 0; i < n; ++i) order[pos[level[i]]++] = i;
+    }
+    s.gptr.assign(1, 0);
+    s.gwidth.clear();
+    s.grows.clear();
+    for (int l = 0; l < s.n_levels; ++l)
+      for (int a = cnt[l]; a < cnt[l + 1]; a += kLanes) {
+        const int b = std::min(cnt[l + 1], a + kLanes);
+        int width = 0;
+        for (int t = a; t < b; ++t)
+          width = std::max<int>(width, static_cast<int>(rp[order[t] + 1] - rp[order[t]]));
+        s.gwidth.push_back(width);
+        for (int lane = 0; lane < kLanes; ++lane) s.grows.push_back(a + lane < b ? order[a + lane] : -1);
+        s.gptr.push_back(s.gptr.back() + static_cast<int64_t>(width) * kLanes);
+      }
+    s.n_groups = static_cast<int>(s.gwidth.size());
+    s.cols.assign(s.gptr.back(), -1);
+    s.vals.assign(s.gptr.back(), 0.0);
+    for (int g = 0; g < s.n_groups; ++g)
+      for (int lane = 0; lane < kLanes; ++lane) {
+        const int r = s.grows[static_cast<size_t>(g) * kLanes + lane];
+        if (r < 0) continue;
+        int kk = 0;
+        for (int64_t k = rp[r]; k < rp[r + 1]; ++k, ++kk) {
+          s.cols[s.gptr[g] + static_cast<int64_t>(kk) * kLanes + lane] = ci[k];
+          s.vals[s.gptr[g] + static_cast<int64_t>(kk) * kLanes + lane] = v[k];
+        }
+      }
+  };
+
+  std::vector<double> diag(n);
+  for (int i = 0; i < n; ++i) diag[i] = L.vals[L.row_ptr[i + 1] - 1];
+  // forward rows: L row i without its diagonal (columns ascending)
+  std::vector<int64_t> frp(n + 1, 0);
+  std::vector<int32_t> fci;
+  std::vector<double> fv;
+  fci.reserve(L.row_ptr[n] - n);
+  fv.reserve(L.row_ptr[n] - n);
+  for (int i = 0; i < n; ++i) {
+    for (int64_t k = L.row_ptr[i]; k < L.row_ptr[i + 1] - 1; ++k) {
+      fci.push_back(L.cols[k]);
+      fv.push_back(L.vals[k]);
+    }
+    frp[i + 1] = static_cast<int64_t>(fci.size());
+  }
+  build(fwd, frp, fci.data(), fv.data(), diag, false);
+  build(bwd, urp, uci.data(), uv.data(), diag, true);
+}
+
+void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu_csr* Bt,
+                const dsgpu_csr* Q_nu, int top_kind, const int32_t* perm_A, const dsgpu_csr* L_A,
+                int bottom_kind, const int32_t* perm_Q, const dsgpu_csr* L_Q,
+                const dsgpu_csr* Q_filter) {
+  if (!A || !B || !Bt || !Q_nu) throw std::invalid_argument("dsgpu_setup: null block");
+  const int n_u = A->n_rows, n_p = Q_nu->n_rows;
+  if (n_u <= 0 || n_p <= 0) throw std::invalid_argument("dsgpu_setup: empty system");
+  check_csr(A, n_u, n_u, "A");
+  check_csr(B, n_p, n_u, "B");
+  check_csr(Bt, n_u, n_p, "Bt");
+  check_csr(Q_nu, n_p, n_p, "Q_nu");
+  for (int kind : {top_kind, bottom_kind})
+    if (kind < DSGPU_BLOCK_JACOBI || kind > DSGPU_BLOCK_PCG_IC0)
+      throw std::invalid_argument("dsgpu_setup: unknown block kind");
+  P.n_u = n_u;
+  P.n_p = n_p;
+  P.n = n_u + n_p;
+
+  const dsgpu_csr* mats[2] = {A, Q_nu};
+  const int kinds[2] = {top_kind, bottom_kind};
+  const int32_t* perms[2] = {perm_A, perm_Q};
+  const dsgpu_csr* facs[2] = {L_A, L_Q};
+  std::vector<int32_t> inv[2];
+  for (int b = 0; b < 2; ++b) {
+    HostBlock& hb = P.blk[b];
+    hb.kind = kinds[b];
+    hb.n = mats[b]->n_rows;
+    hb.off = b == 0 ? 0 : n_u;
+    if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
+      if (!perms[b] || !facs[b])
+        throw std::invalid_argument("dsgpu_setup: IC0 block needs its permutation and factor");
+      check_csr(facs[b], hb.n, hb.n, b == 0 ? "L_A" : "L_Q");
+      hb.perm.assign(perms[b], perms[b] + hb.n);
+    } else {
+      hb.perm.resize(hb.n);
+      std::iota(hb.perm.begin(), hb.perm.end(), 0);
+    }
+    inv[b] = inverse(hb.perm, hb.n, b == 0 ? "perm_A" : "perm_Q");
+  }
+
+  // K' rows
+  P.k_rp.assign(P.n + 1, 0);
+  P.k_na.assign(n_u, 0);
+  for (int r = 0; r < n_u; ++r) {
+    const int o = P.blk[0].perm[r];
+    P.k_na[r] = static_cast<int32_t>(A->row_ptr[o + 1] - A->row_ptr[o]);
+    P.k_rp[r + 1] = P.k_rp[r] + P.k_na[r] + (Bt->row_ptr[o + 1] - Bt->row_ptr[o]);
+  }
+  for (int r = 0; r < n_p; ++r) {
+    const int o = P.blk[1].perm[r];
+    P.k_rp[n_u + r + 1] = P.k_rp[n_u + r] + (B->row_ptr[o + 1] - B->row_ptr[o]);
+  }
+  P.k_ci.resize(P.k_rp[P.n]);
+  P.k_v.resize(P.k_rp[P.n]);
+#pragma omp parallel
+  {
+    std::vector<std::pair<int32_t, double>> row;
+#pragma omp for schedule(dynamic, 256)
+    for (int r = 0; r < P.n; ++r) {
+      int64_t at = P.k_rp[r];
+      auto emit = [&](const dsgpu_csr* m, int o, const std::vector<int32_t>& iv, int shift) {
+        row.clear();
+        for (int64_t k = m->row_ptr[o]; k < m->row_ptr[o + 1]; ++k)
+          row.emplace_back(iv[m->cols[k]] + shift, m->vals[k]);
+        std::sort(row.begin(), row.end(),
+                  [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (const auto& e : row) {
+          P.k_ci[at] = e.first;
+          P.k_v[at++] = e.second;
+        }
+      };
+      if (r < n_u) {
+        const int o = P.blk[0].perm[r];
+        emit(A, o, inv[0], 0);
+        emit(Bt, o, inv[1], n_u);
+      } else {
+        emit(B, P.blk[1].perm[r - n_u], inv[0], 0);
+      }
+    }
+  }
+
+  for (int b = 0; b < 2; ++b) {
+    HostBlock& hb = P.blk[b];
+    const dsgpu_csr* m = mats[b];
+    if (hb.kind != DSGPU_BLOCK_PCG_IC0) {
+      // JacobiBlock / PcgBlock(jacobi): inverse diagonal, nonpositive -> domain_error
+      hb.dinv.resize(hb.n);
+      for (int i = 0; i < hb.n; ++i) {
+        const double d = diag_at(m, i);
+        if (!(d > 0.0)) throw std::domain_error("jacobi block: nonpositive diagonal");
+        hb.dinv[i] = 1.0 / d;
+      }
+    }
+    if (b == 1 && hb.kind != DSGPU_BLOCK_JACOBI) {
+      // permuted Q_nu operator for the pressure PCG
+      hb.rp.assign(hb.n + 1, 0);
+      for (int r = 0; r < hb.n; ++r)
+        hb.rp[r + 1] = hb.rp[r] + (m->row_ptr[hb.perm[r] + 1] - m->row_ptr[hb.perm[r]]);
+      hb.ci.resize(hb.rp[hb.n]);
+      hb.v.resize(hb.rp[hb.n]);
+      std::vector<std::pair<int32_t, double>> row;
+      for (int r = 0; r < hb.n; ++r) {
+        const int o = hb.perm[r];
+        row.clear();
+        for (int64_t k = m->row_ptr[o]; k < m->row_ptr[o + 1]; ++k)
+          row.emplace_back(inv[b][m->cols[k]], m->vals[k]);
+        std::sort(row.begin(), row.end(),
+                  [](const auto& x, const auto& y) { return x.first < y.first; });
+        int64_t at = hb.rp[r];
+        for (const auto& e : row) {
+          hb.ci[at] = e.first;
+          hb.v[at++] = e.second;
+        }
+      }
+    }
+    if (hb.kind == DSGPU_BLOCK_PCG_IC0) build_sweeps(*facs[b], hb.fwd, hb.bwd);
+  }
+
+  P.filter = false;
+  if (Q_filter) {
+    check_csr(Q_filter, n_p, n_p, "Q_filter");
+    // solve_stokes's zero-mean filter test (precond.cpp:266-274), kernel = 1
+    double resid = 0.0, bscale = 0.0;
+    for (int i = 0; i < n_u; ++i) {
+      double acc = 0.0;
+      for (int64_t k = Bt->row_ptr[i]; k < Bt->row_ptr[i + 1]; ++k) acc += Bt->vals[k] * 1.0;
+      resid = std::max(resid, std::abs(acc));
+    }
+    for (int64_t k = 0; k < B->row_ptr[n_p]; ++k) bscale = std::max(bscale, std::abs(B->vals[k]));
+    if (resid <= 1e-10 * bscale) {
+      P.filter = true;
+      std::vector<double> qk(n_p);
+      double den = 0.0;
+      for (int i = 0; i < n_p; ++i) {
+        double acc = 0.0;
+        for (int64_t k = Q_filter->row_ptr[i]; k < Q_filter->row_ptr[i + 1]; ++k)
+          acc += Q_filter->vals[k] * 1.0;
+        qk[i] = acc;
+        den += qk[i] * 1.0;
+      }
+      P.qk.resize(n_p);
+      for (int r = 0; r < n_p; ++r) P.qk[r] = qk[P.blk[1].perm[r]];
+      P.filter_den = den;
+    }
+  }
+}
+
+}  // namespace dsgpu

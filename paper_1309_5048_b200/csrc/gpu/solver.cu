@@ -1,0 +1,1175 @@
+// B200 (sm_100a) MINRES + block-diagonal IC(0)/PCG preconditioned Stokes
+// solve, behind the C ABI of include/dsgpu.h.
+//
+// Execution model: ONE cooperative persistent kernel runs the whole
+// preconditioned MINRES (reference proj/src/solvers.cpp:24-123) including the
+// inner PCG of each preconditioner block (solvers.cpp:125-159, driven as
+// PcgBlock::apply, precond.cpp:75-100) and the IC(0) applies
+// (cholesky.cpp:136-152). Scalars never leave the device: every CTA reduces
+// the same per-CTA partials in the same fixed order and takes identical
+// control decisions, so the only cross-CTA synchronization is one grid
+// barrier per dependent phase:
+//   outer iteration  : [w/aw/x/res update of it-1 + v = y/beta + saddle SpMV
+//                       + alpha partial]  |  [precond]
+//   precond start    : [r := input; IC sweeps or Jacobi]          | reduce rho
+//   inner PCG step   : [q = A p (p = z + beta p on the fly)]      | reduce kappa
+//                      [r -= alpha q; IC sweeps; x += alpha p]    | reduce rho'
+// The IC(0) sweeps of a block run inside one CTA (sync-free, level-grouped,
+// see dsgpu_internal.hpp) while the other CTAs do the element-wise updates;
+// the top (velocity) and bottom (pressure) blocks run concurrently on
+// different CTAs, their PCG loops in lockstep.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dsgpu_internal.hpp"
+#include "kernels.cuh"
+
+using namespace dsgpu;
+using namespace dsgpu::dev;
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kWarps = kThreads / 32;
+
+enum Slot { SL_BB = 0, SL_RES, SL_ALPHA, SL_RHO0, SL_RHO1, SL_KAP0, SL_KAP1, SL_ZR0, SL_ZR1, SL_NUM, NSLOT };
+
+struct DSweep {
+  int n_groups;
+  const int64_t* gptr;
+  const int32_t* gwidth;
+  const int32_t* grows;
+  const int32_t* cols;
+  const double* vals;
+  const double* diag;
+};
+
+struct DBlock {
+  int kind, n, off, ic_cta;
+  const int64_t* rp;  // operator rows (block ordering)
+  const int32_t* ci;
+  const double* v;
+  const int32_t* na;  // top block: A-part length of each K row (nullptr: full row)
+  const double* dinv;
+  DSweep fwd, bwd;
+  double *r, *z, *q, *p0, *p1;  // PCG work (block-local, length n)
+};
+
+struct DevReport {
+  int iterations, converged, status, failed_block, hist_len, pad;
+  double relres_m, relres_e;
+  long long inner[2], apps[2];
+};
+
+struct Args {
+  int n, n_u, n_p;
+  const int64_t* k_rp;
+  const int32_t* k_ci;
+  const double* k_v;
+  const int32_t* row_start;  // G + 1
+  DBlock blk[2];
+  const double* f_in;        // n_u, original order
+  const int32_t* perm_u;     // block ordering -> original
+  const int32_t* perm_p;
+  double* u_out;             // n_u, original order
+  double* p_out;             // n_p, original order
+  double *x, *y, *v, *av, *res;
+  double* rbuf[4];
+  double* w[3];
+  double* aw[3];
+  const double* qk;
+  double filter_den;
+  int filter;
+  double* partial;           // [2][NSLOT][G]
+  unsigned* bar;             // count @ [0], gen @ [32], abort @ [64]
+  double* hist_m;
+  double* hist_e;
+  int hist_cap;
+  double outer_tol, inner_tol;
+  int max_iter, stop_euclid, inner_cap;
+  DevReport* rep;
+  int smem_half;  // doubles per dataflow array (largest IC block)
+};
+
+// ---------------------------------------------------------------------------
+// triangular sweep (one CTA): x = T^{-1} rhs with T unit-free rows
+// x_i = (rhs_i - sum_k T_ik x_k) / d_i, entries in stored order, no FMA.
+template <class Rhs, class Out>
+__device__ void sweep(const DSweep& s, double* xs, int n, Rhs rhs, Out out, unsigned* abort_flag) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) slot_reset(xs, i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int g = warp; g < s.n_groups; g += nw) {
+    const int row = s.grows[static_cast<int64_t>(g) * 32 + lane];
+    double acc = row >= 0 ? rhs(row) : 0.0;
+    const int width = s.gwidth[g];
+    const int32_t* cp = s.cols + s.gptr[g] + lane;
+    const double* vp = s.vals + s.gptr[g] + lane;
+    int k = 0;
+    for (; k + 4 <= width; k += 4) {
+      const int c0 = cp[0], c1 = cp[32], c2 = cp[64], c3 = cp[96];
+      const double v0 = vp[0], v1 = vp[32], v2 = vp[64], v3 = vp[96];
+      cp += 128;
+      vp += 128;
+      if (c0 >= 0) acc = sub_rn(acc, mul_rn(v0, slot_wait(xs, c0, abort_flag)));
+      if (c1 >= 0) acc = sub_rn(acc, mul_rn(v1, slot_wait(xs, c1, abort_flag)));
+      if (c2 >= 0) acc = sub_rn(acc, mul_rn(v2, slot_wait(xs, c2, abort_flag)));
+      if (c3 >= 0) acc = sub_rn(acc, mul_rn(v3, slot_wait(xs, c3, abort_flag)));
+    }
+    for (; k < width; ++k) {
+      const int c0 = cp[0];
+      const double v0 = vp[0];
+      cp += 32;
+      vp += 32;
+      if (c0 >= 0) acc = sub_rn(acc, mul_rn(v0, slot_wait(xs, c0, abort_flag)));
+    }
+    if (row >= 0) {
+      const double xi = div_rn(acc, s.diag[row]);
+      slot_publish(xs, row, xi);
+      out(row, xi);
+    }
+  }
+  __syncthreads();
+}
+
+// IC(0) apply z = (L L^T)^{-1} r (Ic0Factor::solve) in one CTA; returns the
+// CTA sum of r_i z_i in warp 0. rhs(row) yields r_row (and may write it).
+template <class Rhs>
+__device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, double* red,
+                           unsigned* abort_flag) {
+  sweep(B.fwd, xf, B.n, rhs, [](int, double) {}, abort_flag);
+  double rz = 0.0;
+  double* z = B.z;
+  const double* r = B.r;
+  sweep(
+      B.bwd, xb, B.n, [&](int row) { return xf[row]; },
+      [&](int row, double zi) {
+        z[row] = zi;
+        rz += r[row] * zi;
+      },
+      abort_flag);
+  return block_sum(rz, red);
+}
+
+struct Input {
+  const double* src0;
+  const double* src1;
+  double coef;
+  double* dst;
+  __device__ __forceinline__ double at(int i) const {
+    return src1 ? add_rn(src0[i], mul_rn(coef, src1[i])) : src0[i];
+  }
+  __device__ __forceinline__ const double* materialized() const { return dst ? dst : src0; }
+};
+
+struct Ctx {
+  const Args& a;
+  int cta, G, r0, r1;
+  unsigned epoch;
+  double* red;
+  double* sums;
+  double* xf;
+  double* xb;
+  unsigned* abort_flag;
+  int status = DSGPU_OK, failed_block = -1;
+
+  __device__ Ctx(const Args& args, double* red_, double* sums_, double* xs)
+      : a(args), cta(blockIdx.x), G(gridDim.x), epoch(0), red(red_), sums(sums_) {
+    r0 = a.row_start[cta];
+    r1 = a.row_start[cta + 1];
+    xf = xs;
+    xb = xs + a.smem_half;
+    abort_flag = a.bar + 64;
+  }
+  __device__ double* part(int slot) {
+    return a.partial + (static_cast<size_t>(epoch & 1) * NSLOT + slot) * G;
+  }
+  // thread 0 of warp 0 publishes a CTA partial (value valid in warp 0)
+  __device__ void put(int slot, double v) {
+    if (threadIdx.x == 0) part(slot)[cta] = v;
+  }
+  // grid barrier, then reduce `mask` slots of this epoch into sums[]
+  __device__ bool sync_reduce(unsigned mask) {
+    const bool ok = grid_sync(a.bar, a.bar + 32, abort_flag);
+    if (ok) {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      if (warp < NSLOT && (mask >> warp) & 1u) {
+        const double* p = part(warp);
+        double s = 0.0;
+        for (int c = lane; c < G; c += 32) s += __ldcg(p + c);
+        s = warp_sum(s);
+        if (lane == 0) sums[warp] = s;
+      }
+    }
+    __syncthreads();
+    ++epoch;
+    return ok;
+  }
+  // rows of this CTA inside block b: [lo, hi) in global vector indices
+  __device__ void block_rows(int b, int& lo, int& hi) const {
+    lo = max(r0, a.blk[b].off);
+    hi = min(r1, a.blk[b].off + a.blk[b].n);
+  }
+};
+
+// Preconditioner application z = M^{-1} rin (BlockDiagPreconditioner::apply,
+// precond.cpp:139-148). Writes zout (length n), returns the two guard dots
+// <z_b, r_b> in zr[] (identical in all CTAs). False on error.
+__device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
+                        long long inner[2], long long apps[2]) {
+  const Args& a = C.a;
+  const int tid = threadIdx.x;
+  double rho_p[2] = {0.0, 0.0}, zr_p[2] = {0.0, 0.0};
+  // ---- S1: r := input; z := M_b^{-1} r; x := 0 -------------------------
+  for (int b = 0; b < 2; ++b) {
+    const DBlock& B = a.blk[b];
+    if (B.kind == DSGPU_BLOCK_PCG_IC0 && C.cta == B.ic_cta) {
+      const double* src0 = in.src0;
+      const double* src1 = in.src1;
+      const double coef = in.coef;
+      double* dst = in.dst;
+      double* r = B.r;
+      const int off = B.off;
+      rho_p[b] = ic_apply(
+          B,
+          [&](int row) {
+            const int i = off + row;
+            const double ri = src1 ? add_rn(src0[i], mul_rn(coef, src1[i])) : src0[i];
+            if (dst) dst[i] = ri;
+            r[row] = ri;
+            return ri;
+          },
+          C.xf, C.xb, C.red, C.abort_flag);
+    }
+  }
+  for (int b = 0; b < 2; ++b) {
+    const DBlock& B = a.blk[b];
+    int lo, hi;
+    C.block_rows(b, lo, hi);
+    double acc = 0.0;
+    for (int i = lo + tid; i < hi; i += blockDim.x) {
+      const int li = i - B.off;
+      if (B.kind == DSGPU_BLOCK_JACOBI) {
+        const double ri = in.at(i);
+        if (in.dst) in.dst[i] = ri;
+        const double zi = mul_rn(B.dinv[li], ri);
+        zout[i] = zi;
+        acc += zi * ri;
+      } else if (B.kind == DSGPU_BLOCK_PCG_JACOBI) {
+        const double ri = in.at(i);
+        if (in.dst) in.dst[i] = ri;
+        B.r[li] = ri;
+        const double zi = mul_rn(B.dinv[li], ri);
+        B.z[li] = zi;
+        zout[i] = 0.0;
+        acc += ri * zi;
+      } else {
+        zout[i] = 0.0;
+      }
+    }
+    const double s = block_sum(acc, C.red);
+    if (B.kind == DSGPU_BLOCK_JACOBI) zr_p[b] = s;
+    if (B.kind == DSGPU_BLOCK_PCG_JACOBI) rho_p[b] = s;
+  }
+  C.put(SL_RHO0, rho_p[0]);
+  C.put(SL_RHO1, rho_p[1]);
+  C.put(SL_ZR0, zr_p[0]);
+  C.put(SL_ZR1, zr_p[1]);
+  if (!C.sync_reduce((1u << SL_RHO0) | (1u << SL_RHO1) | (1u << SL_ZR0) | (1u << SL_ZR1)))
+    return false;
+
+  bool active[2] = {false, false};
+  double rho[2] = {0, 0}, rho0[2] = {0, 0}, beta[2] = {0, 0}, alpha[2] = {0, 0};
+  int it[2] = {0, 0};
+  for (int b = 0; b < 2; ++b) {
+    const DBlock& B = a.blk[b];
+    if (B.kind == DSGPU_BLOCK_JACOBI) {
+      zr[b] = C.sums[SL_ZR0 + b];
+      ++apps[b];
+      continue;
+    }
+    rho[b] = C.sums[SL_RHO0 + b];
+    if (rho[b] < 0.0) {  // pcg: preconditioner is not positive definite
+      C.status = DSGPU_E_INDEFINITE_PRECOND;
+      C.failed_block = b;
+      return false;
+    }
+    rho0[b] = rho[b];
+    active[b] = rho0[b] != 0.0;
+    zr[b] = 0.0;  // x = 0 if the block returns immediately
+  }
+  const double* rin = in.materialized();
+  int pp = 0;  // p ping-pong: read p[pp], write p[pp ^ 1]
+  int k = 0;
+  while (active[0] || active[1]) {
+    // ---- L1: q = A p_new, p_new = z (+ beta p_old) -----------------------
+    double kap_p[2] = {0.0, 0.0};
+    {
+      const int lane = tid & 31, warp = tid >> 5;
+      for (int b = 0; b < 2; ++b) {
+        if (!active[b]) continue;
+        const DBlock& B = a.blk[b];
+        int lo, hi;
+        C.block_rows(b, lo, hi);
+        const double* z = B.z;
+        const double* po = pp ? B.p1 : B.p0;
+        double* pn = pp ? B.p0 : B.p1;
+        const double bt = beta[b];
+        const bool first = k == 0;
+        double acc_k = 0.0;
+        for (int i = lo + warp; i < hi; i += kWarps) {
+          const int li = i - B.off;
+          const int64_t s = B.rp[li];
+          const int64_t e = B.na ? s + B.na[li] : B.rp[li + 1];
+          double acc = 0.0;
+          for (int64_t kk = s + lane; kk < e; kk += 32) {
+            const int j = B.ci[kk];
+            const double pj = first ? z[j] : add_rn(z[j], mul_rn(bt, po[j]));
+            acc = fma(B.v[kk], pj, acc);
+          }
+          acc = warp_sum(acc);
+          if (lane == 0) {
+            const double pi = first ? z[li] : add_rn(z[li], mul_rn(bt, po[li]));
+            pn[li] = pi;
+            B.q[li] = acc;
+            acc_k += pi * acc;
+          }
+        }
+        kap_p[b] = block_sum(acc_k, C.red);
+      }
+    }
+    C.put(SL_KAP0, kap_p[0]);
+    C.put(SL_KAP1, kap_p[1]);
+    if (!C.sync_reduce((1u << SL_KAP0) | (1u << SL_KAP1))) return false;
+    for (int b = 0; b < 2; ++b) {
+      if (!active[b]) continue;
+      const double kap = C.sums[SL_KAP0 + b];
+      if (kap <= 0.0) {  // pcg: operator is not positive definite
+        C.status = DSGPU_E_NEG_CURVATURE;
+        C.failed_block = b;
+        return false;
+      }
+      alpha[b] = div_rn(rho[b], kap);
+    }
+    // ---- L2: r -= alpha q; z = M^{-1} r; x += alpha p -------------------
+    double rho_n[2] = {0.0, 0.0}, zr_n[2] = {0.0, 0.0};
+    for (int b = 0; b < 2; ++b) {
+      const DBlock& B = a.blk[b];
+      if (active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.cta == B.ic_cta) {
+        double* r = B.r;
+        const double* q = B.q;
+        const double na = -alpha[b];
+        rho_n[b] = ic_apply(
+            B,
+            [&](int row) {
+              const double ri = add_rn(r[row], mul_rn(na, q[row]));
+              r[row] = ri;
+              return ri;
+            },
+            C.xf, C.xb, C.red, C.abort_flag);
+      }
+    }
+    for (int b = 0; b < 2; ++b) {
+      if (!active[b]) continue;
+      const DBlock& B = a.blk[b];
+      int lo, hi;
+      C.block_rows(b, lo, hi);
+      const double* pn = pp ? B.p0 : B.p1;
+      const double al = alpha[b], na = -alpha[b];
+      double acc_r = 0.0, acc_z = 0.0;
+      for (int i = lo + tid; i < hi; i += blockDim.x) {
+        const int li = i - B.off;
+        if (B.kind == DSGPU_BLOCK_PCG_JACOBI) {
+          const double ri = add_rn(B.r[li], mul_rn(na, B.q[li]));
+          B.r[li] = ri;
+          const double zi = mul_rn(B.dinv[li], ri);
+          B.z[li] = zi;
+          acc_r += ri * zi;
+        }
+        const double xi = add_rn(zout[i], mul_rn(al, pn[li]));
+        zout[i] = xi;
+        acc_z += xi * rin[i];
+      }
+      const double sr = block_sum(acc_r, C.red);
+      const double sz = block_sum(acc_z, C.red);
+      if (B.kind == DSGPU_BLOCK_PCG_JACOBI) rho_n[b] = sr;
+      zr_n[b] = sz;
+    }
+    C.put(SL_RHO0, rho_n[0]);
+    C.put(SL_RHO1, rho_n[1]);
+    C.put(SL_ZR0, zr_n[0]);
+    C.put(SL_ZR1, zr_n[1]);
+    if (!C.sync_reduce((1u << SL_RHO0) | (1u << SL_RHO1) | (1u << SL_ZR0) | (1u << SL_ZR1)))
+      return false;
+    for (int b = 0; b < 2; ++b) {
+      if (!active[b]) continue;
+      const double rn = C.sums[SL_RHO0 + b];
+      if (rn < 0.0) {
+        C.status = DSGPU_E_INDEFINITE_PRECOND;
+        C.failed_block = b;
+        return false;
+      }
+      ++it[b];
+      zr[b] = C.sums[SL_ZR0 + b];
+      if (sqrt_rn(div_rn(rn, rho0[b])) <= a.inner_tol || it[b] >= a.inner_cap) {
+        active[b] = false;
+      } else {
+        beta[b] = div_rn(rn, rho[b]);
+        rho[b] = rn;
+      }
+    }
+    pp ^= 1;
+    ++k;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (a.blk[b].kind != DSGPU_BLOCK_JACOBI) {
+      inner[b] += it[b];
+      ++apps[b];
+    }
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
+  extern __shared__ double xs_dyn[];
+  __shared__ double red[32];
+  __shared__ double sums[NSLOT];
+  Ctx C(a, red, sums, xs_dyn);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = C.r0, r1 = C.r1;
+  long long inner[2] = {0, 0}, apps[2] = {0, 0};
+  int iterations = 0, converged = 0, hist_len = 0;
+  double relres_m = 1.0, relres_e = 1.0;
+  const bool writer = (blockIdx.x == 0 && tid == 0);
+
+  // ---- P0: b = [f'; 0]; res = b; x = w* = aw* = 0; ||b||^2 --------------
+  double* bvec = a.rbuf[0];
+  {
+    double acc = 0.0;
+    for (int i = r0 + tid; i < r1; i += blockDim.x) {
+      const double bi = i < a.n_u ? a.f_in[a.perm_u[i]] : 0.0;
+      bvec[i] = bi;
+      a.res[i] = bi;
+      a.x[i] = 0.0;
+      a.w[0][i] = a.w[1][i] = a.w[2][i] = 0.0;
+      a.aw[0][i] = a.aw[1][i] = a.aw[2][i] = 0.0;
+      acc += bi * bi;
+    }
+    C.put(SL_BB, block_sum(acc, red));
+  }
+  if (!C.sync_reduce(1u << SL_BB)) goto finish;
+  {
+    const double rnorm0 = sqrt_rn(sums[SL_BB]);
+    double* r1v = a.rbuf[0];
+    double* r2v = a.rbuf[0];
+    double* spare = a.rbuf[1];
+    double* free4 = a.rbuf[2];
+    double* y = a.y;
+    double zr[2];
+    if (!precond(C, Input{r1v, nullptr, 0.0, nullptr}, y, zr, inner, apps)) goto finish;
+    if (zr[0] < 0.0 || zr[1] < 0.0) {  // BlockDiagPreconditioner guards
+      C.status = DSGPU_E_INDEFINITE_PRECOND;
+      C.failed_block = zr[0] < 0.0 ? 0 : 1;
+      goto finish;
+    }
+    double beta1 = zr[0] + zr[1];
+    if (beta1 < 0.0) {
+      C.status = DSGPU_E_INDEFINITE_PRECOND;
+      goto finish;
+    }
+    beta1 = sqrt_rn(beta1);
+    if (writer && a.hist_cap > 0) {
+      a.hist_m[0] = 1.0;
+      a.hist_e[0] = 1.0;
+    }
+    hist_len = 1;
+    if (beta1 == 0.0) {
+      converged = 1;
+      goto finish;
+    }
+    double oldb = 0.0, beta = beta1, dbar = 0.0, epsln = 0.0, phibar = beta1;
+    double cs = -1.0, sn = 0.0, oldeps = 0.0;
+    double delta = 0.0, gamma = 1.0, phi = 0.0;
+    int wi = 0;  // w[wi] = current w; rotation per reference swaps
+    bool pending = false;
+    bool do_spmv = true;
+    for (int it = 1;; ++it) {
+      // ---- M1: finish iteration it-1 (vector recurrences) + SpMV of it --
+      double acc_res = 0.0, acc_alpha = 0.0;
+      if (pending) {
+        // w1<->w2, w2<->w  =>  w1 = old w2, w2 = old w, w = old w1
+        const int iw = wi, iw1 = (wi + 1) % 3, iw2 = (wi + 2) % 3;  // current roles
+        const int nw = iw1;            // new w reuses old w1's buffer
+        const double* w1 = a.w[iw2];   // new w1 = old w2
+        const double* w2 = a.w[iw];    // new w2 = old w
+        double* wn = a.w[nw];
+        const double* aw1 = a.aw[iw2];
+        const double* aw2 = a.aw[iw];
+        double* awn = a.aw[nw];
+        wi = nw;
+        for (int i = r0 + tid; i < r1; i += blockDim.x) {
+          const double wv = div_rn(sub_rn(sub_rn(a.v[i], mul_rn(oldeps, w1[i])), mul_rn(delta, w2[i])), gamma);
+          const double awv =
+              div_rn(sub_rn(sub_rn(a.av[i], mul_rn(oldeps, aw1[i])), mul_rn(delta, aw2[i])), gamma);
+          wn[i] = wv;
+          awn[i] = awv;
+          a.x[i] = add_rn(a.x[i], mul_rn(phi, wv));
+          const double rv = add_rn(a.res[i], mul_rn(-phi, awv));
+          a.res[i] = rv;
+          acc_res += rv * rv;
+        }
+        C.put(SL_RES, block_sum(acc_res, red));
+      }
+      if (do_spmv) {
+        const double s = div_rn(1.0, beta);
+        const double c1 = it >= 2 ? div_rn(-beta, oldb) : 0.0;
+        for (int i = r0 + tid; i < r1; i += blockDim.x) a.v[i] = mul_rn(s, y[i]);
+        __syncthreads();  // old av consumed above before the new av is written
+        for (int i = r0 + warp; i < r1; i += kWarps) {
+          const int64_t ks = a.k_rp[i], ke = a.k_rp[i + 1];
+          double acc = 0.0;
+          for (int64_t kk = ks + lane; kk < ke; kk += 32)
+            acc = fma(a.k_v[kk], mul_rn(s, y[a.k_ci[kk]]), acc);
+          acc = warp_sum(acc);
+          if (lane == 0) {
+            a.av[i] = acc;
+            const double t = it >= 2 ? add_rn(acc, mul_rn(c1, r1v[i])) : acc;
+            spare[i] = t;
+            acc_alpha += mul_rn(s, y[i]) * t;
+          }
+        }
+        C.put(SL_ALPHA, block_sum(acc_alpha, red));
+      }
+      if (!C.sync_reduce((pending ? (1u << SL_RES) : 0u) | (do_spmv ? (1u << SL_ALPHA) : 0u)))
+        goto finish;
+      if (pending) {
+        // stop test of iteration it-1 (solvers.cpp:102-117)
+        relres_e = rnorm0 > 0.0 ? div_rn(sqrt_rn(sums[SL_RES]), rnorm0) : 0.0;
+        iterations = it - 1;
+        if (writer && hist_len < a.hist_cap) {
+          a.hist_m[hist_len] = relres_m;
+          a.hist_e[hist_len] = relres_e;
+        }
+        ++hist_len;
+        const double stop_value = a.stop_euclid ? relres_e : relres_m;
+        if (stop_value <= a.outer_tol) {
+          converged = 1;
+          break;
+        }
+        if (beta == 0.0) {
+          converged = relres_m <= a.outer_tol;
+          break;
+        }
+        if (!do_spmv) break;  // max_iter reached
+      }
+      const double alfa = sums[SL_ALPHA];
+      // ---- precond: r2_new = spare - (alfa/beta) r2;  y = M^{-1} r2_new ----
+      if (!precond(C, Input{spare, r2v, div_rn(-alfa, beta), spare}, y, zr, inner, apps))
+        goto finish;
+      {
+        double* nr1 = r2v;
+        double* nr2 = spare;
+        double* nsp = (r1v != r2v) ? r1v : free4;
+        r1v = nr1;
+        r2v = nr2;
+        spare = nsp;
+      }
+      if (zr[0] < 0.0 || zr[1] < 0.0) {
+        C.status = DSGPU_E_INDEFINITE_PRECOND;
+        C.failed_block = zr[0] < 0.0 ? 0 : 1;
+        goto finish;
+      }
+      oldb = beta;
+      const double betasq = zr[0] + zr[1];
+      if (betasq < 0.0) {
+        C.status = DSGPU_E_INDEFINITE_PRECOND;
+        goto finish;
+      }
+      beta = sqrt_rn(betasq);
+      // Givens (solvers.cpp:79-91)
+      oldeps = epsln;
+      delta = add_rn(mul_rn(cs, dbar), mul_rn(sn, alfa));
+      const double gbar = sub_rn(mul_rn(sn, dbar), mul_rn(cs, alfa));
+      epsln = mul_rn(sn, beta);
+      dbar = mul_rn(-cs, beta);
+      gamma = sqrt_rn(add_rn(mul_rn(gbar, gbar), mul_rn(beta, beta)));
+      gamma = fmax(gamma, 2.220446049250313e-16);
+      cs = div_rn(gbar, gamma);
+      sn = div_rn(beta, gamma);
+      phi = mul_rn(cs, phibar);
+      phibar = mul_rn(sn, phibar);
+      relres_m = div_rn(phibar, beta1);
+      pending = true;
+      do_spmv = (it < a.max_iter) && beta != 0.0;
+      if (it >= a.max_iter) iterations = it;
+    }
+  }
+finish:
+  // ---- F: zero-mean pressure filter + un-permute -------------------------
+  {
+    double mean = 0.0;
+    if (a.filter && C.status == DSGPU_OK) {
+      double acc = 0.0;
+      const int lo = max(r0, a.n_u);
+      for (int i = lo + tid; i < r1; i += blockDim.x) acc += a.qk[i - a.n_u] * a.x[i];
+      C.put(SL_NUM, block_sum(acc, red));
+      if (C.sync_reduce(1u << SL_NUM)) mean = div_rn(sums[SL_NUM], a.filter_den);
+    }
+    for (int i = r0 + tid; i < r1; i += blockDim.x) {
+      if (i < a.n_u)
+        a.u_out[a.perm_u[i]] = a.x[i];
+      else
+        a.p_out[a.perm_p[i - a.n_u]] = a.filter ? sub_rn(a.x[i], mul_rn(mean, 1.0)) : a.x[i];
+    }
+  }
+  if (writer) {
+    DevReport* R = a.rep;
+    R->iterations = iterations;
+    R->converged = converged;
+    R->status = C.status;
+    R->failed_block = C.failed_block;
+    R->hist_len = hist_len;
+    R->relres_m = relres_m;
+    R->relres_e = relres_e;
+    R->inner[0] = inner[0];
+    R->inner[1] = inner[1];
+    R->apps[0] = apps[0];
+    R->apps[1] = apps[1];
+    if (*reinterpret_cast<volatile unsigned*>(a.bar + 64)) R->status = DSGPU_E_CUDA;
+  }
+}
+
+// ---- standalone kernels (parity / microbenchmarks) -------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+    ic_apply_kernel(const __grid_constant__ DBlock B, const double* r, double* z, unsigned* abort_flag) {
+  extern __shared__ double xs_dyn[];
+  __shared__ double red[32];
+  double* xf = xs_dyn;
+  double* xb = xs_dyn + B.n;
+  sweep(B.fwd, xf, B.n, [&](int row) { return r[row]; }, [](int, double) {}, abort_flag);
+  sweep(
+      B.bwd, xb, B.n, [&](int row) { return xf[row]; }, [&](int row, double zi) { z[row] = zi; },
+      abort_flag);
+  (void)red;
+}
+
+// y = M x, warp per row; na != nullptr limits each row to its first na[i] entries
+__global__ void spmv_kernel(int n_rows, const int64_t* rp, const int32_t* ci, const double* v,
+                            const int32_t* na, const double* x, double* y) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n_rows) return;
+  const int64_t s = rp[row], e = na ? s + na[row] : rp[row + 1];
+  double acc = 0.0;
+  for (int64_t k = s + lane; k < e; k += 32) acc = fma(v[k], x[ci[k]], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) y[row] = acc;
+}
+
+__global__ void gather_kernel(int n, const int32_t* perm, const double* src, double* dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[perm[i]];
+}
+__global__ void scatter_kernel(int n, const int32_t* perm, const double* src, double* dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[perm[i]] = src[i];
+}
+
+// ---- device memory -----------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct dsgpu_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  bool ready = false;
+  HostPlan plan;
+  std::vector<DevBuf> bufs;
+  Args args{};
+  int grid = 0;
+  size_t smem = 0;
+  std::vector<int32_t> row_start;
+  int64_t levels[4] = {0, 0, 0, 0};
+  double* d_f = nullptr;
+  double* d_u = nullptr;
+  double* d_p = nullptr;
+  double* d_tmp[3] = {nullptr, nullptr, nullptr};
+  DevReport* d_rep = nullptr;
+  int64_t nnz_k = 0, nnz_a = 0, nnz_l[2] = {0, 0}, nnz_q = 0;
+
+  template <class T>
+  T* alloc(size_t count) {
+    DevBuf b;
+    b.bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (cudaMalloc(&b.p, b.bytes) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+    bufs.push_back(b);
+    return static_cast<T*>(b.p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* d = alloc<T>(v.size());
+    if (!v.empty() &&
+        cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+      throw std::runtime_error("cudaMemcpy H2D failed");
+    return d;
+  }
+  void free_all() {
+    for (auto& b : bufs) cudaFree(b.p);
+    bufs.clear();
+    ready = false;
+  }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(dsgpu_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  g_err = msg;
+  return code;
+}
+
+int cuda_check(dsgpu_handle* h, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return DSGPU_OK;
+  return fail(h, DSGPU_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+DSweep upload_sweep(dsgpu_handle* h, const HostSweep& s) {
+  DSweep d{};
+  d.n_groups = s.n_groups;
+  d.gptr = h->upload(s.gptr);
+  d.gwidth = h->upload(s.gwidth);
+  d.grows = h->upload(s.grows);
+  d.cols = h->upload(s.cols);
+  d.vals = h->upload(s.vals);
+  d.diag = h->upload(s.diag);
+  return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dsgpu_last_error(const dsgpu_handle* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+void dsgpu_default_opts(dsgpu_opts* o) {
+  o->outer_tol = 1e-12;
+  o->inner_tol = 1e-6;
+  o->max_iter = 20000;
+  o->stop = DSGPU_STOP_EUCLIDEAN;
+  o->inner_cap = 100000;
+}
+
+int dsgpu_create(int device, dsgpu_handle** out) {
+  *out = nullptr;
+  auto h = std::make_unique<dsgpu_handle>();
+  h->device = device;
+  int rc = cuda_check(nullptr, cudaSetDevice(device), "cudaSetDevice");
+  if (rc) return rc;
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+  if (!coop) return fail(nullptr, DSGPU_E_CUDA, "device lacks cooperative launch");
+  rc = cuda_check(nullptr, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking),
+                  "cudaStreamCreate");
+  if (rc) return rc;
+  *out = h.release();
+  return DSGPU_OK;
+}
+
+void dsgpu_destroy(dsgpu_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  h->free_all();
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu_csr* Bt,
+                const dsgpu_csr* Q_nu, int top_kind, const int32_t* perm_A, const dsgpu_csr* L_A,
+                int bottom_kind, const int32_t* perm_Q, const dsgpu_csr* L_Q,
+                const dsgpu_csr* Q_filter) {
+  if (!h) return fail(nullptr, DSGPU_E_BAD_INPUT, "null handle");
+  cudaSetDevice(h->device);
+  h->free_all();
+  h->plan = HostPlan{};
+  try {
+    build_plan(h->plan, A, B, Bt, Q_nu, top_kind, perm_A, L_A, bottom_kind, perm_Q, L_Q,
+               Q_filter);
+  } catch (const std::domain_error& e) {
+    return fail(h, DSGPU_E_NONPOS_DIAG, e.what());
+  } catch (const std::exception& e) {
+    return fail(h, DSGPU_E_BAD_INPUT, e.what());
+  }
+  HostPlan& P = h->plan;
+  try {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    // smem: two dataflow arrays of the largest IC block
+    int nmax = 0;
+    for (int b = 0; b < 2; ++b)
+      if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0) nmax = std::max(nmax, P.blk[b].n);
+    h->smem = static_cast<size_t>(2) * nmax * sizeof(double);
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+    const size_t static_smem = 1024;
+    if (h->smem + static_smem > static_cast<size_t>(smem_optin))
+      return fail(h, DSGPU_E_UNSUPPORTED,
+                  "IC(0) block too large for the shared-memory dataflow sweep in this build (n=" +
+                      std::to_string(nmax) + ")");
+    int rc = cuda_check(h,
+                        cudaFuncSetAttribute(minres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(h->smem)),
+                        "cudaFuncSetAttribute");
+    if (rc) return rc;
+    rc = cuda_check(h,
+                    cudaFuncSetAttribute(ic_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(h->smem)),
+                    "cudaFuncSetAttribute");
+    if (rc) return rc;
+    int per_sm = 0;
+    rc = cuda_check(h,
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minres_kernel, kThreads,
+                                                                  h->smem),
+                    "occupancy");
+    if (rc) return rc;
+    if (per_sm < 1) return fail(h, DSGPU_E_CUDA, "minres kernel cannot be resident");
+    // grid: one CTA per SM, fewer for tiny systems (barrier cost grows with CTAs)
+    const int64_t nnz = P.k_rp[P.n];
+    int G = static_cast<int>(std::min<int64_t>(sms, std::max<int64_t>(2, (nnz + 16383) / 16384)));
+    G = std::max(G, 2);
+    if (const char* env = std::getenv("DSGPU_GRID")) G = std::max(2, std::min(sms, std::atoi(env)));
+    h->grid = G;
+    // K-row partition balanced by nnz + per-row vector work
+    h->row_start.assign(G + 1, 0);
+    {
+      const double total = static_cast<double>(nnz) + 24.0 * P.n;
+      int c = 1;
+      for (int i = 0; i < P.n && c < G; ++i) {
+        const double done = static_cast<double>(P.k_rp[i + 1]) + 24.0 * (i + 1);
+        while (c < G && done >= total * c / G) h->row_start[c++] = i + 1;
+      }
+      while (c < G) h->row_start[c++] = P.n;
+      h->row_start[G] = P.n;
+    }
+    Args& a = h->args;
+    a = Args{};
+    a.n = P.n;
+    a.n_u = P.n_u;
+    a.n_p = P.n_p;
+    a.k_rp = h->upload(P.k_rp);
+    a.k_ci = h->upload(P.k_ci);
+    a.k_v = h->upload(P.k_v);
+    a.row_start = h->upload(h->row_start);
+    const int32_t* d_na = h->upload(P.k_na);
+    for (int b = 0; b < 2; ++b) {
+      HostBlock& hb = P.blk[b];
+      DBlock& d = a.blk[b];
+      d.kind = hb.kind;
+      d.n = hb.n;
+      d.off = hb.off;
+      d.ic_cta = b;
+      if (b == 0) {
+        d.rp = a.k_rp;
+        d.ci = a.k_ci;
+        d.v = a.k_v;
+        d.na = d_na;
+      } else if (hb.kind != DSGPU_BLOCK_JACOBI) {
+        d.rp = h->upload(hb.rp);
+        d.ci = h->upload(hb.ci);
+        d.v = h->upload(hb.v);
+        d.na = nullptr;
+      }
+      if (!hb.dinv.empty()) d.dinv = h->upload(hb.dinv);
+      if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
+        d.fwd = upload_sweep(h, hb.fwd);
+        d.bwd = upload_sweep(h, hb.bwd);
+      }
+      d.r = h->alloc<double>(hb.n);
+      d.z = h->alloc<double>(hb.n);
+      d.q = h->alloc<double>(hb.n);
+      d.p0 = h->alloc<double>(hb.n);
+      d.p1 = h->alloc<double>(hb.n);
+    }
+    h->levels[0] = P.blk[0].fwd.n_levels;
+    h->levels[1] = P.blk[0].bwd.n_levels;
+    h->levels[2] = P.blk[1].fwd.n_levels;
+    h->levels[3] = P.blk[1].bwd.n_levels;
+    h->nnz_k = nnz;
+    {
+      int64_t s = 0;
+      for (int i = 0; i < P.n_u; ++i) s += P.k_na[i];
+      h->nnz_a = s;
+    }
+    for (int b = 0; b < 2; ++b)
+      h->nnz_l[b] = P.blk[b].kind == DSGPU_BLOCK_PCG_IC0
+                        ? static_cast<int64_t>(P.blk[b].fwd.diag.size()) +
+                              [&] {
+                                int64_t c = 0;
+                                for (auto x : P.blk[b].fwd.cols) c += x >= 0;
+                                return c;
+                              }()
+                        : 0;
+    h->nnz_q = P.blk[1].rp.empty() ? 0 : P.blk[1].rp.back();
+    a.perm_u = h->upload(P.blk[0].perm);
+    a.perm_p = h->upload(P.blk[1].perm);
+    a.x = h->alloc<double>(P.n);
+    a.y = h->alloc<double>(P.n);
+    a.v = h->alloc<double>(P.n);
+    a.av = h->alloc<double>(P.n);
+    a.res = h->alloc<double>(P.n);
+    for (int i = 0; i < 4; ++i) a.rbuf[i] = h->alloc<double>(P.n);
+    for (int i = 0; i < 3; ++i) {
+      a.w[i] = h->alloc<double>(P.n);
+      a.aw[i] = h->alloc<double>(P.n);
+    }
+    a.smem_half = nmax;
+    a.filter = P.filter ? 1 : 0;
+    a.qk = P.filter ? h->upload(P.qk) : nullptr;
+    a.filter_den = P.filter_den;
+    a.partial = h->alloc<double>(static_cast<size_t>(2) * NSLOT * G);
+    a.bar = h->alloc<unsigned>(128);
+    rc = cuda_check(h, cudaMemset(a.bar, 0, 128 * sizeof(unsigned)), "cudaMemset");
+    if (rc) return rc;
+    h->d_rep = h->alloc<DevReport>(1);
+    a.rep = h->d_rep;
+    h->d_f = h->alloc<double>(P.n_u);
+    h->d_u = h->alloc<double>(P.n_u);
+    h->d_p = h->alloc<double>(P.n_p);
+    for (int i = 0; i < 3; ++i) h->d_tmp[i] = h->alloc<double>(P.n);
+  } catch (const std::exception& e) {
+    h->free_all();
+    return fail(h, DSGPU_E_CUDA, e.what());
+  }
+  h->ready = true;
+  return DSGPU_OK;
+}
+
+static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, double* d_u,
+                     double* d_p, dsgpu_report* rep, double* d_hm, double* d_he, int hist_cap) {
+  Args a = h->args;
+  a.f_in = d_f;
+  a.u_out = d_u;
+  a.p_out = d_p;
+  dsgpu_opts def;
+  dsgpu_default_opts(&def);
+  if (!o) o = &def;
+  if (!(o->outer_tol > 0.0) || o->max_iter < 1 || o->inner_cap < 1)
+    return fail(h, DSGPU_E_BAD_INPUT, "dsgpu_solve: bad options");
+  a.outer_tol = o->outer_tol;
+  a.inner_tol = o->inner_tol;
+  a.max_iter = o->max_iter;
+  a.stop_euclid = o->stop == DSGPU_STOP_EUCLIDEAN ? 1 : 0;
+  a.inner_cap = o->inner_cap;
+  a.hist_m = d_hm;
+  a.hist_e = d_he;
+  a.hist_cap = (d_hm && d_he) ? hist_cap : 0;
+  int rc = cuda_check(h, cudaMemsetAsync(a.bar, 0, 128 * sizeof(unsigned), h->stream), "memset");
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, h->stream);
+  void* params[] = {&a};
+  rc = cuda_check(h,
+                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_kernel), dim3(h->grid),
+                                              dim3(kThreads), params, h->smem, h->stream),
+                  "cooperative launch");
+  cudaEventRecord(e1, h->stream);
+  if (rc) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  DevReport R{};
+  rc = cuda_check(h, cudaMemcpyAsync(&R, h->d_rep, sizeof(R), cudaMemcpyDeviceToHost, h->stream),
+                  "report D2H");
+  if (!rc) rc = cuda_check(h, cudaStreamSynchronize(h->stream), "solve");
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->iterations = R.iterations;
+  rep->converged = R.converged;
+  rep->status = R.status;
+  rep->failed_block = R.failed_block;
+  rep->wall_seconds = ms * 1e-3;
+  rep->relres_m = R.relres_m;
+  rep->relres_e = R.relres_e;
+  rep->inner_top = R.inner[0];
+  rep->inner_bottom = R.inner[1];
+  rep->apps_top = R.apps[0];
+  rep->apps_bottom = R.apps[1];
+  rep->mean_inner_top = (h->plan.blk[0].kind != DSGPU_BLOCK_JACOBI && R.apps[0] > 0)
+                            ? static_cast<double>(R.inner[0]) / R.apps[0]
+                            : 0.0;
+  rep->mean_inner_bottom = (h->plan.blk[1].kind != DSGPU_BLOCK_JACOBI && R.apps[1] > 0)
+                               ? static_cast<double>(R.inner[1]) / R.apps[1]
+                               : 0.0;
+  rep->hist_len = R.hist_len;
+  rep->gpu_launches = 1;
+  if (R.status == DSGPU_E_CUDA) return fail(h, DSGPU_E_CUDA, "device spin timeout (aborted)");
+  if (R.status != DSGPU_OK)
+    return fail(h, R.status,
+                R.status == DSGPU_E_NEG_CURVATURE
+                    ? "pcg: operator is not positive definite"
+                    : std::string("preconditioner: ") + (R.failed_block == 1 ? "pressure" : "velocity") +
+                          " block produced a negative inner product");
+  return DSGPU_OK;
+}
+
+int dsgpu_solve_device(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, double* d_u_out,
+                       double* d_p_out, dsgpu_report* rep) {
+  if (!h || !h->ready) return fail(h, DSGPU_E_BAD_INPUT, "dsgpu_solve_device: not set up");
+  cudaSetDevice(h->device);
+  return run_solve(h, d_f, o, d_u_out, d_p_out, rep, nullptr, nullptr, 0);
+}
+
+int dsgpu_solve(dsgpu_handle* h, const double* f, const dsgpu_opts* o, double* u_out,
+                double* p_out, dsgpu_report* rep, double* hist_m, double* hist_e,
+                int32_t hist_cap) {
+  if (!h || !h->ready) return fail(h, DSGPU_E_BAD_INPUT, "dsgpu_solve: not set up");
+  cudaSetDevice(h->device);
+  const HostPlan& P = h->plan;
+  int rc = cuda_check(h,
+                      cudaMemcpyAsync(h->d_f, f, sizeof(double) * P.n_u, cudaMemcpyHostToDevice,
+                                      h->stream),
+                      "f H2D");
+  if (rc) return rc;
+  double* d_hm = nullptr;
+  double* d_he = nullptr;
+  if (hist_m && hist_e && hist_cap > 0) {
+    if (cudaMallocAsync(&d_hm, sizeof(double) * hist_cap, h->stream) != cudaSuccess ||
+        cudaMallocAsync(&d_he, sizeof(double) * hist_cap, h->stream) != cudaSuccess)
+      return fail(h, DSGPU_E_CUDA, "history alloc failed");
+  }
+  const int src = run_solve(h, h->d_f, o, h->d_u, h->d_p, rep, d_hm, d_he, hist_cap);
+  if (src == DSGPU_OK || src == DSGPU_E_INDEFINITE_PRECOND || src == DSGPU_E_NEG_CURVATURE) {
+    cudaMemcpyAsync(u_out, h->d_u, sizeof(double) * P.n_u, cudaMemcpyDeviceToHost, h->stream);
+    cudaMemcpyAsync(p_out, h->d_p, sizeof(double) * P.n_p, cudaMemcpyDeviceToHost, h->stream);
+    if (d_hm) {
+      const int len = std::min(rep->hist_len, hist_cap);
+      cudaMemcpyAsync(hist_m, d_hm, sizeof(double) * len, cudaMemcpyDeviceToHost, h->stream);
+      cudaMemcpyAsync(hist_e, d_he, sizeof(double) * len, cudaMemcpyDeviceToHost, h->stream);
+    }
+  }
+  if (d_hm) {
+    cudaFreeAsync(d_hm, h->stream);
+    cudaFreeAsync(d_he, h->stream);
+  }
+  rc = cuda_check(h, cudaStreamSynchronize(h->stream), "solve D2H");
+  return src ? src : rc;
+}
+
+int dsgpu_apply_saddle(dsgpu_handle* h, const double* x, double* y) {
+  if (!h || !h->ready) return fail(h, DSGPU_E_BAD_INPUT, "not set up");
+  cudaSetDevice(h->device);
+  const HostPlan& P = h->plan;
+  const Args& a = h->args;
+  double *d0 = h->d_tmp[0], *d1 = h->d_tmp[1], *d2 = h->d_tmp[2];
+  cudaMemcpyAsync(d0, x, sizeof(double) * P.n, cudaMemcpyHostToDevice, h->stream);
+  // to RCM basis: x'[i] = x[perm_u[i]] / x'[n_u+i] = x[n_u + perm_p[i]]
+  gather_kernel<<<(P.n_u + 255) / 256, 256, 0, h->stream>>>(P.n_u, a.perm_u, d0, d1);
+  gather_kernel<<<(P.n_p + 255) / 256, 256, 0, h->stream>>>(P.n_p, a.perm_p, d0 + P.n_u, d1 + P.n_u);
+  spmv_kernel<<<(P.n * 32 + 255) / 256, 256, 0, h->stream>>>(P.n, a.k_rp, a.k_ci, a.k_v, nullptr, d1, d2);
+  scatter_kernel<<<(P.n_u + 255) / 256, 256, 0, h->stream>>>(P.n_u, a.perm_u, d2, d0);
+  scatter_kernel<<<(P.n_p + 255) / 256, 256, 0, h->stream>>>(P.n_p, a.perm_p, d2 + P.n_u, d0 + P.n_u);
+  cudaMemcpyAsync(y, d0, sizeof(double) * P.n, cudaMemcpyDeviceToHost, h->stream);
+  return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_saddle");
+}
+
+int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z) {
+  if (!h || !h->ready) return fail(h, DSGPU_E_BAD_INPUT, "not set up");
+  if (block < 0 || block > 1 || h->plan.blk[block].kind != DSGPU_BLOCK_PCG_IC0)
+    return fail(h, DSGPU_E_BAD_INPUT, "block has no IC(0) factor");
+  cudaSetDevice(h->device);
+  const int n = h->plan.blk[block].n;
+  double *d0 = h->d_tmp[0], *d1 = h->d_tmp[1];
+  cudaMemcpyAsync(d0, r, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream);
+  cudaMemsetAsync(h->args.bar, 0, 128 * sizeof(unsigned), h->stream);
+  ic_apply_kernel<<<1, kThreads, 2 * n * sizeof(double), h->stream>>>(h->args.blk[block], d0, d1,
+                                                                      h->args.bar + 64);
+  cudaMemcpyAsync(z, d1, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream);
+  return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_ic0");
+}
+
+int dsgpu_apply_block_matrix(dsgpu_handle* h, int block, const double* x, double* y) {
+  if (!h || !h->ready) return fail(h, DSGPU_E_BAD_INPUT, "not set up");
+  if (block < 0 || block > 1 || !h->args.blk[block].rp)
+    return fail(h, DSGPU_E_BAD_INPUT, "block has no device operator");
+  cudaSetDevice(h->device);
+  const DBlock& B = h->args.blk[block];
+  double *d0 = h->d_tmp[0], *d1 = h->d_tmp[1];
+  cudaMemcpyAsync(d0, x, sizeof(double) * B.n, cudaMemcpyHostToDevice, h->stream);
+  spmv_kernel<<<(B.n * 32 + 255) / 256, 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1);
+  cudaMemcpyAsync(y, d1, sizeof(double) * B.n, cudaMemcpyDeviceToHost, h->stream);
+  return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_block_matrix");
+}
+
+int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
+  if (!h || !h->ready || reps < 1) return fail(h, DSGPU_E_BAD_INPUT, "not set up");
+  cudaSetDevice(h->device);
+  const HostPlan& P = h->plan;
+  const Args& a = h->args;
+  double *d0 = h->d_tmp[0], *d1 = h->d_tmp[1];
+  cudaMemsetAsync(d0, 0, sizeof(double) * P.n, h->stream);
+  cudaMemsetAsync(a.bar, 0, 128 * sizeof(unsigned), h->stream);
+  auto launch = [&]() {
+    if (which == 0) {
+      spmv_kernel<<<(P.n * 32 + 255) / 256, 256, 0, h->stream>>>(P.n, a.k_rp, a.k_ci, a.k_v, nullptr, d0, d1);
+    } else if (which == 1 || which == 2) {
+      const DBlock& B = a.blk[which - 1];
+      ic_apply_kernel<<<1, kThreads, 2 * B.n * sizeof(double), h->stream>>>(B, d0, d1, a.bar + 64);
+    } else {
+      const DBlock& B = a.blk[0];
+      spmv_kernel<<<(B.n * 32 + 255) / 256, 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1);
+    }
+  };
+  if ((which == 1 || which == 2) && a.blk[which - 1].kind != DSGPU_BLOCK_PCG_IC0)
+    return fail(h, DSGPU_E_BAD_INPUT, "block has no IC(0) factor");
+  launch();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, h->stream);
+  for (int r = 0; r < reps; ++r) launch();
+  cudaEventRecord(e1, h->stream);
+  const int rc = cuda_check(h, cudaEventSynchronize(e1), "time_kernel");
+  float t = 0.0f;
+  cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = t / reps;
+  return rc;
+}
+
+int dsgpu_info(const dsgpu_handle* h, int64_t* info) {
+  if (!h || !h->ready) return DSGPU_E_BAD_INPUT;
+  info[0] = h->plan.n_u;
+  info[1] = h->plan.n_p;
+  info[2] = h->nnz_k;
+  info[3] = h->nnz_a;
+  info[4] = h->nnz_l[0];
+  info[5] = h->nnz_l[1];
+  info[6] = h->nnz_q;
+  for (int i = 0; i < 4; ++i) info[7 + i] = h->levels[i];
+  info[11] = h->grid;
+  return DSGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,195 @@
+"""GPU parity: the sm_100a solve through the C ABI against the CPU oracle
+(the reference itself when oracle/_ref is built, else the C restatement) on
+identical inputs. Bar (BASELINE north_star): solution rel-L2 <= 1e-8, outer
+iterations within +-2, final relative residual <= tol. Kernel-level checks:
+saddle SpMV to 1e-14 (fp64, different summation order), IC(0) apply
+bit-identical (same per-row operation order as Ic0Factor::solve)."""
+import numpy as np
+import pytest
+
+from conftest import golden_csr, load_golden, to_oracle
+
+pytestmark = pytest.mark.gpu
+
+STRATS = ["IC0-PCG(A,Q)", "IC0-PCG(A)+Diag(Q)", "PCG(A,Q)", "PCG(A)+Diag(Q)", "Diag(A,Q)"]
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1309_5048_b200 import host, solver
+    return host, solver
+
+
+def reference_solve(port, system, strategy, outer, inner, max_iter=20000):
+    """CPU oracle solve on the identical system (reference-exact restatement)."""
+    o = port.solve_stokes(to_oracle(system.A), to_oracle(system.B), to_oracle(system.Bt),
+                          to_oracle(system.Q_nu), system.f, strategy, outer, inner,
+                          max_iter=max_iter, Q_filter=to_oracle(system.Q))
+    assert o["status"] == 0
+    return o
+
+
+def check_parity(sol, o, tol):
+    x = np.concatenate([sol.u, sol.p])
+    xr = np.concatenate([o["u"], o["p"]])
+    rel = np.linalg.norm(x - xr) / np.linalg.norm(xr)
+    assert rel <= 1e-8, rel
+    assert abs(sol.report.iterations - o["iterations"]) <= 2
+    assert sol.report.converged and o["converged"]
+    assert sol.report.relres_e <= tol
+    return rel
+
+
+def test_saddle_apply_matches_reference(gpu, port):
+    host, solver = gpu
+    d = load_golden("c1_psi_k2_n8.npz")
+    s = host.assemble("psi-mms", 2, 8)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    y = g.apply(d["apply_x"])
+    ref = d["apply_y"]
+    assert np.abs(y - ref).max() <= 1e-14 * np.abs(ref).max()
+
+
+def test_ic0_apply_bit_identical(gpu, port):
+    host, solver = gpu
+    d = load_golden("c1_psi_k2_n8.npz")
+    s = host.assemble("psi-mms", 2, 8)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    for b, tag in ((0, "A"), (1, "Q")):
+        z = g.apply_ic0(b, d["ic_r_" + tag])
+        assert np.array_equal(z, d["ic_z_" + tag])  # the reference's own output
+    # larger: C2 velocity block against the restatement
+    s = host.assemble("psi-mms", 2, 64)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    r = np.random.default_rng(3).standard_normal(s.n_u)
+    z = g.apply_ic0(0, r)
+    assert np.array_equal(z, port.ic0_solve(to_oracle(g.top.factor), r))
+
+
+def test_block_matrix_apply(gpu, port):
+    host, solver = gpu
+    s = host.assemble("cavity", 2, 16)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    P = port.permute(to_oracle(s.A), g.top.perm)
+    x = np.random.default_rng(4).standard_normal(s.n_u)
+    y = g.apply_block_matrix(0, x)
+    yr = port.spmv(P, x)
+    assert np.abs(y - yr).max() <= 1e-14 * np.abs(yr).max()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_small_system_all_strategies_vs_golden(gpu, strategy):
+    """Reference solutions committed by make_golden.py (reference run)."""
+    host, solver = gpu
+    d = load_golden("c1_psi_k2_n8.npz")
+    s = host.assemble("psi-mms", 2, 8)
+    for itol in (1e-1, 1e-6):
+        key = f"{strategy}|{itol:g}"
+        sol = solver.solve_stokes(s, strategy, solver.SolverOptions(outer_tol=1e-8, inner_tol=itol))
+        meta = d["sol_meta|" + key]
+        x = np.concatenate([sol.u, sol.p])
+        xr = np.concatenate([d["sol_u|" + key], d["sol_p|" + key]])
+        assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+        assert abs(sol.report.iterations - int(meta[0])) <= 2
+        assert sol.report.converged
+        hm = sol.report.residual_history
+        assert hm[0] == 1.0 and len(hm) == sol.report.iterations + 1
+        assert np.all(hm[1:] <= hm[:-1] * (1 + 1e-10))  # M^-1-norm nonincreasing
+
+
+def test_config1_vs_golden(gpu):
+    """BASELINE config 1: 16x16, IC0-PCG(A)+Diag(Q), outer 1e-8, inner 1e-1."""
+    host, solver = gpu
+    g = load_golden("c1_psi_k2_n16.npz")
+    s = host.assemble("psi-mms", 2, 16)
+    sol = solver.solve_stokes(s, "IC0-PCG(A)+Diag(Q)",
+                              solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+    x = np.concatenate([sol.u, sol.p])
+    xr = np.concatenate([g["u"], g["p"]])
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+    assert abs(sol.report.iterations - int(g["meta"][0])) <= 2
+    assert abs(sol.report.mean_inner_top - g["meta"][2]) < 0.1
+    assert sol.report.relres_e <= 1e-8
+
+
+@pytest.mark.parametrize("inner", [1e-1, 1e-8])
+def test_config2_both_variants(gpu, port, inner):
+    """BASELINE config 2: 64x64 k'=2, IC0-PCG(A,Q), exact-ish and relaxed inner CG."""
+    host, solver = gpu
+    s = host.assemble("psi-mms", 2, 64)
+    sol = solver.solve_stokes(s, "IC0-PCG(A,Q)", solver.SolverOptions(outer_tol=1e-8, inner_tol=inner))
+    o = reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, inner)
+    check_parity(sol, o, 1e-8)
+    assert abs(sol.report.mean_inner_top - o["mean_inner_top"]) < 0.2
+
+
+def test_random_rhs_k3(gpu, port):
+    """Config-3 data (k'=3, U[-1,1] RHS, seed 1234) at a CI-sized mesh."""
+    host, solver = gpu
+    s = host.assemble("random", 3, 16, seed=1234)
+    sol = solver.solve_stokes(s, "IC0-PCG(A,Q)", solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+    check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+
+
+def test_3d_small(gpu, port):
+    """Config-4 data (3D psi-MMS, k'=2) at 4^3: no reference 3D code exists, the
+    oracle is the reference's solver layer restated."""
+    host, solver = gpu
+    s = host.assemble("psi-mms", 2, 4, dim=3)
+    sol = solver.solve_stokes(s, "IC0-PCG(A,Q)", solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+    check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+
+
+def test_cavity_ic0_windows(gpu):
+    """test_system.cpp:178-197: cavity k'=2 h=1/32, default options."""
+    host, solver = gpu
+    s = host.assemble("cavity", 2, 32)
+    for tol, lo, hi in ((1e-3, 4.0, 9.0), (1e-6, 9.0, 17.0)):
+        sol = solver.solve_stokes(s, "IC0-PCG(A,Q)", solver.SolverOptions(inner_tol=tol))
+        r = sol.report
+        assert r.converged and 34 <= r.iterations <= 44
+        assert r.mean_inner_bottom <= 2.0 and lo <= r.mean_inner_top <= hi
+
+
+def test_nu_rescaling_identical(gpu):
+    """test_system.cpp:199-215 (with the GPU strategy): nu = 1 vs 4."""
+    host, solver = gpu
+    a = host.assemble("cavity", 2, 8, nu=1.0)
+    b = host.assemble("cavity", 2, 8, nu=4.0)
+    ra = solver.solve_stokes(a, "IC0-PCG(A,Q)", solver.SolverOptions()).report
+    rb = solver.solve_stokes(b, "IC0-PCG(A,Q)", solver.SolverOptions()).report
+    assert ra.iterations == rb.iterations
+    np.testing.assert_allclose(ra.residual_history, rb.residual_history, rtol=1e-13)
+
+
+def test_bit_deterministic(gpu):
+    host, solver = gpu
+    s = host.assemble("cavity", 2, 8)
+    g = solver.GpuStokesSolver(s, "PCG(A,Q)")
+    a = g.solve()
+    b = g.solve()
+    assert a.report.iterations == b.report.iterations
+    assert np.array_equal(a.u, b.u) and np.array_equal(a.p, b.p)
+    assert np.array_equal(a.report.euclid_history, b.report.euclid_history)
+
+
+def test_max_iter_and_errors(gpu):
+    host, solver = gpu
+    s = host.assemble("psi-mms", 2, 8)
+    sol = solver.solve_stokes(s, "IC0-PCG(A,Q)", solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1, max_iter=3))
+    assert not sol.report.converged and sol.report.iterations == 3
+    from paper_1309_5048_b200.host import CsrMatrix, StokesSystem
+    negQ = CsrMatrix(s.Q_nu.n_rows, s.Q_nu.n_cols, s.Q_nu.row_ptr, s.Q_nu.cols, -s.Q_nu.vals)
+    bad = StokesSystem(s.A, s.B, s.Bt, s.Q, negQ, s.f)
+    with pytest.raises(ArithmeticError):
+        solver.solve_stokes(bad, "IC0-PCG(A)+Diag(Q)")
+    # indefinite A: PCG(A) hits negative curvature
+    negA = CsrMatrix(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.cols, s.A.vals.copy())
+    diag = negA.cols == np.repeat(np.arange(negA.n_rows), np.diff(negA.row_ptr))
+    negA.vals[~diag] *= 40.0
+    bad = StokesSystem(negA, s.B, s.Bt, s.Q, s.Q_nu, s.f)
+    with pytest.raises(solver.PreconditionerError):
+        solver.solve_stokes(bad, "PCG(A)+Diag(Q)", solver.SolverOptions(inner_tol=1e-6))
