@@ -36,6 +36,36 @@ struct HostSweep {
   std::vector<double> diag;    // n
 };
 
+// Staged ("flow") sweep plan: the production triangular-solve layout.
+// One CTA runs a sweep with two roles:
+//   * one MAIN warp walks the groups strictly in order; for group g it only
+//     has to add the group's "B" entries (dependencies on group g-1, fetched
+//     from the previous group's registers with warp shuffles) and its "A"
+//     entries (dependencies on groups g-D+1 .. g-2, gathered from shared
+//     memory one iteration ahead), then scale by the reciprocal diagonal with
+//     one Markstein correction (= the correctly rounded quotient);
+//   * HELPER warps run ahead: for group g they wait until groups <= need[g]
+//     are done, sum the row's "prefix" entries (all older dependencies) into
+//     psum = rhs - sum, and stage psum, diag, 1/diag, the A and B entries into
+//     a shared-memory ring slot for the main warp.
+// Within a row the entries are summed in dependency-level order with tree
+// reductions (reassociated w.r.t. the reference's column order: results
+// agree to round-off); the factor and the operation are the
+// same. kTA / kTB are the per-lane register budgets for A and B entries.
+constexpr int kTA = 8, kTB = 4, kRing = 16, kFlowD = 7;
+struct HostFlow {
+  int n = 0, G = 0, n_levels = 0;
+  std::vector<int32_t> nr, need, pw, grows;  // per group (grows: G*32)
+  std::vector<int64_t> pptr;                 // G + 1, prefix entries (lane-interleaved, stride nr)
+  std::vector<int32_t> pcols;                // pad = n (a zero slot)
+  std::vector<double> pvals;
+  std::vector<int32_t> acol;                 // G*kTA*32, pad = n
+  std::vector<double> aval;
+  std::vector<int32_t> bsrc;                 // G*kTB*32: lane in group g-1 (pad 0 with value 0)
+  std::vector<double> bval;
+  std::vector<double> diag, dinv;            // n
+};
+
 struct HostBlock {
   int kind = DSGPU_BLOCK_JACOBI;
   int n = 0, off = 0;
@@ -45,7 +75,8 @@ struct HostBlock {
   std::vector<int32_t> ci;
   std::vector<double> v;
   std::vector<double> dinv;      // Jacobi / Jacobi-PCG
-  HostSweep fwd, bwd;            // IC0-PCG
+  HostSweep fwd, bwd;            // IC0-PCG, exact column-order sweeps (bit-identical mode)
+  HostFlow ffwd, fbwd;           // IC0-PCG, staged sweeps (production)
 };
 
 struct HostPlan {
@@ -69,5 +100,7 @@ void build_plan(HostPlan& plan, const dsgpu_csr* A, const dsgpu_csr* B, const ds
                 const dsgpu_csr* Q_filter);
 
 void build_sweeps(const dsgpu_csr& L, HostSweep& fwd, HostSweep& bwd);
+// Throws std::invalid_argument if a group needs more than kTB B entries.
+void build_flow(const HostSweep& s, HostFlow& f);
 
 }  // namespace dsgpu

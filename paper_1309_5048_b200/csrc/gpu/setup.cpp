@@ -263,7 +263,11 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
         }
       }
     }
-    if (hb.kind == DSGPU_BLOCK_PCG_IC0) build_sweeps(*facs[b], hb.fwd, hb.bwd);
+    if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
+      build_sweeps(*facs[b], hb.fwd, hb.bwd);
+      build_flow(hb.fwd, hb.ffwd);
+      build_flow(hb.bwd, hb.fbwd);
+    }
   }
 
   P.filter = false;
@@ -292,6 +296,99 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
       for (int r = 0; r < n_p; ++r) P.qk[r] = qk[P.blk[1].perm[r]];
       P.filter_den = den;
     }
+  }
+}
+
+}  // namespace dsgpu
+
+namespace dsgpu {
+
+// Staged sweep plan from the level-grouped SELL sweep (same groups, same
+// dependency levels; see HostFlow in dsgpu_internal.hpp).
+void build_flow(const HostSweep& s, HostFlow& f) {
+  const int n = s.n;
+  f = HostFlow{};
+  f.n = n;
+  f.G = s.n_groups;
+  f.n_levels = s.n_levels;
+  f.diag = s.diag;
+  f.dinv.resize(n);
+  for (int i = 0; i < n; ++i) f.dinv[i] = 1.0 / s.diag[i];
+  std::vector<int> gof(n, -1), lof(n, -1);
+  for (int g = 0; g < s.n_groups; ++g)
+    for (int l = 0; l < kLanes; ++l) {
+      const int r = s.grows[static_cast<size_t>(g) * kLanes + l];
+      if (r >= 0) {
+        gof[r] = g;
+        lof[r] = l;
+      }
+    }
+  f.pptr.assign(1, 0);
+  f.acol.assign(static_cast<size_t>(f.G) * kTA * kLanes, n);
+  f.aval.assign(f.acol.size(), 0.0);
+  f.bsrc.assign(static_cast<size_t>(f.G) * kTB * kLanes, 0);
+  f.bval.assign(f.bsrc.size(), 0.0);
+  std::vector<std::pair<int, double>> P[kLanes], A[kLanes], B[kLanes];
+  for (int g = 0; g < s.n_groups; ++g) {
+    int nr = 0;
+    for (int l = 0; l < kLanes; ++l)
+      if (s.grows[static_cast<size_t>(g) * kLanes + l] >= 0) nr = l + 1;
+    int pw = 0, need = -1;
+    for (int l = 0; l < nr; ++l) {
+      P[l].clear();
+      A[l].clear();
+      B[l].clear();
+      std::vector<std::pair<int, double>> e;
+      for (int k = 0; k < s.gwidth[g]; ++k) {
+        const int64_t at = s.gptr[g] + static_cast<int64_t>(k) * kLanes + l;
+        if (s.cols[at] >= 0) e.emplace_back(s.cols[at], s.vals[at]);
+      }
+      // dependency-level order (oldest first), stable
+      std::stable_sort(e.begin(), e.end(),
+                       [&](const auto& a, const auto& b) { return gof[a.first] < gof[b.first]; });
+      for (const auto& x : e) {
+        const int dg = gof[x.first];
+        if (dg == g - 1)
+          B[l].push_back(x);
+        else if (dg > g - kFlowD)
+          A[l].push_back(x);
+        else
+          P[l].push_back(x);
+      }
+      while (static_cast<int>(A[l].size()) > kTA) {  // oldest A entries go to the helpers
+        P[l].push_back(A[l].front());
+        A[l].erase(A[l].begin());
+      }
+      if (static_cast<int>(B[l].size()) > kTB)
+        throw std::invalid_argument("flow sweep: a row depends on more than " +
+                                    std::to_string(kTB) + " rows of the previous group");
+      for (const auto& x : P[l]) need = std::max(need, gof[x.first]);
+      pw = std::max(pw, static_cast<int>(P[l].size()));
+    }
+    f.nr.push_back(nr);
+    f.need.push_back(need);
+    f.pw.push_back(pw);
+    for (int l = 0; l < kLanes; ++l) f.grows.push_back(s.grows[static_cast<size_t>(g) * kLanes + l]);
+    const int64_t pb = f.pptr.back();
+    f.pcols.resize(pb + static_cast<int64_t>(pw) * nr, n);
+    f.pvals.resize(pb + static_cast<int64_t>(pw) * nr, 0.0);
+    for (int l = 0; l < nr; ++l) {
+      for (size_t k = 0; k < P[l].size(); ++k) {
+        f.pcols[pb + static_cast<int64_t>(k) * nr + l] = P[l][k].first;
+        f.pvals[pb + static_cast<int64_t>(k) * nr + l] = P[l][k].second;
+      }
+      for (size_t k = 0; k < A[l].size(); ++k) {
+        const size_t at = (static_cast<size_t>(g) * kTA + k) * kLanes + l;
+        f.acol[at] = A[l][k].first;
+        f.aval[at] = A[l][k].second;
+      }
+      for (size_t k = 0; k < B[l].size(); ++k) {
+        const size_t at = (static_cast<size_t>(g) * kTB + k) * kLanes + l;
+        f.bsrc[at] = lof[B[l][k].first];
+        f.bval[at] = B[l][k].second;
+      }
+    }
+    f.pptr.push_back(pb + static_cast<int64_t>(pw) * nr);
   }
 }
 

@@ -38,7 +38,7 @@ using namespace dsgpu::dev;
 
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 
 enum Slot { SL_BB = 0, SL_RES, SL_ALPHA, SL_RHO0, SL_RHO1, SL_KAP0, SL_KAP1, SL_ZR0, SL_ZR1, SL_NUM, NSLOT };
@@ -53,6 +53,13 @@ struct DSweep {
   const double* diag;
 };
 
+struct DFlow {
+  int G;
+  const int32_t *nr, *need, *pw, *grows, *pcols, *acol, *bsrc;
+  const int64_t* pptr;
+  const double *pvals, *aval, *bval, *diag, *dinv;
+};
+
 struct DBlock {
   int kind, n, off, ic_cta;
   const int64_t* rp;  // operator rows (block ordering)
@@ -60,8 +67,11 @@ struct DBlock {
   const double* v;
   const int32_t* na;  // top block: A-part length of each K row (nullptr: full row)
   const double* dinv;
-  DSweep fwd, bwd;
+  DSweep fwd, bwd;    // exact column-order sweeps (bit-identical mode)
+  DFlow ffwd, fbwd;   // staged sweeps (production)
+  int exact;          // 1: use the exact sweeps
   double *r, *z, *q, *p0, *p1;  // PCG work (block-local, length n)
+  double* y;                    // forward-sweep result (staged mode)
 };
 
 struct DevReport {
@@ -141,22 +151,303 @@ __device__ void sweep(const DSweep& s, double* xs, int n, Rhs rhs, Out out, unsi
   __syncthreads();
 }
 
+
+// ---------------------------------------------------------------------------
+// Staged dataflow sweep (production): see HostFlow in dsgpu_internal.hpp.
+// Shared memory: xs[n+1] (results; xs[n] = 0 is the padding slot) followed by
+// a ring of kRing slots. Executed by every thread of one CTA; on return
+// (after a CTA barrier) xs holds the solution.
+template <int N>
+__device__ __forceinline__ double tree_sum(double* p) {
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int k = 0; k + w < N; k += 2 * w) p[k] = add_rn(p[k], p[k + w]);
+  return p[0];
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  unsigned lo, hi, rlo, rhi;
+  asm volatile("mov.b64 {%0,%1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(rlo) : "r"(lo), "r"(src));
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(rhi) : "r"(hi), "r"(src));
+  double out;
+  asm volatile("mov.b64 %0, {%1,%2};" : "=d"(out) : "r"(rlo), "r"(rhi));
+  return out;
+}
+
+struct FlowSmem {
+  double* xs;
+  double *psum, *dg, *di, *av, *bv;
+  int *ac, *bsr, *rows;
+  volatile int* ready;
+  int* snr;
+  volatile int* progress;
+  __device__ FlowSmem(double* base, int n) {
+    xs = base;
+    psum = xs + n + 1;
+    dg = psum + kRing * 32;
+    di = dg + kRing * 32;
+    av = di + kRing * 32;
+    bv = av + kRing * kTA * 32;
+    ac = reinterpret_cast<int*>(bv + kRing * kTB * 32);
+    bsr = ac + kRing * kTA * 32;
+    rows = bsr + kRing * kTB * 32;
+    ready = rows + kRing * 32;
+    snr = const_cast<int*>(ready) + kRing;
+    progress = ready + 2 * kRing;
+  }
+  static constexpr size_t ring_bytes() {
+    return static_cast<size_t>(kRing) * 32 * (3 * 8 + kTA * 12 + kTB * 12 + 4) + 3 * kRing * 4 + 64;
+  }
+};
+
+template <class Rhs>
+__device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigned* abort_flag) {
+  FlowSmem S(smem, n);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < kRing; i += blockDim.x) S.ready[i] = -1;
+  if (threadIdx.x == 0) {
+    *S.progress = 0;
+    S.xs[n] = 0.0;
+  }
+  __syncthreads();
+  // main = last warp; helpers = warps not sharing the main warp's SM sub-partition
+  const int mainw = nw - 1;
+  int hid = -1, nh = 0;
+  for (int w = 0; w < nw; ++w)
+    if (w != mainw && (w & 3) != (mainw & 3)) {
+      if (w == warp) hid = nh;
+      ++nh;
+    }
+  if (warp == mainw && s.G > 0) {
+    double xprev = 0.0;
+    double acc_pre, d, dv;
+    int row, nr;
+    double bvl[kTB];
+    int bsl[kTB];
+    long long t0 = clock64();
+    {  // group 0
+      while (S.ready[0] != 0) {
+        if (clock64() - t0 > kSpinTimeoutCycles) { atomicExch(abort_flag, 1u); break; }
+      }
+      nr = S.snr[0];
+      d = S.dg[lane];
+      dv = S.di[lane];
+      row = S.rows[lane];
+      double pa[kTA];
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(S.av[k * 32 + lane], S.xs[S.ac[k * 32 + lane]]);
+      acc_pre = sub_rn(S.psum[lane], tree_sum<kTA>(pa));
+#pragma unroll
+      for (int k = 0; k < kTB; ++k) {
+        bsl[k] = S.bsr[k * 32 + lane];
+        bvl[k] = S.bv[k * 32 + lane];
+      }
+    }
+    for (int g = 0; g < s.G; ++g) {
+      // (1) B(g) shuffles from the previous group's results
+      double sx[kTB];
+#pragma unroll
+      for (int k = 0; k < kTB; ++k) sx[k] = shfl_d(xprev, bsl[k]);
+      asm volatile("" ::: "memory");
+      // (2) next group's slot (its A entries depend on groups <= g-1: ready)
+      const int g1 = g + 1 < s.G ? g + 1 : g;
+      const int sl = g1 % kRing;
+      if (S.ready[sl] != g1) {
+        t0 = clock64();
+        while (S.ready[sl] != g1) {
+          if (clock64() - t0 > kSpinTimeoutCycles) { atomicExch(abort_flag, 1u); break; }
+        }
+      }
+      const int nr1 = S.snr[sl];
+      const double ps1 = S.psum[sl * 32 + lane];
+      const double d1 = S.dg[sl * 32 + lane], dv1 = S.di[sl * 32 + lane];
+      const int row1 = S.rows[sl * 32 + lane];
+      double avl[kTA], axv[kTA], bvl1[kTB];
+      int bsl1[kTB];
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) {
+        avl[k] = S.av[(sl * kTA + k) * 32 + lane];
+        axv[k] = S.xs[S.ac[(sl * kTA + k) * 32 + lane]];
+      }
+#pragma unroll
+      for (int k = 0; k < kTB; ++k) {
+        bsl1[k] = S.bsr[(sl * kTB + k) * 32 + lane];
+        bvl1[k] = S.bv[(sl * kTB + k) * 32 + lane];
+      }
+      // (3) B(g): the critical chain
+      double pb[kTB];
+#pragma unroll
+      for (int k = 0; k < kTB; ++k) pb[k] = mul_rn(bvl[k], sx[k]);
+      const double acc = sub_rn(acc_pre, tree_sum<kTB>(pb));
+      // correctly rounded acc / d from the reciprocal (one Markstein step)
+      const double q0 = mul_rn(acc, dv);
+      const double rr = fma(-q0, d, acc);
+      const double x = fma(rr, dv, q0);
+      xprev = x;
+      if (lane < nr) S.xs[row] = x;
+      __syncwarp();
+      if (lane == 0) *S.progress = g + 1;
+      // (4) A(g+1)
+      double pa[kTA];
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(avl[k], axv[k]);
+      acc_pre = sub_rn(ps1, tree_sum<kTA>(pa));
+      d = d1;
+      dv = dv1;
+      row = row1;
+      nr = nr1;
+#pragma unroll
+      for (int k = 0; k < kTB; ++k) {
+        bsl[k] = bsl1[k];
+        bvl[k] = bvl1[k];
+      }
+    }
+  } else if (hid >= 0) {
+    constexpr int PW = 16;
+    int g = hid;
+    int nr = 0, pw = 0, need = 0;
+    int64_t pb0 = 0;
+    if (g < s.G) {
+      nr = __ldg(s.nr + g);
+      pw = __ldg(s.pw + g);
+      need = __ldg(s.need + g);
+      pb0 = __ldg(s.pptr + g);
+    }
+    for (; g < s.G; g += nh) {
+      const int sl = g % kRing;
+      const int gn = g + nh;
+      int nrn = 0, pwn = 0, needn = 0;
+      int64_t pbn = 0;
+      if (gn < s.G) {
+        nrn = __ldg(s.nr + gn);
+        pwn = __ldg(s.pw + gn);
+        needn = __ldg(s.need + gn);
+        pbn = __ldg(s.pptr + gn);
+      }
+      int row = -1;
+      double dd = 1.0, ddi = 1.0;
+      if (lane < nr) {
+        row = __ldg(s.grows + static_cast<int64_t>(g) * 32 + lane);
+        dd = __ldg(s.diag + row);
+        ddi = __ldg(s.dinv + row);
+      }
+      int acl[kTA];
+      double avl[kTA], bvl[kTB];
+      int bsl[kTB];
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) {
+        acl[k] = __ldg(s.acol + (static_cast<int64_t>(g) * kTA + k) * 32 + lane);
+        avl[k] = __ldg(s.aval + (static_cast<int64_t>(g) * kTA + k) * 32 + lane);
+      }
+#pragma unroll
+      for (int k = 0; k < kTB; ++k) {
+        bvl[k] = __ldg(s.bval + (static_cast<int64_t>(g) * kTB + k) * 32 + lane);
+        bsl[k] = __ldg(s.bsrc + (static_cast<int64_t>(g) * kTB + k) * 32 + lane);
+      }
+      const int32_t* cp = s.pcols + pb0 + lane;
+      const double* vp = s.pvals + pb0 + lane;
+      double part = 0.0;
+      long long t0 = clock64();
+      for (int k0 = 0; k0 < pw; k0 += PW) {
+        int pc[PW];
+        double pv[PW];
+#pragma unroll
+        for (int q = 0; q < PW; ++q) {
+          const bool ok = lane < nr && k0 + q < pw;
+          pc[q] = ok ? __ldg(cp + static_cast<int64_t>(k0 + q) * nr) : n;
+          pv[q] = ok ? __ldg(vp + static_cast<int64_t>(k0 + q) * nr) : 0.0;
+        }
+        if (k0 == 0)
+          while (*S.progress <= need) {
+            __nanosleep(20);
+            if (clock64() - t0 > kSpinTimeoutCycles || *reinterpret_cast<volatile unsigned*>(abort_flag)) {
+              atomicExch(abort_flag, 1u);
+              break;
+            }
+          }
+        double pp[PW];
+#pragma unroll
+        for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], S.xs[pc[q]]);
+        part = add_rn(part, tree_sum<PW>(pp));
+      }
+      if (pw == 0)
+        while (*S.progress <= need) {
+          __nanosleep(20);
+          if (clock64() - t0 > kSpinTimeoutCycles || *reinterpret_cast<volatile unsigned*>(abort_flag)) {
+            atomicExch(abort_flag, 1u);
+            break;
+          }
+        }
+      const double acc = lane < nr ? sub_rn(rhs(row), part) : 0.0;
+      // slot reuse: the main warp must be past group g - kRing + 1
+      while (*S.progress < g - kRing + 2) {
+        __nanosleep(20);
+        if (clock64() - t0 > kSpinTimeoutCycles || *reinterpret_cast<volatile unsigned*>(abort_flag)) {
+          atomicExch(abort_flag, 1u);
+          break;
+        }
+      }
+      S.psum[sl * 32 + lane] = acc;
+      S.dg[sl * 32 + lane] = dd;
+      S.di[sl * 32 + lane] = ddi;
+      S.rows[sl * 32 + lane] = row;
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) {
+        S.ac[(sl * kTA + k) * 32 + lane] = acl[k];
+        S.av[(sl * kTA + k) * 32 + lane] = avl[k];
+      }
+#pragma unroll
+      for (int k = 0; k < kTB; ++k) {
+        S.bv[(sl * kTB + k) * 32 + lane] = bvl[k];
+        S.bsr[(sl * kTB + k) * 32 + lane] = bsl[k];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        S.snr[sl] = nr;
+        __threadfence_block();
+        S.ready[sl] = g;
+      }
+      nr = nrn;
+      pw = pwn;
+      need = needn;
+      pb0 = pbn;
+    }
+  }
+  __syncthreads();
+}
+
 // IC(0) apply z = (L L^T)^{-1} r (Ic0Factor::solve) in one CTA; returns the
 // CTA sum of r_i z_i in warp 0. rhs(row) yields r_row (and may write it).
 template <class Rhs>
 __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, double* red,
                            unsigned* abort_flag) {
-  sweep(B.fwd, xf, B.n, rhs, [](int, double) {}, abort_flag);
-  double rz = 0.0;
   double* z = B.z;
   const double* r = B.r;
-  sweep(
-      B.bwd, xb, B.n, [&](int row) { return xf[row]; },
-      [&](int row, double zi) {
-        z[row] = zi;
-        rz += r[row] * zi;
-      },
-      abort_flag);
+  double rz = 0.0;
+  if (B.exact) {
+    sweep(B.fwd, xf, B.n, rhs, [](int, double) {}, abort_flag);
+    sweep(
+        B.bwd, xb, B.n, [&](int row) { return xf[row]; },
+        [&](int row, double zi) {
+          z[row] = zi;
+          rz += r[row] * zi;
+        },
+        abort_flag);
+    return block_sum(rz, red);
+  }
+  // staged sweeps: xf is the shared-memory base of the flow workspace
+  flow_sweep(B.ffwd, B.n, xf, rhs, abort_flag);
+  double* y = B.y;
+  for (int i = threadIdx.x; i < B.n; i += blockDim.x) y[i] = xf[i];
+  __syncthreads();
+  flow_sweep(B.fbwd, B.n, xf, [&](int row) { return y[row]; }, abort_flag);
+  for (int i = threadIdx.x; i < B.n; i += blockDim.x) {
+    const double zi = xf[i];
+    z[i] = zi;
+    rz += r[i] * zi;
+  }
   return block_sum(rz, red);
 }
 
@@ -649,16 +940,11 @@ finish:
 
 // ---- standalone kernels (parity / microbenchmarks) -------------------------
 __global__ void __launch_bounds__(kThreads, 1)
-    ic_apply_kernel(const __grid_constant__ DBlock B, const double* r, double* z, unsigned* abort_flag) {
+    ic_apply_kernel(const __grid_constant__ DBlock B, const double* r, unsigned* abort_flag) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
-  double* xf = xs_dyn;
-  double* xb = xs_dyn + B.n;
-  sweep(B.fwd, xf, B.n, [&](int row) { return r[row]; }, [](int, double) {}, abort_flag);
-  sweep(
-      B.bwd, xb, B.n, [&](int row) { return xf[row]; }, [&](int row, double zi) { z[row] = zi; },
-      abort_flag);
-  (void)red;
+  // B.r = r (input), B.z = output, B.y = forward-sweep scratch (set by the host)
+  ic_apply(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag);
 }
 
 // y = M x, warp per row; na != nullptr limits each row to its first na[i] entries
@@ -709,6 +995,7 @@ struct dsgpu_handle {
   double* d_tmp[3] = {nullptr, nullptr, nullptr};
   DevReport* d_rep = nullptr;
   int64_t nnz_k = 0, nnz_a = 0, nnz_l[2] = {0, 0}, nnz_q = 0;
+  bool exact = false;
 
   template <class T>
   T* alloc(size_t count) {
@@ -746,6 +1033,25 @@ int fail(dsgpu_handle* h, int code, const std::string& msg) {
 int cuda_check(dsgpu_handle* h, cudaError_t e, const char* what) {
   if (e == cudaSuccess) return DSGPU_OK;
   return fail(h, DSGPU_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
+  DFlow d{};
+  d.G = f.G;
+  d.nr = h->upload(f.nr);
+  d.need = h->upload(f.need);
+  d.pw = h->upload(f.pw);
+  d.grows = h->upload(f.grows);
+  d.pcols = h->upload(f.pcols);
+  d.acol = h->upload(f.acol);
+  d.bsrc = h->upload(f.bsrc);
+  d.pptr = h->upload(f.pptr);
+  d.pvals = h->upload(f.pvals);
+  d.aval = h->upload(f.aval);
+  d.bval = h->upload(f.bval);
+  d.diag = h->upload(f.diag);
+  d.dinv = h->upload(f.dinv);
+  return d;
 }
 
 DSweep upload_sweep(dsgpu_handle* h, const HostSweep& s) {
@@ -822,7 +1128,9 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     int nmax = 0;
     for (int b = 0; b < 2; ++b)
       if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0) nmax = std::max(nmax, P.blk[b].n);
-    h->smem = static_cast<size_t>(2) * nmax * sizeof(double);
+    h->exact = std::getenv("DSGPU_EXACT") && std::atoi(std::getenv("DSGPU_EXACT")) != 0;
+    h->smem = h->exact ? static_cast<size_t>(2) * nmax * sizeof(double)
+                       : static_cast<size_t>(nmax + 1) * sizeof(double) + FlowSmem::ring_bytes();
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const size_t static_smem = 1024;
@@ -894,9 +1202,16 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         d.na = nullptr;
       }
       if (!hb.dinv.empty()) d.dinv = h->upload(hb.dinv);
+      d.exact = h->exact ? 1 : 0;
       if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
-        d.fwd = upload_sweep(h, hb.fwd);
-        d.bwd = upload_sweep(h, hb.bwd);
+        if (h->exact) {
+          d.fwd = upload_sweep(h, hb.fwd);
+          d.bwd = upload_sweep(h, hb.bwd);
+        } else {
+          d.ffwd = upload_flow(h, hb.ffwd);
+          d.fbwd = upload_flow(h, hb.fbwd);
+        }
+        d.y = h->alloc<double>(hb.n);
       }
       d.r = h->alloc<double>(hb.n);
       d.z = h->alloc<double>(hb.n);
@@ -1102,8 +1417,10 @@ int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z) {
   double *d0 = h->d_tmp[0], *d1 = h->d_tmp[1];
   cudaMemcpyAsync(d0, r, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream);
   cudaMemsetAsync(h->args.bar, 0, 128 * sizeof(unsigned), h->stream);
-  ic_apply_kernel<<<1, kThreads, 2 * n * sizeof(double), h->stream>>>(h->args.blk[block], d0, d1,
-                                                                      h->args.bar + 64);
+  DBlock B = h->args.blk[block];
+  B.r = d0;
+  B.z = d1;
+  ic_apply_kernel<<<1, kThreads, h->smem, h->stream>>>(B, d0, h->args.bar + 64);
   cudaMemcpyAsync(z, d1, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream);
   return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_ic0");
 }
@@ -1133,8 +1450,10 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
     if (which == 0) {
       spmv_kernel<<<(P.n * 32 + 255) / 256, 256, 0, h->stream>>>(P.n, a.k_rp, a.k_ci, a.k_v, nullptr, d0, d1);
     } else if (which == 1 || which == 2) {
-      const DBlock& B = a.blk[which - 1];
-      ic_apply_kernel<<<1, kThreads, 2 * B.n * sizeof(double), h->stream>>>(B, d0, d1, a.bar + 64);
+      DBlock B = a.blk[which - 1];
+      B.r = d0;
+      B.z = d1;
+      ic_apply_kernel<<<1, kThreads, h->smem, h->stream>>>(B, d0, a.bar + 64);
     } else {
       const DBlock& B = a.blk[0];
       spmv_kernel<<<(B.n * 32 + 255) / 256, 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1);

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <cmath>
 #include <algorithm>
+#include <type_traits>
 #include "dshost.h"
 #include "../paper_1309_5048_b200/csrc/gpu/dsgpu_internal.hpp"
 #include "../paper_1309_5048_b200/csrc/gpu/kernels.cuh"
@@ -679,6 +680,776 @@ __global__ void __launch_bounds__(256,1) sweep9(S8 s, int n, const double* __res
   if (threadIdx.x == 0) { t[0] = clock64() - c0; t[1] = gtimer() - g0; }
 }
 
+
+// ---- v10: software-pipelined serial main warp (A(g+1) || B(g)), shuffles for
+// deps on the previous group, helpers stage slots and far prefix sums ---------
+constexpr int R10 = 16;
+struct H10 { int G, TAm, TBm; std::vector<int32_t> nr, need, amax, bmax, grows, pw; std::vector<int64_t> pptr; std::vector<int32_t> pcols; std::vector<double> pvals;
+             std::vector<int32_t> acol, bcol; std::vector<int8_t> bsrc; std::vector<double> aval, bval; };
+template <int TA, int TB>
+H10 build10(const HostSweep& s, int D, bool level_order) {
+  int n = s.n; std::vector<int> lev(n, 0), gof(n), lof(n);
+  std::vector<std::vector<std::pair<int,double>>> rows(n);
+  for (int g = 0; g < s.n_groups; ++g) for (int l = 0; l < 32; ++l) { int r = s.grows[g*32+l]; if (r < 0) continue; gof[r] = g; lof[r] = l;
+      for (int k = 0; k < s.gwidth[g]; ++k) { int64_t e = s.gptr[g] + (int64_t)k*32 + l; if (s.cols[e] >= 0) rows[r].push_back({s.cols[e], s.vals[e]}); } }
+  if (level_order) for (int r = 0; r < n; ++r) std::stable_sort(rows[r].begin(), rows[r].end(), [&](auto& a, auto& b) { return gof[a.first] < gof[b.first]; });
+  H10 h; h.G = s.n_groups; h.TAm = 0; h.TBm = 0; h.pptr.push_back(0);
+  for (int g = 0; g < s.n_groups; ++g) {
+    int nr = 0; for (int l = 0; l < 32; ++l) if (s.grows[g*32+l] >= 0) nr = l + 1;
+    int pw = 0, need = -1, am = 0, bm = 0;
+    std::vector<int> ps(nr), as(nr), bs(nr);
+    for (int l = 0; l < nr; ++l) { int r = s.grows[g*32+l]; auto& e = rows[r]; int len = e.size();
+      int cb = len; for (int k = 0; k < len; ++k) if (gof[e[k].first] == g - 1) { cb = k; break; }   // crit-tail start
+      if (len - cb > TB) { printf("row %d crit tail %d > TB\n", r, len - cb); exit(1); }
+      int ca = cb; for (int k = 0; k < cb; ++k) if (gof[e[k].first] > g - D) { ca = k; break; }     // pre-tail start
+      if (cb - ca > TA) ca = cb - TA;
+      ps[l] = ca; as[l] = cb - ca; bs[l] = len - cb;
+      pw = std::max(pw, ca); am = std::max(am, cb - ca); bm = std::max(bm, len - cb);
+      for (int k = 0; k < ca; ++k) need = std::max(need, gof[e[k].first]); }
+    h.nr.push_back(nr); h.need.push_back(need); h.pw.push_back(pw); h.amax.push_back(am); h.bmax.push_back(bm);
+    h.TAm = std::max(h.TAm, am); h.TBm = std::max(h.TBm, bm);
+    for (int l = 0; l < 32; ++l) h.grows.push_back(s.grows[g*32+l]);
+    int64_t pb = h.pptr.back(); h.pcols.resize(pb + (int64_t)pw*nr, -1); h.pvals.resize(pb + (int64_t)pw*nr, 0.0);
+    size_t a0 = h.acol.size(); h.acol.resize(a0 + TA*32, n); h.aval.resize(a0 + TA*32, 0.0);   // pad: col n (xs[n] = 0), val 0
+    size_t b0 = h.bcol.size(); h.bcol.resize(b0 + TB*32, n); h.bval.resize(b0 + TB*32, 0.0); h.bsrc.resize(b0 + TB*32, -1);
+    for (int l = 0; l < nr; ++l) { int r = s.grows[g*32+l]; auto& e = rows[r];
+      for (int k = 0; k < ps[l]; ++k) { h.pcols[pb + (int64_t)k*nr + l] = e[k].first; h.pvals[pb + (int64_t)k*nr + l] = e[k].second; }
+      for (int k = 0; k < as[l]; ++k) { auto& x = e[ps[l] + k]; h.acol[a0 + k*32 + l] = x.first; h.aval[a0 + k*32 + l] = x.second; }
+      for (int k = 0; k < bs[l]; ++k) { auto& x = e[ps[l] + as[l] + k]; h.bval[b0 + k*32 + l] = x.second;
+        if (gof[x.first] == g - 1) { h.bsrc[b0 + k*32 + l] = (int8_t)lof[x.first]; h.bcol[b0 + k*32 + l] = n; } else h.bcol[b0 + k*32 + l] = x.first; } }
+    h.pptr.push_back(pb + (int64_t)pw*nr);
+  }
+  return h;
+}
+struct S10d { int G; const int32_t *nr, *need, *amax, *bmax, *grows, *pw, *pcols, *acol, *bcol; const int8_t* bsrc; const int64_t* pptr; const double *pvals, *aval, *bval, *diag; };
+template <int TA, int TB, bool MARK, int EXCL = 0>
+__global__ void __launch_bounds__(512,1) sweep10(S10d s, int n, const double* __restrict__ r, double* out, unsigned long long* t, int nsweeps, long long* tsg) {
+  extern __shared__ double sm[];
+  double* xs = sm;                                    // n + 1 (xs[n] = 0 pad)
+  double* psum = xs + n + 1;                          // R*32
+  double* dg = psum + R10*32;                         // R*32 (diag)
+  double* av = dg + R10*32;                           // R*TA*32
+  double* bv = av + R10*TA*32;                        // R*TB*32
+  int* ac = reinterpret_cast<int*>(bv + R10*TB*32);   // R*TA*32
+  int* bc = ac + R10*TA*32;                           // R*TB*32
+  int* rows = bc + R10*TB*32;                         // R*32
+  int8_t* bsr = reinterpret_cast<int8_t*>(rows + R10*32); // R*TB*32
+  volatile int* meta = reinterpret_cast<volatile int*>(bsr + R10*TB*32); // ready[R], nr[R], amax[R], bmax[R], progress
+  volatile int* ready = meta; int* snr = const_cast<int*>(meta) + R10; int* sam = snr + R10; int* sbm = sam + R10;
+  volatile int* progress = meta + 4*R10;
+  unsigned long long c0 = 0, g0 = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int sw = 0; sw < nsweeps; ++sw) {
+    for (int i = threadIdx.x; i < R10; i += blockDim.x) ready[i] = -1;
+    if (threadIdx.x == 0) { *progress = 0; xs[n] = 0.0; }
+    __syncthreads();
+    if (sw == nsweeps - 1) { c0 = clock64(); g0 = gtimer(); }
+    const int mainw = EXCL ? nw - 1 : 0;
+    int hid = -1, nh = 0;   // helper index among helper warps
+    for (int w = 0; w < nw; ++w) { const bool isH = (w != mainw) && !(EXCL == 2 && (w & 3) == (mainw & 3)); if (isH) { if (w == warp) hid = nh; ++nh; } }
+    if (warp == mainw) {
+      double xprev = 0.0;
+      // state for group g (prepared by A)
+      double acc_pre = 0.0, d = 1.0; int row = -1, nr = 0, bm = 0;
+      double bvl[TB], bx[TB]; int bsl[TB];
+      auto prep = [&](int g) {   // A(g): needs x of groups <= g-2 (already in xs)
+        const int sl = g % R10;
+        while (ready[sl] != g) {}
+        nr = snr[sl]; const int am = sam[sl]; bm = sbm[sl];
+        double acc = psum[sl*32 + lane];
+        d = dg[sl*32 + lane]; row = rows[sl*32 + lane];
+        int acl[TA]; double avl[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { acl[k] = ac[(sl*TA + k)*32 + lane]; avl[k] = av[(sl*TA + k)*32 + lane]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl[k] = bsr[(sl*TB + k)*32 + lane]; bvl[k] = bv[(sl*TB + k)*32 + lane]; bx[k] = xs[bc[(sl*TB + k)*32 + lane]]; }
+        double axv[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) axv[k] = xs[acl[k]];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) if (k < am) acc = sub_rn(acc, mul_rn(avl[k], axv[k]));
+        acc_pre = acc;
+      };
+      prep(0);
+      for (int g = 0; g < s.G; ++g) {
+        const long long w0 = clock64();
+        // B(g)
+        double acc = acc_pre;
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          if (k < bm) {
+            const double sx = __shfl_sync(0xffffffffu, xprev, bsl[k] < 0 ? 0 : bsl[k]);
+            const double X = bsl[k] >= 0 ? sx : bx[k];
+            acc = sub_rn(acc, mul_rn(bvl[k], X));
+          }
+        }
+        double x;
+        if (MARK) { const double q0 = mul_rn(acc, 1.0 / d); const double rr = fma(-q0, d, acc); x = fma(rr, 1.0 / d, q0); }
+        else x = div_rn(acc, d);
+        if (lane < nr) xs[row] = x;
+        xprev = x;
+        __syncwarp();
+        if (lane == 0) *progress = g + 1;
+        const long long w1 = clock64();
+        if (g + 1 < s.G) prep(g + 1);
+        const long long w2 = clock64();
+        if (tsg && lane == 0 && sw == nsweeps - 1) { tsg[g*2] = w1 - w0; tsg[g*2+1] = w2 - w1; }
+      }
+    } else if (hid >= 0) {
+      for (int g = hid; g < s.G; g += nh) {
+        const int sl = g % R10;
+        const int nr = __ldg(s.nr + g), pw = __ldg(s.pw + g), need = __ldg(s.need + g);
+        const int64_t pb = __ldg(s.pptr + g);
+        int row = -1; double acc = 0.0, dd = 1.0;
+        if (lane < nr) { row = __ldg(s.grows + g*32 + lane); acc = r[row]; dd = __ldg(s.diag + row); }
+        int acl[TA]; double avl[TA]; int bcl[TB]; double bvl[TB]; int8_t bsl[TB];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { acl[k] = __ldg(s.acol + (int64_t)(g*TA + k)*32 + lane); avl[k] = __ldg(s.aval + (int64_t)(g*TA + k)*32 + lane); }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bcl[k] = __ldg(s.bcol + (int64_t)(g*TB + k)*32 + lane); bvl[k] = __ldg(s.bval + (int64_t)(g*TB + k)*32 + lane); bsl[k] = s.bsrc[(int64_t)(g*TB + k)*32 + lane]; }
+        constexpr int CH = 8;
+        int pc[CH]; double pv[CH];
+        const int32_t* cp = s.pcols + pb + lane; const double* vp = s.pvals + pb + lane;
+        if (lane < nr) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) { pc[q] = q < pw ? __ldg(cp + (int64_t)q*nr) : -1; pv[q] = q < pw ? __ldg(vp + (int64_t)q*nr) : 0.0; }
+        }
+        while (*progress <= need) { __nanosleep(32); }
+        if (lane < nr) {
+          for (int k = 0; k < pw; k += CH) {
+            int nc[CH]; double nv[CH];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) { const int kk = k + CH + q; nc[q] = kk < pw ? __ldg(cp + (int64_t)kk*nr) : -1; nv[q] = kk < pw ? __ldg(vp + (int64_t)kk*nr) : 0.0; }
+            double xv[CH];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) xv[q] = xs[pc[q] < 0 ? n : pc[q]];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) if (pc[q] >= 0) acc = sub_rn(acc, mul_rn(pv[q], xv[q]));
+#pragma unroll
+            for (int q = 0; q < CH; ++q) { pc[q] = nc[q]; pv[q] = nv[q]; }
+          }
+        }
+        while (*progress < g - R10 + 2) { __nanosleep(32); }
+        psum[sl*32 + lane] = acc; dg[sl*32 + lane] = dd; rows[sl*32 + lane] = row;
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { ac[(sl*TA + k)*32 + lane] = acl[k]; av[(sl*TA + k)*32 + lane] = avl[k]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bc[(sl*TB + k)*32 + lane] = bcl[k]; bv[(sl*TB + k)*32 + lane] = bvl[k]; bsr[(sl*TB + k)*32 + lane] = bsl[k]; }
+        __syncwarp();
+        if (lane == 0) { snr[sl] = nr; sam[sl] = __ldg(s.amax + g); sbm[sl] = __ldg(s.bmax + g); __threadfence_block(); ready[sl] = g; }
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = xs[i];
+  }
+  if (threadIdx.x == 0) { t[0] = clock64() - c0; t[1] = gtimer() - g0; }
+}
+
+
+// ---- v11: branch-free software-pipelined main (loads(g+1) | B(g) | A(g+1)), dinv staged
+template <int TA, int TB, bool MARK>
+__global__ void __launch_bounds__(512,1) sweep11(S10d s, const double* __restrict__ dinv, int n, const double* __restrict__ r, double* out, unsigned long long* t, int nsweeps, long long* tsg) {
+  extern __shared__ double sm[];
+  double* xs = sm;                                    // n + 1
+  double* psum = xs + n + 1;                          // R*32
+  double* dg = psum + R10*32;                         // R*32
+  double* di = dg + R10*32;                           // R*32
+  double* av = di + R10*32;                           // R*TA*32
+  double* bv = av + R10*TA*32;                        // R*TB*32
+  int* ac = reinterpret_cast<int*>(bv + R10*TB*32);   // R*TA*32
+  int* bc = ac + R10*TA*32;                           // R*TB*32
+  int* rows = bc + R10*TB*32;                         // R*32
+  int* bsr = rows + R10*32;                           // R*TB*32 (int)
+  volatile int* meta = reinterpret_cast<volatile int*>(bsr + R10*TB*32);
+  volatile int* ready = meta; int* snr = const_cast<int*>(meta) + R10;
+  volatile int* progress = meta + 2*R10;
+  unsigned long long c0 = 0, g0 = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int mainw = nw - 1;
+  int hid = -1, nh = 0;
+  for (int w = 0; w < nw; ++w) { const bool isH = (w != mainw) && ((w & 3) != (mainw & 3)); if (isH) { if (w == warp) hid = nh; ++nh; } }
+  for (int sw = 0; sw < nsweeps; ++sw) {
+    for (int i = threadIdx.x; i < R10; i += blockDim.x) ready[i] = -1;
+    if (threadIdx.x == 0) { *progress = 0; xs[n] = 0.0; }
+    __syncthreads();
+    if (sw == nsweeps - 1) { c0 = clock64(); g0 = gtimer(); }
+    if (warp == mainw) {
+      double xprev = 0.0;
+      // registers of group g
+      double acc_pre, d, dv; int row, nr; double bvl[TB], bx[TB]; int bsl[TB];
+      // prologue: A(0)
+      {
+        while (ready[0] != 0) {}
+        nr = snr[0]; acc_pre = psum[lane]; d = dg[lane]; dv = di[lane]; row = rows[lane];
+        double avl[TA]; int acl[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { acl[k] = ac[k*32 + lane]; avl[k] = av[k*32 + lane]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl[k] = bsr[k*32 + lane]; bvl[k] = bv[k*32 + lane]; bx[k] = xs[bc[k*32 + lane]]; }
+#pragma unroll
+        for (int k = 0; k < TA; ++k) acc_pre = sub_rn(acc_pre, mul_rn(avl[k], xs[acl[k]]));
+      }
+      for (int g = 0; g < s.G; ++g) {
+        const long long w0 = clock64();
+        const int g1 = g + 1 < s.G ? g + 1 : g;   // last iteration: dummy reload of g
+        const int sl = g1 % R10;
+        const long long wr0 = clock64();
+        while (ready[sl] != g1) {}
+        const long long wr1 = clock64();
+        if (tsg && lane == 0 && sw == nsweeps - 1) tsg[g*2+1] = wr1 - wr0;
+        // loads for g+1 (independent of x_g)
+        const int nr1 = snr[sl];
+        double acc1 = psum[sl*32 + lane];
+        const double d1 = dg[sl*32 + lane], dv1 = di[sl*32 + lane]; const int row1 = rows[sl*32 + lane];
+        double avl[TA]; int acl[TA]; double bvl1[TB], bx1[TB]; int bsl1[TB], bcl1[TB];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { acl[k] = ac[(sl*TA + k)*32 + lane]; avl[k] = av[(sl*TA + k)*32 + lane]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl1[k] = bsr[(sl*TB + k)*32 + lane]; bvl1[k] = bv[(sl*TB + k)*32 + lane]; bcl1[k] = bc[(sl*TB + k)*32 + lane]; }
+        double axv[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) axv[k] = xs[acl[k]];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) bx1[k] = xs[bcl1[k]];
+        // B(g): critical
+        double acc = acc_pre;
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          const double sx = __shfl_sync(0xffffffffu, xprev, bsl[k] & 31);
+          const double X = bsl[k] >= 0 ? sx : bx[k];
+          acc = sub_rn(acc, mul_rn(bvl[k], X));
+        }
+        double x;
+        if (MARK) { const double q0 = mul_rn(acc, dv); const double rr = fma(-q0, d, acc); x = fma(rr, dv, q0); }
+        else x = div_rn(acc, d);
+        if (lane < nr) xs[row] = x;
+        xprev = x;
+        // A(g+1): pre-tail chain (deps on groups <= g-1)
+#pragma unroll
+        for (int k = 0; k < TA; ++k) acc1 = sub_rn(acc1, mul_rn(avl[k], axv[k]));
+        __syncwarp();
+        if (lane == 0) *progress = g + 1;
+        acc_pre = acc1; d = d1; dv = dv1; row = row1; nr = nr1;
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl[k] = bsl1[k]; bvl[k] = bvl1[k]; bx[k] = bx1[k]; }
+        if (tsg && lane == 0 && sw == nsweeps - 1) tsg[g*2] = clock64() - w0;
+      }
+    } else if (hid >= 0) {
+      for (int g = hid; g < s.G; g += nh) {
+        const int sl = g % R10;
+        const int nr = __ldg(s.nr + g), pw = __ldg(s.pw + g), need = __ldg(s.need + g);
+        const int64_t pb = __ldg(s.pptr + g);
+        int row = -1; double acc = 0.0, dd = 1.0, ddi = 1.0;
+        if (lane < nr) { row = __ldg(s.grows + g*32 + lane); acc = r[row]; dd = __ldg(s.diag + row); ddi = __ldg(dinv + row); }
+        int acl[TA]; double avl[TA]; int bcl[TB]; double bvl[TB]; int bsl[TB];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { acl[k] = __ldg(s.acol + (int64_t)(g*TA + k)*32 + lane); avl[k] = __ldg(s.aval + (int64_t)(g*TA + k)*32 + lane); }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bcl[k] = __ldg(s.bcol + (int64_t)(g*TB + k)*32 + lane); bvl[k] = __ldg(s.bval + (int64_t)(g*TB + k)*32 + lane); bsl[k] = s.bsrc[(int64_t)(g*TB + k)*32 + lane]; }
+        constexpr int CH = 8;
+        int pc[CH]; double pv[CH];
+        const int32_t* cp = s.pcols + pb + lane; const double* vp = s.pvals + pb + lane;
+        if (lane < nr) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) { pc[q] = q < pw ? __ldg(cp + (int64_t)q*nr) : -1; pv[q] = q < pw ? __ldg(vp + (int64_t)q*nr) : 0.0; }
+        }
+        while (*progress <= need) { __nanosleep(20); }
+        if (lane < nr) {
+          for (int k = 0; k < pw; k += CH) {
+            int nc[CH]; double nv[CH];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) { const int kk = k + CH + q; nc[q] = kk < pw ? __ldg(cp + (int64_t)kk*nr) : -1; nv[q] = kk < pw ? __ldg(vp + (int64_t)kk*nr) : 0.0; }
+            double xv[CH];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) xv[q] = xs[pc[q] < 0 ? n : pc[q]];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) if (pc[q] >= 0) acc = sub_rn(acc, mul_rn(pv[q], xv[q]));
+#pragma unroll
+            for (int q = 0; q < CH; ++q) { pc[q] = nc[q]; pv[q] = nv[q]; }
+          }
+        }
+        while (*progress < g - R10 + 2) { __nanosleep(20); }
+        psum[sl*32 + lane] = acc; dg[sl*32 + lane] = dd; di[sl*32 + lane] = ddi; rows[sl*32 + lane] = row;
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { ac[(sl*TA + k)*32 + lane] = acl[k]; av[(sl*TA + k)*32 + lane] = avl[k]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bc[(sl*TB + k)*32 + lane] = bcl[k]; bv[(sl*TB + k)*32 + lane] = bvl[k]; bsr[(sl*TB + k)*32 + lane] = bsl[k]; }
+        __syncwarp();
+        if (lane == 0) { snr[sl] = nr; __threadfence_block(); ready[sl] = g; }
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = xs[i];
+  }
+  if (threadIdx.x == 0) { t[0] = clock64() - c0; t[1] = gtimer() - g0; }
+}
+
+
+// ---- v12: FAST (reassociated) sums: tree reductions in main A/B and helper prefix; helper prefetch
+template <int N>
+__device__ __forceinline__ double tree_sum(double* p) {
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int k = 0; k + w < N; k += 2 * w) p[k] = add_rn(p[k], p[k + w]);
+  return p[0];
+}
+template <int TA, int TB, int PW, bool ISO = false>
+__global__ void __launch_bounds__(512,1) sweep12(S10d s, const double* __restrict__ dinv, int n, const double* __restrict__ r, double* out, unsigned long long* t, int nsweeps, long long* tsg) {
+  extern __shared__ double sm[];
+  double* xs = sm;
+  double* psum = xs + n + 1;
+  double* dg = psum + R10*32;
+  double* di = dg + R10*32;
+  double* av = di + R10*32;
+  double* bv = av + R10*TA*32;
+  int* ac = reinterpret_cast<int*>(bv + R10*TB*32);
+  int* bc = ac + R10*TA*32;
+  int* rows = bc + R10*TB*32;
+  int* bsr = rows + R10*32;
+  volatile int* meta = reinterpret_cast<volatile int*>(bsr + R10*TB*32);
+  volatile int* ready = meta; int* snr = const_cast<int*>(meta) + R10;
+  volatile int* progress = meta + 2*R10;
+  unsigned long long c0 = 0, g0 = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int mainw = nw - 1;
+  int hid = -1, nh = 0;
+  for (int w = 0; w < nw; ++w) { const bool isH = (w != mainw) && ((w & 3) != (mainw & 3)); if (isH) { if (w == warp) hid = nh; ++nh; } }
+  for (int sw = 0; sw < nsweeps; ++sw) {
+    for (int i = threadIdx.x; i < R10; i += blockDim.x) ready[i] = -1;
+    if (threadIdx.x == 0) { *progress = 0; xs[n] = 0.0; }
+    __syncthreads();
+    if (ISO) {
+      // prefill all ring slots with group 0's layout pattern (valid indices), mark ready
+      for (int i = threadIdx.x; i < R10*32; i += blockDim.x) { psum[i] = 1.0; dg[i] = 2.0; di[i] = 0.5; rows[i] = (i % 32) + 32 * ((i / 32) % 8); }
+      for (int i = threadIdx.x; i < R10*TA*32; i += blockDim.x) { ac[i] = (i * 7) % n; av[i] = 0.25; }
+      for (int i = threadIdx.x; i < R10*TB*32; i += blockDim.x) { bc[i] = (i * 13) % n; bv[i] = 0.125; bsr[i] = (i % 3 == 0) ? (i % 32) : -1; }
+      for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = 1.0;
+      for (int i = threadIdx.x; i < R10; i += blockDim.x) { snr[i] = 8; }
+      __syncthreads();
+    }
+    if (sw == nsweeps - 1) { c0 = clock64(); g0 = gtimer(); }
+    if (warp == mainw) {
+      double xprev = 0.0;
+      double acc_pre, d, dv; int row, nr; double bvl[TB], bx[TB]; int bsl[TB];
+      {
+        if (!ISO) while (ready[0] != 0) {}
+        nr = snr[0]; d = dg[lane]; dv = di[lane]; row = rows[lane];
+        double pa[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) pa[k] = mul_rn(av[k*32 + lane], xs[ac[k*32 + lane]]);
+        acc_pre = sub_rn(psum[lane], tree_sum<TA>(pa));
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl[k] = bsr[k*32 + lane]; bvl[k] = bv[k*32 + lane]; bx[k] = xs[bc[k*32 + lane]]; }
+      }
+      for (int g = 0; g < s.G; ++g) {
+        const long long w0 = clock64();
+        const int g1 = g + 1 < s.G ? g + 1 : g;
+        const int sl = g1 % R10;
+        const long long wr0 = clock64();
+        if (!ISO) while (ready[sl] != g1) {}
+        const long long wr1 = clock64();
+        const int nr1 = snr[sl];
+        const double ps1 = psum[sl*32 + lane];
+        const double d1 = dg[sl*32 + lane], dv1 = di[sl*32 + lane]; const int row1 = rows[sl*32 + lane];
+        double pa[TA]; double bvl1[TB], bx1[TB]; int bsl1[TB];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) pa[k] = mul_rn(av[(sl*TA + k)*32 + lane], xs[ac[(sl*TA + k)*32 + lane]]);
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl1[k] = bsr[(sl*TB + k)*32 + lane]; bvl1[k] = bv[(sl*TB + k)*32 + lane]; bx1[k] = xs[bc[(sl*TB + k)*32 + lane]]; }
+        // B(g)
+        double pb[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          const double sx = __shfl_sync(0xffffffffu, xprev, bsl[k] & 31);
+          pb[k] = mul_rn(bvl[k], bsl[k] >= 0 ? sx : bx[k]);
+        }
+        const double acc = sub_rn(acc_pre, tree_sum<TB>(pb));
+        const double q0 = mul_rn(acc, dv); const double rr = fma(-q0, d, acc); const double x = fma(rr, dv, q0);
+        if (lane < nr) xs[row] = x;
+        xprev = x;
+        const double acc1 = sub_rn(ps1, tree_sum<TA>(pa));
+        __syncwarp();
+        if (lane == 0) *progress = g + 1;
+        acc_pre = acc1; d = d1; dv = dv1; row = row1; nr = nr1;
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl[k] = bsl1[k]; bvl[k] = bvl1[k]; bx[k] = bx1[k]; }
+        if (tsg && lane == 0 && sw == nsweeps - 1) { tsg[g*2] = clock64() - w0; tsg[g*2+1] = wr1 - wr0; }
+      }
+    } else if (hid >= 0 && !ISO) {
+      int g = hid;
+      // prefetched header of the current group
+      int nr = 0, pw = 0, need = 0; int64_t pb0 = 0;
+      if (g < s.G) { nr = __ldg(s.nr + g); pw = __ldg(s.pw + g); need = __ldg(s.need + g); pb0 = __ldg(s.pptr + g); }
+      for (; g < s.G; g += nh) {
+        const int sl = g % R10;
+        const int gn = g + nh;
+        int nrn = 0, pwn = 0, needn = 0; int64_t pbn = 0;
+        if (gn < s.G) { nrn = __ldg(s.nr + gn); pwn = __ldg(s.pw + gn); needn = __ldg(s.need + gn); pbn = __ldg(s.pptr + gn); }
+        int row = -1; double acc = 0.0, dd = 1.0, ddi = 1.0;
+        if (lane < nr) { row = __ldg(s.grows + g*32 + lane); dd = __ldg(s.diag + row); ddi = __ldg(dinv + row); }
+        int acl[TA]; double avl[TA]; int bcl[TB]; double bvl[TB]; int bsl[TB];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { acl[k] = __ldg(s.acol + (int64_t)(g*TA + k)*32 + lane); avl[k] = __ldg(s.aval + (int64_t)(g*TA + k)*32 + lane); }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bcl[k] = __ldg(s.bcol + (int64_t)(g*TB + k)*32 + lane); bvl[k] = __ldg(s.bval + (int64_t)(g*TB + k)*32 + lane); bsl[k] = s.bsrc[(int64_t)(g*TB + k)*32 + lane]; }
+        const int32_t* cp = s.pcols + pb0 + lane; const double* vp = s.pvals + pb0 + lane;
+        double part = 0.0;
+        for (int k0 = 0; k0 < pw; k0 += PW) {
+          int pc[PW]; double pv[PW];
+#pragma unroll
+          for (int q = 0; q < PW; ++q) { const bool ok = lane < nr && k0 + q < pw; pc[q] = ok ? __ldg(cp + (int64_t)(k0+q)*nr) : n; pv[q] = ok ? __ldg(vp + (int64_t)(k0+q)*nr) : 0.0; }
+          if (k0 == 0) while (*progress <= need) { __nanosleep(20); }
+          double pp[PW];
+#pragma unroll
+          for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], xs[pc[q]]);
+          part = add_rn(part, tree_sum<PW>(pp));
+        }
+        if (pw == 0) while (*progress <= need) { __nanosleep(20); }
+        if (lane < nr) acc = sub_rn(r[row], part);
+        while (*progress < g - R10 + 2) { __nanosleep(20); }
+        psum[sl*32 + lane] = acc; dg[sl*32 + lane] = dd; di[sl*32 + lane] = ddi; rows[sl*32 + lane] = row;
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { ac[(sl*TA + k)*32 + lane] = acl[k]; av[(sl*TA + k)*32 + lane] = avl[k]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bc[(sl*TB + k)*32 + lane] = bcl[k]; bv[(sl*TB + k)*32 + lane] = bvl[k]; bsr[(sl*TB + k)*32 + lane] = bsl[k]; }
+        __syncwarp();
+        if (lane == 0) { snr[sl] = nr; __threadfence_block(); ready[sl] = g; }
+        nr = nrn; pw = pwn; need = needn; pb0 = pbn;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = xs[i];
+  }
+  if (threadIdx.x == 0) { t[0] = clock64() - c0; t[1] = gtimer() - g0; }
+}
+
+
+// ---- v13: v12 with explicit ordering: SHFL(B(g)) -> loads(g+1) -> B math -> STS -> A(g+1) math
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  unsigned lo, hi, rlo, rhi;
+  asm volatile("mov.b64 {%0,%1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(rlo) : "r"(lo), "r"(src));
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(rhi) : "r"(hi), "r"(src));
+  double out;
+  asm volatile("mov.b64 %0, {%1,%2};" : "=d"(out) : "r"(rlo), "r"(rhi));
+  return out;
+}
+template <int TA, int TB, int PW, bool ISO = false>
+__global__ void __launch_bounds__(512,1) sweep13(S10d s, const double* __restrict__ dinv, int n, const double* __restrict__ r, double* out, unsigned long long* t, int nsweeps, long long* tsg) {
+  extern __shared__ double sm[];
+  double* xs = sm;
+  double* psum = xs + n + 1;
+  double* dg = psum + R10*32;
+  double* di = dg + R10*32;
+  double* av = di + R10*32;
+  double* bv = av + R10*TA*32;
+  int* ac = reinterpret_cast<int*>(bv + R10*TB*32);
+  int* bc = ac + R10*TA*32;
+  int* rows = bc + R10*TB*32;
+  int* bsr = rows + R10*32;
+  volatile int* meta = reinterpret_cast<volatile int*>(bsr + R10*TB*32);
+  volatile int* ready = meta; int* snr = const_cast<int*>(meta) + R10;
+  volatile int* progress = meta + 2*R10;
+  unsigned long long c0 = 0, g0 = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int mainw = nw - 1;
+  int hid = -1, nh = 0;
+  for (int w = 0; w < nw; ++w) { const bool isH = (w != mainw) && ((w & 3) != (mainw & 3)); if (isH) { if (w == warp) hid = nh; ++nh; } }
+  for (int sw = 0; sw < nsweeps; ++sw) {
+    for (int i = threadIdx.x; i < R10; i += blockDim.x) ready[i] = -1;
+    if (threadIdx.x == 0) { *progress = 0; xs[n] = 0.0; }
+    __syncthreads();
+    if (ISO) {
+      for (int i = threadIdx.x; i < R10*32; i += blockDim.x) { psum[i] = 1.0; dg[i] = 2.0; di[i] = 0.5; rows[i] = (i % 32) + 32 * ((i / 32) % 8); }
+      for (int i = threadIdx.x; i < R10*TA*32; i += blockDim.x) { ac[i] = (i * 7) % n; av[i] = 0.25; }
+      for (int i = threadIdx.x; i < R10*TB*32; i += blockDim.x) { bc[i] = (i * 13) % n; bv[i] = 0.125; bsr[i] = (i % 3 == 0) ? (i % 32) : -1; }
+      for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = 1.0;
+      for (int i = threadIdx.x; i < R10; i += blockDim.x) { snr[i] = 8; }
+      __syncthreads();
+    }
+    if (sw == nsweeps - 1) { c0 = clock64(); g0 = gtimer(); }
+    if (warp == mainw) {
+      double xprev = 0.0;
+      double acc_pre, d, dv; int row, nr; double bvl[TB], bx[TB]; int bsl[TB];
+      {
+        if (!ISO) while (ready[0] != 0) {}
+        nr = snr[0]; d = dg[lane]; dv = di[lane]; row = rows[lane];
+        double pa[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) pa[k] = mul_rn(av[k*32 + lane], xs[ac[k*32 + lane]]);
+        acc_pre = sub_rn(psum[lane], tree_sum<TA>(pa));
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl[k] = bsr[k*32 + lane]; bvl[k] = bv[k*32 + lane]; bx[k] = xs[bc[k*32 + lane]]; }
+      }
+      for (int g = 0; g < s.G; ++g) {
+        const long long w0 = clock64();
+        // (1) shuffles for B(g): x_{g-1} lives in xprev
+        double sx[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) sx[k] = shfl_d(xprev, bsl[k] & 31);
+        asm volatile("" ::: "memory");
+        // (2) next group's slot
+        const int g1 = g + 1 < s.G ? g + 1 : g;
+        const int sl = g1 % R10;
+        if (!ISO) while (ready[sl] != g1) {}
+        const int nr1 = snr[sl];
+        const double ps1 = psum[sl*32 + lane];
+        const double d1 = dg[sl*32 + lane], dv1 = di[sl*32 + lane]; const int row1 = rows[sl*32 + lane];
+        double avl[TA], axv[TA]; double bvl1[TB], bx1[TB]; int bsl1[TB];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { avl[k] = av[(sl*TA + k)*32 + lane]; axv[k] = xs[ac[(sl*TA + k)*32 + lane]]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl1[k] = bsr[(sl*TB + k)*32 + lane]; bvl1[k] = bv[(sl*TB + k)*32 + lane]; bx1[k] = xs[bc[(sl*TB + k)*32 + lane]]; }
+        // (3) B(g) math
+        double pb[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) pb[k] = mul_rn(bvl[k], bsl[k] >= 0 ? sx[k] : bx[k]);
+        const double acc = sub_rn(acc_pre, tree_sum<TB>(pb));
+        const double q0 = mul_rn(acc, dv); const double rr = fma(-q0, d, acc); const double x = fma(rr, dv, q0);
+        xprev = x;
+        if (lane < nr) xs[row] = x;
+        __syncwarp();
+        if (lane == 0) *progress = g + 1;
+        // (4) A(g+1)
+        double pa[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) pa[k] = mul_rn(avl[k], axv[k]);
+        acc_pre = sub_rn(ps1, tree_sum<TA>(pa)); d = d1; dv = dv1; row = row1; nr = nr1;
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bsl[k] = bsl1[k]; bvl[k] = bvl1[k]; bx[k] = bx1[k]; }
+        if (tsg && lane == 0 && sw == nsweeps - 1) { tsg[g*2] = clock64() - w0; tsg[g*2+1] = 0; }
+      }
+    } else if (hid >= 0 && !ISO) {
+      int g = hid;
+      int nr = 0, pw = 0, need = 0; int64_t pb0 = 0;
+      if (g < s.G) { nr = __ldg(s.nr + g); pw = __ldg(s.pw + g); need = __ldg(s.need + g); pb0 = __ldg(s.pptr + g); }
+      for (; g < s.G; g += nh) {
+        const int sl = g % R10;
+        const int gn = g + nh;
+        int nrn = 0, pwn = 0, needn = 0; int64_t pbn = 0;
+        if (gn < s.G) { nrn = __ldg(s.nr + gn); pwn = __ldg(s.pw + gn); needn = __ldg(s.need + gn); pbn = __ldg(s.pptr + gn); }
+        int row = -1; double acc = 0.0, dd = 1.0, ddi = 1.0;
+        if (lane < nr) { row = __ldg(s.grows + g*32 + lane); dd = __ldg(s.diag + row); ddi = __ldg(dinv + row); }
+        int acl[TA]; double avl[TA]; int bcl[TB]; double bvl[TB]; int bsl[TB];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { acl[k] = __ldg(s.acol + (int64_t)(g*TA + k)*32 + lane); avl[k] = __ldg(s.aval + (int64_t)(g*TA + k)*32 + lane); }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bcl[k] = __ldg(s.bcol + (int64_t)(g*TB + k)*32 + lane); bvl[k] = __ldg(s.bval + (int64_t)(g*TB + k)*32 + lane); bsl[k] = s.bsrc[(int64_t)(g*TB + k)*32 + lane]; }
+        const int32_t* cp = s.pcols + pb0 + lane; const double* vp = s.pvals + pb0 + lane;
+        double part = 0.0;
+        for (int k0 = 0; k0 < pw; k0 += PW) {
+          int pc[PW]; double pv[PW];
+#pragma unroll
+          for (int q = 0; q < PW; ++q) { const bool ok = lane < nr && k0 + q < pw; pc[q] = ok ? __ldg(cp + (int64_t)(k0+q)*nr) : n; pv[q] = ok ? __ldg(vp + (int64_t)(k0+q)*nr) : 0.0; }
+          if (k0 == 0) while (*progress <= need) { __nanosleep(20); }
+          double pp[PW];
+#pragma unroll
+          for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], xs[pc[q]]);
+          part = add_rn(part, tree_sum<PW>(pp));
+        }
+        if (pw == 0) while (*progress <= need) { __nanosleep(20); }
+        if (lane < nr) acc = sub_rn(r[row], part);
+        while (*progress < g - R10 + 2) { __nanosleep(20); }
+        psum[sl*32 + lane] = acc; dg[sl*32 + lane] = dd; di[sl*32 + lane] = ddi; rows[sl*32 + lane] = row;
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { ac[(sl*TA + k)*32 + lane] = acl[k]; av[(sl*TA + k)*32 + lane] = avl[k]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bc[(sl*TB + k)*32 + lane] = bcl[k]; bv[(sl*TB + k)*32 + lane] = bvl[k]; bsr[(sl*TB + k)*32 + lane] = bsl[k]; }
+        __syncwarp();
+        if (lane == 0) { snr[sl] = nr; __threadfence_block(); ready[sl] = g; }
+        nr = nrn; pw = pwn; need = needn; pb0 = pbn;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = xs[i];
+  }
+  if (threadIdx.x == 0) { t[0] = clock64() - c0; t[1] = gtimer() - g0; }
+}
+
+
+// ---- v14: deeper pipeline. Group G entries: prefix (dep <= G-D, helpers), A (G-D < dep <= G-3,
+// main gathers one iteration ahead), B (dep in {G-2, G-1}: two register shuffles).
+struct H14 { int G; std::vector<int32_t> nr, need, grows, pw; std::vector<int64_t> pptr; std::vector<int32_t> pcols, acol; std::vector<double> pvals, aval, bval; std::vector<int32_t> bsrc; };
+template <int TA, int TB>
+H14 build14(const HostSweep& s, int D) {
+  int n = s.n; std::vector<int> gof(n), lof(n);
+  std::vector<std::vector<std::pair<int,double>>> rows(n);
+  for (int g = 0; g < s.n_groups; ++g) for (int l = 0; l < 32; ++l) { int r = s.grows[g*32+l]; if (r < 0) continue; gof[r] = g; lof[r] = l;
+      for (int k = 0; k < s.gwidth[g]; ++k) { int64_t e = s.gptr[g] + (int64_t)k*32 + l; if (s.cols[e] >= 0) rows[r].push_back({s.cols[e], s.vals[e]}); } }
+  H14 h; h.G = s.n_groups; h.pptr.push_back(0);
+  int ta_max = 0, tb_max = 0;
+  for (int g = 0; g < s.n_groups; ++g) {
+    int nr = 0; for (int l = 0; l < 32; ++l) if (s.grows[g*32+l] >= 0) nr = l + 1;
+    std::vector<std::vector<std::pair<int,double>>> P(nr), A(nr), B(nr);
+    int need = -1, pw = 0;
+    for (int l = 0; l < nr; ++l) for (auto& e : rows[s.grows[g*32+l]]) {
+      int dg = gof[e.first];
+      if (dg >= g - 2) B[l].push_back(e); else if (dg > g - D) A[l].push_back(e); else P[l].push_back(e);
+    }
+    for (int l = 0; l < nr; ++l) {
+      while ((int)A[l].size() > TA) { P[l].push_back(A[l].front()); A[l].erase(A[l].begin()); }  // oldest to prefix
+      if ((int)B[l].size() > TB) { printf("B overflow %zu\n", B[l].size()); exit(1); }
+      for (auto& e : P[l]) need = std::max(need, gof[e.first]);
+      pw = std::max(pw, (int)P[l].size()); ta_max = std::max(ta_max, (int)A[l].size()); tb_max = std::max(tb_max, (int)B[l].size()); }
+    h.nr.push_back(nr); h.need.push_back(need); h.pw.push_back(pw);
+    for (int l = 0; l < 32; ++l) h.grows.push_back(s.grows[g*32+l]);
+    int64_t pb = h.pptr.back(); h.pcols.resize(pb + (int64_t)pw*nr, n); h.pvals.resize(pb + (int64_t)pw*nr, 0.0);
+    size_t a0 = h.acol.size(); h.acol.resize(a0 + TA*32, n); h.aval.resize(a0 + TA*32, 0.0);
+    size_t b0 = h.bval.size(); h.bval.resize(b0 + TB*32, 0.0); h.bsrc.resize(b0 + TB*32, 0);
+    for (int l = 0; l < nr; ++l) {
+      for (size_t k = 0; k < P[l].size(); ++k) { h.pcols[pb + (int64_t)k*nr + l] = P[l][k].first; h.pvals[pb + (int64_t)k*nr + l] = P[l][k].second; }
+      for (size_t k = 0; k < A[l].size(); ++k) { h.acol[a0 + k*32 + l] = A[l][k].first; h.aval[a0 + k*32 + l] = A[l][k].second; }
+      for (size_t k = 0; k < B[l].size(); ++k) { int dg = gof[B[l][k].first]; h.bval[b0 + k*32 + l] = B[l][k].second; h.bsrc[b0 + k*32 + l] = lof[B[l][k].first] | (dg == g - 2 ? 32 : 0); } }
+    h.pptr.push_back(pb + (int64_t)pw*nr);
+  }
+  printf("build14 D=%d: max A %d, max B %d\n", D, ta_max, tb_max);
+  return h;
+}
+struct S14d { int G; const int32_t *nr, *need, *grows, *pw, *pcols, *acol, *bsrc; const int64_t* pptr; const double *pvals, *aval, *bval, *diag, *dinv; };
+template <int TA, int TB, int PW, bool ISO = false>
+__global__ void __launch_bounds__(512,1) sweep14(S14d s, int n, const double* __restrict__ r, double* out, unsigned long long* t, int nsweeps, long long* tsg) {
+  extern __shared__ double sm[];
+  double* xs = sm;                                  // n+1
+  double* psum = xs + n + 1;                        // R*32
+  double* dg = psum + R10*32;
+  double* di = dg + R10*32;
+  double* av = di + R10*32;                         // R*TA*32
+  double* bv = av + R10*TA*32;                      // R*TB*32
+  int* ac = reinterpret_cast<int*>(bv + R10*TB*32); // R*TA*32
+  int* rows = ac + R10*TA*32;                       // R*32
+  int* bsr = rows + R10*32;                         // R*TB*32
+  volatile int* meta = reinterpret_cast<volatile int*>(bsr + R10*TB*32);
+  volatile int* ready = meta; int* snr = const_cast<int*>(meta) + R10;
+  volatile int* progress = meta + 2*R10;
+  unsigned long long c0 = 0, g0 = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int mainw = nw - 1;
+  int hid = -1, nh = 0;
+  for (int w = 0; w < nw; ++w) { const bool isH = (w != mainw) && ((w & 3) != (mainw & 3)); if (isH) { if (w == warp) hid = nh; ++nh; } }
+  for (int sw = 0; sw < nsweeps; ++sw) {
+    for (int i = threadIdx.x; i < R10; i += blockDim.x) ready[i] = -1;
+    if (threadIdx.x == 0) { *progress = 0; xs[n] = 0.0; }
+    __syncthreads();
+    if (ISO) {
+      for (int i = threadIdx.x; i < R10*32; i += blockDim.x) { psum[i] = 1.0; dg[i] = 2.0; di[i] = 0.5; rows[i] = (i % 32) + 32 * ((i / 32) % 8); }
+      for (int i = threadIdx.x; i < R10*TA*32; i += blockDim.x) { ac[i] = (i * 7) % n; av[i] = 0.25; }
+      for (int i = threadIdx.x; i < R10*TB*32; i += blockDim.x) { bv[i] = 0.125; bsr[i] = i % 64; }
+      for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = 1.0;
+      for (int i = threadIdx.x; i < R10; i += blockDim.x) { snr[i] = 8; }
+      __syncthreads();
+    }
+    if (sw == nsweeps - 1) { c0 = clock64(); g0 = gtimer(); }
+    if (warp == mainw) {
+      double x1 = 0.0, x2 = 0.0;          // x of groups g-1, g-2 (per lane)
+      // group g state (B pending): acc_pre, d, dv, row, nr, bvl, bsl
+      // group g+1 state (A pending): ps1, avl1, axv1, d1, dv1, row1, nr1, bvl1, bsl1
+      double acc_pre = 0.0, d = 1.0, dv = 1.0; int row = -1, nr = 0; double bvl[TB]; int bsl[TB];
+      double ps1 = 0.0, d1 = 1.0, dv1 = 1.0; int row1 = -1, nr1 = 0; double avl1[TA], axv1[TA], bvl1[TB]; int bsl1[TB];
+      auto load = [&](int gg, double& ps, double& dd, double& ddv, int& rr, int& nn, double* avl, double* axv, double* bvl_, int* bsl_) {
+        const int sl = gg % R10;
+        if (!ISO) while (ready[sl] != gg) {}
+        nn = snr[sl]; ps = psum[sl*32 + lane]; dd = dg[sl*32 + lane]; ddv = di[sl*32 + lane]; rr = rows[sl*32 + lane];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { avl[k] = av[(sl*TA + k)*32 + lane]; axv[k] = xs[ac[(sl*TA + k)*32 + lane]]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bvl_[k] = bv[(sl*TB + k)*32 + lane]; bsl_[k] = bsr[(sl*TB + k)*32 + lane]; }
+      };
+      // prologue: group 0 (A done now), group 1 loaded
+      {
+        double avl[TA], axv[TA];
+        load(0, acc_pre, d, dv, row, nr, avl, axv, bvl, bsl);
+        double pa[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) pa[k] = mul_rn(avl[k], axv[k]);
+        acc_pre = sub_rn(acc_pre, tree_sum<TA>(pa));
+        if (s.G > 1) load(1, ps1, d1, dv1, row1, nr1, avl1, axv1, bvl1, bsl1);
+      }
+      for (int g = 0; g < s.G; ++g) {
+        const long long w0 = clock64();
+        // (1) B(g) shuffles
+        double X[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          const int src = bsl[k] & 31;
+          const double a1 = shfl_d(x1, src), a2 = shfl_d(x2, src);
+          X[k] = (bsl[k] & 32) ? a2 : a1;
+        }
+        asm volatile("" ::: "memory");
+        // (2) loads for g+2 (deps <= g-1 for its A part: available)
+        double ps2 = 0.0, d2 = 1.0, dv2 = 1.0; int row2 = -1, nr2 = 0; double avl2[TA], axv2[TA], bvl2[TB]; int bsl2[TB];
+        if (g + 2 < s.G) load(g + 2, ps2, d2, dv2, row2, nr2, avl2, axv2, bvl2, bsl2);
+        // (3) B(g) math
+        double pb[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) pb[k] = mul_rn(bvl[k], X[k]);
+        const double acc = sub_rn(acc_pre, tree_sum<TB>(pb));
+        const double q0 = mul_rn(acc, dv); const double rr = fma(-q0, d, acc); const double x = fma(rr, dv, q0);
+        if (lane < nr) xs[row] = x;
+        __syncwarp();
+        if (lane == 0) *progress = g + 1;
+        x2 = x1; x1 = x;
+        // (4) A(g+1) with registers loaded one iteration ago
+        double pa[TA];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) pa[k] = mul_rn(avl1[k], axv1[k]);
+        acc_pre = sub_rn(ps1, tree_sum<TA>(pa)); d = d1; dv = dv1; row = row1; nr = nr1;
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bvl[k] = bvl1[k]; bsl[k] = bsl1[k]; }
+        ps1 = ps2; d1 = d2; dv1 = dv2; row1 = row2; nr1 = nr2;
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { avl1[k] = avl2[k]; axv1[k] = axv2[k]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bvl1[k] = bvl2[k]; bsl1[k] = bsl2[k]; }
+        if (tsg && lane == 0 && sw == nsweeps - 1) tsg[g] = clock64() - w0;
+      }
+    } else if (hid >= 0 && !ISO) {
+      int g = hid;
+      int nr = 0, pw = 0, need = 0; int64_t pb0 = 0;
+      if (g < s.G) { nr = __ldg(s.nr + g); pw = __ldg(s.pw + g); need = __ldg(s.need + g); pb0 = __ldg(s.pptr + g); }
+      for (; g < s.G; g += nh) {
+        const int sl = g % R10;
+        const int gn = g + nh;
+        int nrn = 0, pwn = 0, needn = 0; int64_t pbn = 0;
+        if (gn < s.G) { nrn = __ldg(s.nr + gn); pwn = __ldg(s.pw + gn); needn = __ldg(s.need + gn); pbn = __ldg(s.pptr + gn); }
+        int row = -1; double acc = 0.0, dd = 1.0, ddi = 1.0;
+        if (lane < nr) { row = __ldg(s.grows + g*32 + lane); dd = __ldg(s.diag + row); ddi = __ldg(s.dinv + row); }
+        int acl[TA]; double avl[TA]; double bvl[TB]; int bsl[TB];
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { acl[k] = __ldg(s.acol + (int64_t)(g*TA + k)*32 + lane); avl[k] = __ldg(s.aval + (int64_t)(g*TA + k)*32 + lane); }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bvl[k] = __ldg(s.bval + (int64_t)(g*TB + k)*32 + lane); bsl[k] = __ldg(s.bsrc + (int64_t)(g*TB + k)*32 + lane); }
+        const int32_t* cp = s.pcols + pb0 + lane; const double* vp = s.pvals + pb0 + lane;
+        double part = 0.0;
+        for (int k0 = 0; k0 < pw; k0 += PW) {
+          int pc[PW]; double pv[PW];
+#pragma unroll
+          for (int q = 0; q < PW; ++q) { const bool ok = lane < nr && k0 + q < pw; pc[q] = ok ? __ldg(cp + (int64_t)(k0+q)*nr) : n; pv[q] = ok ? __ldg(vp + (int64_t)(k0+q)*nr) : 0.0; }
+          if (k0 == 0) while (*progress <= need) { __nanosleep(20); }
+          double pp[PW];
+#pragma unroll
+          for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], xs[pc[q]]);
+          part = add_rn(part, tree_sum<PW>(pp));
+        }
+        if (pw == 0) while (*progress <= need) { __nanosleep(20); }
+        if (lane < nr) acc = sub_rn(r[row], part);
+        while (*progress < g - R10 + 3) { __nanosleep(20); }
+        psum[sl*32 + lane] = acc; dg[sl*32 + lane] = dd; di[sl*32 + lane] = ddi; rows[sl*32 + lane] = row;
+#pragma unroll
+        for (int k = 0; k < TA; ++k) { ac[(sl*TA + k)*32 + lane] = acl[k]; av[(sl*TA + k)*32 + lane] = avl[k]; }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) { bv[(sl*TB + k)*32 + lane] = bvl[k]; bsr[(sl*TB + k)*32 + lane] = bsl[k]; }
+        __syncwarp();
+        if (lane == 0) { snr[sl] = nr; __threadfence_block(); ready[sl] = g; }
+        nr = nrn; pw = pwn; need = needn; pb0 = pbn;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = xs[i];
+  }
+  if (threadIdx.x == 0) { t[0] = clock64() - c0; t[1] = gtimer() - g0; }
+}
+
 template <class T> T* up(const std::vector<T>& v) { T* d; cudaMalloc(&d, v.size()*sizeof(T)+8); cudaMemcpy(d, v.data(), v.size()*sizeof(T), cudaMemcpyHostToDevice); return d; }
 
 int main(int argc, char** argv) {
@@ -693,6 +1464,7 @@ int main(int argc, char** argv) {
   dshost_ic0(n, prp.data(), pci.data(), pv.data(), lrp.data(), lci.data(), lv.data(), &bad);
   dsgpu_csr L{n, n, lrp.data(), lci.data(), lv.data()};
   HostSweep f, b; build_sweeps(L, f, b);
+  const bool only11 = argc > 3 && strcmp(argv[3], "v11") == 0;
   printf("n=%d nnzL=%ld levels=%d groups=%d sell_entries=%ld\n", n, (long)ln, f.n_levels, f.n_groups, (long)f.gptr.back());
   S s{f.n_groups, up(f.gptr), up(f.gwidth), up(f.grows), up(f.cols), up(f.vals), up(f.diag)};
   std::vector<double> rh(n, 1.0); double* r = up(rh); double* out; cudaMalloc(&out, n*8);
@@ -702,7 +1474,7 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(sweep_k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(sweep_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(sweep_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int threads : {1024}) {
+  if (!only11) for (int threads : {1024}) {
     for (int mode = 0; mode < 4; ++mode) {
       unsigned long long th[2]; float best = 1e9;
       for (int rep = 0; rep < 5; ++rep) {
@@ -731,7 +1503,7 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(sweep2<true,8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sweep_k<0><<<1, 1024, smem>>>(s, n, r, out_ref, ab, t);
     std::vector<double> o1(n), o2(n); cudaMemcpy(o1.data(), out_ref, n*8, cudaMemcpyDeviceToHost);
-    for (int var = 0; var < 3; ++var) for (int threads : {1024, 512}) {
+    if (!only11) for (int var = 0; var < 3; ++var) for (int threads : {1024, 512}) {
       unsigned long long th[2]; float best = 1e9;
       for (int rep = 0; rep < 5; ++rep) {
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -747,7 +1519,7 @@ int main(int argc, char** argv) {
       printf("v2 var=%d (%s) threads=%d: %.1f us cyc/level=%.0f bitexact=%d maxrel=%.2e err=%s\n", var, var==0?"div,ch4":var==1?"div,ch8":"recip,ch8", threads, best*1e3, th[0]/(double)f.n_levels, (int)eq, md, cudaGetErrorString(cudaGetLastError()));
     }
 
-    {
+    if (!only11) {
       size_t smem3 = n * 16;
       cudaFuncSetAttribute(sweep3<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
       cudaFuncSetAttribute(sweep3<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
@@ -769,7 +1541,7 @@ int main(int argc, char** argv) {
       }
     }
 
-    {
+    if (!only11) {
       size_t smem3 = n * 8;
       cudaFuncSetAttribute(sweep4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
       long long* ts; cudaMalloc(&ts, f.n_groups * 32);
@@ -790,7 +1562,7 @@ int main(int argc, char** argv) {
       printf("L2 pointer-chase latency: %.0f cycles\n", hl[0] / 10000.0);
     }
 
-    {
+    if (!only11) {
       size_t smem3 = n * 8;
       for (int extra : {0, 69000}) {
       cudaFuncSetAttribute(sweep5<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem3+extra));
@@ -810,7 +1582,7 @@ int main(int argc, char** argv) {
       }
     }
 
-    {
+    if (!only11) {
       std::vector<int> lev; H2 h6 = build6(f, lev);
       S2 s6{f.n_groups, up(h6.gptr), up(h6.gnrow), up(h6.gpw), up(h6.grows), up(h6.cols), up(h6.vals), up(f.diag), up(dinv)};
       size_t smem3 = n * 8;
@@ -848,7 +1620,7 @@ int main(int argc, char** argv) {
       printf("pure chain: %.0f cycles/level err=%s\n", tt[0]/1024.0, cudaGetErrorString(cudaGetLastError()));
     }
 
-    {
+    if (!only11) {
       unsigned long long tt[2];
       cudaFuncSetAttribute(chain8<false,0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192);
       cudaFuncSetAttribute(chain8<true,0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192);
@@ -863,7 +1635,7 @@ int main(int argc, char** argv) {
       chain9<true><<<1,1>>>(1024, t, out); cudaDeviceSynchronize(); cudaMemcpy(tt, t, 16, cudaMemcpyDeviceToHost); printf("chain9 recip: %.1f cycles/level\n", tt[0]/1024.0);
     }
 
-    for (int D : {2, 3, 4, 6, 8}) {
+    if (!only11) for (int D : {2, 3, 4, 6, 8}) {
       H8 h8 = build8(f, D);
       if (h8.TW > 16) { printf("v8 D=%d TW=%d too big\n", D, h8.TW); continue; }
       S8 s8{h8.G, up(h8.nr), up(h8.need), up(h8.grows), up(h8.pw), up(h8.tw), up(h8.pcols), up(h8.tcols), up(h8.pptr), up(h8.tptr), up(h8.pvals), up(h8.tvals), up(f.diag)};
@@ -885,7 +1657,7 @@ int main(int argc, char** argv) {
       }
     }
 
-    {
+    if (!only11) {
       H8 h8 = build8(f, 6);
       S8 s8{h8.G, up(h8.nr), up(h8.need), up(h8.grows), up(h8.pw), up(h8.tw), up(h8.pcols), up(h8.tcols), up(h8.pptr), up(h8.tptr), up(h8.pvals), up(h8.tvals), up(f.diag)};
       const int TWM = 16;
@@ -897,7 +1669,7 @@ int main(int argc, char** argv) {
       printf("v8 main breakdown (cycles/group): wait-ready %.0f, compute %.0f, fence+progress %.0f ; tw mean %.1f\n", a/h8.G, b/h8.G, c/h8.G, [&]{double s=0; for (int x : h8.tw) s+=x; return s/h8.G;}());
     }
 
-    for (int D : {6}) {
+    if (!only11) for (int D : {6}) {
       H8 h8 = build8(f, D);
       S8 s8{h8.G, up(h8.nr), up(h8.need), up(h8.grows), up(h8.pw), up(h8.tw), up(h8.pcols), up(h8.tcols), up(h8.pptr), up(h8.tptr), up(h8.pvals), up(h8.tvals), up(f.diag)};
       const int TWM = 16;
@@ -921,6 +1693,174 @@ int main(int argc, char** argv) {
         bool eq = true; for (int i = 0; i < n; ++i) eq &= o1[i]==o2[i];
         printf("v9 mode=%d %s D=%d threads=%d: %.1f us/sweep cyc/level=%.0f [main: wait %.0f compute %.0f fence %.0f] bitexact=%d err=%s\n", rc, rc==1?"recip":"div", D, threads, best, bc/(double)f.n_levels, a/h8.G, b/h8.G, c/h8.G, (int)eq, cudaGetErrorString(cudaGetLastError()));
       }
+    }
+
+    if (!only11) for (int lo = 0; lo < 2; ++lo) for (int D : {6}) {
+      constexpr int TA = 8, TB = 10;
+      H10 h = build10<TA, TB>(f, D, lo == 1);
+      S10d sd{h.G, up(h.nr), up(h.need), up(h.amax), up(h.bmax), up(h.grows), up(h.pw), up(h.pcols), up(h.acol), up(h.bcol), up(h.bsrc), up(h.pptr), up(h.pvals), up(h.aval), up(h.bval), up(f.diag)};
+      size_t smem10 = (n + 1) * 8 + R10*32*8*2 + R10*TA*32*12 + R10*TB*32*13 + R10*32*4 + 4*R10*4 + 64;
+      cudaFuncSetAttribute(sweep10<TA,TB,false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem10);
+      cudaFuncSetAttribute(sweep10<TA,TB,true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem10);
+      cudaFuncSetAttribute(sweep10<TA,TB,true,1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem10);
+      cudaFuncSetAttribute(sweep10<TA,TB,true,2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem10);
+      long long* tsg; cudaMalloc(&tsg, h.G * 16);
+      for (int mk = 1; mk < 4; ++mk) for (int threads : {512, 256}) {
+        unsigned long long tt[2]; float best = 1e9; unsigned long long bc = 0;
+        for (int rep = 0; rep < 3; ++rep) {
+          if (mk == 1) sweep10<TA,TB,true><<<1, threads, smem10>>>(sd, n, r, out, t, 4, tsg);
+          else if (mk == 2) sweep10<TA,TB,true,1><<<1, threads, smem10>>>(sd, n, r, out, t, 4, tsg);
+          else sweep10<TA,TB,true,2><<<1, threads, smem10>>>(sd, n, r, out, t, 4, tsg);
+          cudaDeviceSynchronize(); cudaMemcpy(tt, t, 16, cudaMemcpyDeviceToHost);
+          if (tt[1]*1e-3 < best) { best = tt[1]*1e-3; bc = tt[0]; }
+        }
+        std::vector<long long> hh(h.G*2); cudaMemcpy(hh.data(), tsg, hh.size()*8, cudaMemcpyDeviceToHost);
+        double a=0,b=0; for (int g = 0; g < h.G; ++g) { a += hh[g*2]; b += hh[g*2+1]; }
+        cudaMemcpy(o2.data(), out, n*8, cudaMemcpyDeviceToHost);
+        bool eq = true; double md = 0; for (int i = 0; i < n; ++i) { eq &= o1[i]==o2[i]; md = std::max(md, std::abs(o1[i]-o2[i])/std::max(1e-300,std::abs(o1[i]))); }
+        printf("v10 excl=%d %s %s D=%d TAm=%d TBm=%d threads=%d: %.1f us/sweep cyc/level=%.0f [B %.0f, A %.0f] bitexact=%d maxrel=%.1e err=%s\n", mk-1, lo?"levelord":"colord", mk?"markstein":"div", D, h.TAm, h.TBm, threads, best, bc/(double)f.n_levels, a/h.G, b/h.G, (int)eq, md, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+
+    {
+      std::vector<double> dinvh(n); for (int i = 0; i < n; ++i) dinvh[i] = 1.0 / f.diag[i];
+      double* ddinv = up(dinvh);
+      auto runv11 = [&](auto TAc, auto TBc, int D, bool lo) {
+        constexpr int TA = decltype(TAc)::value, TB = decltype(TBc)::value;
+        H10 h = build10<TA, TB>(f, D, lo);
+        S10d sd{h.G, up(h.nr), up(h.need), up(h.amax), up(h.bmax), up(h.grows), up(h.pw), up(h.pcols), up(h.acol), up(h.bcol), up(h.bsrc), up(h.pptr), up(h.pvals), up(h.aval), up(h.bval), up(f.diag)};
+        size_t smem = (n + 1) * 8 + R10*32*8*3 + R10*TA*32*12 + R10*TB*32*16 + R10*32*4 + 2*R10*4 + 64;
+        cudaFuncSetAttribute(sweep11<TA,TB,true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        long long* tsg; cudaMalloc(&tsg, h.G * 16);
+        for (int threads : {512, 256}) {
+          unsigned long long tt[2]; float best = 1e9; unsigned long long bc = 0;
+          for (int rep = 0; rep < 3; ++rep) {
+            sweep11<TA,TB,true><<<1, threads, smem>>>(sd, ddinv, n, r, out, t, 4, tsg);
+            cudaDeviceSynchronize(); cudaMemcpy(tt, t, 16, cudaMemcpyDeviceToHost);
+            if (tt[1]*1e-3 < best) { best = tt[1]*1e-3; bc = tt[0]; }
+          }
+          std::vector<long long> hh(h.G*2); cudaMemcpy(hh.data(), tsg, hh.size()*8, cudaMemcpyDeviceToHost);
+          double a=0, wsum=0; for (int g = 0; g < h.G; ++g) { a += hh[g*2]; wsum += hh[g*2+1]; }
+          cudaMemcpy(o2.data(), out, n*8, cudaMemcpyDeviceToHost);
+          bool eq = true; double md = 0; for (int i = 0; i < n; ++i) { eq &= o1[i]==o2[i]; md = std::max(md, std::abs(o1[i]-o2[i])/std::max(1e-300,std::abs(o1[i]))); }
+          printf("v11 %s TA=%d TB=%d D=%d (TAm=%d TBm=%d) threads=%d: %.1f us/sweep cyc/level=%.0f [main iter %.0f, ready-wait %.0f] bitexact=%d maxrel=%.1e err=%s\n", lo?"levelord":"colord", TA, TB, D, h.TAm, h.TBm, threads, best, bc/(double)f.n_levels, a/h.G, wsum/h.G, (int)eq, md, cudaGetErrorString(cudaGetLastError()));
+        }
+      };
+      runv11(std::integral_constant<int,8>(), std::integral_constant<int,8>(), 6, false);
+      runv11(std::integral_constant<int,8>(), std::integral_constant<int,3>(), 6, true);
+      runv11(std::integral_constant<int,12>(), std::integral_constant<int,3>(), 10, true);
+      runv11(std::integral_constant<int,4>(), std::integral_constant<int,2>(), 4, true);
+    }
+
+    {
+      std::vector<double> dinvh(n); for (int i = 0; i < n; ++i) dinvh[i] = 1.0 / f.diag[i];
+      double* ddinv = up(dinvh);
+      auto runv12 = [&](auto TAc, auto TBc, int D) {
+        constexpr int TA = decltype(TAc)::value, TB = decltype(TBc)::value;
+        H10 h = build10<TA, TB>(f, D, true);
+        S10d sd{h.G, up(h.nr), up(h.need), up(h.amax), up(h.bmax), up(h.grows), up(h.pw), up(h.pcols), up(h.acol), up(h.bcol), up(h.bsrc), up(h.pptr), up(h.pvals), up(h.aval), up(h.bval), up(f.diag)};
+        size_t smem = (n + 1) * 8 + R10*32*8*3 + R10*TA*32*12 + R10*TB*32*16 + R10*32*4 + 2*R10*4 + 64;
+        cudaFuncSetAttribute(sweep12<TA,TB,16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        long long* tsg; cudaMalloc(&tsg, h.G * 16);
+        for (int threads : {512, 256}) {
+          unsigned long long tt[2]; float best = 1e9; unsigned long long bc = 0;
+          for (int rep = 0; rep < 3; ++rep) {
+            sweep12<TA,TB,16><<<1, threads, smem>>>(sd, ddinv, n, r, out, t, 4, tsg);
+            cudaDeviceSynchronize(); cudaMemcpy(tt, t, 16, cudaMemcpyDeviceToHost);
+            if (tt[1]*1e-3 < best) { best = tt[1]*1e-3; bc = tt[0]; }
+          }
+          std::vector<long long> hh(h.G*2); cudaMemcpy(hh.data(), tsg, hh.size()*8, cudaMemcpyDeviceToHost);
+          double a=0, wsum=0; for (int g = 0; g < h.G; ++g) { a += hh[g*2]; wsum += hh[g*2+1]; }
+          cudaMemcpy(o2.data(), out, n*8, cudaMemcpyDeviceToHost);
+          double md = 0; for (int i = 0; i < n; ++i) md = std::max(md, std::abs(o1[i]-o2[i])/std::max(1e-300,std::abs(o1[i])));
+          printf("v12 TA=%d TB=%d D=%d (TAm=%d TBm=%d) threads=%d: %.1f us/sweep cyc/level=%.0f [main iter %.0f, ready-wait %.0f] maxrel=%.1e err=%s\n", TA, TB, D, h.TAm, h.TBm, threads, best, bc/(double)f.n_levels, a/h.G, wsum/h.G, md, cudaGetErrorString(cudaGetLastError()));
+        }
+      };
+      runv12(std::integral_constant<int,8>(), std::integral_constant<int,4>(), 6);
+      runv12(std::integral_constant<int,16>(), std::integral_constant<int,4>(), 10);
+      runv12(std::integral_constant<int,4>(), std::integral_constant<int,4>(), 4);
+    }
+
+    {
+      std::vector<double> dinvh(n); for (int i = 0; i < n; ++i) dinvh[i] = 1.0 / f.diag[i];
+      double* ddinv = up(dinvh);
+      H10 h = build10<8, 4>(f, 6, true);
+      S10d sd{h.G, up(h.nr), up(h.need), up(h.amax), up(h.bmax), up(h.grows), up(h.pw), up(h.pcols), up(h.acol), up(h.bcol), up(h.bsrc), up(h.pptr), up(h.pvals), up(h.aval), up(h.bval), up(f.diag)};
+      size_t smem = (n + 1) * 8 + R10*32*8*3 + R10*8*32*12 + R10*4*32*16 + R10*32*4 + 2*R10*4 + 64;
+      cudaFuncSetAttribute(sweep12<8,4,16,true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      long long* tsg; cudaMalloc(&tsg, h.G * 16);
+      for (int threads : {512, 32}) {
+        sweep12<8,4,16,true><<<1, threads, smem>>>(sd, ddinv, n, r, out, t, 2, tsg); cudaDeviceSynchronize();
+        std::vector<long long> hh(h.G*2); cudaMemcpy(hh.data(), tsg, hh.size()*8, cudaMemcpyDeviceToHost);
+        double a=0; for (int g = 0; g < h.G; ++g) a += hh[g*2];
+        printf("v12-ISO threads=%d main iter %.0f cycles err=%s\n", threads, a/h.G, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+
+    {
+      std::vector<double> dinvh(n); for (int i = 0; i < n; ++i) dinvh[i] = 1.0 / f.diag[i];
+      double* ddinv = up(dinvh);
+      auto runv13 = [&](auto TAc, auto TBc, int D) {
+        constexpr int TA = decltype(TAc)::value, TB = decltype(TBc)::value;
+        H10 h = build10<TA, TB>(f, D, true);
+        S10d sd{h.G, up(h.nr), up(h.need), up(h.amax), up(h.bmax), up(h.grows), up(h.pw), up(h.pcols), up(h.acol), up(h.bcol), up(h.bsrc), up(h.pptr), up(h.pvals), up(h.aval), up(h.bval), up(f.diag)};
+        size_t smem = (n + 1) * 8 + R10*32*8*3 + R10*TA*32*12 + R10*TB*32*16 + R10*32*4 + 2*R10*4 + 64;
+        cudaFuncSetAttribute(sweep13<TA,TB,16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(sweep13<TA,TB,16,true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        long long* tsg; cudaMalloc(&tsg, h.G * 16);
+        sweep13<TA,TB,16,true><<<1, 512, smem>>>(sd, ddinv, n, r, out, t, 2, tsg); cudaDeviceSynchronize();
+        { std::vector<long long> hh(h.G*2); cudaMemcpy(hh.data(), tsg, hh.size()*8, cudaMemcpyDeviceToHost);
+          double a=0; for (int g = 0; g < h.G; ++g) a += hh[g*2]; printf("v13-ISO TA=%d TB=%d main iter %.0f\n", TA, TB, a/h.G); }
+        for (int threads : {512, 256}) {
+          unsigned long long tt[2]; float best = 1e9; unsigned long long bc = 0;
+          for (int rep = 0; rep < 3; ++rep) {
+            sweep13<TA,TB,16><<<1, threads, smem>>>(sd, ddinv, n, r, out, t, 4, tsg);
+            cudaDeviceSynchronize(); cudaMemcpy(tt, t, 16, cudaMemcpyDeviceToHost);
+            if (tt[1]*1e-3 < best) { best = tt[1]*1e-3; bc = tt[0]; }
+          }
+          std::vector<long long> hh(h.G*2); cudaMemcpy(hh.data(), tsg, hh.size()*8, cudaMemcpyDeviceToHost);
+          double a=0; for (int g = 0; g < h.G; ++g) a += hh[g*2];
+          cudaMemcpy(o2.data(), out, n*8, cudaMemcpyDeviceToHost);
+          double md = 0; for (int i = 0; i < n; ++i) md = std::max(md, std::abs(o1[i]-o2[i])/std::max(1e-300,std::abs(o1[i])));
+          printf("v13 TA=%d TB=%d D=%d (TAm=%d TBm=%d) threads=%d: %.1f us/sweep cyc/level=%.0f [main iter %.0f] maxrel=%.1e err=%s\n", TA, TB, D, h.TAm, h.TBm, threads, best, bc/(double)f.n_levels, a/h.G, md, cudaGetErrorString(cudaGetLastError()));
+        }
+      };
+      runv13(std::integral_constant<int,8>(), std::integral_constant<int,4>(), 6);
+      runv13(std::integral_constant<int,16>(), std::integral_constant<int,4>(), 10);
+      runv13(std::integral_constant<int,8>(), std::integral_constant<int,2>(), 6);
+    }
+
+    {
+      std::vector<double> dinvh(n); for (int i = 0; i < n; ++i) dinvh[i] = 1.0 / f.diag[i];
+      double* ddinv = up(dinvh);
+      auto runv14 = [&](auto TAc, auto TBc, int D) {
+        constexpr int TA = decltype(TAc)::value, TB = decltype(TBc)::value;
+        H14 h = build14<TA, TB>(f, D);
+        S14d sd{h.G, up(h.nr), up(h.need), up(h.grows), up(h.pw), up(h.pcols), up(h.acol), up(h.bsrc), up(h.pptr), up(h.pvals), up(h.aval), up(h.bval), up(f.diag), ddinv};
+        size_t smem = (n + 1) * 8 + R10*32*8*3 + R10*TA*32*12 + R10*TB*32*12 + R10*32*4 + 2*R10*4 + 64;
+        cudaFuncSetAttribute(sweep14<TA,TB,16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(sweep14<TA,TB,16,true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        long long* tsg; cudaMalloc(&tsg, h.G * 8);
+        sweep14<TA,TB,16,true><<<1, 512, smem>>>(sd, n, r, out, t, 2, tsg); cudaDeviceSynchronize();
+        { std::vector<long long> hh(h.G); cudaMemcpy(hh.data(), tsg, hh.size()*8, cudaMemcpyDeviceToHost);
+          double a=0; for (int g = 0; g < h.G; ++g) a += hh[g]; printf("v14-ISO TA=%d TB=%d main iter %.0f\n", TA, TB, a/h.G); }
+        for (int threads : {512, 256}) {
+          unsigned long long tt[2]; float best = 1e9; unsigned long long bc = 0;
+          for (int rep = 0; rep < 3; ++rep) {
+            sweep14<TA,TB,16><<<1, threads, smem>>>(sd, n, r, out, t, 4, tsg);
+            cudaDeviceSynchronize(); cudaMemcpy(tt, t, 16, cudaMemcpyDeviceToHost);
+            if (tt[1]*1e-3 < best) { best = tt[1]*1e-3; bc = tt[0]; }
+          }
+          std::vector<long long> hh(h.G); cudaMemcpy(hh.data(), tsg, hh.size()*8, cudaMemcpyDeviceToHost);
+          double a=0; for (int g = 0; g < h.G; ++g) a += hh[g];
+          cudaMemcpy(o2.data(), out, n*8, cudaMemcpyDeviceToHost);
+          double md = 0; for (int i = 0; i < n; ++i) md = std::max(md, std::abs(o1[i]-o2[i])/std::max(1e-300,std::abs(o1[i])));
+          printf("v14 TA=%d TB=%d D=%d threads=%d: %.1f us/sweep cyc/level=%.0f [main iter %.0f] maxrel=%.1e err=%s\n", TA, TB, D, threads, best, bc/(double)f.n_levels, a/h.G, md, cudaGetErrorString(cudaGetLastError()));
+        }
+      };
+      runv14(std::integral_constant<int,8>(), std::integral_constant<int,4>(), 7);
+      runv14(std::integral_constant<int,12>(), std::integral_constant<int,4>(), 10);
+      runv14(std::integral_constant<int,6>(), std::integral_constant<int,4>(), 5);
     }
   }
   return 0;
