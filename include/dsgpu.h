@@ -137,6 +137,10 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms);
  * levels_fwd_A, levels_bwd_A, levels_fwd_Q, levels_bwd_Q, grid_ctas. */
 int dsgpu_info(const dsgpu_handle* h, int64_t* info);
 
+/* Process-wide sweep diagnostics (summed since the last reset):
+ * out4 = main-warp cycles, main cycles waiting for helper slots, groups, 0. */
+int dsgpu_debug_counters(int reset, int64_t* out4);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,16 +52,30 @@ struct HostSweep {
 // reductions (reassociated w.r.t. the reference's column order: results
 // agree to round-off); the factor and the operation are the
 // same. kTA / kTB are the per-lane register budgets for A and B entries.
-constexpr int kTA = 8, kTB = 4, kRing = 16, kFlowD = 7;
+constexpr int kTA = 8, kRing = 16, kFlowD = 7;
+// Supported per-lane B capacities (templates); the plan picks the smallest that fits.
+constexpr int kTBMax = 16;
+
+// Dependency form of one triangular sweep: row i computes
+//   y_i = (sum_j w_ij b_j - sum_k a_ik y_k) / d_i      (w_ii = 1 implied)
+// The plain sweep has no w entries; level merging (merge_levels) adds them.
+struct DepRows {
+  int n = 0;
+  std::vector<int> level;
+  std::vector<std::vector<std::pair<int, double>>> ent;  // a_ik
+  std::vector<std::vector<std::pair<int, double>>> w;    // w_ij, j != i
+  std::vector<double> diag;
+};
+
 struct HostFlow {
-  int n = 0, G = 0, n_levels = 0;
-  std::vector<int32_t> nr, need, pw, grows;  // per group (grows: G*32)
-  std::vector<int64_t> pptr;                 // G + 1, prefix entries (lane-interleaved, stride nr)
-  std::vector<int32_t> pcols;                // pad = n (a zero slot)
-  std::vector<double> pvals;
+  int n = 0, G = 0, n_levels = 0, tb = 4, merge = 1;
+  std::vector<int32_t> nr, need, pw, ww, grows;  // per group (grows: G*32)
+  std::vector<int64_t> pptr, wptr;           // G + 1, lane-interleaved (stride nr)
+  std::vector<int32_t> pcols, wcols;         // pad = n (a zero slot)
+  std::vector<double> pvals, wvals;
   std::vector<int32_t> acol;                 // G*kTA*32, pad = n
   std::vector<double> aval;
-  std::vector<int32_t> bsrc;                 // G*kTB*32: lane in group g-1 (pad 0 with value 0)
+  std::vector<int32_t> bsrc;                 // G*tb*32: lane in group g-1 (pad 0 with value 0)
   std::vector<double> bval;
   std::vector<double> diag, dinv;            // n
 };
@@ -100,7 +114,14 @@ void build_plan(HostPlan& plan, const dsgpu_csr* A, const dsgpu_csr* B, const ds
                 const dsgpu_csr* Q_filter);
 
 void build_sweeps(const dsgpu_csr& L, HostSweep& fwd, HostSweep& bwd);
-// Throws std::invalid_argument if a group needs more than kTB B entries.
-void build_flow(const HostSweep& s, HostFlow& f);
+DepRows rows_from_sweep(const HostSweep& s);
+// Exact algebraic merge of M consecutive dependency levels into one:
+// within each block, dependencies are substituted away (fill in a_ik, and a
+// right-hand-side transform w_ij over the block's rows). Depth / M.
+DepRows merge_levels(const DepRows& r, int M);
+// Largest number of B entries (dependencies on the previous group) of any row.
+int flow_b_needed(const DepRows& r);
+void build_flow(const DepRows& r, int tb, HostFlow& f);
+int build_block_flows(HostPlan& P, int merge, int* merge_used);
 
 }  // namespace dsgpu

@@ -263,11 +263,7 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
         }
       }
     }
-    if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
-      build_sweeps(*facs[b], hb.fwd, hb.bwd);
-      build_flow(hb.fwd, hb.ffwd);
-      build_flow(hb.bwd, hb.fbwd);
-    }
+    if (hb.kind == DSGPU_BLOCK_PCG_IC0) build_sweeps(*facs[b], hb.fwd, hb.bwd);
   }
 
   P.filter = false;
@@ -303,47 +299,158 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
 
 namespace dsgpu {
 
-// Staged sweep plan from the level-grouped SELL sweep (same groups, same
-// dependency levels; see HostFlow in dsgpu_internal.hpp).
-void build_flow(const HostSweep& s, HostFlow& f) {
-  const int n = s.n;
-  f = HostFlow{};
-  f.n = n;
-  f.G = s.n_groups;
-  f.n_levels = s.n_levels;
-  f.diag = s.diag;
-  f.dinv.resize(n);
-  for (int i = 0; i < n; ++i) f.dinv[i] = 1.0 / s.diag[i];
-  std::vector<int> gof(n, -1), lof(n, -1);
+// Dependency rows of a level-grouped SELL sweep.
+DepRows rows_from_sweep(const HostSweep& s) {
+  DepRows r;
+  r.n = s.n;
+  r.level.assign(s.n, 0);
+  r.ent.assign(s.n, {});
+  r.w.assign(s.n, {});
+  r.diag = s.diag;
   for (int g = 0; g < s.n_groups; ++g)
     for (int l = 0; l < kLanes; ++l) {
-      const int r = s.grows[static_cast<size_t>(g) * kLanes + l];
-      if (r >= 0) {
-        gof[r] = g;
-        lof[r] = l;
+      const int row = s.grows[static_cast<size_t>(g) * kLanes + l];
+      if (row < 0) continue;
+      for (int k = 0; k < s.gwidth[g]; ++k) {
+        const int64_t at = s.gptr[g] + static_cast<int64_t>(k) * kLanes + l;
+        if (s.cols[at] >= 0) r.ent[row].emplace_back(s.cols[at], s.vals[at]);
       }
     }
+  // levels in dependency order (rows of a group's lanes all share a level)
+  int lv = 0;
+  for (int g = 0; g < s.n_groups; ++g) {
+    for (int l = 0; l < kLanes; ++l) {
+      const int row = s.grows[static_cast<size_t>(g) * kLanes + l];
+      if (row < 0) continue;
+      int v = 0;
+      for (const auto& e : r.ent[row]) v = std::max(v, r.level[e.first] + 1);
+      r.level[row] = v;
+      lv = std::max(lv, v);
+    }
+  }
+  return r;
+}
+
+DepRows merge_levels(const DepRows& in, int M) {
+  if (M <= 1) return in;
+  const int n = in.n;
+  DepRows out;
+  out.n = n;
+  out.diag = in.diag;
+  out.level.resize(n);
+  for (int i = 0; i < n; ++i) out.level[i] = in.level[i] / M;
+  out.ent.assign(n, {});
+  out.w.assign(n, {});
+  // rows in original level order, so every in-block dependency is final first
+  std::vector<int> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return in.level[a] < in.level[b]; });
+  std::vector<double> acc_a(n, 0.0), acc_w(n, 0.0);
+  std::vector<char> has_a(n, 0), has_w(n, 0);
+  std::vector<int> list_a, list_w;
+  for (const int i : order) {
+    const int blk = out.level[i];
+    list_a.clear();
+    list_w.clear();
+    auto add_a = [&](int k, double v) {
+      if (!has_a[k]) { has_a[k] = 1; acc_a[k] = 0.0; list_a.push_back(k); }
+      acc_a[k] += v;
+    };
+    auto add_w = [&](int j, double v) {
+      if (!has_w[j]) { has_w[j] = 1; acc_w[j] = 0.0; list_w.push_back(j); }
+      acc_w[j] += v;
+    };
+    for (const auto& e : in.ent[i]) {
+      const int j = e.first;
+      if (out.level[j] == blk) {
+        // substitute y_j = (b_j + sum w_jl b_l - sum a'_jk y_k) / d_j
+        const double c = e.second / in.diag[j];
+        add_w(j, -c);
+        for (const auto& x : out.w[j]) add_w(x.first, -c * x.second);
+        for (const auto& x : out.ent[j]) add_a(x.first, -c * x.second);
+      } else {
+        add_a(j, e.second);
+      }
+    }
+    for (const int k : list_a) {
+      out.ent[i].emplace_back(k, acc_a[k]);
+      has_a[k] = 0;
+    }
+    for (const int j : list_w) {
+      out.w[i].emplace_back(j, acc_w[j]);
+      has_w[j] = 0;
+    }
+  }
+  return out;
+}
+
+namespace {
+// groups: rows of one level, <= 32 per group, ascending row index
+void make_groups(const DepRows& r, std::vector<int>& gof, std::vector<int>& lof,
+                 std::vector<std::vector<int>>& groups) {
+  const int n = r.n;
+  int L = 0;
+  for (int i = 0; i < n; ++i) L = std::max(L, r.level[i] + 1);
+  std::vector<std::vector<int>> by(L);
+  for (int i = 0; i < n; ++i) by[r.level[i]].push_back(i);
+  groups.clear();
+  gof.assign(n, -1);
+  lof.assign(n, -1);
+  for (int l = 0; l < L; ++l)
+    for (size_t a = 0; a < by[l].size(); a += kLanes) {
+      groups.emplace_back();
+      for (size_t t = a; t < std::min(by[l].size(), a + kLanes); ++t) {
+        gof[by[l][t]] = static_cast<int>(groups.size()) - 1;
+        lof[by[l][t]] = static_cast<int>(t - a);
+        groups.back().push_back(by[l][t]);
+      }
+    }
+}
+}  // namespace
+
+int flow_b_needed(const DepRows& r) {
+  std::vector<int> gof, lof;
+  std::vector<std::vector<int>> groups;
+  make_groups(r, gof, lof, groups);
+  int need = 0;
+  for (int i = 0; i < r.n; ++i) {
+    int c = 0;
+    for (const auto& e : r.ent[i]) c += gof[e.first] == gof[i] - 1;
+    need = std::max(need, c);
+  }
+  return need;
+}
+
+// Staged sweep plan (see HostFlow in dsgpu_internal.hpp).
+void build_flow(const DepRows& r, int tb, HostFlow& f) {
+  const int n = r.n;
+  f = HostFlow{};
+  f.n = n;
+  f.tb = tb;
+  f.diag = r.diag;
+  f.dinv.resize(n);
+  for (int i = 0; i < n; ++i) f.dinv[i] = 1.0 / r.diag[i];
+  std::vector<int> gof, lof;
+  std::vector<std::vector<int>> groups;
+  make_groups(r, gof, lof, groups);
+  f.G = static_cast<int>(groups.size());
+  for (int i = 0; i < n; ++i) f.n_levels = std::max(f.n_levels, r.level[i] + 1);
   f.pptr.assign(1, 0);
+  f.wptr.assign(1, 0);
   f.acol.assign(static_cast<size_t>(f.G) * kTA * kLanes, n);
   f.aval.assign(f.acol.size(), 0.0);
-  f.bsrc.assign(static_cast<size_t>(f.G) * kTB * kLanes, 0);
+  f.bsrc.assign(static_cast<size_t>(f.G) * tb * kLanes, 0);
   f.bval.assign(f.bsrc.size(), 0.0);
   std::vector<std::pair<int, double>> P[kLanes], A[kLanes], B[kLanes];
-  for (int g = 0; g < s.n_groups; ++g) {
-    int nr = 0;
-    for (int l = 0; l < kLanes; ++l)
-      if (s.grows[static_cast<size_t>(g) * kLanes + l] >= 0) nr = l + 1;
-    int pw = 0, need = -1;
+  for (int g = 0; g < f.G; ++g) {
+    const std::vector<int>& rows = groups[g];
+    const int nr = static_cast<int>(rows.size());
+    int pw = 0, need = -1, ww = 0;
     for (int l = 0; l < nr; ++l) {
       P[l].clear();
       A[l].clear();
       B[l].clear();
-      std::vector<std::pair<int, double>> e;
-      for (int k = 0; k < s.gwidth[g]; ++k) {
-        const int64_t at = s.gptr[g] + static_cast<int64_t>(k) * kLanes + l;
-        if (s.cols[at] >= 0) e.emplace_back(s.cols[at], s.vals[at]);
-      }
-      // dependency-level order (oldest first), stable
+      std::vector<std::pair<int, double>> e = r.ent[rows[l]];
       std::stable_sort(e.begin(), e.end(),
                        [&](const auto& a, const auto& b) { return gof[a.first] < gof[b.first]; });
       for (const auto& x : e) {
@@ -359,23 +466,31 @@ void build_flow(const HostSweep& s, HostFlow& f) {
         P[l].push_back(A[l].front());
         A[l].erase(A[l].begin());
       }
-      if (static_cast<int>(B[l].size()) > kTB)
-        throw std::invalid_argument("flow sweep: a row depends on more than " +
-                                    std::to_string(kTB) + " rows of the previous group");
+      if (static_cast<int>(B[l].size()) > tb)
+        throw std::invalid_argument("flow sweep: B capacity exceeded");
       for (const auto& x : P[l]) need = std::max(need, gof[x.first]);
       pw = std::max(pw, static_cast<int>(P[l].size()));
+      ww = std::max(ww, static_cast<int>(r.w[rows[l]].size()));
     }
     f.nr.push_back(nr);
     f.need.push_back(need);
     f.pw.push_back(pw);
-    for (int l = 0; l < kLanes; ++l) f.grows.push_back(s.grows[static_cast<size_t>(g) * kLanes + l]);
-    const int64_t pb = f.pptr.back();
+    f.ww.push_back(ww);
+    for (int l = 0; l < kLanes; ++l) f.grows.push_back(l < nr ? rows[l] : -1);
+    const int64_t pb = f.pptr.back(), wb = f.wptr.back();
     f.pcols.resize(pb + static_cast<int64_t>(pw) * nr, n);
     f.pvals.resize(pb + static_cast<int64_t>(pw) * nr, 0.0);
+    f.wcols.resize(wb + static_cast<int64_t>(ww) * nr, n);
+    f.wvals.resize(wb + static_cast<int64_t>(ww) * nr, 0.0);
     for (int l = 0; l < nr; ++l) {
       for (size_t k = 0; k < P[l].size(); ++k) {
         f.pcols[pb + static_cast<int64_t>(k) * nr + l] = P[l][k].first;
         f.pvals[pb + static_cast<int64_t>(k) * nr + l] = P[l][k].second;
+      }
+      const auto& wl = r.w[rows[l]];
+      for (size_t k = 0; k < wl.size(); ++k) {
+        f.wcols[wb + static_cast<int64_t>(k) * nr + l] = wl[k].first;
+        f.wvals[wb + static_cast<int64_t>(k) * nr + l] = wl[k].second;
       }
       for (size_t k = 0; k < A[l].size(); ++k) {
         const size_t at = (static_cast<size_t>(g) * kTA + k) * kLanes + l;
@@ -383,12 +498,39 @@ void build_flow(const HostSweep& s, HostFlow& f) {
         f.aval[at] = A[l][k].second;
       }
       for (size_t k = 0; k < B[l].size(); ++k) {
-        const size_t at = (static_cast<size_t>(g) * kTB + k) * kLanes + l;
+        const size_t at = (static_cast<size_t>(g) * tb + k) * kLanes + l;
         f.bsrc[at] = lof[B[l][k].first];
         f.bval[at] = B[l][k].second;
       }
     }
     f.pptr.push_back(pb + static_cast<int64_t>(pw) * nr);
+    f.wptr.push_back(wb + static_cast<int64_t>(ww) * nr);
+  }
+}
+
+// Staged plans for every IC(0) block with one shared B capacity; lowers the
+// merge factor until the B entries fit kTBMax. Returns the capacity used.
+int build_block_flows(HostPlan& P, int merge, int* merge_used) {
+  for (int M = std::max(1, merge);; M = M > 1 ? M / 2 : 0) {
+    if (M == 0) throw std::invalid_argument("flow sweep: dependency fan-in too large");
+    DepRows rows[2][2];
+    int need = 1;
+    for (int b = 0; b < 2; ++b) {
+      if (P.blk[b].kind != DSGPU_BLOCK_PCG_IC0) continue;
+      rows[b][0] = merge_levels(rows_from_sweep(P.blk[b].fwd), M);
+      rows[b][1] = merge_levels(rows_from_sweep(P.blk[b].bwd), M);
+      need = std::max({need, flow_b_needed(rows[b][0]), flow_b_needed(rows[b][1])});
+    }
+    if (need > kTBMax) continue;
+    const int tb = need <= 4 ? 4 : need <= 8 ? 8 : 16;
+    for (int b = 0; b < 2; ++b) {
+      if (P.blk[b].kind != DSGPU_BLOCK_PCG_IC0) continue;
+      build_flow(rows[b][0], tb, P.blk[b].ffwd);
+      build_flow(rows[b][1], tb, P.blk[b].fbwd);
+      P.blk[b].ffwd.merge = P.blk[b].fbwd.merge = M;
+    }
+    if (merge_used) *merge_used = M;
+    return tb;
   }
 }
 

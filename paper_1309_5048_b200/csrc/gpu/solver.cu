@@ -39,6 +39,7 @@ using namespace dsgpu::dev;
 namespace {
 
 constexpr int kThreads = 512;
+constexpr int kDefaultMerge = 1;
 constexpr int kWarps = kThreads / 32;
 
 enum Slot { SL_BB = 0, SL_RES, SL_ALPHA, SL_RHO0, SL_RHO1, SL_KAP0, SL_KAP1, SL_ZR0, SL_ZR1, SL_NUM, NSLOT };
@@ -55,9 +56,9 @@ struct DSweep {
 
 struct DFlow {
   int G;
-  const int32_t *nr, *need, *pw, *grows, *pcols, *acol, *bsrc;
-  const int64_t* pptr;
-  const double *pvals, *aval, *bval, *diag, *dinv;
+  const int32_t *nr, *need, *pw, *ww, *grows, *pcols, *wcols, *acol, *bsrc;
+  const int64_t *pptr, *wptr;
+  const double *pvals, *wvals, *aval, *bval, *diag, *dinv;
 };
 
 struct DBlock {
@@ -71,7 +72,8 @@ struct DBlock {
   DFlow ffwd, fbwd;   // staged sweeps (production)
   int exact;          // 1: use the exact sweeps
   double *r, *z, *q, *p0, *p1;  // PCG work (block-local, length n)
-  double* y;                    // forward-sweep result (staged mode)
+  double* y;                    // forward-sweep result (staged mode), n + 1 (y[n] = 0)
+  double* bb;                   // materialized right-hand side (staged mode), n + 1
 };
 
 struct DevReport {
@@ -176,6 +178,7 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
   return out;
 }
 
+template <int TB>
 struct FlowSmem {
   double* xs;
   double *psum, *dg, *di, *av, *bv;
@@ -190,21 +193,26 @@ struct FlowSmem {
     di = dg + kRing * 32;
     av = di + kRing * 32;
     bv = av + kRing * kTA * 32;
-    ac = reinterpret_cast<int*>(bv + kRing * kTB * 32);
+    ac = reinterpret_cast<int*>(bv + kRing * TB * 32);
     bsr = ac + kRing * kTA * 32;
-    rows = bsr + kRing * kTB * 32;
+    rows = bsr + kRing * TB * 32;
     ready = rows + kRing * 32;
     snr = const_cast<int*>(ready) + kRing;
     progress = ready + 2 * kRing;
   }
   static constexpr size_t ring_bytes() {
-    return static_cast<size_t>(kRing) * 32 * (3 * 8 + kTA * 12 + kTB * 12 + 4) + 3 * kRing * 4 + 64;
+    return static_cast<size_t>(kRing) * 32 * (3 * 8 + kTA * 12 + TB * 12 + 4) + 3 * kRing * 4 + 64;
   }
 };
 
-template <class Rhs>
-__device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigned* abort_flag) {
-  FlowSmem S(smem, n);
+// diagnostics: [0] main-warp cycles, [1] main cycles waiting for helper slots,
+// [2] groups processed by the main warp (summed over sweeps)
+__device__ unsigned long long g_flow_dbg[4];
+
+template <int TB>
+__device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __restrict__ b,
+                           unsigned* abort_flag) {
+  FlowSmem<TB> S(smem, n);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = threadIdx.x; i < kRing; i += blockDim.x) S.ready[i] = -1;
   if (threadIdx.x == 0) {
@@ -224,9 +232,11 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigne
     double xprev = 0.0;
     double acc_pre, d, dv;
     int row, nr;
-    double bvl[kTB];
-    int bsl[kTB];
+    double bvl[TB];
+    int bsl[TB];
     long long t0 = clock64();
+    const long long t_main0 = t0;
+    long long wait_cyc = 0;
     {  // group 0
       while (S.ready[0] != 0) {
         if (clock64() - t0 > kSpinTimeoutCycles) { atomicExch(abort_flag, 1u); break; }
@@ -240,16 +250,16 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigne
       for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(S.av[k * 32 + lane], S.xs[S.ac[k * 32 + lane]]);
       acc_pre = sub_rn(S.psum[lane], tree_sum<kTA>(pa));
 #pragma unroll
-      for (int k = 0; k < kTB; ++k) {
+      for (int k = 0; k < TB; ++k) {
         bsl[k] = S.bsr[k * 32 + lane];
         bvl[k] = S.bv[k * 32 + lane];
       }
     }
     for (int g = 0; g < s.G; ++g) {
       // (1) B(g) shuffles from the previous group's results
-      double sx[kTB];
+      double sx[TB];
 #pragma unroll
-      for (int k = 0; k < kTB; ++k) sx[k] = shfl_d(xprev, bsl[k]);
+      for (int k = 0; k < TB; ++k) sx[k] = shfl_d(xprev, bsl[k]);
       asm volatile("" ::: "memory");
       // (2) next group's slot (its A entries depend on groups <= g-1: ready)
       const int g1 = g + 1 < s.G ? g + 1 : g;
@@ -259,28 +269,29 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigne
         while (S.ready[sl] != g1) {
           if (clock64() - t0 > kSpinTimeoutCycles) { atomicExch(abort_flag, 1u); break; }
         }
+        wait_cyc += clock64() - t0;
       }
       const int nr1 = S.snr[sl];
       const double ps1 = S.psum[sl * 32 + lane];
       const double d1 = S.dg[sl * 32 + lane], dv1 = S.di[sl * 32 + lane];
       const int row1 = S.rows[sl * 32 + lane];
-      double avl[kTA], axv[kTA], bvl1[kTB];
-      int bsl1[kTB];
+      double avl[kTA], axv[kTA], bvl1[TB];
+      int bsl1[TB];
 #pragma unroll
       for (int k = 0; k < kTA; ++k) {
         avl[k] = S.av[(sl * kTA + k) * 32 + lane];
         axv[k] = S.xs[S.ac[(sl * kTA + k) * 32 + lane]];
       }
 #pragma unroll
-      for (int k = 0; k < kTB; ++k) {
-        bsl1[k] = S.bsr[(sl * kTB + k) * 32 + lane];
-        bvl1[k] = S.bv[(sl * kTB + k) * 32 + lane];
+      for (int k = 0; k < TB; ++k) {
+        bsl1[k] = S.bsr[(sl * TB + k) * 32 + lane];
+        bvl1[k] = S.bv[(sl * TB + k) * 32 + lane];
       }
       // (3) B(g): the critical chain
-      double pb[kTB];
+      double pb[TB];
 #pragma unroll
-      for (int k = 0; k < kTB; ++k) pb[k] = mul_rn(bvl[k], sx[k]);
-      const double acc = sub_rn(acc_pre, tree_sum<kTB>(pb));
+      for (int k = 0; k < TB; ++k) pb[k] = mul_rn(bvl[k], sx[k]);
+      const double acc = sub_rn(acc_pre, tree_sum<TB>(pb));
       // correctly rounded acc / d from the reciprocal (one Markstein step)
       const double q0 = mul_rn(acc, dv);
       const double rr = fma(-q0, d, acc);
@@ -299,10 +310,15 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigne
       row = row1;
       nr = nr1;
 #pragma unroll
-      for (int k = 0; k < kTB; ++k) {
+      for (int k = 0; k < TB; ++k) {
         bsl[k] = bsl1[k];
         bvl[k] = bvl1[k];
       }
+    }
+    if (lane == 0) {
+      atomicAdd(&g_flow_dbg[0], static_cast<unsigned long long>(clock64() - t_main0));
+      atomicAdd(&g_flow_dbg[1], static_cast<unsigned long long>(wait_cyc));
+      atomicAdd(&g_flow_dbg[2], static_cast<unsigned long long>(s.G));
     }
   } else if (hid >= 0) {
     constexpr int PW = 16;
@@ -334,17 +350,17 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigne
         ddi = __ldg(s.dinv + row);
       }
       int acl[kTA];
-      double avl[kTA], bvl[kTB];
-      int bsl[kTB];
+      double avl[kTA], bvl[TB];
+      int bsl[TB];
 #pragma unroll
       for (int k = 0; k < kTA; ++k) {
         acl[k] = __ldg(s.acol + (static_cast<int64_t>(g) * kTA + k) * 32 + lane);
         avl[k] = __ldg(s.aval + (static_cast<int64_t>(g) * kTA + k) * 32 + lane);
       }
 #pragma unroll
-      for (int k = 0; k < kTB; ++k) {
-        bvl[k] = __ldg(s.bval + (static_cast<int64_t>(g) * kTB + k) * 32 + lane);
-        bsl[k] = __ldg(s.bsrc + (static_cast<int64_t>(g) * kTB + k) * 32 + lane);
+      for (int k = 0; k < TB; ++k) {
+        bvl[k] = __ldg(s.bval + (static_cast<int64_t>(g) * TB + k) * 32 + lane);
+        bsl[k] = __ldg(s.bsrc + (static_cast<int64_t>(g) * TB + k) * 32 + lane);
       }
       const int32_t* cp = s.pcols + pb0 + lane;
       const double* vp = s.pvals + pb0 + lane;
@@ -380,7 +396,17 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigne
             break;
           }
         }
-      const double acc = lane < nr ? sub_rn(rhs(row), part) : 0.0;
+      double rhs = 0.0;
+      if (lane < nr) {
+        const int ww = __ldg(s.ww + g);
+        const int64_t wb = __ldg(s.wptr + g);
+        rhs = b[row];
+        for (int k = 0; k < ww; ++k) {  // level-merge right-hand-side transform
+          const int j = __ldg(s.wcols + wb + static_cast<int64_t>(k) * nr + lane);
+          rhs = add_rn(rhs, mul_rn(__ldg(s.wvals + wb + static_cast<int64_t>(k) * nr + lane), b[j]));
+        }
+      }
+      const double acc = lane < nr ? sub_rn(rhs, part) : 0.0;
       // slot reuse: the main warp must be past group g - kRing + 1
       while (*S.progress < g - kRing + 2) {
         __nanosleep(20);
@@ -399,9 +425,9 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigne
         S.av[(sl * kTA + k) * 32 + lane] = avl[k];
       }
 #pragma unroll
-      for (int k = 0; k < kTB; ++k) {
-        S.bv[(sl * kTB + k) * 32 + lane] = bvl[k];
-        S.bsr[(sl * kTB + k) * 32 + lane] = bsl[k];
+      for (int k = 0; k < TB; ++k) {
+        S.bv[(sl * TB + k) * 32 + lane] = bvl[k];
+        S.bsr[(sl * TB + k) * 32 + lane] = bsl[k];
       }
       __syncwarp();
       if (lane == 0) {
@@ -420,7 +446,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, Rhs rhs, unsigne
 
 // IC(0) apply z = (L L^T)^{-1} r (Ic0Factor::solve) in one CTA; returns the
 // CTA sum of r_i z_i in warp 0. rhs(row) yields r_row (and may write it).
-template <class Rhs>
+template <int TB, class Rhs>
 __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, double* red,
                            unsigned* abort_flag) {
   double* z = B.z;
@@ -437,12 +463,15 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
         abort_flag);
     return block_sum(rz, red);
   }
-  // staged sweeps: xf is the shared-memory base of the flow workspace
-  flow_sweep(B.ffwd, B.n, xf, rhs, abort_flag);
+  // staged sweeps: materialize the right-hand side once (it may update r)
+  double* bb = B.bb;
+  for (int i = threadIdx.x; i < B.n; i += blockDim.x) bb[i] = rhs(i);
+  __syncthreads();
+  flow_sweep<TB>(B.ffwd, B.n, xf, bb, abort_flag);
   double* y = B.y;
   for (int i = threadIdx.x; i < B.n; i += blockDim.x) y[i] = xf[i];
   __syncthreads();
-  flow_sweep(B.fbwd, B.n, xf, [&](int row) { return y[row]; }, abort_flag);
+  flow_sweep<TB>(B.fbwd, B.n, xf, y, abort_flag);
   for (int i = threadIdx.x; i < B.n; i += blockDim.x) {
     const double zi = xf[i];
     z[i] = zi;
@@ -515,6 +544,7 @@ struct Ctx {
 // Preconditioner application z = M^{-1} rin (BlockDiagPreconditioner::apply,
 // precond.cpp:139-148). Writes zout (length n), returns the two guard dots
 // <z_b, r_b> in zr[] (identical in all CTAs). False on error.
+template <int TB>
 __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
                         long long inner[2], long long apps[2]) {
   const Args& a = C.a;
@@ -530,7 +560,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
       double* dst = in.dst;
       double* r = B.r;
       const int off = B.off;
-      rho_p[b] = ic_apply(
+      rho_p[b] = ic_apply<TB>(
           B,
           [&](int row) {
             const int i = off + row;
@@ -659,7 +689,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
         double* r = B.r;
         const double* q = B.q;
         const double na = -alpha[b];
-        rho_n[b] = ic_apply(
+        rho_n[b] = ic_apply<TB>(
             B,
             [&](int row) {
               const double ri = add_rn(r[row], mul_rn(na, q[row]));
@@ -729,6 +759,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
   return true;
 }
 
+template <int TB>
 __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
@@ -765,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
     double* free4 = a.rbuf[2];
     double* y = a.y;
     double zr[2];
-    if (!precond(C, Input{r1v, nullptr, 0.0, nullptr}, y, zr, inner, apps)) goto finish;
+    if (!precond<TB>(C, Input{r1v, nullptr, 0.0, nullptr}, y, zr, inner, apps)) goto finish;
     if (zr[0] < 0.0 || zr[1] < 0.0) {  // BlockDiagPreconditioner guards
       C.status = DSGPU_E_INDEFINITE_PRECOND;
       C.failed_block = zr[0] < 0.0 ? 0 : 1;
@@ -863,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
       }
       const double alfa = sums[SL_ALPHA];
       // ---- precond: r2_new = spare - (alfa/beta) r2;  y = M^{-1} r2_new ----
-      if (!precond(C, Input{spare, r2v, div_rn(-alfa, beta), spare}, y, zr, inner, apps))
+      if (!precond<TB>(C, Input{spare, r2v, div_rn(-alfa, beta), spare}, y, zr, inner, apps))
         goto finish;
       {
         double* nr1 = r2v;
@@ -939,12 +970,22 @@ finish:
 }
 
 // ---- standalone kernels (parity / microbenchmarks) -------------------------
+template <int TB>
 __global__ void __launch_bounds__(kThreads, 1)
     ic_apply_kernel(const __grid_constant__ DBlock B, const double* r, unsigned* abort_flag) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
   // B.r = r (input), B.z = output, B.y = forward-sweep scratch (set by the host)
-  ic_apply(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag);
+  ic_apply<TB>(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag);
+}
+
+using MinresFn = void (*)(Args);
+using IcFn = void (*)(DBlock, const double*, unsigned*);
+MinresFn minres_for(int tb) {
+  return tb <= 4 ? minres_kernel<4> : tb <= 8 ? minres_kernel<8> : minres_kernel<16>;
+}
+IcFn ic_for(int tb) {
+  return tb <= 4 ? ic_apply_kernel<4> : tb <= 8 ? ic_apply_kernel<8> : ic_apply_kernel<16>;
 }
 
 // y = M x, warp per row; na != nullptr limits each row to its first na[i] entries
@@ -996,6 +1037,7 @@ struct dsgpu_handle {
   DevReport* d_rep = nullptr;
   int64_t nnz_k = 0, nnz_a = 0, nnz_l[2] = {0, 0}, nnz_q = 0;
   bool exact = false;
+  int tb = 4, merge = 1;
 
   template <class T>
   T* alloc(size_t count) {
@@ -1047,6 +1089,10 @@ DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
   d.bsrc = h->upload(f.bsrc);
   d.pptr = h->upload(f.pptr);
   d.pvals = h->upload(f.pvals);
+  d.ww = h->upload(f.ww);
+  d.wptr = h->upload(f.wptr);
+  d.wcols = h->upload(f.wcols);
+  d.wvals = h->upload(f.wvals);
   d.aval = h->upload(f.aval);
   d.bval = h->upload(f.bval);
   d.diag = h->upload(f.diag);
@@ -1129,8 +1175,14 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     for (int b = 0; b < 2; ++b)
       if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0) nmax = std::max(nmax, P.blk[b].n);
     h->exact = std::getenv("DSGPU_EXACT") && std::atoi(std::getenv("DSGPU_EXACT")) != 0;
+    if (!h->exact && nmax > 0) {
+      const int merge = std::getenv("DSGPU_MERGE") ? std::atoi(std::getenv("DSGPU_MERGE")) : kDefaultMerge;
+      h->tb = build_block_flows(P, merge, &h->merge);
+    }
+    const size_t ring = static_cast<size_t>(kRing) * 32 * (3 * 8 + kTA * 12 + h->tb * 12 + 4) +
+                        3 * kRing * 4 + 64;
     h->smem = h->exact ? static_cast<size_t>(2) * nmax * sizeof(double)
-                       : static_cast<size_t>(nmax + 1) * sizeof(double) + FlowSmem::ring_bytes();
+                       : static_cast<size_t>(nmax + 1) * sizeof(double) + ring;
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const size_t static_smem = 1024;
@@ -1139,18 +1191,18 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
                   "IC(0) block too large for the shared-memory dataflow sweep in this build (n=" +
                       std::to_string(nmax) + ")");
     int rc = cuda_check(h,
-                        cudaFuncSetAttribute(minres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                        cudaFuncSetAttribute(minres_for(h->tb), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(h->smem)),
                         "cudaFuncSetAttribute");
     if (rc) return rc;
     rc = cuda_check(h,
-                    cudaFuncSetAttribute(ic_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    cudaFuncSetAttribute(ic_for(h->tb), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(h->smem)),
                     "cudaFuncSetAttribute");
     if (rc) return rc;
     int per_sm = 0;
     rc = cuda_check(h,
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minres_kernel, kThreads,
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minres_for(h->tb), kThreads,
                                                                   h->smem),
                     "occupancy");
     if (rc) return rc;
@@ -1211,7 +1263,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
           d.ffwd = upload_flow(h, hb.ffwd);
           d.fbwd = upload_flow(h, hb.fbwd);
         }
-        d.y = h->alloc<double>(hb.n);
+        d.y = h->alloc<double>(hb.n + 1);
+        d.bb = h->alloc<double>(hb.n + 1);
+        cudaMemset(d.y, 0, sizeof(double) * (hb.n + 1));
+        cudaMemset(d.bb, 0, sizeof(double) * (hb.n + 1));
       }
       d.r = h->alloc<double>(hb.n);
       d.z = h->alloc<double>(hb.n);
@@ -1300,7 +1355,7 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   cudaEventRecord(e0, h->stream);
   void* params[] = {&a};
   rc = cuda_check(h,
-                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_kernel), dim3(h->grid),
+                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_for(h->tb)), dim3(h->grid),
                                               dim3(kThreads), params, h->smem, h->stream),
                   "cooperative launch");
   cudaEventRecord(e1, h->stream);
@@ -1420,7 +1475,7 @@ int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z) {
   DBlock B = h->args.blk[block];
   B.r = d0;
   B.z = d1;
-  ic_apply_kernel<<<1, kThreads, h->smem, h->stream>>>(B, d0, h->args.bar + 64);
+  ic_for(h->tb)<<<1, kThreads, h->smem, h->stream>>>(B, d0, h->args.bar + 64);
   cudaMemcpyAsync(z, d1, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream);
   return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_ic0");
 }
@@ -1453,7 +1508,7 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
       DBlock B = a.blk[which - 1];
       B.r = d0;
       B.z = d1;
-      ic_apply_kernel<<<1, kThreads, h->smem, h->stream>>>(B, d0, a.bar + 64);
+      ic_for(h->tb)<<<1, kThreads, h->smem, h->stream>>>(B, d0, a.bar + 64);
     } else {
       const DBlock& B = a.blk[0];
       spmv_kernel<<<(B.n * 32 + 255) / 256, 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1);
@@ -1475,6 +1530,17 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
   cudaEventDestroy(e1);
   *ms = t / reps;
   return rc;
+}
+
+int dsgpu_debug_counters(int reset, int64_t* out4) {
+  unsigned long long v[4] = {0, 0, 0, 0};
+  cudaMemcpyFromSymbol(v, g_flow_dbg, sizeof(v));
+  for (int i = 0; i < 4; ++i) out4[i] = static_cast<int64_t>(v[i]);
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_flow_dbg, z, sizeof(z));
+  }
+  return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
 }
 
 int dsgpu_info(const dsgpu_handle* h, int64_t* info) {

@@ -1,0 +1,31 @@
+"""IC(0) apply time and solve time vs level-merge factor (DSGPU_MERGE)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from oracle import PortLib, CSR
+from paper_1309_5048_b200 import host, solver
+P = PortLib()
+k, n = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (2, 64)
+s = host.assemble("psi-mms", k, n)
+c = lambda m: CSR(m.n_rows, m.n_cols, m.row_ptr, m.cols, m.vals)
+for M in (1, 2, 4, 8):
+    os.environ["DSGPU_MERGE"] = str(M)
+    t0 = time.time()
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    ts = time.time() - t0
+    r = np.random.default_rng(0).standard_normal(s.n_u)
+    z = g.apply_ic0(0, r)
+    zr = P.ic0_solve(c(g.top.factor), r)
+    err = np.abs(z - zr).max() / np.abs(zr).max()
+    import ctypes as C
+    cnt = np.zeros(4, np.int64)
+    g.L.dsgpu_debug_counters.argtypes = [C.c_int, np.ctypeslib.ndpointer(dtype=np.int64)]
+    g.L.dsgpu_debug_counters(1, cnt)
+    ms = g.time_kernel(1, 10)
+    g.L.dsgpu_debug_counters(1, cnt)
+    print(f"   main cycles/group {cnt[0]/max(cnt[2],1):.0f}, waiting {cnt[1]/max(cnt[2],1):.0f}, groups/sweep {cnt[2]/22:.0f}")
+    out = []
+    for itol in (1e-1, 1e-8):
+        sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=itol), history=False)
+        out.append((sol.report.iterations, round(sol.report.mean_inner_top, 3), round(sol.report.wall_seconds * 1e3, 2)))
+    print(f"M={M}: setup {ts:.2f}s  IC apply {ms*1e3:.1f} us  maxrel {err:.1e}  solves (it, inner, ms) {out}", flush=True)
