@@ -67,8 +67,21 @@ struct DepRows {
   std::vector<double> diag;
 };
 
+// Byte layout of one group's static main-warp data, identical in HBM (one
+// contiguous block per group, copied by a TMA bulk copy) and in the shared-
+// memory ring slot: diag[32] f64 | dinv[32] f64 | aval[kTA][32] f64 |
+// bval[tb][32] f64 | rows[32] i32 | acol[kTA][32] i32 | bsrc[tb][32] i32 | nr.
+struct SlotLayout {
+  int diag, dinv, aval, bval, rows, acol, bsrc, nr, bytes;
+  constexpr explicit SlotLayout(int tb)
+      : diag(0), dinv(256), aval(512), bval(512 + 256 * kTA), rows(bval + 256 * tb),
+        acol(rows + 128), bsrc(acol + 128 * kTA), nr(bsrc + 128 * tb),
+        bytes(((nr + 4) + 15) / 16 * 16) {}
+};
+
 struct HostFlow {
   int n = 0, G = 0, n_levels = 0, tb = 4, merge = 1;
+  std::vector<uint8_t> stat;                 // G * SlotLayout(tb).bytes
   std::vector<int32_t> nr, need, pw, ww, grows;  // per group (grows: G*32)
   std::vector<int64_t> pptr, wptr;           // G + 1, lane-interleaved (stride nr)
   std::vector<int32_t> pcols, wcols;         // pad = n (a zero slot)

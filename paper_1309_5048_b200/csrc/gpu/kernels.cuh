@@ -15,7 +15,7 @@ namespace dev {
 
 constexpr unsigned long long kSentinel = 0xFFF4A11C0DEDBEEFull;  // "not yet computed" (a NaN payload)
 constexpr unsigned long long kCanonNaN = 0x7FF8000000000000ull;
-constexpr long long kSpinTimeoutCycles = 8000000000ll;  // ~4 s at 1.9 GHz: abort instead of hanging
+constexpr long long kSpinTimeoutCycles = 2000000000ll;  // ~1 s at 1.96 GHz: abort instead of hanging
 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -89,6 +89,36 @@ __device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, unsign
   __syncthreads();
   return ok_sh != 0;
 }
+
+// Bounded spin: expires after kSpinTimeoutCycles (sets the abort flag) or as
+// soon as another thread has aborted; the flag is only read after a short
+// grace period so the fast path stays free of global loads.
+struct SpinGuard {
+  long long t0;
+  unsigned* ab;
+  __device__ __forceinline__ explicit SpinGuard(unsigned* a) {
+#ifdef __CUDA_ARCH__
+    t0 = clock64();
+#else
+    t0 = 0;
+#endif
+    ab = a;
+  }
+  __device__ __forceinline__ bool expired() {
+#ifdef __CUDA_ARCH__
+    const long long dt = clock64() - t0;
+#else
+    const long long dt = 0;
+#endif
+    if (dt < (1ll << 16)) return false;
+    if (*reinterpret_cast<volatile unsigned*>(ab)) return true;
+    if (dt > kSpinTimeoutCycles) {
+      atomicExch(ab, 1u);
+      return true;
+    }
+    return false;
+  }
+};
 
 // ---- shared-memory dataflow slots for the triangular sweeps --------------
 __device__ __forceinline__ void slot_reset(double* xs, int i) {

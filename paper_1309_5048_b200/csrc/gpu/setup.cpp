@@ -2,6 +2,7 @@
 // operator, the block operators and the level-grouped triangular sweeps.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -505,6 +506,31 @@ void build_flow(const DepRows& r, int tb, HostFlow& f) {
     }
     f.pptr.push_back(pb + static_cast<int64_t>(pw) * nr);
     f.wptr.push_back(wb + static_cast<int64_t>(ww) * nr);
+  }
+  // pre-formatted static slot blocks (TMA bulk-copied into the ring)
+  const SlotLayout lay(tb);
+  f.stat.assign(static_cast<size_t>(f.G) * lay.bytes, 0);
+  for (int g = 0; g < f.G; ++g) {
+    uint8_t* blk = f.stat.data() + static_cast<size_t>(g) * lay.bytes;
+    auto put_d = [&](int off, int idx, double v) { std::memcpy(blk + off + 8 * idx, &v, 8); };
+    auto put_i = [&](int off, int idx, int32_t v) { std::memcpy(blk + off + 4 * idx, &v, 4); };
+    for (int l = 0; l < kLanes; ++l) {
+      const int row = f.grows[static_cast<size_t>(g) * kLanes + l];
+      put_d(lay.diag, l, row >= 0 ? f.diag[row] : 1.0);
+      put_d(lay.dinv, l, row >= 0 ? f.dinv[row] : 1.0);
+      put_i(lay.rows, l, row);
+      for (int k = 0; k < kTA; ++k) {
+        const size_t at = (static_cast<size_t>(g) * kTA + k) * kLanes + l;
+        put_d(lay.aval, k * kLanes + l, f.aval[at]);
+        put_i(lay.acol, k * kLanes + l, f.acol[at]);
+      }
+      for (int k = 0; k < tb; ++k) {
+        const size_t at = (static_cast<size_t>(g) * tb + k) * kLanes + l;
+        put_d(lay.bval, k * kLanes + l, f.bval[at]);
+        put_i(lay.bsrc, k * kLanes + l, f.bsrc[at]);
+      }
+    }
+    put_i(lay.nr, 0, f.nr[g]);
   }
 }
 

@@ -59,6 +59,7 @@ struct DFlow {
   const int32_t *nr, *need, *pw, *ww, *grows, *pcols, *wcols, *acol, *bsrc;
   const int64_t *pptr, *wptr;
   const double *pvals, *wvals, *aval, *bval, *diag, *dinv;
+  const uint8_t* stat;  // G * SlotLayout(tb).bytes, 16-byte aligned
 };
 
 struct DBlock {
@@ -178,50 +179,98 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
   return out;
 }
 
-template <int TB>
+// ---- mbarrier / bulk-copy (TMA) helpers -----------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mb, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* mb, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+      : "=r"(ok)
+      : "r"(smem_u32(mb)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mb) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(mb))
+      : "memory");
+}
+
+// Shared-memory workspace of one staged sweep: xs[n+1] | ring of kRing static
+// slots (SlotLayout, filled by TMA bulk copies) | psum[kRing][32] | mbarriers
+// | psum flags | progress.
 struct FlowSmem {
   double* xs;
-  double *psum, *dg, *di, *av, *bv;
-  int *ac, *bsr, *rows;
-  volatile int* ready;
-  int* snr;
+  uint8_t* slots;
+  double* psum;
+  uint64_t* mbar;
+  volatile int* pready;
   volatile int* progress;
-  __device__ FlowSmem(double* base, int n) {
+  int* base_use;  // completed mbarrier phases per slot before this sweep
+  int slot_bytes;
+  __device__ FlowSmem(double* base, int n, int sb) : slot_bytes(sb) {
     xs = base;
-    psum = xs + n + 1;
-    dg = psum + kRing * 32;
-    di = dg + kRing * 32;
-    av = di + kRing * 32;
-    bv = av + kRing * kTA * 32;
-    ac = reinterpret_cast<int*>(bv + kRing * TB * 32);
-    bsr = ac + kRing * kTA * 32;
-    rows = bsr + kRing * TB * 32;
-    ready = rows + kRing * 32;
-    snr = const_cast<int*>(ready) + kRing;
-    progress = ready + 2 * kRing;
+    const size_t xbytes = (static_cast<size_t>(n + 1) * 8 + 127) / 128 * 128;
+    slots = reinterpret_cast<uint8_t*>(base) + xbytes;
+    psum = reinterpret_cast<double*>(slots + static_cast<size_t>(kRing) * sb);
+    mbar = reinterpret_cast<uint64_t*>(psum + kRing * 32);
+    pready = reinterpret_cast<volatile int*>(mbar + kRing);
+    progress = pready + kRing;
+    base_use = const_cast<int*>(progress) + 1;
   }
-  static constexpr size_t ring_bytes() {
-    return static_cast<size_t>(kRing) * 32 * (3 * 8 + kTA * 12 + TB * 12 + 4) + 3 * kRing * 4 + 64;
+  static size_t bytes(int n, int sb) {
+    return (static_cast<size_t>(n + 1) * 8 + 127) / 128 * 128 + static_cast<size_t>(kRing) * sb +
+           kRing * 32 * 8 + kRing * 8 + 2 * kRing * 4 + 64;
   }
 };
 
-// diagnostics: [0] main-warp cycles, [1] main cycles waiting for helper slots,
+// Once per kernel launch and CTA, before any staged sweep: the ring's
+// mbarriers are initialized once and then only ever advance (re-initializing
+// an mbarrier the bulk-copy unit has used is not safe).
+template <int TB>
+__device__ void flow_setup(double* smem, int n) {
+  FlowSmem S(smem, n, SlotLayout(TB).bytes);
+  for (int i = threadIdx.x; i < kRing; i += blockDim.x) {
+    mbar_init(S.mbar + i, 1);
+    S.base_use[i] = 0;
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+}
+
+// diagnostics: [0] main-warp cycles, [1] main cycles waiting for slots,
 // [2] groups processed by the main warp (summed over sweeps)
 __device__ unsigned long long g_flow_dbg[4];
 
 template <int TB>
 __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __restrict__ b,
                            unsigned* abort_flag) {
-  FlowSmem<TB> S(smem, n);
+  const SlotLayout lay(TB);
+  FlowSmem S(smem, n, lay.bytes);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < kRing; i += blockDim.x) S.ready[i] = -1;
+  for (int i = threadIdx.x; i < kRing; i += blockDim.x) S.pready[i] = -1;
   if (threadIdx.x == 0) {
     *S.progress = 0;
     S.xs[n] = 0.0;
   }
   __syncthreads();
-  // main = last warp; helpers = warps not sharing the main warp's SM sub-partition
-  const int mainw = nw - 1;
+  // roles: main = last warp; producer = lane 0 of the warp 4 below it (same
+  // SM sub-partition, nearly idle); helpers = warps on the other three
+  // sub-partitions.
+  const int mainw = nw - 1, prodw = nw - 5;
   int hid = -1, nh = 0;
   for (int w = 0; w < nw; ++w)
     if (w != mainw && (w & 3) != (mainw & 3)) {
@@ -230,29 +279,50 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     }
   if (warp == mainw && s.G > 0) {
     double xprev = 0.0;
-    double acc_pre, d, dv;
-    int row, nr;
+    double acc_pre = 0.0, d = 1.0, dv = 1.0;
+    int row = -1, nr = 0;
     double bvl[TB];
     int bsl[TB];
-    long long t0 = clock64();
-    const long long t_main0 = t0;
+    const long long t_main0 = clock64();
     long long wait_cyc = 0;
-    {  // group 0
-      while (S.ready[0] != 0) {
-        if (clock64() - t0 > kSpinTimeoutCycles) { atomicExch(abort_flag, 1u); break; }
+    auto slot_wait = [&](int gg) {
+      const int sl = gg % kRing;
+      const unsigned par = (S.base_use[sl] + gg / kRing) & 1;
+      if (!mbar_test(S.mbar + sl, par) || S.pready[sl] != gg) {
+        SpinGuard sg(abort_flag);
+        while (!mbar_test(S.mbar + sl, par))
+          if (sg.expired()) {
+            g_flow_dbg[3] = 1000000000ull * 1 + 100000ull * s.G + gg;
+            break;
+          }
+        while (S.pready[sl] != gg)
+          if (sg.expired()) {
+            g_flow_dbg[3] = 1000000000ull * 2 + 100000ull * s.G + gg;
+            break;
+          }
+        wait_cyc += clock64() - sg.t0;
       }
-      nr = S.snr[0];
-      d = S.dg[lane];
-      dv = S.di[lane];
-      row = S.rows[lane];
+      return sl;
+    };
+    {  // group 0
+      const int sl = slot_wait(0);
+      const uint8_t* base = S.slots;
+      nr = *reinterpret_cast<const int*>(base + lay.nr);
+      d = reinterpret_cast<const double*>(base + lay.diag)[lane];
+      dv = reinterpret_cast<const double*>(base + lay.dinv)[lane];
+      row = reinterpret_cast<const int*>(base + lay.rows)[lane];
+      const double* av = reinterpret_cast<const double*>(base + lay.aval);
+      const int* ac = reinterpret_cast<const int*>(base + lay.acol);
       double pa[kTA];
 #pragma unroll
-      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(S.av[k * 32 + lane], S.xs[S.ac[k * 32 + lane]]);
-      acc_pre = sub_rn(S.psum[lane], tree_sum<kTA>(pa));
+      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(av[k * 32 + lane], S.xs[ac[k * 32 + lane]]);
+      acc_pre = sub_rn(S.psum[sl * 32 + lane], tree_sum<kTA>(pa));
+      const double* bv = reinterpret_cast<const double*>(base + lay.bval);
+      const int* bs = reinterpret_cast<const int*>(base + lay.bsrc);
 #pragma unroll
       for (int k = 0; k < TB; ++k) {
-        bsl[k] = S.bsr[k * 32 + lane];
-        bvl[k] = S.bv[k * 32 + lane];
+        bsl[k] = bs[k * 32 + lane];
+        bvl[k] = bv[k * 32 + lane];
       }
     }
     for (int g = 0; g < s.G; ++g) {
@@ -263,29 +333,28 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       asm volatile("" ::: "memory");
       // (2) next group's slot (its A entries depend on groups <= g-1: ready)
       const int g1 = g + 1 < s.G ? g + 1 : g;
-      const int sl = g1 % kRing;
-      if (S.ready[sl] != g1) {
-        t0 = clock64();
-        while (S.ready[sl] != g1) {
-          if (clock64() - t0 > kSpinTimeoutCycles) { atomicExch(abort_flag, 1u); break; }
-        }
-        wait_cyc += clock64() - t0;
-      }
-      const int nr1 = S.snr[sl];
+      const int sl = slot_wait(g1);
+      const uint8_t* base = S.slots + static_cast<size_t>(sl) * lay.bytes;
+      const int nr1 = *reinterpret_cast<const int*>(base + lay.nr);
       const double ps1 = S.psum[sl * 32 + lane];
-      const double d1 = S.dg[sl * 32 + lane], dv1 = S.di[sl * 32 + lane];
-      const int row1 = S.rows[sl * 32 + lane];
+      const double d1 = reinterpret_cast<const double*>(base + lay.diag)[lane];
+      const double dv1 = reinterpret_cast<const double*>(base + lay.dinv)[lane];
+      const int row1 = reinterpret_cast<const int*>(base + lay.rows)[lane];
+      const double* av = reinterpret_cast<const double*>(base + lay.aval);
+      const int* ac = reinterpret_cast<const int*>(base + lay.acol);
+      const double* bv = reinterpret_cast<const double*>(base + lay.bval);
+      const int* bs = reinterpret_cast<const int*>(base + lay.bsrc);
       double avl[kTA], axv[kTA], bvl1[TB];
       int bsl1[TB];
 #pragma unroll
       for (int k = 0; k < kTA; ++k) {
-        avl[k] = S.av[(sl * kTA + k) * 32 + lane];
-        axv[k] = S.xs[S.ac[(sl * kTA + k) * 32 + lane]];
+        avl[k] = av[k * 32 + lane];
+        axv[k] = S.xs[ac[k * 32 + lane]];
       }
 #pragma unroll
       for (int k = 0; k < TB; ++k) {
-        bsl1[k] = S.bsr[(sl * TB + k) * 32 + lane];
-        bvl1[k] = S.bv[(sl * TB + k) * 32 + lane];
+        bsl1[k] = bs[k * 32 + lane];
+        bvl1[k] = bv[k * 32 + lane];
       }
       // (3) B(g): the critical chain
       double pb[TB];
@@ -320,6 +389,25 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       atomicAdd(&g_flow_dbg[1], static_cast<unsigned long long>(wait_cyc));
       atomicAdd(&g_flow_dbg[2], static_cast<unsigned long long>(s.G));
     }
+  } else if (warp == prodw) {
+    if (lane == 0) {
+      for (int g = 0; g < s.G; ++g) {
+        const int sl = g % kRing;
+        // the slot's previous group (g - kRing) was loaded by main iteration g - kRing - 1
+        SpinGuard sg(abort_flag);
+        while (*S.progress < g - kRing + 2) {
+          __nanosleep(32);
+          if (sg.expired()) {
+            g_flow_dbg[3] = 1000000ull * (blockIdx.x + 1) + 1000ull * 3 + (g % 1000);
+            break;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(S.mbar + sl, lay.bytes);
+        bulk_g2s(S.slots + static_cast<size_t>(sl) * lay.bytes,
+                 s.stat + static_cast<size_t>(g) * lay.bytes, lay.bytes, S.mbar + sl);
+      }
+    }
   } else if (hid >= 0) {
     constexpr int PW = 16;
     int g = hid;
@@ -343,30 +431,22 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         pbn = __ldg(s.pptr + gn);
       }
       int row = -1;
-      double dd = 1.0, ddi = 1.0;
+      double rhs = 0.0;
       if (lane < nr) {
         row = __ldg(s.grows + static_cast<int64_t>(g) * 32 + lane);
-        dd = __ldg(s.diag + row);
-        ddi = __ldg(s.dinv + row);
-      }
-      int acl[kTA];
-      double avl[kTA], bvl[TB];
-      int bsl[TB];
-#pragma unroll
-      for (int k = 0; k < kTA; ++k) {
-        acl[k] = __ldg(s.acol + (static_cast<int64_t>(g) * kTA + k) * 32 + lane);
-        avl[k] = __ldg(s.aval + (static_cast<int64_t>(g) * kTA + k) * 32 + lane);
-      }
-#pragma unroll
-      for (int k = 0; k < TB; ++k) {
-        bvl[k] = __ldg(s.bval + (static_cast<int64_t>(g) * TB + k) * 32 + lane);
-        bsl[k] = __ldg(s.bsrc + (static_cast<int64_t>(g) * TB + k) * 32 + lane);
+        rhs = b[row];
+        const int ww = __ldg(s.ww + g);
+        const int64_t wb = __ldg(s.wptr + g);
+        for (int k = 0; k < ww; ++k) {  // level-merge right-hand-side transform
+          const int j = __ldg(s.wcols + wb + static_cast<int64_t>(k) * nr + lane);
+          rhs = add_rn(rhs, mul_rn(__ldg(s.wvals + wb + static_cast<int64_t>(k) * nr + lane), b[j]));
+        }
       }
       const int32_t* cp = s.pcols + pb0 + lane;
       const double* vp = s.pvals + pb0 + lane;
       double part = 0.0;
-      long long t0 = clock64();
-      for (int k0 = 0; k0 < pw; k0 += PW) {
+      SpinGuard sg(abort_flag);
+      for (int k0 = 0; k0 < pw || k0 == 0; k0 += PW) {
         int pc[PW];
         double pv[PW];
 #pragma unroll
@@ -378,8 +458,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         if (k0 == 0)
           while (*S.progress <= need) {
             __nanosleep(20);
-            if (clock64() - t0 > kSpinTimeoutCycles || *reinterpret_cast<volatile unsigned*>(abort_flag)) {
-              atomicExch(abort_flag, 1u);
+            if (sg.expired()) {
+              g_flow_dbg[3] = 1000000ull * (blockIdx.x + 1) + 1000ull * 4 + (g % 1000);
               break;
             }
           }
@@ -388,58 +468,31 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], S.xs[pc[q]]);
         part = add_rn(part, tree_sum<PW>(pp));
       }
-      if (pw == 0)
-        while (*S.progress <= need) {
-          __nanosleep(20);
-          if (clock64() - t0 > kSpinTimeoutCycles || *reinterpret_cast<volatile unsigned*>(abort_flag)) {
-            atomicExch(abort_flag, 1u);
-            break;
-          }
-        }
-      double rhs = 0.0;
-      if (lane < nr) {
-        const int ww = __ldg(s.ww + g);
-        const int64_t wb = __ldg(s.wptr + g);
-        rhs = b[row];
-        for (int k = 0; k < ww; ++k) {  // level-merge right-hand-side transform
-          const int j = __ldg(s.wcols + wb + static_cast<int64_t>(k) * nr + lane);
-          rhs = add_rn(rhs, mul_rn(__ldg(s.wvals + wb + static_cast<int64_t>(k) * nr + lane), b[j]));
-        }
-      }
       const double acc = lane < nr ? sub_rn(rhs, part) : 0.0;
-      // slot reuse: the main warp must be past group g - kRing + 1
+      // psum slot reuse: group g - kRing's psum was read by main iteration g - kRing - 1
       while (*S.progress < g - kRing + 2) {
         __nanosleep(20);
-        if (clock64() - t0 > kSpinTimeoutCycles || *reinterpret_cast<volatile unsigned*>(abort_flag)) {
-          atomicExch(abort_flag, 1u);
+        if (sg.expired()) {
+          g_flow_dbg[3] = 1000000ull * (blockIdx.x + 1) + 1000ull * 5 + (g % 1000);
           break;
         }
       }
       S.psum[sl * 32 + lane] = acc;
-      S.dg[sl * 32 + lane] = dd;
-      S.di[sl * 32 + lane] = ddi;
-      S.rows[sl * 32 + lane] = row;
-#pragma unroll
-      for (int k = 0; k < kTA; ++k) {
-        S.ac[(sl * kTA + k) * 32 + lane] = acl[k];
-        S.av[(sl * kTA + k) * 32 + lane] = avl[k];
-      }
-#pragma unroll
-      for (int k = 0; k < TB; ++k) {
-        S.bv[(sl * TB + k) * 32 + lane] = bvl[k];
-        S.bsr[(sl * TB + k) * 32 + lane] = bsl[k];
-      }
       __syncwarp();
       if (lane == 0) {
-        S.snr[sl] = nr;
         __threadfence_block();
-        S.ready[sl] = g;
+        S.pready[sl] = g;
       }
       nr = nrn;
       pw = pwn;
       need = needn;
       pb0 = pbn;
     }
+  }
+  __syncthreads();
+  if (threadIdx.x < kRing) {
+    const int sl = threadIdx.x;
+    if (s.G > sl) S.base_use[sl] += (s.G - 1 - sl) / kRing + 1;
   }
   __syncthreads();
 }
@@ -766,6 +819,9 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
   __shared__ double sums[NSLOT];
   Ctx C(a, red, sums, xs_dyn);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = 0; b < 2; ++b)
+    if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0 && !a.blk[b].exact && C.cta == a.blk[b].ic_cta)
+      flow_setup<TB>(xs_dyn, a.blk[b].n);
   const int r0 = C.r0, r1 = C.r1;
   long long inner[2] = {0, 0}, apps[2] = {0, 0};
   int iterations = 0, converged = 0, hist_len = 0;
@@ -976,6 +1032,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
   // B.r = r (input), B.z = output, B.y = forward-sweep scratch (set by the host)
+  if (!B.exact) flow_setup<TB>(xs_dyn, B.n);
   ic_apply<TB>(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag);
 }
 
@@ -1090,6 +1147,7 @@ DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
   d.pptr = h->upload(f.pptr);
   d.pvals = h->upload(f.pvals);
   d.ww = h->upload(f.ww);
+  d.stat = h->upload(f.stat);
   d.wptr = h->upload(f.wptr);
   d.wcols = h->upload(f.wcols);
   d.wvals = h->upload(f.wvals);
@@ -1179,10 +1237,8 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       const int merge = std::getenv("DSGPU_MERGE") ? std::atoi(std::getenv("DSGPU_MERGE")) : kDefaultMerge;
       h->tb = build_block_flows(P, merge, &h->merge);
     }
-    const size_t ring = static_cast<size_t>(kRing) * 32 * (3 * 8 + kTA * 12 + h->tb * 12 + 4) +
-                        3 * kRing * 4 + 64;
     h->smem = h->exact ? static_cast<size_t>(2) * nmax * sizeof(double)
-                       : static_cast<size_t>(nmax + 1) * sizeof(double) + ring;
+                       : FlowSmem::bytes(nmax, SlotLayout(h->tb).bytes);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const size_t static_smem = 1024;
