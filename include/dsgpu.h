@@ -140,6 +140,10 @@ int dsgpu_info(const dsgpu_handle* h, int64_t* info);
 /* Process-wide sweep diagnostics (summed since the last reset):
  * out4 = main-warp cycles, main cycles waiting for helper slots, groups, 0. */
 int dsgpu_debug_counters(int reset, int64_t* out4);
+/* Persistent-kernel phase diagnostics (cycles): out8 = CTA0 grid-barrier
+ * wait, CTA0 IC(0) apply, CTA2 grid-barrier wait, barriers, CTA0 kernel,
+ * CTA1 IC(0) apply, 0, 0. */
+int dsgpu_debug_phases(int reset, int64_t* out8);
 
 #ifdef __cplusplus
 }

@@ -216,7 +216,8 @@ struct FlowSmem {
   uint8_t* slots;
   double* psum;
   uint64_t* mbar;
-  volatile int* pready;
+  volatile int* pready;   // psum of group g staged (helpers)
+  volatile int* sready;   // static data of group g landed (producer, after its mbarrier)
   volatile int* progress;
   int* base_use;  // completed mbarrier phases per slot before this sweep
   int slot_bytes;
@@ -227,12 +228,13 @@ struct FlowSmem {
     psum = reinterpret_cast<double*>(slots + static_cast<size_t>(kRing) * sb);
     mbar = reinterpret_cast<uint64_t*>(psum + kRing * 32);
     pready = reinterpret_cast<volatile int*>(mbar + kRing);
-    progress = pready + kRing;
+    sready = pready + kRing;
+    progress = sready + kRing;
     base_use = const_cast<int*>(progress) + 1;
   }
   static size_t bytes(int n, int sb) {
     return (static_cast<size_t>(n + 1) * 8 + 127) / 128 * 128 + static_cast<size_t>(kRing) * sb +
-           kRing * 32 * 8 + kRing * 8 + 2 * kRing * 4 + 64;
+           kRing * 32 * 8 + kRing * 8 + 3 * kRing * 4 + 64;
   }
 };
 
@@ -254,6 +256,10 @@ __device__ void flow_setup(double* smem, int n) {
 // diagnostics: [0] main-warp cycles, [1] main cycles waiting for slots,
 // [2] groups processed by the main warp (summed over sweeps)
 __device__ unsigned long long g_flow_dbg[4];
+// phase diagnostics of the persistent kernel: [0] CTA0 cycles in grid barriers,
+// [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
+// [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
+__device__ unsigned long long g_phase_dbg[8];
 
 template <int TB>
 __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __restrict__ b,
@@ -261,7 +267,10 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
   const SlotLayout lay(TB);
   FlowSmem S(smem, n, lay.bytes);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < kRing; i += blockDim.x) S.pready[i] = -1;
+  for (int i = threadIdx.x; i < kRing; i += blockDim.x) {
+    S.pready[i] = -1;
+    S.sready[i] = -1;
+  }
   if (threadIdx.x == 0) {
     *S.progress = 0;
     S.xs[n] = 0.0;
@@ -285,12 +294,13 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     int bsl[TB];
     const long long t_main0 = clock64();
     long long wait_cyc = 0;
+    // readiness flags of the next group, prefetched one iteration ahead
+    int pf_p = -2, pf_s = -2;
     auto slot_wait = [&](int gg) {
       const int sl = gg % kRing;
-      const unsigned par = (S.base_use[sl] + gg / kRing) & 1;
-      if (!mbar_test(S.mbar + sl, par) || S.pready[sl] != gg) {
+      if (pf_p != gg || pf_s != gg) {
         SpinGuard sg(abort_flag);
-        while (!mbar_test(S.mbar + sl, par))
+        while (S.sready[sl] != gg)
           if (sg.expired()) {
             g_flow_dbg[3] = 1000000000ull * 1 + 100000ull * s.G + gg;
             break;
@@ -356,6 +366,11 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         bsl1[k] = bs[k * 32 + lane];
         bvl1[k] = bv[k * 32 + lane];
       }
+      {  // prefetch the readiness flags of group g+2 (consumed next iteration)
+        const int g2 = g + 2 < s.G ? g + 2 : g1;
+        pf_p = S.pready[g2 % kRing];
+        pf_s = S.sready[g2 % kRing];
+      }
       // (3) B(g): the critical chain
       double pb[TB];
 #pragma unroll
@@ -391,21 +406,38 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     }
   } else if (warp == prodw) {
     if (lane == 0) {
-      for (int g = 0; g < s.G; ++g) {
-        const int sl = g % kRing;
-        // the slot's previous group (g - kRing) was loaded by main iteration g - kRing - 1
-        SpinGuard sg(abort_flag);
-        while (*S.progress < g - kRing + 2) {
-          __nanosleep(32);
-          if (sg.expired()) {
-            g_flow_dbg[3] = 1000000ull * (blockIdx.x + 1) + 1000ull * 3 + (g % 1000);
-            break;
+      int issued = 0, done = 0;
+      SpinGuard sg(abort_flag);
+      while (done < s.G) {
+        bool idle = true;
+        // issue: the slot's previous group (issued - kRing) was loaded by main
+        // iteration issued - kRing - 1
+        if (issued < s.G && *S.progress >= issued - kRing + 2) {
+          const int sl = issued % kRing;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(S.mbar + sl, lay.bytes);
+          bulk_g2s(S.slots + static_cast<size_t>(sl) * lay.bytes,
+                   s.stat + static_cast<size_t>(issued) * lay.bytes, lay.bytes, S.mbar + sl);
+          ++issued;
+          idle = false;
+        }
+        // complete: publish the oldest outstanding copy once it has landed
+        if (done < issued) {
+          const int sl = done % kRing;
+          if (mbar_test(S.mbar + sl, (S.base_use[sl] + done / kRing) & 1)) {
+            S.sready[sl] = done;
+            ++done;
+            idle = false;
           }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(S.mbar + sl, lay.bytes);
-        bulk_g2s(S.slots + static_cast<size_t>(sl) * lay.bytes,
-                 s.stat + static_cast<size_t>(g) * lay.bytes, lay.bytes, S.mbar + sl);
+        if (idle) {
+          if (sg.expired()) {
+            g_flow_dbg[3] = 1000000000ull * 3 + 100000ull * s.G + done;
+            break;
+          }
+        } else {
+          sg.t0 = clock64();
+        }
       }
     }
   } else if (hid >= 0) {
@@ -572,7 +604,15 @@ struct Ctx {
   }
   // grid barrier, then reduce `mask` slots of this epoch into sums[]
   __device__ bool sync_reduce(unsigned mask) {
+    const long long tb0 = clock64();
     const bool ok = grid_sync(a.bar, a.bar + 32, abort_flag);
+    if (threadIdx.x == 0) {
+      if (cta == 0) {
+        atomicAdd(&g_phase_dbg[0], static_cast<unsigned long long>(clock64() - tb0));
+        atomicAdd(&g_phase_dbg[3], 1ull);
+      }
+      if (cta == 2) atomicAdd(&g_phase_dbg[2], static_cast<unsigned long long>(clock64() - tb0));
+    }
     if (ok) {
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       if (warp < NSLOT && (mask >> warp) & 1u) {
@@ -613,6 +653,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
       double* dst = in.dst;
       double* r = B.r;
       const int off = B.off;
+      const long long ti0 = clock64();
       rho_p[b] = ic_apply<TB>(
           B,
           [&](int row) {
@@ -623,6 +664,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
             return ri;
           },
           C.xf, C.xb, C.red, C.abort_flag);
+      if (threadIdx.x == 0) atomicAdd(&g_phase_dbg[C.cta == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));
     }
   }
   for (int b = 0; b < 2; ++b) {
@@ -742,6 +784,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
         double* r = B.r;
         const double* q = B.q;
         const double na = -alpha[b];
+        const long long ti0 = clock64();
         rho_n[b] = ic_apply<TB>(
             B,
             [&](int row) {
@@ -750,6 +793,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
               return ri;
             },
             C.xf, C.xb, C.red, C.abort_flag);
+        if (threadIdx.x == 0) atomicAdd(&g_phase_dbg[C.cta == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));
       }
     }
     for (int b = 0; b < 2; ++b) {
@@ -819,6 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
   __shared__ double sums[NSLOT];
   Ctx C(a, red, sums, xs_dyn);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long t_kernel0 = clock64();
   for (int b = 0; b < 2; ++b)
     if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0 && !a.blk[b].exact && C.cta == a.blk[b].ic_cta)
       flow_setup<TB>(xs_dyn, a.blk[b].n);
@@ -1008,6 +1053,8 @@ finish:
         a.p_out[a.perm_p[i - a.n_u]] = a.filter ? sub_rn(a.x[i], mul_rn(mean, 1.0)) : a.x[i];
     }
   }
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    atomicAdd(&g_phase_dbg[4], static_cast<unsigned long long>(clock64() - t_kernel0));
   if (writer) {
     DevReport* R = a.rep;
     R->iterations = iterations;
@@ -1595,6 +1642,17 @@ int dsgpu_debug_counters(int reset, int64_t* out4) {
   if (reset) {
     const unsigned long long z[4] = {0, 0, 0, 0};
     cudaMemcpyToSymbol(g_flow_dbg, z, sizeof(z));
+  }
+  return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
+}
+
+int dsgpu_debug_phases(int reset, int64_t* out8) {
+  unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyFromSymbol(v, g_phase_dbg, sizeof(v));
+  for (int i = 0; i < 8; ++i) out8[i] = static_cast<int64_t>(v[i]);
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_phase_dbg, z, sizeof(z));
   }
   return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
 }
