@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_DIR = os.path.join(HERE, "lib")
+LIB_DIR = os.environ.get("DSGPU_LIB_DIR", os.path.join(HERE, "lib"))
 HOST_SO = os.path.join(LIB_DIR, "libdshost.so")
 GPU_SO = os.path.join(LIB_DIR, "libdsgpu.so")
 

@@ -53,6 +53,10 @@ struct HostSweep {
 // agree to round-off); the factor and the operation are the
 // same. kTA / kTB are the per-lane register budgets for A and B entries.
 constexpr int kTA = 8, kRing = 16, kFlowD = 7;
+// Ring mode (systems whose solution vector does not fit shared memory): the
+// last kXRing groups' results live in a shared-memory ring, older ones in
+// global memory (published every kFenceEvery groups after a fence).
+constexpr int kXRing = 64, kFenceEvery = 8;
 // Supported per-lane B capacities (templates); the plan picks the smallest that fits.
 constexpr int kTBMax = 16;
 
@@ -81,6 +85,11 @@ struct SlotLayout {
 
 struct HostFlow {
   int n = 0, G = 0, n_levels = 0, tb = 4, merge = 1;
+  int ring = 0;                              // 1: ring mode (see kXRing)
+  std::vector<int32_t> gw, gneed;            // ring mode: global-prefix width / newest dep group
+  std::vector<int64_t> gptr;                 // G + 1
+  std::vector<int32_t> gcols;                // rows (pad = n, gx[n] = 0)
+  std::vector<double> gvals;
   std::vector<uint8_t> stat;                 // G * SlotLayout(tb).bytes
   std::vector<int32_t> nr, need, pw, ww, grows;  // per group (grows: G*32)
   std::vector<int64_t> pptr, wptr;           // G + 1, lane-interleaved (stride nr)
@@ -134,7 +143,14 @@ DepRows rows_from_sweep(const HostSweep& s);
 DepRows merge_levels(const DepRows& r, int M);
 // Largest number of B entries (dependencies on the previous group) of any row.
 int flow_b_needed(const DepRows& r);
-void build_flow(const DepRows& r, int tb, HostFlow& f);
-int build_block_flows(HostPlan& P, int merge, int* merge_used);
+void build_flow(const DepRows& r, int tb, int ring, HostFlow& f);
+// Shared memory of one staged sweep with `slots` x entries (rows in full mode,
+// kXRing*32 in ring mode); mirrors FlowSmem in solver.cu.
+inline size_t flow_smem_bytes(int slots, int slot_bytes) {
+  return (static_cast<size_t>(slots + 1) * 8 + 127) / 128 * 128 +
+         static_cast<size_t>(kRing) * slot_bytes + kRing * 32 * 8 + kRing * 8 + 3 * kRing * 4 + 64;
+}
+// Ring mode when a full-vector workspace exceeds smem_budget (or n >= force_ring_n).
+int build_block_flows(HostPlan& P, int merge, int* merge_used, size_t smem_budget, int force_ring_n);
 
 }  // namespace dsgpu

@@ -423,11 +423,14 @@ int flow_b_needed(const DepRows& r) {
 }
 
 // Staged sweep plan (see HostFlow in dsgpu_internal.hpp).
-void build_flow(const DepRows& r, int tb, HostFlow& f) {
+void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
   const int n = r.n;
   f = HostFlow{};
   f.n = n;
   f.tb = tb;
+  f.ring = ring;
+  // smem index of an entry's x: the full vector (row) or the ring slot
+  const int zero_idx = ring ? kXRing * kLanes : n;
   f.diag = r.diag;
   f.dinv.resize(n);
   for (int i = 0; i < n; ++i) f.dinv[i] = 1.0 / r.diag[i];
@@ -438,19 +441,22 @@ void build_flow(const DepRows& r, int tb, HostFlow& f) {
   for (int i = 0; i < n; ++i) f.n_levels = std::max(f.n_levels, r.level[i] + 1);
   f.pptr.assign(1, 0);
   f.wptr.assign(1, 0);
-  f.acol.assign(static_cast<size_t>(f.G) * kTA * kLanes, n);
+  f.gptr.assign(1, 0);
+  f.acol.assign(static_cast<size_t>(f.G) * kTA * kLanes, zero_idx);
   f.aval.assign(f.acol.size(), 0.0);
   f.bsrc.assign(static_cast<size_t>(f.G) * tb * kLanes, 0);
   f.bval.assign(f.bsrc.size(), 0.0);
-  std::vector<std::pair<int, double>> P[kLanes], A[kLanes], B[kLanes];
+  auto sidx = [&](int row) { return ring ? (gof[row] % kXRing) * kLanes + lof[row] : row; };
+  std::vector<std::pair<int, double>> P[kLanes], A[kLanes], B[kLanes], GP[kLanes];
   for (int g = 0; g < f.G; ++g) {
     const std::vector<int>& rows = groups[g];
     const int nr = static_cast<int>(rows.size());
-    int pw = 0, need = -1, ww = 0;
+    int pw = 0, need = -1, ww = 0, gw = 0, gneed = -1;
     for (int l = 0; l < nr; ++l) {
       P[l].clear();
       A[l].clear();
       B[l].clear();
+      GP[l].clear();
       std::vector<std::pair<int, double>> e = r.ent[rows[l]];
       std::stable_sort(e.begin(), e.end(),
                        [&](const auto& a, const auto& b) { return gof[a.first] < gof[b.first]; });
@@ -469,6 +475,14 @@ void build_flow(const DepRows& r, int tb, HostFlow& f) {
       }
       if (static_cast<int>(B[l].size()) > tb)
         throw std::invalid_argument("flow sweep: B capacity exceeded");
+      if (ring) {  // prefix entries too old for the ring come from global memory
+        std::vector<std::pair<int, double>> keep;
+        for (const auto& x : P[l])
+          (gof[x.first] >= g - kXRing + 2 ? keep : GP[l]).push_back(x);
+        P[l].swap(keep);
+        for (const auto& x : GP[l]) gneed = std::max(gneed, gof[x.first]);
+        gw = std::max(gw, static_cast<int>(GP[l].size()));
+      }
       for (const auto& x : P[l]) need = std::max(need, gof[x.first]);
       pw = std::max(pw, static_cast<int>(P[l].size()));
       ww = std::max(ww, static_cast<int>(r.w[rows[l]].size()));
@@ -477,16 +491,24 @@ void build_flow(const DepRows& r, int tb, HostFlow& f) {
     f.need.push_back(need);
     f.pw.push_back(pw);
     f.ww.push_back(ww);
+    f.gw.push_back(gw);
+    f.gneed.push_back(gneed);
     for (int l = 0; l < kLanes; ++l) f.grows.push_back(l < nr ? rows[l] : -1);
-    const int64_t pb = f.pptr.back(), wb = f.wptr.back();
-    f.pcols.resize(pb + static_cast<int64_t>(pw) * nr, n);
+    const int64_t pb = f.pptr.back(), wb = f.wptr.back(), gb = f.gptr.back();
+    f.gcols.resize(gb + static_cast<int64_t>(gw) * nr, n);
+    f.gvals.resize(gb + static_cast<int64_t>(gw) * nr, 0.0);
+    f.pcols.resize(pb + static_cast<int64_t>(pw) * nr, zero_idx);
     f.pvals.resize(pb + static_cast<int64_t>(pw) * nr, 0.0);
     f.wcols.resize(wb + static_cast<int64_t>(ww) * nr, n);
     f.wvals.resize(wb + static_cast<int64_t>(ww) * nr, 0.0);
     for (int l = 0; l < nr; ++l) {
       for (size_t k = 0; k < P[l].size(); ++k) {
-        f.pcols[pb + static_cast<int64_t>(k) * nr + l] = P[l][k].first;
+        f.pcols[pb + static_cast<int64_t>(k) * nr + l] = sidx(P[l][k].first);
         f.pvals[pb + static_cast<int64_t>(k) * nr + l] = P[l][k].second;
+      }
+      for (size_t k = 0; k < GP[l].size(); ++k) {
+        f.gcols[gb + static_cast<int64_t>(k) * nr + l] = GP[l][k].first;
+        f.gvals[gb + static_cast<int64_t>(k) * nr + l] = GP[l][k].second;
       }
       const auto& wl = r.w[rows[l]];
       for (size_t k = 0; k < wl.size(); ++k) {
@@ -495,7 +517,7 @@ void build_flow(const DepRows& r, int tb, HostFlow& f) {
       }
       for (size_t k = 0; k < A[l].size(); ++k) {
         const size_t at = (static_cast<size_t>(g) * kTA + k) * kLanes + l;
-        f.acol[at] = A[l][k].first;
+        f.acol[at] = sidx(A[l][k].first);
         f.aval[at] = A[l][k].second;
       }
       for (size_t k = 0; k < B[l].size(); ++k) {
@@ -506,6 +528,7 @@ void build_flow(const DepRows& r, int tb, HostFlow& f) {
     }
     f.pptr.push_back(pb + static_cast<int64_t>(pw) * nr);
     f.wptr.push_back(wb + static_cast<int64_t>(ww) * nr);
+    f.gptr.push_back(gb + static_cast<int64_t>(gw) * nr);
   }
   // pre-formatted static slot blocks (TMA bulk-copied into the ring)
   const SlotLayout lay(tb);
@@ -536,7 +559,7 @@ void build_flow(const DepRows& r, int tb, HostFlow& f) {
 
 // Staged plans for every IC(0) block with one shared B capacity; lowers the
 // merge factor until the B entries fit kTBMax. Returns the capacity used.
-int build_block_flows(HostPlan& P, int merge, int* merge_used) {
+int build_block_flows(HostPlan& P, int merge, int* merge_used, size_t smem_budget, int force_ring_n) {
   for (int M = std::max(1, merge);; M = M > 1 ? M / 2 : 0) {
     if (M == 0) throw std::invalid_argument("flow sweep: dependency fan-in too large");
     DepRows rows[2][2];
@@ -549,10 +572,18 @@ int build_block_flows(HostPlan& P, int merge, int* merge_used) {
     }
     if (need > kTBMax) continue;
     const int tb = need <= 4 ? 4 : need <= 8 ? 8 : 16;
+    // one kernel variant per handle: ring mode for all IC blocks if any block's
+    // full-vector workspace (flow_smem_bytes) does not fit shared memory
+    int ring = 0;
+    for (int b = 0; b < 2; ++b)
+      if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0 &&
+          (flow_smem_bytes(P.blk[b].n, SlotLayout(tb).bytes) > smem_budget ||
+           P.blk[b].n >= force_ring_n))
+        ring = 1;
     for (int b = 0; b < 2; ++b) {
       if (P.blk[b].kind != DSGPU_BLOCK_PCG_IC0) continue;
-      build_flow(rows[b][0], tb, P.blk[b].ffwd);
-      build_flow(rows[b][1], tb, P.blk[b].fbwd);
+      build_flow(rows[b][0], tb, ring, P.blk[b].ffwd);
+      build_flow(rows[b][1], tb, ring, P.blk[b].fbwd);
       P.blk[b].ffwd.merge = P.blk[b].fbwd.merge = M;
     }
     if (merge_used) *merge_used = M;

@@ -60,6 +60,10 @@ struct DFlow {
   const int64_t *pptr, *wptr;
   const double *pvals, *wvals, *aval, *bval, *diag, *dinv;
   const uint8_t* stat;  // G * SlotLayout(tb).bytes, 16-byte aligned
+  int ring;
+  const int32_t *gw, *gneed, *gcols;
+  const int64_t* gptr;
+  const double* gvals;
 };
 
 struct DBlock {
@@ -219,8 +223,10 @@ struct FlowSmem {
   volatile int* pready;   // psum of group g staged (helpers)
   volatile int* sready;   // static data of group g landed (producer, after its mbarrier)
   volatile int* progress;
+  volatile int* gprogress;  // ring mode: groups whose results are visible in global memory
   int* base_use;  // completed mbarrier phases per slot before this sweep
   int slot_bytes;
+  // n = number of x slots (rows in full mode, kXRing*32 in ring mode); xs[n] = 0
   __device__ FlowSmem(double* base, int n, int sb) : slot_bytes(sb) {
     xs = base;
     const size_t xbytes = (static_cast<size_t>(n + 1) * 8 + 127) / 128 * 128;
@@ -230,20 +236,18 @@ struct FlowSmem {
     pready = reinterpret_cast<volatile int*>(mbar + kRing);
     sready = pready + kRing;
     progress = sready + kRing;
-    base_use = const_cast<int*>(progress) + 1;
+    gprogress = progress + 1;
+    base_use = const_cast<int*>(gprogress) + 1;
   }
-  static size_t bytes(int n, int sb) {
-    return (static_cast<size_t>(n + 1) * 8 + 127) / 128 * 128 + static_cast<size_t>(kRing) * sb +
-           kRing * 32 * 8 + kRing * 8 + 3 * kRing * 4 + 64;
-  }
+  static size_t bytes(int n, int sb) { return flow_smem_bytes(n, sb); }
 };
 
 // Once per kernel launch and CTA, before any staged sweep: the ring's
 // mbarriers are initialized once and then only ever advance (re-initializing
 // an mbarrier the bulk-copy unit has used is not safe).
 template <int TB>
-__device__ void flow_setup(double* smem, int n) {
-  FlowSmem S(smem, n, SlotLayout(TB).bytes);
+__device__ void flow_setup(double* smem, int n, int ring) {
+  FlowSmem S(smem, ring ? kXRing * 32 : n, SlotLayout(TB).bytes);
   for (int i = threadIdx.x; i < kRing; i += blockDim.x) {
     mbar_init(S.mbar + i, 1);
     S.base_use[i] = 0;
@@ -261,11 +265,13 @@ __device__ unsigned long long g_flow_dbg[4];
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
 __device__ unsigned long long g_phase_dbg[8];
 
-template <int TB>
+// gx: ring mode only -- results are written there (global, n+1 with gx[n] = 0).
+template <int TB, bool RING>
 __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __restrict__ b,
-                           unsigned* abort_flag) {
+                           double* gx, unsigned* abort_flag) {
   const SlotLayout lay(TB);
-  FlowSmem S(smem, n, lay.bytes);
+  const int xcount = RING ? kXRing * 32 : n;
+  FlowSmem S(smem, xcount, lay.bytes);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = threadIdx.x; i < kRing; i += blockDim.x) {
     S.pready[i] = -1;
@@ -273,7 +279,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
   }
   if (threadIdx.x == 0) {
     *S.progress = 0;
-    S.xs[n] = 0.0;
+    *S.gprogress = 0;
+    S.xs[xcount] = 0.0;
   }
   __syncthreads();
   // roles: main = last warp; producer = lane 0 of the warp 4 below it (same
@@ -371,6 +378,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         pf_p = S.pready[g2 % kRing];
         pf_s = S.sready[g2 % kRing];
       }
+      asm volatile("" ::: "memory");  // keep the slot loads ahead of the critical chain
       // (3) B(g): the critical chain
       double pb[TB];
 #pragma unroll
@@ -381,9 +389,19 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       const double rr = fma(-q0, d, acc);
       const double x = fma(rr, dv, q0);
       xprev = x;
-      if (lane < nr) S.xs[row] = x;
+      if (RING) {
+        S.xs[(g % kXRing) * 32 + lane] = x;
+        if (lane < nr) gx[row] = x;
+      } else if (lane < nr) {
+        S.xs[row] = x;
+      }
       __syncwarp();
       if (lane == 0) *S.progress = g + 1;
+      if (RING && ((g + 1) % kFenceEvery == 0 || g + 1 == s.G)) {
+        __threadfence();  // publish older results in global memory
+        __syncwarp();
+        if (lane == 0) *S.gprogress = g + 1;
+      }
       // (4) A(g+1)
       double pa[kTA];
 #pragma unroll
@@ -484,7 +502,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
 #pragma unroll
         for (int q = 0; q < PW; ++q) {
           const bool ok = lane < nr && k0 + q < pw;
-          pc[q] = ok ? __ldg(cp + static_cast<int64_t>(k0 + q) * nr) : n;
+          pc[q] = ok ? __ldg(cp + static_cast<int64_t>(k0 + q) * nr) : xcount;
           pv[q] = ok ? __ldg(vp + static_cast<int64_t>(k0 + q) * nr) : 0.0;
         }
         if (k0 == 0)
@@ -499,6 +517,34 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
 #pragma unroll
         for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], S.xs[pc[q]]);
         part = add_rn(part, tree_sum<PW>(pp));
+      }
+      if (RING) {  // entries older than the ring: global memory, once published
+        const int gw = __ldg(s.gw + g);
+        if (gw > 0) {
+          const int gneed = __ldg(s.gneed + g);
+          const int64_t gb = __ldg(s.gptr + g);
+          while (*S.gprogress <= gneed) {
+            __nanosleep(20);
+            if (sg.expired()) {
+              g_flow_dbg[3] = 1000000000ull * 6 + 100000ull * s.G + g;
+              break;
+            }
+          }
+          for (int k0 = 0; k0 < gw; k0 += PW) {
+            int pc[PW];
+            double pv[PW];
+#pragma unroll
+            for (int q = 0; q < PW; ++q) {
+              const bool ok = lane < nr && k0 + q < gw;
+              pc[q] = ok ? __ldg(s.gcols + gb + static_cast<int64_t>(k0 + q) * nr + lane) : n;
+              pv[q] = ok ? __ldg(s.gvals + gb + static_cast<int64_t>(k0 + q) * nr + lane) : 0.0;
+            }
+            double pp[PW];
+#pragma unroll
+            for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], __ldcg(gx + pc[q]));
+            part = add_rn(part, tree_sum<PW>(pp));
+          }
+        }
       }
       const double acc = lane < nr ? sub_rn(rhs, part) : 0.0;
       // psum slot reuse: group g - kRing's psum was read by main iteration g - kRing - 1
@@ -531,7 +577,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
 
 // IC(0) apply z = (L L^T)^{-1} r (Ic0Factor::solve) in one CTA; returns the
 // CTA sum of r_i z_i in warp 0. rhs(row) yields r_row (and may write it).
-template <int TB, class Rhs>
+template <int TB, bool RING, class Rhs>
 __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, double* red,
                            unsigned* abort_flag) {
   double* z = B.z;
@@ -552,11 +598,18 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
   double* bb = B.bb;
   for (int i = threadIdx.x; i < B.n; i += blockDim.x) bb[i] = rhs(i);
   __syncthreads();
-  flow_sweep<TB>(B.ffwd, B.n, xf, bb, abort_flag);
   double* y = B.y;
+  if (RING) {
+    // results go straight to global memory (y, then z)
+    flow_sweep<TB, true>(B.ffwd, B.n, xf, bb, y, abort_flag);
+    flow_sweep<TB, true>(B.fbwd, B.n, xf, y, z, abort_flag);
+    for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += r[i] * z[i];
+    return block_sum(rz, red);
+  }
+  flow_sweep<TB, false>(B.ffwd, B.n, xf, bb, nullptr, abort_flag);
   for (int i = threadIdx.x; i < B.n; i += blockDim.x) y[i] = xf[i];
   __syncthreads();
-  flow_sweep<TB>(B.fbwd, B.n, xf, y, abort_flag);
+  flow_sweep<TB, false>(B.fbwd, B.n, xf, y, nullptr, abort_flag);
   for (int i = threadIdx.x; i < B.n; i += blockDim.x) {
     const double zi = xf[i];
     z[i] = zi;
@@ -637,7 +690,7 @@ struct Ctx {
 // Preconditioner application z = M^{-1} rin (BlockDiagPreconditioner::apply,
 // precond.cpp:139-148). Writes zout (length n), returns the two guard dots
 // <z_b, r_b> in zr[] (identical in all CTAs). False on error.
-template <int TB>
+template <int TB, bool RING>
 __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
                         long long inner[2], long long apps[2]) {
   const Args& a = C.a;
@@ -654,7 +707,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
       double* r = B.r;
       const int off = B.off;
       const long long ti0 = clock64();
-      rho_p[b] = ic_apply<TB>(
+      rho_p[b] = ic_apply<TB, RING>(
           B,
           [&](int row) {
             const int i = off + row;
@@ -785,7 +838,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
         const double* q = B.q;
         const double na = -alpha[b];
         const long long ti0 = clock64();
-        rho_n[b] = ic_apply<TB>(
+        rho_n[b] = ic_apply<TB, RING>(
             B,
             [&](int row) {
               const double ri = add_rn(r[row], mul_rn(na, q[row]));
@@ -856,7 +909,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
   return true;
 }
 
-template <int TB>
+template <int TB, bool RING>
 __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
@@ -866,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
   const long long t_kernel0 = clock64();
   for (int b = 0; b < 2; ++b)
     if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0 && !a.blk[b].exact && C.cta == a.blk[b].ic_cta)
-      flow_setup<TB>(xs_dyn, a.blk[b].n);
+      flow_setup<TB>(xs_dyn, a.blk[b].n, a.blk[b].ffwd.ring);
   const int r0 = C.r0, r1 = C.r1;
   long long inner[2] = {0, 0}, apps[2] = {0, 0};
   int iterations = 0, converged = 0, hist_len = 0;
@@ -897,7 +950,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
     double* free4 = a.rbuf[2];
     double* y = a.y;
     double zr[2];
-    if (!precond<TB>(C, Input{r1v, nullptr, 0.0, nullptr}, y, zr, inner, apps)) goto finish;
+    if (!precond<TB, RING>(C, Input{r1v, nullptr, 0.0, nullptr}, y, zr, inner, apps)) goto finish;
     if (zr[0] < 0.0 || zr[1] < 0.0) {  // BlockDiagPreconditioner guards
       C.status = DSGPU_E_INDEFINITE_PRECOND;
       C.failed_block = zr[0] < 0.0 ? 0 : 1;
@@ -995,7 +1048,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
       }
       const double alfa = sums[SL_ALPHA];
       // ---- precond: r2_new = spare - (alfa/beta) r2;  y = M^{-1} r2_new ----
-      if (!precond<TB>(C, Input{spare, r2v, div_rn(-alfa, beta), spare}, y, zr, inner, apps))
+      if (!precond<TB, RING>(C, Input{spare, r2v, div_rn(-alfa, beta), spare}, y, zr, inner, apps))
         goto finish;
       {
         double* nr1 = r2v;
@@ -1073,23 +1126,25 @@ finish:
 }
 
 // ---- standalone kernels (parity / microbenchmarks) -------------------------
-template <int TB>
+template <int TB, bool RING>
 __global__ void __launch_bounds__(kThreads, 1)
     ic_apply_kernel(const __grid_constant__ DBlock B, const double* r, unsigned* abort_flag) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
   // B.r = r (input), B.z = output, B.y = forward-sweep scratch (set by the host)
-  if (!B.exact) flow_setup<TB>(xs_dyn, B.n);
-  ic_apply<TB>(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag);
+  if (!B.exact) flow_setup<TB>(xs_dyn, B.n, B.ffwd.ring);
+  ic_apply<TB, RING>(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag);
 }
 
 using MinresFn = void (*)(Args);
 using IcFn = void (*)(DBlock, const double*, unsigned*);
-MinresFn minres_for(int tb) {
-  return tb <= 4 ? minres_kernel<4> : tb <= 8 ? minres_kernel<8> : minres_kernel<16>;
+MinresFn minres_for(int tb, bool ring) {
+  if (ring) return tb <= 4 ? minres_kernel<4, true> : tb <= 8 ? minres_kernel<8, true> : minres_kernel<16, true>;
+  return tb <= 4 ? minres_kernel<4, false> : tb <= 8 ? minres_kernel<8, false> : minres_kernel<16, false>;
 }
-IcFn ic_for(int tb) {
-  return tb <= 4 ? ic_apply_kernel<4> : tb <= 8 ? ic_apply_kernel<8> : ic_apply_kernel<16>;
+IcFn ic_for(int tb, bool ring) {
+  if (ring) return tb <= 4 ? ic_apply_kernel<4, true> : tb <= 8 ? ic_apply_kernel<8, true> : ic_apply_kernel<16, true>;
+  return tb <= 4 ? ic_apply_kernel<4, false> : tb <= 8 ? ic_apply_kernel<8, false> : ic_apply_kernel<16, false>;
 }
 
 // y = M x, warp per row; na != nullptr limits each row to its first na[i] entries
@@ -1141,6 +1196,7 @@ struct dsgpu_handle {
   DevReport* d_rep = nullptr;
   int64_t nnz_k = 0, nnz_a = 0, nnz_l[2] = {0, 0}, nnz_q = 0;
   bool exact = false;
+  bool ring = false;
   int tb = 4, merge = 1;
 
   template <class T>
@@ -1195,6 +1251,12 @@ DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
   d.pvals = h->upload(f.pvals);
   d.ww = h->upload(f.ww);
   d.stat = h->upload(f.stat);
+  d.ring = f.ring;
+  d.gw = h->upload(f.gw);
+  d.gneed = h->upload(f.gneed);
+  d.gptr = h->upload(f.gptr);
+  d.gcols = h->upload(f.gcols);
+  d.gvals = h->upload(f.gvals);
   d.wptr = h->upload(f.wptr);
   d.wcols = h->upload(f.wcols);
   d.wvals = h->upload(f.wvals);
@@ -1282,7 +1344,18 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     h->exact = std::getenv("DSGPU_EXACT") && std::atoi(std::getenv("DSGPU_EXACT")) != 0;
     if (!h->exact && nmax > 0) {
       const int merge = std::getenv("DSGPU_MERGE") ? std::atoi(std::getenv("DSGPU_MERGE")) : kDefaultMerge;
-      h->tb = build_block_flows(P, merge, &h->merge);
+      // ring mode when the full solution vector + ring would not fit shared memory
+      int smem_optin0 = 0;
+      cudaDeviceGetAttribute(&smem_optin0, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+      const size_t budget = static_cast<size_t>(smem_optin0) - 2048;
+      const int force_ring_n = std::getenv("DSGPU_RING_N") ? std::atoi(std::getenv("DSGPU_RING_N")) : (1 << 30);
+      h->tb = build_block_flows(P, merge, &h->merge, budget, force_ring_n);
+      h->ring = (P.blk[0].kind == DSGPU_BLOCK_PCG_IC0 && P.blk[0].ffwd.ring) ||
+                (P.blk[1].kind == DSGPU_BLOCK_PCG_IC0 && P.blk[1].ffwd.ring);
+      nmax = 0;  // shared-memory footprint per block (x slots)
+      for (int b = 0; b < 2; ++b)
+        if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0)
+          nmax = std::max(nmax, P.blk[b].ffwd.ring ? kXRing * 32 : P.blk[b].n);
     }
     h->smem = h->exact ? static_cast<size_t>(2) * nmax * sizeof(double)
                        : FlowSmem::bytes(nmax, SlotLayout(h->tb).bytes);
@@ -1294,18 +1367,18 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
                   "IC(0) block too large for the shared-memory dataflow sweep in this build (n=" +
                       std::to_string(nmax) + ")");
     int rc = cuda_check(h,
-                        cudaFuncSetAttribute(minres_for(h->tb), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                        cudaFuncSetAttribute(minres_for(h->tb, h->ring), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(h->smem)),
                         "cudaFuncSetAttribute");
     if (rc) return rc;
     rc = cuda_check(h,
-                    cudaFuncSetAttribute(ic_for(h->tb), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    cudaFuncSetAttribute(ic_for(h->tb, h->ring), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(h->smem)),
                     "cudaFuncSetAttribute");
     if (rc) return rc;
     int per_sm = 0;
     rc = cuda_check(h,
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minres_for(h->tb), kThreads,
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minres_for(h->tb, h->ring), kThreads,
                                                                   h->smem),
                     "occupancy");
     if (rc) return rc;
@@ -1458,7 +1531,7 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   cudaEventRecord(e0, h->stream);
   void* params[] = {&a};
   rc = cuda_check(h,
-                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_for(h->tb)), dim3(h->grid),
+                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_for(h->tb, h->ring)), dim3(h->grid),
                                               dim3(kThreads), params, h->smem, h->stream),
                   "cooperative launch");
   cudaEventRecord(e1, h->stream);
@@ -1578,7 +1651,7 @@ int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z) {
   DBlock B = h->args.blk[block];
   B.r = d0;
   B.z = d1;
-  ic_for(h->tb)<<<1, kThreads, h->smem, h->stream>>>(B, d0, h->args.bar + 64);
+  ic_for(h->tb, h->ring)<<<1, kThreads, h->smem, h->stream>>>(B, d0, h->args.bar + 64);
   cudaMemcpyAsync(z, d1, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream);
   return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_ic0");
 }
@@ -1611,7 +1684,7 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
       DBlock B = a.blk[which - 1];
       B.r = d0;
       B.z = d1;
-      ic_for(h->tb)<<<1, kThreads, h->smem, h->stream>>>(B, d0, a.bar + 64);
+      ic_for(h->tb, h->ring)<<<1, kThreads, h->smem, h->stream>>>(B, d0, a.bar + 64);
     } else {
       const DBlock& B = a.blk[0];
       spmv_kernel<<<(B.n * 32 + 255) / 256, 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1);

@@ -214,3 +214,27 @@ def test_max_iter_and_errors(gpu):
     bad = StokesSystem(negA, s.B, s.Bt, s.Q, s.Q_nu, s.f)
     with pytest.raises(solver.PreconditionerError):
         solver.solve_stokes(bad, "PCG(A)+Diag(Q)", solver.SolverOptions(inner_tol=1e-6))
+
+
+def test_ring_mode_forced_small(gpu, port, monkeypatch):
+    """Ring mode (results beyond the shared-memory ring published in global
+    memory) forced on a small system: same answers as the full-vector mode."""
+    host, solver = gpu
+    monkeypatch.setenv("DSGPU_RING_N", "1")
+    s = host.assemble("psi-mms", 2, 16)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    r = np.random.default_rng(5).standard_normal(s.n_u)
+    z = g.apply_ic0(0, r)
+    ref = port.ic0_solve(to_oracle(g.top.factor), r)
+    assert np.abs(z - ref).max() <= 1e-12 * np.abs(ref).max()
+    sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+    check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+
+
+def test_large_system_ring_mode(gpu, port):
+    """k'=3, 96x96 (n_u = 19,404 > shared memory): ring mode chosen by setup."""
+    host, solver = gpu
+    s = host.assemble("random", 3, 96, seed=1234)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+    check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
