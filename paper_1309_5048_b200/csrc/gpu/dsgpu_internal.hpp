@@ -59,6 +59,7 @@ constexpr int kTA = 8, kRing = 16, kFlowD = 7;
 constexpr int kXRing = 64, kFenceEvery = 8;
 // Supported per-lane B capacities (templates); the plan picks the smallest that fits.
 constexpr int kTBMax = 16;
+constexpr int kPW = 16;  // helper prefix-list chunk (entries per lane)
 
 // Dependency form of one triangular sweep: row i computes
 //   y_i = (sum_j w_ij b_j - sum_k a_ik y_k) / d_i      (w_ii = 1 implied)
@@ -93,6 +94,7 @@ struct HostFlow {
   std::vector<uint8_t> stat;                 // G * SlotLayout(tb).bytes
   std::vector<int32_t> nr, need, pw, ww, grows;  // per group (grows: G*32)
   std::vector<int64_t> pptr, wptr;           // G + 1, lane-interleaved (stride nr)
+  std::vector<int32_t> cptr, cneed;          // per kPW-entry chunk of the prefix list: newest dep group
   std::vector<int32_t> pcols, wcols;         // pad = n (a zero slot)
   std::vector<double> pvals, wvals;
   std::vector<int32_t> acol;                 // G*kTA*32, pad = n

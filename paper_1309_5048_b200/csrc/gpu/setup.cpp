@@ -441,6 +441,7 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
   for (int i = 0; i < n; ++i) f.n_levels = std::max(f.n_levels, r.level[i] + 1);
   f.pptr.assign(1, 0);
   f.wptr.assign(1, 0);
+  f.cptr.assign(1, 0);
   f.gptr.assign(1, 0);
   f.acol.assign(static_cast<size_t>(f.G) * kTA * kLanes, zero_idx);
   f.aval.assign(f.acol.size(), 0.0);
@@ -452,6 +453,7 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
     const std::vector<int>& rows = groups[g];
     const int nr = static_cast<int>(rows.size());
     int pw = 0, need = -1, ww = 0, gw = 0, gneed = -1;
+    std::vector<int> cneed_g;
     for (int l = 0; l < nr; ++l) {
       P[l].clear();
       A[l].clear();
@@ -484,11 +486,18 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
         gw = std::max(gw, static_cast<int>(GP[l].size()));
       }
       for (const auto& x : P[l]) need = std::max(need, gof[x.first]);
+      for (size_t k = 0; k < P[l].size(); ++k) {  // per-chunk newest dependency
+        const size_t c = k / kPW;
+        if (cneed_g.size() <= c) cneed_g.resize(c + 1, -1);
+        cneed_g[c] = std::max(cneed_g[c], gof[P[l][k].first]);
+      }
       pw = std::max(pw, static_cast<int>(P[l].size()));
       ww = std::max(ww, static_cast<int>(r.w[rows[l]].size()));
     }
     f.nr.push_back(nr);
     f.need.push_back(need);
+    for (const int c : cneed_g) f.cneed.push_back(c);
+    f.cptr.push_back(f.cptr.back() + static_cast<int32_t>(cneed_g.size()));
     f.pw.push_back(pw);
     f.ww.push_back(ww);
     f.gw.push_back(gw);

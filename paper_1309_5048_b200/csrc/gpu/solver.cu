@@ -64,6 +64,7 @@ struct DFlow {
   const int32_t *gw, *gneed, *gcols;
   const int64_t* gptr;
   const double* gvals;
+  const int32_t *cptr, *cneed;  // prefix-list chunks: newest dependency group of each
 };
 
 struct DBlock {
@@ -79,6 +80,12 @@ struct DBlock {
   double *r, *z, *q, *p0, *p1;  // PCG work (block-local, length n)
   double* y;                    // forward-sweep result (staged mode), n + 1 (y[n] = 0)
   double* bb;                   // materialized right-hand side (staged mode), n + 1
+  // ring mode: partial sums of the entries older than the ring are computed by
+  // "remote" helper CTAs and handed over through global memory
+  double* rpsum;                // max(G) * 32
+  unsigned* rflag;              // max(G): sweep tag once rpsum[g] is final
+  unsigned long long* gprog;    // (sweep tag << 32) | groups published by the main warp
+  int remote_cta0, n_remote;    // remote helper CTAs (0: none)
 };
 
 struct DevReport {
@@ -115,6 +122,7 @@ struct Args {
   int max_iter, stop_euclid, inner_cap;
   DevReport* rep;
   int smem_half;  // doubles per dataflow array (largest IC block)
+  unsigned launch_id;  // distinguishes the sweep tags of successive launches
 };
 
 // ---------------------------------------------------------------------------
@@ -258,17 +266,93 @@ __device__ void flow_setup(double* smem, int n, int ring) {
 }
 
 // diagnostics: [0] main-warp cycles, [1] main cycles waiting for slots,
-// [2] groups processed by the main warp (summed over sweeps)
-__device__ unsigned long long g_flow_dbg[4];
+// [2] groups processed by the main warp (summed over sweeps), [3] abort code,
+// [4] main cycles waiting for the producer (static slot data), [5] helper
+// cycles waiting for their ring-list dependencies, [6] helper cycles waiting
+// for remote partial sums, [7] helper cycles in total (all helper warps)
+__device__ unsigned long long g_flow_dbg[8];
 // phase diagnostics of the persistent kernel: [0] CTA0 cycles in grid barriers,
 // [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
 __device__ unsigned long long g_phase_dbg[8];
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Hand-off state of one ring-mode sweep with remote helpers.
+struct FlowRemote {
+  double* rpsum;
+  unsigned* rflag;
+  unsigned long long* gprog;
+  unsigned tag;  // unique per sweep within a launch, launch id in the top bits
+  int on;        // remote helpers active
+};
+
+__device__ __forceinline__ unsigned sweep_tag(unsigned launch_id, unsigned sweep_no) {
+  return ((launch_id & 0xFFFu) << 20) | (sweep_no & 0xFFFFFu);
+}
+
+// Remote helpers (other CTAs): for every group, the partial sum of the entries
+// older than the shared-memory ring, from the results the main warp has
+// published in global memory. rank / nranks: this CTA among the remote CTAs.
+__device__ void flow_remote(const DFlow& s, int n, const double* __restrict__ gx, FlowRemote R,
+                            int rank, int nranks, unsigned* abort_flag) {
+  constexpr int PW = 16;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int wid = rank * nw + (threadIdx.x >> 5), W = nranks * nw;
+  for (int g = wid; g < s.G; g += W) {
+    const int gw = __ldg(s.gw + g);
+    if (gw == 0) continue;
+    const int nr = __ldg(s.nr + g), gneed = __ldg(s.gneed + g);
+    const int64_t gb = __ldg(s.gptr + g);
+    const unsigned need = static_cast<unsigned>(gneed + 1);
+    double part = 0.0;
+    SpinGuard sg(abort_flag);
+    for (int k0 = 0; k0 < gw; k0 += PW) {
+      int pc[PW];
+      double pv[PW];
+#pragma unroll
+      for (int q = 0; q < PW; ++q) {
+        const bool ok = lane < nr && k0 + q < gw;
+        pc[q] = ok ? __ldg(s.gcols + gb + static_cast<int64_t>(k0 + q) * nr + lane) : n;
+        pv[q] = ok ? __ldg(s.gvals + gb + static_cast<int64_t>(k0 + q) * nr + lane) : 0.0;
+      }
+      if (k0 == 0)
+        for (;;) {  // the tag must match: stale words of other sweeps never count
+          const unsigned long long v = ld_acquire_u64(R.gprog);
+          if (static_cast<unsigned>(v >> 32) == R.tag && static_cast<unsigned>(v) >= need) break;
+          __nanosleep(100);
+          if (sg.expired()) {
+            g_flow_dbg[3] = 1000000000ull * 7 + 100000ull * s.G + g;
+            break;
+          }
+        }
+      double pp[PW];
+#pragma unroll
+      for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], __ldcg(gx + pc[q]));
+      part = add_rn(part, tree_sum<PW>(pp));
+    }
+    __stcg(R.rpsum + static_cast<int64_t>(g) * 32 + lane, part);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(R.rflag + g, R.tag);
+  }
+}
+
 // gx: ring mode only -- results are written there (global, n+1 with gx[n] = 0).
 template <int TB, bool RING>
 __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __restrict__ b,
-                           double* gx, unsigned* abort_flag) {
+                           double* gx, FlowRemote R, unsigned* abort_flag) {
   const SlotLayout lay(TB);
   const int xcount = RING ? kXRing * 32 : n;
   FlowSmem S(smem, xcount, lay.bytes);
@@ -300,7 +384,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     double bvl[TB];
     int bsl[TB];
     const long long t_main0 = clock64();
-    long long wait_cyc = 0;
+    long long wait_cyc = 0, wait_s = 0;
     // readiness flags of the next group, prefetched one iteration ahead
     int pf_p = -2, pf_s = -2;
     auto slot_wait = [&](int gg) {
@@ -312,6 +396,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
             g_flow_dbg[3] = 1000000000ull * 1 + 100000ull * s.G + gg;
             break;
           }
+        wait_s += clock64() - sg.t0;
         while (S.pready[sl] != gg)
           if (sg.expired()) {
             g_flow_dbg[3] = 1000000000ull * 2 + 100000ull * s.G + gg;
@@ -400,7 +485,11 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       if (RING && ((g + 1) % kFenceEvery == 0 || g + 1 == s.G)) {
         __threadfence();  // publish older results in global memory
         __syncwarp();
-        if (lane == 0) *S.gprogress = g + 1;
+        if (lane == 0) {
+          *S.gprogress = g + 1;
+          if (R.on)  // ordered by the fence above
+            st_relaxed_u64(R.gprog, (static_cast<unsigned long long>(R.tag) << 32) | (g + 1));
+        }
       }
       // (4) A(g+1)
       double pa[kTA];
@@ -421,6 +510,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       atomicAdd(&g_flow_dbg[0], static_cast<unsigned long long>(clock64() - t_main0));
       atomicAdd(&g_flow_dbg[1], static_cast<unsigned long long>(wait_cyc));
       atomicAdd(&g_flow_dbg[2], static_cast<unsigned long long>(s.G));
+      atomicAdd(&g_flow_dbg[4], static_cast<unsigned long long>(wait_s));
     }
   } else if (warp == prodw) {
     if (lane == 0) {
@@ -459,25 +549,25 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       }
     }
   } else if (hid >= 0) {
-    constexpr int PW = 16;
+    constexpr int PW = kPW;
+    const long long th0 = clock64();
+    long long tw_need = 0, tw_rem = 0;
     int g = hid;
-    int nr = 0, pw = 0, need = 0;
+    int nr = 0, pw = 0;
     int64_t pb0 = 0;
     if (g < s.G) {
       nr = __ldg(s.nr + g);
       pw = __ldg(s.pw + g);
-      need = __ldg(s.need + g);
       pb0 = __ldg(s.pptr + g);
     }
     for (; g < s.G; g += nh) {
       const int sl = g % kRing;
       const int gn = g + nh;
-      int nrn = 0, pwn = 0, needn = 0;
+      int nrn = 0, pwn = 0;
       int64_t pbn = 0;
       if (gn < s.G) {
         nrn = __ldg(s.nr + gn);
         pwn = __ldg(s.pw + gn);
-        needn = __ldg(s.need + gn);
         pbn = __ldg(s.pptr + gn);
       }
       int row = -1;
@@ -496,29 +586,20 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       const double* vp = s.pvals + pb0 + lane;
       double part = 0.0;
       SpinGuard sg(abort_flag);
-      for (int k0 = 0; k0 < pw || k0 == 0; k0 += PW) {
-        int pc[PW];
-        double pv[PW];
-#pragma unroll
-        for (int q = 0; q < PW; ++q) {
-          const bool ok = lane < nr && k0 + q < pw;
-          pc[q] = ok ? __ldg(cp + static_cast<int64_t>(k0 + q) * nr) : xcount;
-          pv[q] = ok ? __ldg(vp + static_cast<int64_t>(k0 + q) * nr) : 0.0;
-        }
-        if (k0 == 0)
-          while (*S.progress <= need) {
+      if (RING && R.on) {  // entries older than the ring: remote helpers' partial sum
+        if (__ldg(s.gw + g) > 0) {
+          const long long t0 = clock64();
+          while (ld_acquire(R.rflag + g) != R.tag) {
             __nanosleep(20);
             if (sg.expired()) {
-              g_flow_dbg[3] = 1000000ull * (blockIdx.x + 1) + 1000ull * 4 + (g % 1000);
+              g_flow_dbg[3] = 1000000000ull * 8 + 100000ull * s.G + g;
               break;
             }
           }
-        double pp[PW];
-#pragma unroll
-        for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], S.xs[pc[q]]);
-        part = add_rn(part, tree_sum<PW>(pp));
-      }
-      if (RING) {  // entries older than the ring: global memory, once published
+          tw_rem += clock64() - t0;
+          part = __ldcg(R.rpsum + static_cast<int64_t>(g) * 32 + lane);
+        }
+      } else if (RING) {  // entries older than the ring: global memory, once published
         const int gw = __ldg(s.gw + g);
         if (gw > 0) {
           const int gneed = __ldg(s.gneed + g);
@@ -546,6 +627,33 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
           }
         }
       }
+      // ring-list entries, oldest chunk first; each chunk waits for its own
+      // newest dependency, so the next chunk's loads overlap that wait
+      const int c0 = __ldg(s.cptr + g);
+      for (int k0 = 0, c = c0; k0 < pw; k0 += PW, ++c) {
+        int pc[PW];
+        double pv[PW];
+        const int cn = __ldg(s.cneed + c);
+#pragma unroll
+        for (int q = 0; q < PW; ++q) {
+          const bool ok = lane < nr && k0 + q < pw;
+          pc[q] = ok ? __ldg(cp + static_cast<int64_t>(k0 + q) * nr) : xcount;
+          pv[q] = ok ? __ldg(vp + static_cast<int64_t>(k0 + q) * nr) : 0.0;
+        }
+        const long long t0 = clock64();
+        while (*S.progress <= cn) {
+          __nanosleep(20);
+          if (sg.expired()) {
+            g_flow_dbg[3] = 1000000ull * (blockIdx.x + 1) + 1000ull * 4 + (g % 1000);
+            break;
+          }
+        }
+        tw_need += clock64() - t0;
+        double pp[PW];
+#pragma unroll
+        for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], S.xs[pc[q]]);
+        part = add_rn(part, tree_sum<PW>(pp));
+      }
       const double acc = lane < nr ? sub_rn(rhs, part) : 0.0;
       // psum slot reuse: group g - kRing's psum was read by main iteration g - kRing - 1
       while (*S.progress < g - kRing + 2) {
@@ -563,8 +671,12 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       }
       nr = nrn;
       pw = pwn;
-      need = needn;
       pb0 = pbn;
+    }
+    if (lane == 0) {
+      atomicAdd(&g_flow_dbg[5], static_cast<unsigned long long>(tw_need));
+      atomicAdd(&g_flow_dbg[6], static_cast<unsigned long long>(tw_rem));
+      atomicAdd(&g_flow_dbg[7], static_cast<unsigned long long>(clock64() - th0));
     }
   }
   __syncthreads();
@@ -579,7 +691,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
 // CTA sum of r_i z_i in warp 0. rhs(row) yields r_row (and may write it).
 template <int TB, bool RING, class Rhs>
 __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, double* red,
-                           unsigned* abort_flag) {
+                           unsigned* abort_flag, unsigned launch_id = 0, unsigned sweep_no = 0) {
   double* z = B.z;
   const double* r = B.r;
   double rz = 0.0;
@@ -601,21 +713,38 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
   double* y = B.y;
   if (RING) {
     // results go straight to global memory (y, then z)
-    flow_sweep<TB, true>(B.ffwd, B.n, xf, bb, y, abort_flag);
-    flow_sweep<TB, true>(B.fbwd, B.n, xf, y, z, abort_flag);
+    const int on = B.n_remote > 0;
+    flow_sweep<TB, true>(B.ffwd, B.n, xf, bb, y,
+                         FlowRemote{B.rpsum, B.rflag, B.gprog, sweep_tag(launch_id, sweep_no), on},
+                         abort_flag);
+    flow_sweep<TB, true>(B.fbwd, B.n, xf, y, z,
+                         FlowRemote{B.rpsum, B.rflag, B.gprog, sweep_tag(launch_id, sweep_no + 1), on},
+                         abort_flag);
     for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += r[i] * z[i];
     return block_sum(rz, red);
   }
-  flow_sweep<TB, false>(B.ffwd, B.n, xf, bb, nullptr, abort_flag);
+  const FlowRemote none{nullptr, nullptr, nullptr, 0u, 0};
+  flow_sweep<TB, false>(B.ffwd, B.n, xf, bb, nullptr, none, abort_flag);
   for (int i = threadIdx.x; i < B.n; i += blockDim.x) y[i] = xf[i];
   __syncthreads();
-  flow_sweep<TB, false>(B.fbwd, B.n, xf, y, nullptr, abort_flag);
+  flow_sweep<TB, false>(B.fbwd, B.n, xf, y, nullptr, none, abort_flag);
   for (int i = threadIdx.x; i < B.n; i += blockDim.x) {
     const double zi = xf[i];
     z[i] = zi;
     rz += r[i] * zi;
   }
   return block_sum(rz, red);
+}
+
+// What a remote helper CTA does while the IC CTA runs one IC(0) apply.
+__device__ void ic_apply_remote(const DBlock& B, int rank, unsigned* abort_flag, unsigned launch_id,
+                                unsigned sweep_no) {
+  flow_remote(B.ffwd, B.n, B.y,
+              FlowRemote{B.rpsum, B.rflag, B.gprog, sweep_tag(launch_id, sweep_no), 1}, rank,
+              B.n_remote, abort_flag);
+  flow_remote(B.fbwd, B.n, B.z,
+              FlowRemote{B.rpsum, B.rflag, B.gprog, sweep_tag(launch_id, sweep_no + 1), 1}, rank,
+              B.n_remote, abort_flag);
 }
 
 struct Input {
@@ -638,6 +767,7 @@ struct Ctx {
   double* xf;
   double* xb;
   unsigned* abort_flag;
+  unsigned sweeps[2] = {0u, 0u};  // IC(0) sweeps issued per block (same count in every CTA)
   int status = DSGPU_OK, failed_block = -1;
 
   __device__ Ctx(const Args& args, double* red_, double* sums_, double* xs)
@@ -647,6 +777,12 @@ struct Ctx {
     xf = xs;
     xb = xs + a.smem_half;
     abort_flag = a.bar + 64;
+  }
+  // remote-helper rank of this CTA for block b, or -1
+  __device__ int remote_rank(int b) const {
+    const DBlock& B = a.blk[b];
+    const int k = cta - B.remote_cta0;
+    return (B.n_remote > 0 && k >= 0 && k < B.n_remote) ? k : -1;
   }
   __device__ double* part(int slot) {
     return a.partial + (static_cast<size_t>(epoch & 1) * NSLOT + slot) * G;
@@ -716,9 +852,12 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
             r[row] = ri;
             return ri;
           },
-          C.xf, C.xb, C.red, C.abort_flag);
+          C.xf, C.xb, C.red, C.abort_flag, a.launch_id, C.sweeps[b]);
       if (threadIdx.x == 0) atomicAdd(&g_phase_dbg[C.cta == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));
+    } else if (RING && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0) {
+      ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
     }
+    if (B.kind == DSGPU_BLOCK_PCG_IC0) C.sweeps[b] += 2;
   }
   for (int b = 0; b < 2; ++b) {
     const DBlock& B = a.blk[b];
@@ -845,9 +984,12 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
               r[row] = ri;
               return ri;
             },
-            C.xf, C.xb, C.red, C.abort_flag);
+            C.xf, C.xb, C.red, C.abort_flag, a.launch_id, C.sweeps[b]);
         if (threadIdx.x == 0) atomicAdd(&g_phase_dbg[C.cta == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));
+      } else if (RING && active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0) {
+        ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
       }
+      if (active[b] && B.kind == DSGPU_BLOCK_PCG_IC0) C.sweeps[b] += 2;
     }
     for (int b = 0; b < 2; ++b) {
       if (!active[b]) continue;
@@ -1128,16 +1270,23 @@ finish:
 // ---- standalone kernels (parity / microbenchmarks) -------------------------
 template <int TB, bool RING>
 __global__ void __launch_bounds__(kThreads, 1)
-    ic_apply_kernel(const __grid_constant__ DBlock B, const double* r, unsigned* abort_flag) {
+    ic_apply_kernel(const __grid_constant__ DBlock B, const double* r, unsigned* abort_flag,
+                    unsigned launch_id) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
-  // B.r = r (input), B.z = output, B.y = forward-sweep scratch (set by the host)
+  // B.r = r (input), B.z = output, B.y = forward-sweep scratch (set by the host).
+  // Ring mode: CTAs 1..n_remote are the remote helpers (B.remote_cta0 == 1).
+  if (RING && blockIdx.x > 0) {
+    ic_apply_remote(B, blockIdx.x - 1, abort_flag, launch_id, 0u);
+    return;
+  }
   if (!B.exact) flow_setup<TB>(xs_dyn, B.n, B.ffwd.ring);
-  ic_apply<TB, RING>(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag);
+  ic_apply<TB, RING>(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag,
+                     launch_id, 0u);
 }
 
 using MinresFn = void (*)(Args);
-using IcFn = void (*)(DBlock, const double*, unsigned*);
+using IcFn = void (*)(DBlock, const double*, unsigned*, unsigned);
 MinresFn minres_for(int tb, bool ring) {
   if (ring) return tb <= 4 ? minres_kernel<4, true> : tb <= 8 ? minres_kernel<8, true> : minres_kernel<16, true>;
   return tb <= 4 ? minres_kernel<4, false> : tb <= 8 ? minres_kernel<8, false> : minres_kernel<16, false>;
@@ -1198,6 +1347,13 @@ struct dsgpu_handle {
   bool exact = false;
   bool ring = false;
   int tb = 4, merge = 1;
+  int remote_max = 8;         // remote helper CTAs per IC block (ring mode)
+  int sms = 148;
+  unsigned launch_id = 0;     // 1..4095, cycled per launch (sweep tags)
+  unsigned next_launch_id() {
+    launch_id = launch_id % 4095u + 1u;
+    return launch_id;
+  }
 
   template <class T>
   T* alloc(size_t count) {
@@ -1242,6 +1398,8 @@ DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
   d.G = f.G;
   d.nr = h->upload(f.nr);
   d.need = h->upload(f.need);
+  d.cptr = h->upload(f.cptr);
+  d.cneed = h->upload(f.cneed);
   d.pw = h->upload(f.pw);
   d.grows = h->upload(f.grows);
   d.pcols = h->upload(f.pcols);
@@ -1337,6 +1495,8 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
   try {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    h->sms = sms;
+    if (const char* env = std::getenv("DSGPU_REMOTE")) h->remote_max = std::max(0, std::atoi(env));
     // smem: two dataflow arrays of the largest IC block
     int nmax = 0;
     for (int b = 0; b < 2; ++b)
@@ -1387,6 +1547,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     const int64_t nnz = P.k_rp[P.n];
     int G = static_cast<int>(std::min<int64_t>(sms, std::max<int64_t>(2, (nnz + 16383) / 16384)));
     G = std::max(G, 2);
+    if (h->ring) G = std::min(sms, std::max(G, 2 + 2 * h->remote_max));  // room for remote helpers
     if (const char* env = std::getenv("DSGPU_GRID")) G = std::max(2, std::min(sms, std::atoi(env)));
     h->grid = G;
     // K-row partition balanced by nnz + per-row vector work
@@ -1443,6 +1604,18 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         d.bb = h->alloc<double>(hb.n + 1);
         cudaMemset(d.y, 0, sizeof(double) * (hb.n + 1));
         cudaMemset(d.bb, 0, sizeof(double) * (hb.n + 1));
+      }
+      if (hb.kind == DSGPU_BLOCK_PCG_IC0 && !h->exact && hb.ffwd.ring) {
+        // remote helpers: CTAs [2 + b R, 2 + (b+1) R) of the persistent kernel
+        const int G_max = std::max(hb.ffwd.G, hb.fbwd.G);
+        d.rpsum = h->alloc<double>(static_cast<size_t>(G_max) * 32);
+        d.rflag = h->alloc<unsigned>(G_max);
+        d.gprog = h->alloc<unsigned long long>(1);
+        cudaMemset(d.rflag, 0, sizeof(unsigned) * G_max);
+        cudaMemset(d.gprog, 0, sizeof(unsigned long long));
+        const int R = std::min(h->remote_max, (G - 2) / 2);
+        d.n_remote = R > 0 ? R : 0;
+        d.remote_cta0 = 2 + b * d.n_remote;
       }
       d.r = h->alloc<double>(hb.n);
       d.z = h->alloc<double>(hb.n);
@@ -1523,6 +1696,7 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   a.hist_m = d_hm;
   a.hist_e = d_he;
   a.hist_cap = (d_hm && d_he) ? hist_cap : 0;
+  a.launch_id = h->next_launch_id();
   int rc = cuda_check(h, cudaMemsetAsync(a.bar, 0, 128 * sizeof(unsigned), h->stream), "memset");
   if (rc) return rc;
   cudaEvent_t e0, e1;
@@ -1639,6 +1813,23 @@ int dsgpu_apply_saddle(dsgpu_handle* h, const double* x, double* y) {
   return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_saddle");
 }
 
+// One standalone IC(0) apply of block B (r -> B.z). Ring mode adds the remote
+// helper CTAs (co-resident: cooperative launch).
+static cudaError_t launch_ic(dsgpu_handle* h, DBlock B, const double* r) {
+  unsigned* abort_flag = h->args.bar + 64;
+  unsigned id = h->next_launch_id();
+  const int R = B.n_remote > 0 ? std::min(h->sms - 1, std::max(B.n_remote, 2 * h->remote_max)) : 0;
+  B.remote_cta0 = 1;
+  B.n_remote = R;
+  if (R == 0) {
+    ic_for(h->tb, h->ring)<<<1, kThreads, h->smem, h->stream>>>(B, r, abort_flag, id);
+    return cudaGetLastError();
+  }
+  void* params[] = {&B, &r, &abort_flag, &id};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(ic_for(h->tb, h->ring)), dim3(1 + R),
+                                     dim3(kThreads), params, h->smem, h->stream);
+}
+
 int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z) {
   if (!h || !h->ready) return fail(h, DSGPU_E_BAD_INPUT, "not set up");
   if (block < 0 || block > 1 || h->plan.blk[block].kind != DSGPU_BLOCK_PCG_IC0)
@@ -1651,7 +1842,8 @@ int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z) {
   DBlock B = h->args.blk[block];
   B.r = d0;
   B.z = d1;
-  ic_for(h->tb, h->ring)<<<1, kThreads, h->smem, h->stream>>>(B, d0, h->args.bar + 64);
+  const int rc = cuda_check(h, launch_ic(h, B, d0), "apply_ic0 launch");
+  if (rc) return rc;
   cudaMemcpyAsync(z, d1, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream);
   return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_ic0");
 }
@@ -1684,7 +1876,7 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
       DBlock B = a.blk[which - 1];
       B.r = d0;
       B.z = d1;
-      ic_for(h->tb, h->ring)<<<1, kThreads, h->smem, h->stream>>>(B, d0, a.bar + 64);
+      launch_ic(h, B, d0);
     } else {
       const DBlock& B = a.blk[0];
       spmv_kernel<<<(B.n * 32 + 255) / 256, 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1);
@@ -1708,12 +1900,12 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
   return rc;
 }
 
-int dsgpu_debug_counters(int reset, int64_t* out4) {
-  unsigned long long v[4] = {0, 0, 0, 0};
+int dsgpu_debug_counters(int reset, int64_t* out8) {
+  unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyFromSymbol(v, g_flow_dbg, sizeof(v));
-  for (int i = 0; i < 4; ++i) out4[i] = static_cast<int64_t>(v[i]);
+  for (int i = 0; i < 8; ++i) out8[i] = static_cast<int64_t>(v[i]);
   if (reset) {
-    const unsigned long long z[4] = {0, 0, 0, 0};
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_flow_dbg, z, sizeof(z));
   }
   return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;

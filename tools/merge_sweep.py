@@ -18,7 +18,7 @@ for M in (1, 2, 4, 8):
     zr = P.ic0_solve(c(g.top.factor), r)
     err = np.abs(z - zr).max() / np.abs(zr).max()
     import ctypes as C
-    cnt = np.zeros(4, np.int64)
+    cnt = np.zeros(8, np.int64)
     g.L.dsgpu_debug_counters.argtypes = [C.c_int, np.ctypeslib.ndpointer(dtype=np.int64)]
     g.L.dsgpu_debug_counters(1, cnt)
     ms = g.time_kernel(1, 10)
