@@ -138,10 +138,13 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms);
 int dsgpu_info(const dsgpu_handle* h, int64_t* info);
 
 /* Process-wide sweep diagnostics (summed since the last reset):
- * out8 = main-warp cycles, main cycles waiting for slots, groups, abort code,
- * main cycles waiting for static slot data, helper cycles waiting for ring
- * dependencies, helper cycles waiting for remote partial sums, helper cycles. */
-int dsgpu_debug_counters(int reset, int64_t* out8);
+ * out16[0..7] = main-warp cycles, main cycles waiting for slots, groups, abort
+ * code, main cycles waiting for static slot data, helper cycles waiting for
+ * ring dependencies, helper cycles waiting for remote partial sums, helper
+ * cycles; [8..11] groups by the main warp's distance when their prefix sum was
+ * published (<=1, 2-3, 4-6, >=7 groups ahead), [12..15] the same when the
+ * helper started them (<=3, 4-7, 8-11, >=12). */
+int dsgpu_debug_counters(int reset, int64_t* out16);
 /* Persistent-kernel phase diagnostics (cycles): out8 = CTA0 grid-barrier
  * wait, CTA0 IC(0) apply, CTA2 grid-barrier wait, barriers, CTA0 kernel,
  * CTA1 IC(0) apply, 0, 0. */

@@ -2,6 +2,8 @@
 // operator, the block operators and the level-grouped triangular sweeps.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
@@ -448,6 +450,8 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
   f.bsrc.assign(static_cast<size_t>(f.G) * tb * kLanes, 0);
   f.bval.assign(f.bsrc.size(), 0.0);
   auto sidx = [&](int row) { return ring ? (gof[row] % kXRing) * kLanes + lof[row] : row; };
+  // A window: groups g-flowd+1 .. g-2 are gathered by the main warp
+  const int flowd = std::getenv("DSGPU_FLOWD") ? std::max(3, std::atoi(std::getenv("DSGPU_FLOWD"))) : kFlowD;
   std::vector<std::pair<int, double>> P[kLanes], A[kLanes], B[kLanes], GP[kLanes];
   for (int g = 0; g < f.G; ++g) {
     const std::vector<int>& rows = groups[g];
@@ -466,7 +470,7 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
         const int dg = gof[x.first];
         if (dg == g - 1)
           B[l].push_back(x);
-        else if (dg > g - kFlowD)
+        else if (dg > g - flowd)
           A[l].push_back(x);
         else
           P[l].push_back(x);
@@ -486,13 +490,19 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
         gw = std::max(gw, static_cast<int>(GP[l].size()));
       }
       for (const auto& x : P[l]) need = std::max(need, gof[x.first]);
+
+      pw = std::max(pw, static_cast<int>(P[l].size()));
+      ww = std::max(ww, static_cast<int>(r.w[rows[l]].size()));
+    }
+    // prefix lists are right-aligned (padding first) so every lane's newest
+    // entries share the last chunk and older chunks can go early
+    for (int l = 0; l < nr; ++l) {
+      const int shift = pw - static_cast<int>(P[l].size());
       for (size_t k = 0; k < P[l].size(); ++k) {  // per-chunk newest dependency
-        const size_t c = k / kPW;
+        const size_t c = (k + shift) / kPW;
         if (cneed_g.size() <= c) cneed_g.resize(c + 1, -1);
         cneed_g[c] = std::max(cneed_g[c], gof[P[l][k].first]);
       }
-      pw = std::max(pw, static_cast<int>(P[l].size()));
-      ww = std::max(ww, static_cast<int>(r.w[rows[l]].size()));
     }
     f.nr.push_back(nr);
     f.need.push_back(need);
@@ -511,9 +521,10 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
     f.wcols.resize(wb + static_cast<int64_t>(ww) * nr, n);
     f.wvals.resize(wb + static_cast<int64_t>(ww) * nr, 0.0);
     for (int l = 0; l < nr; ++l) {
+      const int64_t shift = pw - static_cast<int64_t>(P[l].size());
       for (size_t k = 0; k < P[l].size(); ++k) {
-        f.pcols[pb + static_cast<int64_t>(k) * nr + l] = sidx(P[l][k].first);
-        f.pvals[pb + static_cast<int64_t>(k) * nr + l] = P[l][k].second;
+        f.pcols[pb + (static_cast<int64_t>(k) + shift) * nr + l] = sidx(P[l][k].first);
+        f.pvals[pb + (static_cast<int64_t>(k) + shift) * nr + l] = P[l][k].second;
       }
       for (size_t k = 0; k < GP[l].size(); ++k) {
         f.gcols[gb + static_cast<int64_t>(k) * nr + l] = GP[l][k].first;
@@ -566,6 +577,38 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
   }
 }
 
+// Diagnostics (env DSGPU_FLOW_STATS): how far ahead of the main warp the
+// helpers' newest dependency lies, and the entry mix per group.
+static void flow_stats(const HostFlow& f, const char* name) {
+  if (!std::getenv("DSGPU_FLOW_STATS")) return;
+  const int zero_idx = f.ring ? kXRing * kLanes : f.n;
+  long hist[12] = {};  // last-chunk slack 0..9, >=10, none
+  double sa = 0, sb = 0, sp = 0, sw = 0, sn = 0;
+  for (int g = 0; g < f.G; ++g) {
+    const int c1 = f.cptr[g + 1], c0 = f.cptr[g];
+    const int slack = c1 > c0 ? g - f.cneed[c1 - 1] : 1 << 20;
+    hist[slack < 10 ? slack : slack < (1 << 20) ? 10 : 11]++;
+    int na = 0, nb = 0;
+    for (int k = 0; k < kTA; ++k)
+      for (int l = 0; l < kLanes; ++l)
+        if (f.acol[(static_cast<size_t>(g) * kTA + k) * kLanes + l] != zero_idx) { ++na; break; }
+    for (int k = 0; k < f.tb; ++k)
+      for (int l = 0; l < kLanes; ++l)
+        if (f.bval[(static_cast<size_t>(g) * f.tb + k) * kLanes + l] != 0.0) { ++nb; break; }
+    sa += na;
+    sb += nb;
+    sp += f.pw[g];
+    sw += f.ww[g];
+    sn += f.nr[g];
+  }
+  const double G = f.G > 0 ? f.G : 1;
+  std::fprintf(stderr,
+               "[flow %s] n=%d G=%d merge=%d tb=%d ring=%d rows/group %.1f | A %.2f B %.2f P %.2f W %.2f "
+               "per group | last-chunk slack 2:%ld 3:%ld 4:%ld 5:%ld 6:%ld 7:%ld 8:%ld 9:%ld >=10:%ld none:%ld\n",
+               name, f.n, f.G, f.merge, f.tb, f.ring, sn / G, sa / G, sb / G, sp / G, sw / G, hist[2],
+               hist[3], hist[4], hist[5], hist[6], hist[7], hist[8], hist[9], hist[10], hist[11]);
+}
+
 // Staged plans for every IC(0) block with one shared B capacity; lowers the
 // merge factor until the B entries fit kTBMax. Returns the capacity used.
 int build_block_flows(HostPlan& P, int merge, int* merge_used, size_t smem_budget, int force_ring_n) {
@@ -594,6 +637,8 @@ int build_block_flows(HostPlan& P, int merge, int* merge_used, size_t smem_budge
       build_flow(rows[b][0], tb, ring, P.blk[b].ffwd);
       build_flow(rows[b][1], tb, ring, P.blk[b].fbwd);
       P.blk[b].ffwd.merge = P.blk[b].fbwd.merge = M;
+      flow_stats(P.blk[b].ffwd, b == 0 ? "A fwd" : "Q fwd");
+      flow_stats(P.blk[b].fbwd, b == 0 ? "A bwd" : "Q bwd");
     }
     if (merge_used) *merge_used = M;
     return tb;

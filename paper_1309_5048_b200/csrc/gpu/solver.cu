@@ -39,7 +39,7 @@ using namespace dsgpu::dev;
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kDefaultMerge = 1;
+constexpr int kDefaultMerge = 2;
 constexpr int kWarps = kThreads / 32;
 
 enum Slot { SL_BB = 0, SL_RES, SL_ALPHA, SL_RHO0, SL_RHO1, SL_KAP0, SL_KAP1, SL_ZR0, SL_ZR1, SL_NUM, NSLOT };
@@ -269,8 +269,11 @@ __device__ void flow_setup(double* smem, int n, int ring) {
 // [2] groups processed by the main warp (summed over sweeps), [3] abort code,
 // [4] main cycles waiting for the producer (static slot data), [5] helper
 // cycles waiting for their ring-list dependencies, [6] helper cycles waiting
-// for remote partial sums, [7] helper cycles in total (all helper warps)
-__device__ unsigned long long g_flow_dbg[8];
+// for remote partial sums, [7] helper cycles in total (all helper warps),
+// [8..11] groups by main's distance when the helper published them (g minus
+// groups done: <=1, 2-3, 4-6, >=7), [12..15] the same at the helper's start of
+// the group (<=3, 4-7, 8-11, >=12)
+__device__ unsigned long long g_flow_dbg[16];
 // phase diagnostics of the persistent kernel: [0] CTA0 cycles in grid barriers,
 // [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
@@ -378,25 +381,42 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       ++nh;
     }
   if (warp == mainw && s.G > 0) {
+    // Software pipeline, iteration g:
+    //   (1) gather the A(g+1) operands from xs (their groups <= g-1 are final;
+    //       the column indices were loaded in iteration g-1)
+    //   (2) shuffle the B(g) operands out of x(g-1)
+    //   (3) load group g+2's A columns and group g+1's psum + static slot data
+    //   (4) the critical chain: x(g) = (acc_pre(g) - B(g)) / d
+    //   (5) acc_pre(g+1) = psum(g+1) - A(g+1)
     double xprev = 0.0;
     double acc_pre = 0.0, d = 1.0, dv = 1.0;
     int row = -1, nr = 0;
     double bvl[TB];
     int bsl[TB];
+    int acn[kTA];  // A columns of group g+1
     const long long t_main0 = clock64();
     long long wait_cyc = 0, wait_s = 0;
-    // readiness flags of the next group, prefetched one iteration ahead
+    // readiness flags prefetched one iteration ahead: sready of g+3, pready of g+2
     int pf_p = -2, pf_s = -2;
-    auto slot_wait = [&](int gg) {
+    auto wait_static = [&](int gg) {
       const int sl = gg % kRing;
-      if (pf_p != gg || pf_s != gg) {
+      if (pf_s != gg) {
         SpinGuard sg(abort_flag);
         while (S.sready[sl] != gg)
           if (sg.expired()) {
             g_flow_dbg[3] = 1000000000ull * 1 + 100000ull * s.G + gg;
             break;
           }
-        wait_s += clock64() - sg.t0;
+        const long long w = clock64() - sg.t0;
+        wait_cyc += w;
+        wait_s += w;
+      }
+      return sl;
+    };
+    auto wait_psum = [&](int gg) {
+      const int sl = gg % kRing;
+      if (pf_p != gg) {
+        SpinGuard sg(abort_flag);
         while (S.pready[sl] != gg)
           if (sg.expired()) {
             g_flow_dbg[3] = 1000000000ull * 2 + 100000ull * s.G + gg;
@@ -406,8 +426,10 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       }
       return sl;
     };
-    {  // group 0
-      const int sl = slot_wait(0);
+    const int glast = s.G - 1;
+    {  // prologue: group 0 complete, group 1's A columns
+      int sl = wait_static(0);
+      wait_psum(0);
       const uint8_t* base = S.slots;
       nr = *reinterpret_cast<const int*>(base + lay.nr);
       d = reinterpret_cast<const double*>(base + lay.diag)[lane];
@@ -426,16 +448,31 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         bsl[k] = bs[k * 32 + lane];
         bvl[k] = bv[k * 32 + lane];
       }
+      const int g1 = glast < 1 ? glast : 1;
+      sl = wait_static(g1);
+      const int* ac1 = reinterpret_cast<const int*>(S.slots + static_cast<size_t>(sl) * lay.bytes + lay.acol);
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) acn[k] = ac1[k * 32 + lane];
     }
     for (int g = 0; g < s.G; ++g) {
-      // (1) B(g) shuffles from the previous group's results
+      const int g1 = g + 1 < s.G ? g + 1 : glast;
+      const int g2 = g + 2 < s.G ? g + 2 : glast;
+      // (1) A(g+1) operands
+      double axv[kTA];
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) axv[k] = S.xs[acn[k]];
+      // (2) B(g) operands
       double sx[TB];
 #pragma unroll
       for (int k = 0; k < TB; ++k) sx[k] = shfl_d(xprev, bsl[k]);
       asm volatile("" ::: "memory");
-      // (2) next group's slot (its A entries depend on groups <= g-1: ready)
-      const int g1 = g + 1 < s.G ? g + 1 : g;
-      const int sl = slot_wait(g1);
+      // (3) slot data: g+2's A columns, g+1's psum and static block
+      const int sl2 = wait_static(g2);
+      const int* ac2 = reinterpret_cast<const int*>(S.slots + static_cast<size_t>(sl2) * lay.bytes + lay.acol);
+      int acn2[kTA];
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) acn2[k] = ac2[k * 32 + lane];
+      const int sl = wait_psum(g1);
       const uint8_t* base = S.slots + static_cast<size_t>(sl) * lay.bytes;
       const int nr1 = *reinterpret_cast<const int*>(base + lay.nr);
       const double ps1 = S.psum[sl * 32 + lane];
@@ -443,28 +480,24 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       const double dv1 = reinterpret_cast<const double*>(base + lay.dinv)[lane];
       const int row1 = reinterpret_cast<const int*>(base + lay.rows)[lane];
       const double* av = reinterpret_cast<const double*>(base + lay.aval);
-      const int* ac = reinterpret_cast<const int*>(base + lay.acol);
       const double* bv = reinterpret_cast<const double*>(base + lay.bval);
       const int* bs = reinterpret_cast<const int*>(base + lay.bsrc);
-      double avl[kTA], axv[kTA], bvl1[TB];
+      double avl[kTA], bvl1[TB];
       int bsl1[TB];
 #pragma unroll
-      for (int k = 0; k < kTA; ++k) {
-        avl[k] = av[k * 32 + lane];
-        axv[k] = S.xs[ac[k * 32 + lane]];
-      }
+      for (int k = 0; k < kTA; ++k) avl[k] = av[k * 32 + lane];
 #pragma unroll
       for (int k = 0; k < TB; ++k) {
         bsl1[k] = bs[k * 32 + lane];
         bvl1[k] = bv[k * 32 + lane];
       }
-      {  // prefetch the readiness flags of group g+2 (consumed next iteration)
-        const int g2 = g + 2 < s.G ? g + 2 : g1;
+      {  // prefetch readiness flags for the next iteration
+        const int g3 = g + 3 < s.G ? g + 3 : glast;
         pf_p = S.pready[g2 % kRing];
-        pf_s = S.sready[g2 % kRing];
+        pf_s = S.sready[g3 % kRing];
       }
       asm volatile("" ::: "memory");  // keep the slot loads ahead of the critical chain
-      // (3) B(g): the critical chain
+      // (4) B(g): the critical chain
       double pb[TB];
 #pragma unroll
       for (int k = 0; k < TB; ++k) pb[k] = mul_rn(bvl[k], sx[k]);
@@ -491,7 +524,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
             st_relaxed_u64(R.gprog, (static_cast<unsigned long long>(R.tag) << 32) | (g + 1));
         }
       }
-      // (4) A(g+1)
+      // (5) A(g+1)
       double pa[kTA];
 #pragma unroll
       for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(avl[k], axv[k]);
@@ -505,6 +538,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         bsl[k] = bsl1[k];
         bvl[k] = bvl1[k];
       }
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) acn[k] = acn2[k];
     }
     if (lane == 0) {
       atomicAdd(&g_flow_dbg[0], static_cast<unsigned long long>(clock64() - t_main0));
@@ -552,6 +587,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     constexpr int PW = kPW;
     const long long th0 = clock64();
     long long tw_need = 0, tw_rem = 0;
+    unsigned hpub[4] = {0, 0, 0, 0}, hstart[4] = {0, 0, 0, 0};
     int g = hid;
     int nr = 0, pw = 0;
     int64_t pb0 = 0;
@@ -563,6 +599,10 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     for (; g < s.G; g += nh) {
       const int sl = g % kRing;
       const int gn = g + nh;
+      {
+        const int dist = g - *S.progress;
+        ++hstart[dist <= 3 ? 0 : dist <= 7 ? 1 : dist <= 11 ? 2 : 3];
+      }
       int nrn = 0, pwn = 0;
       int64_t pbn = 0;
       if (gn < s.G) {
@@ -669,6 +709,10 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         __threadfence_block();
         S.pready[sl] = g;
       }
+      {
+        const int dist = g - *S.progress;
+        ++hpub[dist <= 1 ? 0 : dist <= 3 ? 1 : dist <= 6 ? 2 : 3];
+      }
       nr = nrn;
       pw = pwn;
       pb0 = pbn;
@@ -677,6 +721,10 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       atomicAdd(&g_flow_dbg[5], static_cast<unsigned long long>(tw_need));
       atomicAdd(&g_flow_dbg[6], static_cast<unsigned long long>(tw_rem));
       atomicAdd(&g_flow_dbg[7], static_cast<unsigned long long>(clock64() - th0));
+      for (int i = 0; i < 4; ++i) {
+        atomicAdd(&g_flow_dbg[8 + i], static_cast<unsigned long long>(hpub[i]));
+        atomicAdd(&g_flow_dbg[12 + i], static_cast<unsigned long long>(hstart[i]));
+      }
     }
   }
   __syncthreads();
@@ -1900,12 +1948,12 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
   return rc;
 }
 
-int dsgpu_debug_counters(int reset, int64_t* out8) {
-  unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+int dsgpu_debug_counters(int reset, int64_t* out16) {
+  unsigned long long v[16] = {};
   cudaMemcpyFromSymbol(v, g_flow_dbg, sizeof(v));
-  for (int i = 0; i < 8; ++i) out8[i] = static_cast<int64_t>(v[i]);
+  for (int i = 0; i < 16; ++i) out16[i] = static_cast<int64_t>(v[i]);
   if (reset) {
-    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long z[16] = {};
     cudaMemcpyToSymbol(g_flow_dbg, z, sizeof(z));
   }
   return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
