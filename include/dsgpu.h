@@ -143,8 +143,10 @@ int dsgpu_info(const dsgpu_handle* h, int64_t* info);
  * ring dependencies, helper cycles waiting for remote partial sums, helper
  * cycles; [8..11] groups by the main warp's distance when their prefix sum was
  * published (<=1, 2-3, 4-6, >=7 groups ahead), [12..15] the same when the
- * helper started them (<=3, 4-7, 8-11, >=12). */
-int dsgpu_debug_counters(int reset, int64_t* out16);
+ * helper started them (<=3, 4-7, 8-11, >=12); [16] helper cycles from the
+ * end of the last dependency wait to publication, [17] groups whose last
+ * dependency wait spun, [18..19] 0. */
+int dsgpu_debug_counters(int reset, int64_t* out20);
 /* Persistent-kernel phase diagnostics (cycles): out8 = CTA0 grid-barrier
  * wait, CTA0 IC(0) apply, CTA2 grid-barrier wait, barriers, CTA0 kernel,
  * CTA1 IC(0) apply, 0, 0. */

@@ -74,14 +74,19 @@ struct DepRows {
 
 // Byte layout of one group's static main-warp data, identical in HBM (one
 // contiguous block per group, copied by a TMA bulk copy) and in the shared-
-// memory ring slot: diag[32] f64 | dinv[32] f64 | aval[kTA][32] f64 |
-// bval[tb][32] f64 | rows[32] i32 | acol[kTA][32] i32 | bsrc[tb][32] i32 | nr.
+// memory ring slot. Arrays are lane-interleaved in 16-byte units so the main
+// warp reads them with 128-bit shared loads, conflict-free:
+//   dd[32]{diag, dinv} | aval[kTA/2][32]{2 x f64} | bval[tb/2][32]{2 x f64} |
+//   acol[kTA/4][32]{4 x i32} | bsrc[tb/4][32]{4 x i32} | rows[32] i32 | nr.
 struct SlotLayout {
-  int diag, dinv, aval, bval, rows, acol, bsrc, nr, bytes;
+  int dd, aval, bval, acol, bsrc, rows, nr, bytes;
   constexpr explicit SlotLayout(int tb)
-      : diag(0), dinv(256), aval(512), bval(512 + 256 * kTA), rows(bval + 256 * tb),
-        acol(rows + 128), bsrc(acol + 128 * kTA), nr(bsrc + 128 * tb),
-        bytes(((nr + 4) + 15) / 16 * 16) {}
+      : dd(0), aval(512), bval(512 + 256 * kTA), acol(bval + 256 * tb), bsrc(acol + 128 * kTA),
+        rows(bsrc + 128 * tb), nr(rows + 128), bytes(nr + 16) {}
+  // byte offset of element k of lane l in a pair-interleaved f64 array / a
+  // quad-interleaved i32 array
+  static constexpr int f64_at(int k, int l) { return ((k >> 1) * 32 + l) * 16 + (k & 1) * 8; }
+  static constexpr int i32_at(int k, int l) { return ((k >> 2) * 32 + l) * 16 + (k & 3) * 4; }
 };
 
 struct HostFlow {
@@ -93,7 +98,7 @@ struct HostFlow {
   std::vector<double> gvals;
   std::vector<uint8_t> stat;                 // G * SlotLayout(tb).bytes
   std::vector<int32_t> nr, need, pw, ww, grows;  // per group (grows: G*32)
-  std::vector<int64_t> pptr, wptr;           // G + 1, lane-interleaved (stride nr)
+  std::vector<int64_t> pptr, wptr;           // G + 1, lane-interleaved (stride 32; pw, gw in whole kPW chunks)
   std::vector<int32_t> cptr, cneed;          // per kPW-entry chunk of the prefix list: newest dep group
   std::vector<int32_t> pcols, wcols;         // pad = n (a zero slot)
   std::vector<double> pvals, wvals;

@@ -494,6 +494,10 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
       pw = std::max(pw, static_cast<int>(P[l].size()));
       ww = std::max(ww, static_cast<int>(r.w[rows[l]].size()));
     }
+    // widths padded to whole chunks; lists lane-interleaved with stride 32 so
+    // the helpers load them with constant offsets and no predicates
+    pw = (pw + kPW - 1) / kPW * kPW;
+    gw = (gw + kPW - 1) / kPW * kPW;
     // prefix lists are right-aligned (padding first) so every lane's newest
     // entries share the last chunk and older chunks can go early
     for (int l = 0; l < nr; ++l) {
@@ -504,6 +508,7 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
         cneed_g[c] = std::max(cneed_g[c], gof[P[l][k].first]);
       }
     }
+    cneed_g.resize(pw / kPW, -1);
     f.nr.push_back(nr);
     f.need.push_back(need);
     for (const int c : cneed_g) f.cneed.push_back(c);
@@ -514,26 +519,26 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
     f.gneed.push_back(gneed);
     for (int l = 0; l < kLanes; ++l) f.grows.push_back(l < nr ? rows[l] : -1);
     const int64_t pb = f.pptr.back(), wb = f.wptr.back(), gb = f.gptr.back();
-    f.gcols.resize(gb + static_cast<int64_t>(gw) * nr, n);
-    f.gvals.resize(gb + static_cast<int64_t>(gw) * nr, 0.0);
-    f.pcols.resize(pb + static_cast<int64_t>(pw) * nr, zero_idx);
-    f.pvals.resize(pb + static_cast<int64_t>(pw) * nr, 0.0);
-    f.wcols.resize(wb + static_cast<int64_t>(ww) * nr, n);
-    f.wvals.resize(wb + static_cast<int64_t>(ww) * nr, 0.0);
+    f.gcols.resize(gb + static_cast<int64_t>(gw) * kLanes, n);
+    f.gvals.resize(gb + static_cast<int64_t>(gw) * kLanes, 0.0);
+    f.pcols.resize(pb + static_cast<int64_t>(pw) * kLanes, zero_idx);
+    f.pvals.resize(pb + static_cast<int64_t>(pw) * kLanes, 0.0);
+    f.wcols.resize(wb + static_cast<int64_t>(ww) * kLanes, n);
+    f.wvals.resize(wb + static_cast<int64_t>(ww) * kLanes, 0.0);
     for (int l = 0; l < nr; ++l) {
       const int64_t shift = pw - static_cast<int64_t>(P[l].size());
       for (size_t k = 0; k < P[l].size(); ++k) {
-        f.pcols[pb + (static_cast<int64_t>(k) + shift) * nr + l] = sidx(P[l][k].first);
-        f.pvals[pb + (static_cast<int64_t>(k) + shift) * nr + l] = P[l][k].second;
+        f.pcols[pb + (static_cast<int64_t>(k) + shift) * kLanes + l] = sidx(P[l][k].first);
+        f.pvals[pb + (static_cast<int64_t>(k) + shift) * kLanes + l] = P[l][k].second;
       }
       for (size_t k = 0; k < GP[l].size(); ++k) {
-        f.gcols[gb + static_cast<int64_t>(k) * nr + l] = GP[l][k].first;
-        f.gvals[gb + static_cast<int64_t>(k) * nr + l] = GP[l][k].second;
+        f.gcols[gb + static_cast<int64_t>(k) * kLanes + l] = GP[l][k].first;
+        f.gvals[gb + static_cast<int64_t>(k) * kLanes + l] = GP[l][k].second;
       }
       const auto& wl = r.w[rows[l]];
       for (size_t k = 0; k < wl.size(); ++k) {
-        f.wcols[wb + static_cast<int64_t>(k) * nr + l] = wl[k].first;
-        f.wvals[wb + static_cast<int64_t>(k) * nr + l] = wl[k].second;
+        f.wcols[wb + static_cast<int64_t>(k) * kLanes + l] = wl[k].first;
+        f.wvals[wb + static_cast<int64_t>(k) * kLanes + l] = wl[k].second;
       }
       for (size_t k = 0; k < A[l].size(); ++k) {
         const size_t at = (static_cast<size_t>(g) * kTA + k) * kLanes + l;
@@ -546,9 +551,9 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
         f.bval[at] = B[l][k].second;
       }
     }
-    f.pptr.push_back(pb + static_cast<int64_t>(pw) * nr);
-    f.wptr.push_back(wb + static_cast<int64_t>(ww) * nr);
-    f.gptr.push_back(gb + static_cast<int64_t>(gw) * nr);
+    f.pptr.push_back(pb + static_cast<int64_t>(pw) * kLanes);
+    f.wptr.push_back(wb + static_cast<int64_t>(ww) * kLanes);
+    f.gptr.push_back(gb + static_cast<int64_t>(gw) * kLanes);
   }
   // pre-formatted static slot blocks (TMA bulk-copied into the ring)
   const SlotLayout lay(tb);
@@ -559,18 +564,18 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
     auto put_i = [&](int off, int idx, int32_t v) { std::memcpy(blk + off + 4 * idx, &v, 4); };
     for (int l = 0; l < kLanes; ++l) {
       const int row = f.grows[static_cast<size_t>(g) * kLanes + l];
-      put_d(lay.diag, l, row >= 0 ? f.diag[row] : 1.0);
-      put_d(lay.dinv, l, row >= 0 ? f.dinv[row] : 1.0);
+      put_d(lay.dd, 2 * l, row >= 0 ? f.diag[row] : 1.0);
+      put_d(lay.dd, 2 * l + 1, row >= 0 ? f.dinv[row] : 1.0);
       put_i(lay.rows, l, row);
       for (int k = 0; k < kTA; ++k) {
         const size_t at = (static_cast<size_t>(g) * kTA + k) * kLanes + l;
-        put_d(lay.aval, k * kLanes + l, f.aval[at]);
-        put_i(lay.acol, k * kLanes + l, f.acol[at]);
+        std::memcpy(blk + lay.aval + SlotLayout::f64_at(k, l), &f.aval[at], 8);
+        std::memcpy(blk + lay.acol + SlotLayout::i32_at(k, l), &f.acol[at], 4);
       }
       for (int k = 0; k < tb; ++k) {
         const size_t at = (static_cast<size_t>(g) * tb + k) * kLanes + l;
-        put_d(lay.bval, k * kLanes + l, f.bval[at]);
-        put_i(lay.bsrc, k * kLanes + l, f.bsrc[at]);
+        std::memcpy(blk + lay.bval + SlotLayout::f64_at(k, l), &f.bval[at], 8);
+        std::memcpy(blk + lay.bsrc + SlotLayout::i32_at(k, l), &f.bsrc[at], 4);
       }
     }
     put_i(lay.nr, 0, f.nr[g]);

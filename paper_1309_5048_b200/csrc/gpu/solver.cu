@@ -272,8 +272,12 @@ __device__ void flow_setup(double* smem, int n, int ring) {
 // for remote partial sums, [7] helper cycles in total (all helper warps),
 // [8..11] groups by main's distance when the helper published them (g minus
 // groups done: <=1, 2-3, 4-6, >=7), [12..15] the same at the helper's start of
-// the group (<=3, 4-7, 8-11, >=12)
-__device__ unsigned long long g_flow_dbg[16];
+// the group (<=3, 4-7, 8-11, >=12), [16] helper cycles from the end of the
+// last dependency wait to the prefix-sum publication, [17] groups whose last
+// dependency wait had to spin
+__device__ unsigned long long g_flow_dbg[20];
+// helper polling back-off (ns); DSGPU_HSLEEP overrides it (experiments)
+__device__ unsigned g_hsleep = 20;
 // phase diagnostics of the persistent kernel: [0] CTA0 cycles in grid barriers,
 // [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
@@ -316,19 +320,20 @@ __device__ void flow_remote(const DFlow& s, int n, const double* __restrict__ gx
   for (int g = wid; g < s.G; g += W) {
     const int gw = __ldg(s.gw + g);
     if (gw == 0) continue;
-    const int nr = __ldg(s.nr + g), gneed = __ldg(s.gneed + g);
+    const int gneed = __ldg(s.gneed + g);
     const int64_t gb = __ldg(s.gptr + g);
     const unsigned need = static_cast<unsigned>(gneed + 1);
     double part = 0.0;
     SpinGuard sg(abort_flag);
-    for (int k0 = 0; k0 < gw; k0 += PW) {
+    const int32_t* gc = s.gcols + gb + lane;
+    const double* gv = s.gvals + gb + lane;
+    for (int k0 = 0; k0 < gw; k0 += PW, gc += PW * 32, gv += PW * 32) {
       int pc[PW];
       double pv[PW];
 #pragma unroll
-      for (int q = 0; q < PW; ++q) {
-        const bool ok = lane < nr && k0 + q < gw;
-        pc[q] = ok ? __ldg(s.gcols + gb + static_cast<int64_t>(k0 + q) * nr + lane) : n;
-        pv[q] = ok ? __ldg(s.gvals + gb + static_cast<int64_t>(k0 + q) * nr + lane) : 0.0;
+      for (int q = 0; q < PW; ++q) {  // widths are whole chunks, pads are (n, 0)
+        pc[q] = __ldg(gc + q * 32);
+        pv[q] = __ldg(gv + q * 32);
       }
       if (k0 == 0)
         for (;;) {  // the tag must match: stale words of other sweeps never count
@@ -386,8 +391,10 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     //       the column indices were loaded in iteration g-1)
     //   (2) shuffle the B(g) operands out of x(g-1)
     //   (3) load group g+2's A columns and group g+1's psum + static slot data
+    //       (128-bit shared loads, see SlotLayout)
     //   (4) the critical chain: x(g) = (acc_pre(g) - B(g)) / d
     //   (5) acc_pre(g+1) = psum(g+1) - A(g+1)
+    static_assert(kTA % 4 == 0 && TB % 4 == 0 && (kRing & (kRing - 1)) == 0, "slot layout");
     double xprev = 0.0;
     double acc_pre = 0.0, d = 1.0, dv = 1.0;
     int row = -1, nr = 0;
@@ -398,11 +405,11 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     long long wait_cyc = 0, wait_s = 0;
     // readiness flags prefetched one iteration ahead: sready of g+3, pready of g+2
     int pf_p = -2, pf_s = -2;
+    auto slot_of = [&](int gg) { return S.slots + (static_cast<unsigned>(gg) & (kRing - 1)) * lay.bytes; };
     auto wait_static = [&](int gg) {
-      const int sl = gg % kRing;
       if (pf_s != gg) {
         SpinGuard sg(abort_flag);
-        while (S.sready[sl] != gg)
+        while (S.sready[gg & (kRing - 1)] != gg)
           if (sg.expired()) {
             g_flow_dbg[3] = 1000000000ull * 1 + 100000ull * s.G + gg;
             break;
@@ -411,48 +418,61 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         wait_cyc += w;
         wait_s += w;
       }
-      return sl;
     };
     auto wait_psum = [&](int gg) {
-      const int sl = gg % kRing;
       if (pf_p != gg) {
         SpinGuard sg(abort_flag);
-        while (S.pready[sl] != gg)
+        while (S.pready[gg & (kRing - 1)] != gg)
           if (sg.expired()) {
             g_flow_dbg[3] = 1000000000ull * 2 + 100000ull * s.G + gg;
             break;
           }
         wait_cyc += clock64() - sg.t0;
       }
-      return sl;
+    };
+    auto ld_f64 = [&](const uint8_t* arr, double* out, int cnt) {
+      const double2* p = reinterpret_cast<const double2*>(arr) + lane;
+#pragma unroll
+      for (int j = 0; j < cnt / 2; ++j) {
+        const double2 t = p[j * 32];
+        out[2 * j] = t.x;
+        out[2 * j + 1] = t.y;
+      }
+    };
+    auto ld_i32 = [&](const uint8_t* arr, int* out, int cnt) {
+      const int4* p = reinterpret_cast<const int4*>(arr) + lane;
+#pragma unroll
+      for (int j = 0; j < cnt / 4; ++j) {
+        const int4 t = p[j * 32];
+        out[4 * j] = t.x;
+        out[4 * j + 1] = t.y;
+        out[4 * j + 2] = t.z;
+        out[4 * j + 3] = t.w;
+      }
     };
     const int glast = s.G - 1;
     {  // prologue: group 0 complete, group 1's A columns
-      int sl = wait_static(0);
+      wait_static(0);
       wait_psum(0);
       const uint8_t* base = S.slots;
       nr = *reinterpret_cast<const int*>(base + lay.nr);
-      d = reinterpret_cast<const double*>(base + lay.diag)[lane];
-      dv = reinterpret_cast<const double*>(base + lay.dinv)[lane];
+      const double2 ddv = reinterpret_cast<const double2*>(base + lay.dd)[lane];
+      d = ddv.x;
+      dv = ddv.y;
       row = reinterpret_cast<const int*>(base + lay.rows)[lane];
-      const double* av = reinterpret_cast<const double*>(base + lay.aval);
-      const int* ac = reinterpret_cast<const int*>(base + lay.acol);
+      double av[kTA];
+      int ac[kTA];
+      ld_f64(base + lay.aval, av, kTA);
+      ld_i32(base + lay.acol, ac, kTA);
       double pa[kTA];
 #pragma unroll
-      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(av[k * 32 + lane], S.xs[ac[k * 32 + lane]]);
-      acc_pre = sub_rn(S.psum[sl * 32 + lane], tree_sum<kTA>(pa));
-      const double* bv = reinterpret_cast<const double*>(base + lay.bval);
-      const int* bs = reinterpret_cast<const int*>(base + lay.bsrc);
-#pragma unroll
-      for (int k = 0; k < TB; ++k) {
-        bsl[k] = bs[k * 32 + lane];
-        bvl[k] = bv[k * 32 + lane];
-      }
+      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(av[k], S.xs[ac[k]]);
+      acc_pre = sub_rn(S.psum[lane], tree_sum<kTA>(pa));
+      ld_f64(base + lay.bval, bvl, TB);
+      ld_i32(base + lay.bsrc, bsl, TB);
       const int g1 = glast < 1 ? glast : 1;
-      sl = wait_static(g1);
-      const int* ac1 = reinterpret_cast<const int*>(S.slots + static_cast<size_t>(sl) * lay.bytes + lay.acol);
-#pragma unroll
-      for (int k = 0; k < kTA; ++k) acn[k] = ac1[k * 32 + lane];
+      wait_static(g1);
+      ld_i32(slot_of(g1) + lay.acol, acn, kTA);
     }
     for (int g = 0; g < s.G; ++g) {
       const int g1 = g + 1 < s.G ? g + 1 : glast;
@@ -467,34 +487,24 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       for (int k = 0; k < TB; ++k) sx[k] = shfl_d(xprev, bsl[k]);
       asm volatile("" ::: "memory");
       // (3) slot data: g+2's A columns, g+1's psum and static block
-      const int sl2 = wait_static(g2);
-      const int* ac2 = reinterpret_cast<const int*>(S.slots + static_cast<size_t>(sl2) * lay.bytes + lay.acol);
+      wait_static(g2);
       int acn2[kTA];
-#pragma unroll
-      for (int k = 0; k < kTA; ++k) acn2[k] = ac2[k * 32 + lane];
-      const int sl = wait_psum(g1);
-      const uint8_t* base = S.slots + static_cast<size_t>(sl) * lay.bytes;
+      ld_i32(slot_of(g2) + lay.acol, acn2, kTA);
+      wait_psum(g1);
+      const uint8_t* base = slot_of(g1);
       const int nr1 = *reinterpret_cast<const int*>(base + lay.nr);
-      const double ps1 = S.psum[sl * 32 + lane];
-      const double d1 = reinterpret_cast<const double*>(base + lay.diag)[lane];
-      const double dv1 = reinterpret_cast<const double*>(base + lay.dinv)[lane];
+      const double ps1 = S.psum[(g1 & (kRing - 1)) * 32 + lane];
+      const double2 dd1 = reinterpret_cast<const double2*>(base + lay.dd)[lane];
       const int row1 = reinterpret_cast<const int*>(base + lay.rows)[lane];
-      const double* av = reinterpret_cast<const double*>(base + lay.aval);
-      const double* bv = reinterpret_cast<const double*>(base + lay.bval);
-      const int* bs = reinterpret_cast<const int*>(base + lay.bsrc);
       double avl[kTA], bvl1[TB];
       int bsl1[TB];
-#pragma unroll
-      for (int k = 0; k < kTA; ++k) avl[k] = av[k * 32 + lane];
-#pragma unroll
-      for (int k = 0; k < TB; ++k) {
-        bsl1[k] = bs[k * 32 + lane];
-        bvl1[k] = bv[k * 32 + lane];
-      }
+      ld_f64(base + lay.aval, avl, kTA);
+      ld_f64(base + lay.bval, bvl1, TB);
+      ld_i32(base + lay.bsrc, bsl1, TB);
       {  // prefetch readiness flags for the next iteration
         const int g3 = g + 3 < s.G ? g + 3 : glast;
-        pf_p = S.pready[g2 % kRing];
-        pf_s = S.sready[g3 % kRing];
+        pf_p = S.pready[g2 & (kRing - 1)];
+        pf_s = S.sready[g3 & (kRing - 1)];
       }
       asm volatile("" ::: "memory");  // keep the slot loads ahead of the critical chain
       // (4) B(g): the critical chain
@@ -508,7 +518,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       const double x = fma(rr, dv, q0);
       xprev = x;
       if (RING) {
-        S.xs[(g % kXRing) * 32 + lane] = x;
+        S.xs[(g & (kXRing - 1)) * 32 + lane] = x;
         if (lane < nr) gx[row] = x;
       } else if (lane < nr) {
         S.xs[row] = x;
@@ -529,8 +539,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
 #pragma unroll
       for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(avl[k], axv[k]);
       acc_pre = sub_rn(ps1, tree_sum<kTA>(pa));
-      d = d1;
-      dv = dv1;
+      d = dd1.x;
+      dv = dd1.y;
       row = row1;
       nr = nr1;
 #pragma unroll
@@ -588,6 +598,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     const long long th0 = clock64();
     long long tw_need = 0, tw_rem = 0;
     unsigned hpub[4] = {0, 0, 0, 0}, hstart[4] = {0, 0, 0, 0};
+    long long t_post = 0;
+    unsigned n_spun = 0;
     int g = hid;
     int nr = 0, pw = 0;
     int64_t pb0 = 0;
@@ -618,8 +630,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         const int ww = __ldg(s.ww + g);
         const int64_t wb = __ldg(s.wptr + g);
         for (int k = 0; k < ww; ++k) {  // level-merge right-hand-side transform
-          const int j = __ldg(s.wcols + wb + static_cast<int64_t>(k) * nr + lane);
-          rhs = add_rn(rhs, mul_rn(__ldg(s.wvals + wb + static_cast<int64_t>(k) * nr + lane), b[j]));
+          const int j = __ldg(s.wcols + wb + k * 32 + lane);
+          rhs = add_rn(rhs, mul_rn(__ldg(s.wvals + wb + k * 32 + lane), b[j]));
         }
       }
       const int32_t* cp = s.pcols + pb0 + lane;
@@ -651,14 +663,15 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
               break;
             }
           }
-          for (int k0 = 0; k0 < gw; k0 += PW) {
+          const int32_t* gc = s.gcols + gb + lane;
+          const double* gv = s.gvals + gb + lane;
+          for (int k0 = 0; k0 < gw; k0 += PW, gc += PW * 32, gv += PW * 32) {
             int pc[PW];
             double pv[PW];
 #pragma unroll
             for (int q = 0; q < PW; ++q) {
-              const bool ok = lane < nr && k0 + q < gw;
-              pc[q] = ok ? __ldg(s.gcols + gb + static_cast<int64_t>(k0 + q) * nr + lane) : n;
-              pv[q] = ok ? __ldg(s.gvals + gb + static_cast<int64_t>(k0 + q) * nr + lane) : 0.0;
+              pc[q] = __ldg(gc + q * 32);
+              pv[q] = __ldg(gv + q * 32);
             }
             double pp[PW];
 #pragma unroll
@@ -669,26 +682,33 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       }
       // ring-list entries, oldest chunk first; each chunk waits for its own
       // newest dependency, so the next chunk's loads overlap that wait
-      const int c0 = __ldg(s.cptr + g);
-      for (int k0 = 0, c = c0; k0 < pw; k0 += PW, ++c) {
+      const int nch = pw / PW;  // whole chunks (padded on the host)
+      long long t_last = clock64();
+      bool spun = false;
+      const int c0 = nch > 0 ? __ldg(s.cptr + g) : 0;
+      for (int ch = 0; ch < nch; ++ch) {
+        const int32_t* cq = cp + ch * (PW * 32);
+        const double* vq = vp + ch * (PW * 32);
+        const int cn = __ldg(s.cneed + c0 + ch);
         int pc[PW];
         double pv[PW];
-        const int cn = __ldg(s.cneed + c);
 #pragma unroll
         for (int q = 0; q < PW; ++q) {
-          const bool ok = lane < nr && k0 + q < pw;
-          pc[q] = ok ? __ldg(cp + static_cast<int64_t>(k0 + q) * nr) : xcount;
-          pv[q] = ok ? __ldg(vp + static_cast<int64_t>(k0 + q) * nr) : 0.0;
+          pc[q] = __ldg(cq + q * 32);
+          pv[q] = __ldg(vq + q * 32);
         }
         const long long t0 = clock64();
+        spun = false;
         while (*S.progress <= cn) {
-          __nanosleep(20);
+          spun = true;
+          __nanosleep(g_hsleep);
           if (sg.expired()) {
             g_flow_dbg[3] = 1000000ull * (blockIdx.x + 1) + 1000ull * 4 + (g % 1000);
             break;
           }
         }
-        tw_need += clock64() - t0;
+        t_last = clock64();
+        tw_need += t_last - t0;
         double pp[PW];
 #pragma unroll
         for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], S.xs[pc[q]]);
@@ -712,6 +732,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       {
         const int dist = g - *S.progress;
         ++hpub[dist <= 1 ? 0 : dist <= 3 ? 1 : dist <= 6 ? 2 : 3];
+        t_post += clock64() - t_last;
+        n_spun += spun;
       }
       nr = nrn;
       pw = pwn;
@@ -721,6 +743,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       atomicAdd(&g_flow_dbg[5], static_cast<unsigned long long>(tw_need));
       atomicAdd(&g_flow_dbg[6], static_cast<unsigned long long>(tw_rem));
       atomicAdd(&g_flow_dbg[7], static_cast<unsigned long long>(clock64() - th0));
+      atomicAdd(&g_flow_dbg[16], static_cast<unsigned long long>(t_post));
+      atomicAdd(&g_flow_dbg[17], static_cast<unsigned long long>(n_spun));
       for (int i = 0; i < 4; ++i) {
         atomicAdd(&g_flow_dbg[8 + i], static_cast<unsigned long long>(hpub[i]));
         atomicAdd(&g_flow_dbg[12 + i], static_cast<unsigned long long>(hstart[i]));
@@ -1545,6 +1569,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
     h->sms = sms;
     if (const char* env = std::getenv("DSGPU_REMOTE")) h->remote_max = std::max(0, std::atoi(env));
+    if (const char* env = std::getenv("DSGPU_HSLEEP")) {
+      const unsigned ns = static_cast<unsigned>(std::max(0, std::atoi(env)));
+      cudaMemcpyToSymbol(g_hsleep, &ns, sizeof(ns));
+    }
     // smem: two dataflow arrays of the largest IC block
     int nmax = 0;
     for (int b = 0; b < 2; ++b)
@@ -1948,12 +1976,12 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
   return rc;
 }
 
-int dsgpu_debug_counters(int reset, int64_t* out16) {
-  unsigned long long v[16] = {};
+int dsgpu_debug_counters(int reset, int64_t* out20) {
+  unsigned long long v[20] = {};
   cudaMemcpyFromSymbol(v, g_flow_dbg, sizeof(v));
-  for (int i = 0; i < 16; ++i) out16[i] = static_cast<int64_t>(v[i]);
+  for (int i = 0; i < 20; ++i) out20[i] = static_cast<int64_t>(v[i]);
   if (reset) {
-    const unsigned long long z[16] = {};
+    const unsigned long long z[20] = {};
     cudaMemcpyToSymbol(g_flow_dbg, z, sizeof(z));
   }
   return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
