@@ -60,6 +60,18 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def measured_traffic(label: str):
+    """DRAM bytes (read + write) of the dominant kernel per step, from the
+    committed ncu --set full capture of tools/minres_profile.py (both launches
+    of one step summed), or None when no capture matches this workload."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_minres_traffic.json")) as fh:
+            t = json.load(fh)
+        return float(t["dram_bytes_per_step"]) if t.get("workload") == label else None
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -246,7 +258,7 @@ def run_ours(args, world, rank, local):
                     "d2h_bytes_per_step": 8 * (s.n_u + s.n_p) * len(opts)},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": measured_traffic(W["label"]),
                          "peak_kind": peak_kind, "kernel": "minres_kernel (persistent, cooperative)",
                          "algorithmic_bytes_per_step": bytes_step},
             "kernels": kernels,

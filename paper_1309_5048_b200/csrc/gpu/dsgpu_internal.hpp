@@ -100,9 +100,9 @@ struct HostFlow {
   std::vector<int32_t> nr, need, pw, ww, grows;  // per group (grows: G*32)
   std::vector<int64_t> pptr, wptr;           // G + 1, lane-interleaved (stride 32; pw, gw in whole kPW chunks)
   std::vector<int32_t> cptr, cneed;          // per kPW-entry chunk of the prefix list: newest dep group
-  std::vector<int32_t> pcols, wcols;         // pad = n (a zero slot)
+  std::vector<int32_t> pcols, wcols;         // pcols: byte offsets into the x workspace (pad: the zero slot); wcols: rows (pad n)
   std::vector<double> pvals, wvals;
-  std::vector<int32_t> acol;                 // G*kTA*32, pad = n
+  std::vector<int32_t> acol;                 // G*kTA*32: byte offsets into the x workspace, pad = 8n
   std::vector<double> aval;
   std::vector<int32_t> bsrc;                 // G*tb*32: lane in group g-1 (pad 0 with value 0)
   std::vector<double> bval;

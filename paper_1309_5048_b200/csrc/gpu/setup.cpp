@@ -445,7 +445,7 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
   f.wptr.assign(1, 0);
   f.cptr.assign(1, 0);
   f.gptr.assign(1, 0);
-  f.acol.assign(static_cast<size_t>(f.G) * kTA * kLanes, zero_idx);
+  f.acol.assign(static_cast<size_t>(f.G) * kTA * kLanes, 8 * zero_idx);
   f.aval.assign(f.acol.size(), 0.0);
   f.bsrc.assign(static_cast<size_t>(f.G) * tb * kLanes, 0);
   f.bval.assign(f.bsrc.size(), 0.0);
@@ -521,14 +521,14 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
     const int64_t pb = f.pptr.back(), wb = f.wptr.back(), gb = f.gptr.back();
     f.gcols.resize(gb + static_cast<int64_t>(gw) * kLanes, n);
     f.gvals.resize(gb + static_cast<int64_t>(gw) * kLanes, 0.0);
-    f.pcols.resize(pb + static_cast<int64_t>(pw) * kLanes, zero_idx);
+    f.pcols.resize(pb + static_cast<int64_t>(pw) * kLanes, 8 * zero_idx);
     f.pvals.resize(pb + static_cast<int64_t>(pw) * kLanes, 0.0);
     f.wcols.resize(wb + static_cast<int64_t>(ww) * kLanes, n);
     f.wvals.resize(wb + static_cast<int64_t>(ww) * kLanes, 0.0);
     for (int l = 0; l < nr; ++l) {
       const int64_t shift = pw - static_cast<int64_t>(P[l].size());
       for (size_t k = 0; k < P[l].size(); ++k) {
-        f.pcols[pb + (static_cast<int64_t>(k) + shift) * kLanes + l] = sidx(P[l][k].first);
+        f.pcols[pb + (static_cast<int64_t>(k) + shift) * kLanes + l] = 8 * sidx(P[l][k].first);
         f.pvals[pb + (static_cast<int64_t>(k) + shift) * kLanes + l] = P[l][k].second;
       }
       for (size_t k = 0; k < GP[l].size(); ++k) {
@@ -542,7 +542,7 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
       }
       for (size_t k = 0; k < A[l].size(); ++k) {
         const size_t at = (static_cast<size_t>(g) * kTA + k) * kLanes + l;
-        f.acol[at] = sidx(A[l][k].first);
+        f.acol[at] = 8 * sidx(A[l][k].first);
         f.aval[at] = A[l][k].second;
       }
       for (size_t k = 0; k < B[l].size(); ++k) {
@@ -596,7 +596,7 @@ static void flow_stats(const HostFlow& f, const char* name) {
     int na = 0, nb = 0;
     for (int k = 0; k < kTA; ++k)
       for (int l = 0; l < kLanes; ++l)
-        if (f.acol[(static_cast<size_t>(g) * kTA + k) * kLanes + l] != zero_idx) { ++na; break; }
+        if (f.acol[(static_cast<size_t>(g) * kTA + k) * kLanes + l] != 8 * zero_idx) { ++na; break; }
     for (int k = 0; k < f.tb; ++k)
       for (int l = 0; l < kLanes; ++l)
         if (f.bval[(static_cast<size_t>(g) * f.tb + k) * kLanes + l] != 0.0) { ++nb; break; }

@@ -365,6 +365,10 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
   const int xcount = RING ? kXRing * 32 : n;
   FlowSmem S(smem, xcount, lay.bytes);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // x workspace read through byte offsets (one shared load, no index scaling)
+  auto xs_at = [&](int boff) {
+    return *reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(S.xs) + boff);
+  };
   for (int i = threadIdx.x; i < kRing; i += blockDim.x) {
     S.pready[i] = -1;
     S.sready[i] = -1;
@@ -466,7 +470,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       ld_i32(base + lay.acol, ac, kTA);
       double pa[kTA];
 #pragma unroll
-      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(av[k], S.xs[ac[k]]);
+      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(av[k], xs_at(ac[k]));
       acc_pre = sub_rn(S.psum[lane], tree_sum<kTA>(pa));
       ld_f64(base + lay.bval, bvl, TB);
       ld_i32(base + lay.bsrc, bsl, TB);
@@ -480,7 +484,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       // (1) A(g+1) operands
       double axv[kTA];
 #pragma unroll
-      for (int k = 0; k < kTA; ++k) axv[k] = S.xs[acn[k]];
+      for (int k = 0; k < kTA; ++k) axv[k] = xs_at(acn[k]);
       // (2) B(g) operands
       double sx[TB];
 #pragma unroll
@@ -711,7 +715,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         tw_need += t_last - t0;
         double pp[PW];
 #pragma unroll
-        for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], S.xs[pc[q]]);
+        for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], xs_at(pc[q]));
         part = add_rn(part, tree_sum<PW>(pp));
       }
       const double acc = lane < nr ? sub_rn(rhs, part) : 0.0;
