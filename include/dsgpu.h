@@ -137,16 +137,20 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms);
  * levels_fwd_A, levels_bwd_A, levels_fwd_Q, levels_bwd_Q, grid_ctas. */
 int dsgpu_info(const dsgpu_handle* h, int64_t* info);
 
-/* Process-wide sweep diagnostics (summed since the last reset):
- * out16[0..7] = main-warp cycles, main cycles waiting for slots, groups, abort
- * code, main cycles waiting for static slot data, helper cycles waiting for
- * ring dependencies, helper cycles waiting for remote partial sums, helper
+/* Process-wide sweep diagnostics (summed since the last reset), out32:
+ * [0] main-warp cycles, [1] main cycles waiting, [2] groups, [3] abort code,
+ * [4] main cycles waiting for static slot data, [5] helper cycles waiting for
+ * dependencies, [6] helper cycles waiting for remote partial sums, [7] helper
  * cycles; [8..11] groups by the main warp's distance when their prefix sum was
  * published (<=1, 2-3, 4-6, >=7 groups ahead), [12..15] the same when the
- * helper started them (<=3, 4-7, 8-11, >=12); [16] helper cycles from the
- * end of the last dependency wait to publication, [17] groups whose last
- * dependency wait spun, [18..19] 0. */
-int dsgpu_debug_counters(int reset, int64_t* out20);
+ * helper started them (<=3, 4-7, 8-11, >=12); [16] helper cycles from the last
+ * dependency wait to publication, [17] groups whose last wait spun, [18]
+ * co-main cycles waiting, [19..22] helper publication phases (last chunk,
+ * slot reuse, store, fence + flag), [23] co-main cycles from its last wait to
+ * publication, [24..27] co-main publications by the main warp's distance
+ * (<=0, 1, 2, >=3 groups ahead), [28..29] co-main waits that found the
+ * prefix sum / the dependencies not ready, [30..31] 0. */
+int dsgpu_debug_counters(int reset, int64_t* out32);
 /* Persistent-kernel phase diagnostics (cycles): out8 = CTA0 grid-barrier
  * wait, CTA0 IC(0) apply, CTA2 grid-barrier wait, barriers, CTA0 kernel,
  * CTA1 IC(0) apply, 0, 0. */

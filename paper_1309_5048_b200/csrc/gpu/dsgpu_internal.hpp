@@ -37,22 +37,27 @@ struct HostSweep {
 };
 
 // Staged ("flow") sweep plan: the production triangular-solve layout.
-// One CTA runs a sweep with two roles:
-//   * one MAIN warp walks the groups strictly in order; for group g it only
-//     has to add the group's "B" entries (dependencies on group g-1, fetched
-//     from the previous group's registers with warp shuffles) and its "A"
-//     entries (dependencies on groups g-D+1 .. g-2, gathered from shared
-//     memory one iteration ahead), then scale by the reciprocal diagonal with
-//     one Markstein correction (= the correctly rounded quotient);
-//   * HELPER warps run ahead: for group g they wait until groups <= need[g]
-//     are done, sum the row's "prefix" entries (all older dependencies) into
-//     psum = rhs - sum, and stage psum, diag, 1/diag, the A and B entries into
-//     a shared-memory ring slot for the main warp.
+// One CTA runs a sweep with four roles:
+//   * one MAIN warp walks the groups strictly in order; for group g it
+//     gathers the "B" entries (dependencies on groups g-1 and g-2) from the
+//     shared-memory x workspace it wrote itself, subtracts them from the
+//     co-main's partial sum and scales by the reciprocal diagonal with one
+//     Markstein correction (= the correctly rounded quotient). Nothing else
+//     is on its per-level chain;
+//   * one CO-MAIN warp (another SM sub-partition) runs two groups behind the
+//     critical path: for group g it gathers the "A" entries (dependencies on
+//     groups g-D+1 .. g-3) from shared memory and hands acc_pre = psum - A to
+//     the main warp;
+//   * HELPER warps run further ahead: for group g they wait until the groups
+//     each chunk of the row's "prefix" entries (all older dependencies)
+//     depends on are done and stage psum = rhs - sum;
+//   * a PRODUCER thread streams each group's static data (diagonal, A/B
+//     entries) into a shared-memory ring with TMA bulk copies.
 // Within a row the entries are summed in dependency-level order with tree
 // reductions (reassociated w.r.t. the reference's column order: results
 // agree to round-off); the factor and the operation are the
-// same. kTA / kTB are the per-lane register budgets for A and B entries.
-constexpr int kTA = 8, kRing = 16, kFlowD = 7;
+// same. kTA / TB are the per-lane capacities for A and B entries.
+constexpr int kTA = 16, kRing = 16, kSRing = 8, kFlowD = 7;
 // Ring mode (systems whose solution vector does not fit shared memory): the
 // last kXRing groups' results live in a shared-memory ring, older ones in
 // global memory (published every kFenceEvery groups after a fence).
@@ -60,6 +65,7 @@ constexpr int kXRing = 64, kFenceEvery = 8;
 // Supported per-lane B capacities (templates); the plan picks the smallest that fits.
 constexpr int kTBMax = 16;
 constexpr int kPW = 16;  // helper prefix-list chunk (entries per lane)
+constexpr int kPL = 4;   // the last (newest) chunk: small, it is summed after the final wait
 
 // Dependency form of one triangular sweep: row i computes
 //   y_i = (sum_j w_ij b_j - sum_k a_ik y_k) / d_i      (w_ii = 1 implied)
@@ -72,17 +78,18 @@ struct DepRows {
   std::vector<double> diag;
 };
 
-// Byte layout of one group's static main-warp data, identical in HBM (one
-// contiguous block per group, copied by a TMA bulk copy) and in the shared-
-// memory ring slot. Arrays are lane-interleaved in 16-byte units so the main
-// warp reads them with 128-bit shared loads, conflict-free:
+// Byte layout of one group's static data, identical in HBM (one contiguous
+// block per group, copied by a TMA bulk copy) and in the shared-memory ring
+// slot. Arrays are lane-interleaved in 16-byte units so the warps read them
+// with 128-bit shared loads, conflict-free:
 //   dd[32]{diag, dinv} | aval[kTA/2][32]{2 x f64} | bval[tb/2][32]{2 x f64} |
-//   acol[kTA/4][32]{4 x i32} | bsrc[tb/4][32]{4 x i32} | rows[32] i32 | nr.
+//   acol[kTA/4][32]{4 x i32} | bcol[tb/4][32]{4 x i32} | rows[32] i32 |
+//   meta{nr, 0, 0, 0}. acol / bcol are byte offsets into the x workspace.
 struct SlotLayout {
-  int dd, aval, bval, acol, bsrc, rows, nr, bytes;
+  int dd, aval, bval, acol, bcol, rows, meta, bytes;
   constexpr explicit SlotLayout(int tb)
-      : dd(0), aval(512), bval(512 + 256 * kTA), acol(bval + 256 * tb), bsrc(acol + 128 * kTA),
-        rows(bsrc + 128 * tb), nr(rows + 128), bytes(nr + 16) {}
+      : dd(0), aval(512), bval(512 + 256 * kTA), acol(bval + 256 * tb), bcol(acol + 128 * kTA),
+        rows(bcol + 128 * tb), meta(rows + 128), bytes(meta + 16) {}
   // byte offset of element k of lane l in a pair-interleaved f64 array / a
   // quad-interleaved i32 array
   static constexpr int f64_at(int k, int l) { return ((k >> 1) * 32 + l) * 16 + (k & 1) * 8; }
@@ -104,7 +111,7 @@ struct HostFlow {
   std::vector<double> pvals, wvals;
   std::vector<int32_t> acol;                 // G*kTA*32: byte offsets into the x workspace, pad = 8n
   std::vector<double> aval;
-  std::vector<int32_t> bsrc;                 // G*tb*32: lane in group g-1 (pad 0 with value 0)
+  std::vector<int32_t> bcol;                 // G*tb*32: byte offsets into the x workspace, pad = 8n
   std::vector<double> bval;
   std::vector<double> diag, dinv;            // n
 };
@@ -148,14 +155,15 @@ DepRows rows_from_sweep(const HostSweep& s);
 // within each block, dependencies are substituted away (fill in a_ik, and a
 // right-hand-side transform w_ij over the block's rows). Depth / M.
 DepRows merge_levels(const DepRows& r, int M);
-// Largest number of B entries (dependencies on the previous group) of any row.
+// Largest number of B entries (dependencies on groups g-1 and g-2) of any row.
 int flow_b_needed(const DepRows& r);
 void build_flow(const DepRows& r, int tb, int ring, HostFlow& f);
 // Shared memory of one staged sweep with `slots` x entries (rows in full mode,
 // kXRing*32 in ring mode); mirrors FlowSmem in solver.cu.
 inline size_t flow_smem_bytes(int slots, int slot_bytes) {
   return (static_cast<size_t>(slots + 1) * 8 + 127) / 128 * 128 +
-         static_cast<size_t>(kRing) * slot_bytes + kRing * 32 * 8 + kRing * 8 + 3 * kRing * 4 + 64;
+         static_cast<size_t>(kSRing) * slot_bytes + kRing * 32 * 8 + kRing * 32 * 8 + kSRing * 8 +
+         (2 * kRing + 2 * kSRing) * 4 + 64;
 }
 // Ring mode when a full-vector workspace exceeds smem_budget (or n >= force_ring_n).
 int build_block_flows(HostPlan& P, int merge, int* merge_used, size_t smem_budget, int force_ring_n);

@@ -57,7 +57,10 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // Fences on both sides make every write before the barrier visible to every
 // read after it (and invalidate this SM's L1 on the way out). Returns false
 // on timeout (abort flag set) instead of hanging the GPU.
-__device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, unsigned* abort_flag) {
+// Barrier over `expected` CTAs (the participating ones; default: the grid).
+__device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, unsigned* abort_flag,
+                                          unsigned expected = 0) {
+  if (expected == 0) expected = gridDim.x;
   __shared__ int ok_sh;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -65,7 +68,7 @@ __device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, unsign
     const unsigned g = ld_acquire(gen);
     __threadfence();
     const unsigned prev = atomicAdd(count, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == expected - 1) {
       atomicExch(count, 0u);
       __threadfence();
       st_release(gen, g + 1);

@@ -418,7 +418,7 @@ int flow_b_needed(const DepRows& r) {
   int need = 0;
   for (int i = 0; i < r.n; ++i) {
     int c = 0;
-    for (const auto& e : r.ent[i]) c += gof[e.first] == gof[i] - 1;
+    for (const auto& e : r.ent[i]) c += gof[e.first] >= gof[i] - 2;
     need = std::max(need, c);
   }
   return need;
@@ -447,10 +447,10 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
   f.gptr.assign(1, 0);
   f.acol.assign(static_cast<size_t>(f.G) * kTA * kLanes, 8 * zero_idx);
   f.aval.assign(f.acol.size(), 0.0);
-  f.bsrc.assign(static_cast<size_t>(f.G) * tb * kLanes, 0);
-  f.bval.assign(f.bsrc.size(), 0.0);
+  f.bcol.assign(static_cast<size_t>(f.G) * tb * kLanes, 8 * zero_idx);
+  f.bval.assign(f.bcol.size(), 0.0);
   auto sidx = [&](int row) { return ring ? (gof[row] % kXRing) * kLanes + lof[row] : row; };
-  // A window: groups g-flowd+1 .. g-2 are gathered by the main warp
+  // A window: groups g-flowd+1 .. g-3 are gathered by the co-main warp
   const int flowd = std::getenv("DSGPU_FLOWD") ? std::max(3, std::atoi(std::getenv("DSGPU_FLOWD"))) : kFlowD;
   std::vector<std::pair<int, double>> P[kLanes], A[kLanes], B[kLanes], GP[kLanes];
   for (int g = 0; g < f.G; ++g) {
@@ -468,7 +468,7 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
                        [&](const auto& a, const auto& b) { return gof[a.first] < gof[b.first]; });
       for (const auto& x : e) {
         const int dg = gof[x.first];
-        if (dg == g - 1)
+        if (dg >= g - 2)
           B[l].push_back(x);
         else if (dg > g - flowd)
           A[l].push_back(x);
@@ -496,19 +496,21 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
     }
     // widths padded to whole chunks; lists lane-interleaved with stride 32 so
     // the helpers load them with constant offsets and no predicates
-    pw = (pw + kPW - 1) / kPW * kPW;
+    // prefix widths: kPW-entry chunks then one kPL-entry last chunk
+    pw = pw > 0 ? kPL + (std::max(pw - kPL, 0) + kPW - 1) / kPW * kPW : 0;
     gw = (gw + kPW - 1) / kPW * kPW;
     // prefix lists are right-aligned (padding first) so every lane's newest
     // entries share the last chunk and older chunks can go early
     for (int l = 0; l < nr; ++l) {
       const int shift = pw - static_cast<int>(P[l].size());
       for (size_t k = 0; k < P[l].size(); ++k) {  // per-chunk newest dependency
-        const size_t c = (k + shift) / kPW;
+        const int pos = static_cast<int>(k) + shift;
+        const size_t c = pos >= pw - kPL ? (pw - kPL) / kPW : pos / kPW;
         if (cneed_g.size() <= c) cneed_g.resize(c + 1, -1);
         cneed_g[c] = std::max(cneed_g[c], gof[P[l][k].first]);
       }
     }
-    cneed_g.resize(pw / kPW, -1);
+    cneed_g.resize(pw > 0 ? (pw - kPL) / kPW + 1 : 0, -1);
     f.nr.push_back(nr);
     f.need.push_back(need);
     for (const int c : cneed_g) f.cneed.push_back(c);
@@ -547,7 +549,7 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
       }
       for (size_t k = 0; k < B[l].size(); ++k) {
         const size_t at = (static_cast<size_t>(g) * tb + k) * kLanes + l;
-        f.bsrc[at] = lof[B[l][k].first];
+        f.bcol[at] = 8 * sidx(B[l][k].first);
         f.bval[at] = B[l][k].second;
       }
     }
@@ -575,10 +577,15 @@ void build_flow(const DepRows& r, int tb, int ring, HostFlow& f) {
       for (int k = 0; k < tb; ++k) {
         const size_t at = (static_cast<size_t>(g) * tb + k) * kLanes + l;
         std::memcpy(blk + lay.bval + SlotLayout::f64_at(k, l), &f.bval[at], 8);
-        std::memcpy(blk + lay.bsrc + SlotLayout::i32_at(k, l), &f.bsrc[at], 4);
+        std::memcpy(blk + lay.bcol + SlotLayout::i32_at(k, l), &f.bcol[at], 4);
       }
     }
-    put_i(lay.nr, 0, f.nr[g]);
+    put_i(lay.meta, 0, f.nr[g]);
+    int nb = 0;  // B entries of the widest lane (left-aligned): the main warp skips empty 4-chunks
+    for (int k = 0; k < tb; ++k)
+      for (int l = 0; l < kLanes; ++l)
+        if (f.bcol[(static_cast<size_t>(g) * tb + k) * kLanes + l] != 8 * zero_idx) nb = k + 1;
+    put_i(lay.meta, 1, (nb + 3) / 4);
   }
 }
 
@@ -600,6 +607,7 @@ static void flow_stats(const HostFlow& f, const char* name) {
     for (int k = 0; k < f.tb; ++k)
       for (int l = 0; l < kLanes; ++l)
         if (f.bval[(static_cast<size_t>(g) * f.tb + k) * kLanes + l] != 0.0) { ++nb; break; }
+
     sa += na;
     sb += nb;
     sp += f.pw[g];
@@ -628,7 +636,7 @@ int build_block_flows(HostPlan& P, int merge, int* merge_used, size_t smem_budge
       need = std::max({need, flow_b_needed(rows[b][0]), flow_b_needed(rows[b][1])});
     }
     if (need > kTBMax) continue;
-    const int tb = need <= 4 ? 4 : need <= 8 ? 8 : 16;
+    const int tb = need <= 8 ? 8 : 16;
     // one kernel variant per handle: ring mode for all IC blocks if any block's
     // full-vector workspace (flow_smem_bytes) does not fit shared memory
     int ring = 0;

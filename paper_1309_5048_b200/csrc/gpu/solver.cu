@@ -28,6 +28,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "dsgpu_internal.hpp"
@@ -56,9 +57,9 @@ struct DSweep {
 
 struct DFlow {
   int G;
-  const int32_t *nr, *need, *pw, *ww, *grows, *pcols, *wcols, *acol, *bsrc;
+  const int32_t *nr, *pw, *ww, *grows, *pcols, *wcols;
   const int64_t *pptr, *wptr;
-  const double *pvals, *wvals, *aval, *bval, *diag, *dinv;
+  const double *pvals, *wvals;
   const uint8_t* stat;  // G * SlotLayout(tb).bytes, 16-byte aligned
   int ring;
   const int32_t *gw, *gneed, *gcols;
@@ -94,6 +95,22 @@ struct DevReport {
   long long inner[2], apps[2];
 };
 
+// Request / completion mailbox of one IC(0) server CTA (one per IC block).
+// Workers post a request with st.release on `req`; the server answers with the
+// CTA's <r, z> on `rz` and st.release on `done`.
+enum { IC_OP_S1 = 1, IC_OP_L2 = 2, IC_OP_EXIT = 3 };
+struct alignas(128) Mailbox {
+  unsigned req;
+  int op;
+  double alpha;          // L2: r -= alpha q
+  const double* src0;    // S1: r = src0 (+ coef src1), also stored to dst
+  const double* src1;
+  double coef;
+  double* dst;
+  alignas(128) unsigned done;
+  double rz;
+};
+
 struct Args {
   int n, n_u, n_p;
   const int64_t* k_rp;
@@ -123,6 +140,8 @@ struct Args {
   DevReport* rep;
   int smem_half;  // doubles per dataflow array (largest IC block)
   unsigned launch_id;  // distinguishes the sweep tags of successive launches
+  int n_srv;           // CTAs [0, n_srv) are IC(0) servers (CTA b serves block b)
+  Mailbox* mbox;       // [2]
 };
 
 // ---------------------------------------------------------------------------
@@ -220,15 +239,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
-// Shared-memory workspace of one staged sweep: xs[n+1] | ring of kRing static
-// slots (SlotLayout, filled by TMA bulk copies) | psum[kRing][32] | mbarriers
-// | psum flags | progress.
+// Shared-memory workspace of one staged sweep: xs[n+1] | ring of kSRing static
+// slots (SlotLayout, filled by TMA bulk copies) | psum[kRing][32] (helpers ->
+// co-main) | apre[kRing][32] (co-main -> main) | mbarriers | flags | progress.
 struct FlowSmem {
   double* xs;
   uint8_t* slots;
   double* psum;
+  double* apre;
   uint64_t* mbar;
   volatile int* pready;   // psum of group g staged (helpers)
+  volatile int* aready;   // acc_pre of group g staged (co-main)
   volatile int* sready;   // static data of group g landed (producer, after its mbarrier)
   volatile int* progress;
   volatile int* gprogress;  // ring mode: groups whose results are visible in global memory
@@ -239,11 +260,13 @@ struct FlowSmem {
     xs = base;
     const size_t xbytes = (static_cast<size_t>(n + 1) * 8 + 127) / 128 * 128;
     slots = reinterpret_cast<uint8_t*>(base) + xbytes;
-    psum = reinterpret_cast<double*>(slots + static_cast<size_t>(kRing) * sb);
-    mbar = reinterpret_cast<uint64_t*>(psum + kRing * 32);
-    pready = reinterpret_cast<volatile int*>(mbar + kRing);
-    sready = pready + kRing;
-    progress = sready + kRing;
+    psum = reinterpret_cast<double*>(slots + static_cast<size_t>(kSRing) * sb);
+    apre = psum + kRing * 32;
+    mbar = reinterpret_cast<uint64_t*>(apre + kRing * 32);
+    pready = reinterpret_cast<volatile int*>(mbar + kSRing);
+    aready = pready + kRing;
+    sready = aready + kRing;
+    progress = sready + kSRing;
     gprogress = progress + 1;
     base_use = const_cast<int*>(gprogress) + 1;
   }
@@ -256,7 +279,7 @@ struct FlowSmem {
 template <int TB>
 __device__ void flow_setup(double* smem, int n, int ring) {
   FlowSmem S(smem, ring ? kXRing * 32 : n, SlotLayout(TB).bytes);
-  for (int i = threadIdx.x; i < kRing; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kSRing; i += blockDim.x) {
     mbar_init(S.mbar + i, 1);
     S.base_use[i] = 0;
   }
@@ -275,9 +298,12 @@ __device__ void flow_setup(double* smem, int n, int ring) {
 // the group (<=3, 4-7, 8-11, >=12), [16] helper cycles from the end of the
 // last dependency wait to the prefix-sum publication, [17] groups whose last
 // dependency wait had to spin
-__device__ unsigned long long g_flow_dbg[20];
+__device__ unsigned long long g_flow_dbg[32];
 // helper polling back-off (ns); DSGPU_HSLEEP overrides it (experiments)
 __device__ unsigned g_hsleep = 20;
+// timing experiments only (DSGPU_NOWAIT=1): the main warp does not wait for
+// the co-mains (results are wrong); isolates the main warp's own loop cost
+__device__ int g_nowait = 0;
 // phase diagnostics of the persistent kernel: [0] CTA0 cycles in grid barriers,
 // [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
@@ -359,8 +385,13 @@ __device__ void flow_remote(const DFlow& s, int n, const double* __restrict__ gx
 
 // gx: ring mode only -- results are written there (global, n+1 with gx[n] = 0).
 template <int TB, bool RING>
-__device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __restrict__ b,
+__device__ void flow_sweep(const DFlow& s_in, int n, double* smem, const double* __restrict__ b,
                            double* gx, FlowRemote R, unsigned* abort_flag) {
+  // Local copy of the plan's header: reached through a generic pointer in the
+  // persistent kernel, its fields would be reloaded after every volatile
+  // shared-memory access otherwise.
+  const DFlow s = s_in;
+  const int G = s.G;
   const SlotLayout lay(TB);
   const int xcount = RING ? kXRing * 32 : n;
   FlowSmem S(smem, xcount, lay.bytes);
@@ -371,7 +402,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
   };
   for (int i = threadIdx.x; i < kRing; i += blockDim.x) {
     S.pready[i] = -1;
-    S.sready[i] = -1;
+    S.aready[i] = -1;
+    if (i < kSRing) S.sready[i] = -1;
   }
   if (threadIdx.x == 0) {
     *S.progress = 0;
@@ -380,42 +412,54 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
   }
   __syncthreads();
   // roles: main = last warp; producer = lane 0 of the warp 4 below it (same
-  // SM sub-partition, nearly idle); helpers = warps on the other three
-  // sub-partitions.
+  // SM sub-partition, nearly idle); co-mains = the kCo warps before main (other
+  // sub-partition); helpers = the remaining warps off main's sub-partition.
+  constexpr int kCo = 2;  // co-main warps (round-robin over groups)
   const int mainw = nw - 1, prodw = nw - 5;
+  const int cid = warp < mainw && warp >= mainw - kCo ? mainw - 1 - warp : -1;
   int hid = -1, nh = 0;
   for (int w = 0; w < nw; ++w)
-    if (w != mainw && (w & 3) != (mainw & 3)) {
+    if (w != mainw && !(w < mainw && w >= mainw - kCo) && (w & 3) != (mainw & 3)) {
       if (w == warp) hid = nh;
       ++nh;
     }
-  if (warp == mainw && s.G > 0) {
-    // Software pipeline, iteration g:
-    //   (1) gather the A(g+1) operands from xs (their groups <= g-1 are final;
-    //       the column indices were loaded in iteration g-1)
-    //   (2) shuffle the B(g) operands out of x(g-1)
-    //   (3) load group g+2's A columns and group g+1's psum + static slot data
-    //       (128-bit shared loads, see SlotLayout)
-    //   (4) the critical chain: x(g) = (acc_pre(g) - B(g)) / d
-    //   (5) acc_pre(g+1) = psum(g+1) - A(g+1)
-    static_assert(kTA % 4 == 0 && TB % 4 == 0 && (kRing & (kRing - 1)) == 0, "slot layout");
-    double xprev = 0.0;
-    double acc_pre = 0.0, d = 1.0, dv = 1.0;
-    int row = -1, nr = 0;
-    double bvl[TB];
-    int bsl[TB];
-    int acn[kTA];  // A columns of group g+1
+  auto ld_f64 = [&](const uint8_t* arr, double* out, int cnt) {
+    const double2* p = reinterpret_cast<const double2*>(arr) + lane;
+#pragma unroll
+    for (int j = 0; j < cnt / 2; ++j) {
+      const double2 t = p[j * 32];
+      out[2 * j] = t.x;
+      out[2 * j + 1] = t.y;
+    }
+  };
+  auto ld_i32 = [&](const uint8_t* arr, int* out, int cnt) {
+    const int4* p = reinterpret_cast<const int4*>(arr) + lane;
+#pragma unroll
+    for (int j = 0; j < cnt / 4; ++j) {
+      const int4 t = p[j * 32];
+      out[4 * j] = t.x;
+      out[4 * j + 1] = t.y;
+      out[4 * j + 2] = t.z;
+      out[4 * j + 3] = t.w;
+    }
+  };
+  auto slot_of = [&](int gg) { return S.slots + (static_cast<unsigned>(gg) & (kSRing - 1)) * lay.bytes; };
+  static_assert(kTA % 4 == 0 && TB % 4 == 0 && (kRing & (kRing - 1)) == 0 &&
+                    (kSRing & (kSRing - 1)) == 0, "slot layout");
+  if (warp == mainw && G > 0) {
+    // iteration g: gather the B operands (groups g-1, g-2: written by this
+    // warp) from xs, take the co-main's acc_pre(g), x(g) = (acc_pre - B) / d.
+    // Group g+1's B offsets are loaded one iteration ahead.
+    int bcn[TB];
     const long long t_main0 = clock64();
     long long wait_cyc = 0, wait_s = 0;
-    // readiness flags prefetched one iteration ahead: sready of g+3, pready of g+2
-    int pf_p = -2, pf_s = -2;
-    auto slot_of = [&](int gg) { return S.slots + (static_cast<unsigned>(gg) & (kRing - 1)) * lay.bytes; };
+    int pf_s = -2;  // sready of g+1, prefetched one iteration ahead
     auto wait_static = [&](int gg) {
       if (pf_s != gg) {
         SpinGuard sg(abort_flag);
-        while (S.sready[gg & (kRing - 1)] != gg)
+        while (S.sready[gg & (kSRing - 1)] != gg)
           if (sg.expired()) {
-            g_flow_dbg[3] = 1000000000ull * 1 + 100000ull * s.G + gg;
+            g_flow_dbg[3] = 1000000000ull * 1 + 100000ull * G + gg;
             break;
           }
         const long long w = clock64() - sg.t0;
@@ -423,104 +467,58 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         wait_s += w;
       }
     };
-    auto wait_psum = [&](int gg) {
-      if (pf_p != gg) {
+    const int glast = G - 1;
+    wait_static(0);
+    ld_i32(S.slots + lay.bcol, bcn, TB);
+    for (int g = 0; g < G; ++g) {
+      const uint8_t* base = slot_of(g);
+      // (1) B operands and values in halves of at most 8 (register pressure)
+      constexpr int TH = TB < 8 ? TB : 8;
+      double bsum[TB / TH];
+#pragma unroll
+      for (int hh = 0; hh < TB / TH; ++hh) {
+        double xb[TH], bv[TH], pb[TH];
+#pragma unroll
+        for (int k = 0; k < TH; ++k) xb[k] = xs_at(bcn[hh * TH + k]);
+        const double2* bvp = reinterpret_cast<const double2*>(base + lay.bval) + lane + hh * (TH / 2) * 32;
+#pragma unroll
+        for (int j = 0; j < TH / 2; ++j) {
+          const double2 t = bvp[j * 32];
+          bv[2 * j] = t.x;
+          bv[2 * j + 1] = t.y;
+        }
+#pragma unroll
+        for (int k = 0; k < TH; ++k) pb[k] = mul_rn(bv[k], xb[k]);
+        bsum[hh] = tree_sum<TH>(pb);
+      }
+      // (2) this group's static values (landed: checked in iteration g-1)
+      const double2 ddv = reinterpret_cast<const double2*>(base + lay.dd)[lane];
+      const int row = reinterpret_cast<const int*>(base + lay.rows)[lane];
+      const int nr = *reinterpret_cast<const int*>(base + lay.meta);
+      // (3) next group's B offsets
+      const int g1 = g + 1 < G ? g + 1 : glast;
+      wait_static(g1);
+      int bcn1[TB];
+      ld_i32(slot_of(g1) + lay.bcol, bcn1, TB);
+      pf_s = S.sready[(g + 2 < G ? g + 2 : glast) & (kSRing - 1)];
+      // (4) acc_pre(g) from the co-mains
+      const int sa = g & (kRing - 1);
+      if (!g_nowait && S.aready[sa] != g) {
         SpinGuard sg(abort_flag);
-        while (S.pready[gg & (kRing - 1)] != gg)
+        while (S.aready[sa] != g)
           if (sg.expired()) {
-            g_flow_dbg[3] = 1000000000ull * 2 + 100000ull * s.G + gg;
+            g_flow_dbg[3] = 1000000000ull * 2 + 100000ull * G + g;
             break;
           }
         wait_cyc += clock64() - sg.t0;
       }
-    };
-    auto ld_f64 = [&](const uint8_t* arr, double* out, int cnt) {
-      const double2* p = reinterpret_cast<const double2*>(arr) + lane;
-#pragma unroll
-      for (int j = 0; j < cnt / 2; ++j) {
-        const double2 t = p[j * 32];
-        out[2 * j] = t.x;
-        out[2 * j + 1] = t.y;
-      }
-    };
-    auto ld_i32 = [&](const uint8_t* arr, int* out, int cnt) {
-      const int4* p = reinterpret_cast<const int4*>(arr) + lane;
-#pragma unroll
-      for (int j = 0; j < cnt / 4; ++j) {
-        const int4 t = p[j * 32];
-        out[4 * j] = t.x;
-        out[4 * j + 1] = t.y;
-        out[4 * j + 2] = t.z;
-        out[4 * j + 3] = t.w;
-      }
-    };
-    const int glast = s.G - 1;
-    {  // prologue: group 0 complete, group 1's A columns
-      wait_static(0);
-      wait_psum(0);
-      const uint8_t* base = S.slots;
-      nr = *reinterpret_cast<const int*>(base + lay.nr);
-      const double2 ddv = reinterpret_cast<const double2*>(base + lay.dd)[lane];
-      d = ddv.x;
-      dv = ddv.y;
-      row = reinterpret_cast<const int*>(base + lay.rows)[lane];
-      double av[kTA];
-      int ac[kTA];
-      ld_f64(base + lay.aval, av, kTA);
-      ld_i32(base + lay.acol, ac, kTA);
-      double pa[kTA];
-#pragma unroll
-      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(av[k], xs_at(ac[k]));
-      acc_pre = sub_rn(S.psum[lane], tree_sum<kTA>(pa));
-      ld_f64(base + lay.bval, bvl, TB);
-      ld_i32(base + lay.bsrc, bsl, TB);
-      const int g1 = glast < 1 ? glast : 1;
-      wait_static(g1);
-      ld_i32(slot_of(g1) + lay.acol, acn, kTA);
-    }
-    for (int g = 0; g < s.G; ++g) {
-      const int g1 = g + 1 < s.G ? g + 1 : glast;
-      const int g2 = g + 2 < s.G ? g + 2 : glast;
-      // (1) A(g+1) operands
-      double axv[kTA];
-#pragma unroll
-      for (int k = 0; k < kTA; ++k) axv[k] = xs_at(acn[k]);
-      // (2) B(g) operands
-      double sx[TB];
-#pragma unroll
-      for (int k = 0; k < TB; ++k) sx[k] = shfl_d(xprev, bsl[k]);
-      asm volatile("" ::: "memory");
-      // (3) slot data: g+2's A columns, g+1's psum and static block
-      wait_static(g2);
-      int acn2[kTA];
-      ld_i32(slot_of(g2) + lay.acol, acn2, kTA);
-      wait_psum(g1);
-      const uint8_t* base = slot_of(g1);
-      const int nr1 = *reinterpret_cast<const int*>(base + lay.nr);
-      const double ps1 = S.psum[(g1 & (kRing - 1)) * 32 + lane];
-      const double2 dd1 = reinterpret_cast<const double2*>(base + lay.dd)[lane];
-      const int row1 = reinterpret_cast<const int*>(base + lay.rows)[lane];
-      double avl[kTA], bvl1[TB];
-      int bsl1[TB];
-      ld_f64(base + lay.aval, avl, kTA);
-      ld_f64(base + lay.bval, bvl1, TB);
-      ld_i32(base + lay.bsrc, bsl1, TB);
-      {  // prefetch readiness flags for the next iteration
-        const int g3 = g + 3 < s.G ? g + 3 : glast;
-        pf_p = S.pready[g2 & (kRing - 1)];
-        pf_s = S.sready[g3 & (kRing - 1)];
-      }
-      asm volatile("" ::: "memory");  // keep the slot loads ahead of the critical chain
-      // (4) B(g): the critical chain
-      double pb[TB];
-#pragma unroll
-      for (int k = 0; k < TB; ++k) pb[k] = mul_rn(bvl[k], sx[k]);
-      const double acc = sub_rn(acc_pre, tree_sum<TB>(pb));
+      const double ap = S.apre[sa * 32 + lane];
+      // (5) the critical chain
+      const double acc = sub_rn(ap, tree_sum<TB / TH>(bsum));
       // correctly rounded acc / d from the reciprocal (one Markstein step)
-      const double q0 = mul_rn(acc, dv);
-      const double rr = fma(-q0, d, acc);
-      const double x = fma(rr, dv, q0);
-      xprev = x;
+      const double q0 = mul_rn(acc, ddv.y);
+      const double rr = fma(-q0, ddv.x, acc);
+      const double x = fma(rr, ddv.y, q0);
       if (RING) {
         S.xs[(g & (kXRing - 1)) * 32 + lane] = x;
         if (lane < nr) gx[row] = x;
@@ -529,7 +527,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       }
       __syncwarp();
       if (lane == 0) *S.progress = g + 1;
-      if (RING && ((g + 1) % kFenceEvery == 0 || g + 1 == s.G)) {
+      if (RING && ((g + 1) % kFenceEvery == 0 || g + 1 == G)) {
         __threadfence();  // publish older results in global memory
         __syncwarp();
         if (lane == 0) {
@@ -538,39 +536,73 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
             st_relaxed_u64(R.gprog, (static_cast<unsigned long long>(R.tag) << 32) | (g + 1));
         }
       }
-      // (5) A(g+1)
-      double pa[kTA];
 #pragma unroll
-      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(avl[k], axv[k]);
-      acc_pre = sub_rn(ps1, tree_sum<kTA>(pa));
-      d = dd1.x;
-      dv = dd1.y;
-      row = row1;
-      nr = nr1;
-#pragma unroll
-      for (int k = 0; k < TB; ++k) {
-        bsl[k] = bsl1[k];
-        bvl[k] = bvl1[k];
-      }
-#pragma unroll
-      for (int k = 0; k < kTA; ++k) acn[k] = acn2[k];
+      for (int k = 0; k < TB; ++k) bcn[k] = bcn1[k];
     }
     if (lane == 0) {
       atomicAdd(&g_flow_dbg[0], static_cast<unsigned long long>(clock64() - t_main0));
       atomicAdd(&g_flow_dbg[1], static_cast<unsigned long long>(wait_cyc));
-      atomicAdd(&g_flow_dbg[2], static_cast<unsigned long long>(s.G));
+      atomicAdd(&g_flow_dbg[2], static_cast<unsigned long long>(G));
       atomicAdd(&g_flow_dbg[4], static_cast<unsigned long long>(wait_s));
+    }
+  } else if (cid >= 0) {
+    // co-main: acc_pre(h) = psum(h) - A(h); A's dependencies are groups <= h-3
+    long long wait_co = 0, t_work = 0;
+    unsigned cpub[4] = {0, 0, 0, 0}, cwhy[2] = {0, 0};
+    for (int h = cid; h < G; h += kCo) {
+      SpinGuard sg(abort_flag);
+      while (S.sready[h & (kSRing - 1)] != h)
+        if (sg.expired()) {
+          g_flow_dbg[3] = 1000000000ull * 9 + 100000ull * G + h;
+          break;
+        }
+      const uint8_t* base = slot_of(h);
+      double av[kTA];
+      int ac[kTA];
+      ld_i32(base + lay.acol, ac, kTA);
+      ld_f64(base + lay.aval, av, kTA);
+      const int sp = h & (kRing - 1);
+      const long long t0 = clock64();
+      cwhy[0] += S.pready[sp] != h;
+      cwhy[1] += *S.progress < h - 2;
+      while (S.pready[sp] != h || *S.progress < h - 2)
+        if (sg.expired()) {
+          g_flow_dbg[3] = 1000000000ull * 10 + 100000ull * G + h;
+          break;
+        }
+      const long long t1 = clock64();
+      wait_co += t1 - t0;
+      const double ps = S.psum[sp * 32 + lane];
+      double pa[kTA];
+#pragma unroll
+      for (int k = 0; k < kTA; ++k) pa[k] = mul_rn(av[k], xs_at(ac[k]));
+      S.apre[sp * 32 + lane] = sub_rn(ps, tree_sum<kTA>(pa));
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        S.aready[sp] = h;
+      }
+      t_work += clock64() - t1;
+      const int dist = h - *S.progress;
+      ++cpub[dist <= 0 ? 0 : dist == 1 ? 1 : dist == 2 ? 2 : 3];
+    }
+    if (lane == 0) {
+      atomicAdd(&g_flow_dbg[18], static_cast<unsigned long long>(wait_co));
+      atomicAdd(&g_flow_dbg[23], static_cast<unsigned long long>(t_work));
+      for (int i = 0; i < 4; ++i) atomicAdd(&g_flow_dbg[24 + i], static_cast<unsigned long long>(cpub[i]));
+      atomicAdd(&g_flow_dbg[28], static_cast<unsigned long long>(cwhy[0]));
+      atomicAdd(&g_flow_dbg[29], static_cast<unsigned long long>(cwhy[1]));
     }
   } else if (warp == prodw) {
     if (lane == 0) {
       int issued = 0, done = 0;
       SpinGuard sg(abort_flag);
-      while (done < s.G) {
+      while (done < G) {
         bool idle = true;
         // issue: the slot's previous group (issued - kRing) was loaded by main
         // iteration issued - kRing - 1
-        if (issued < s.G && *S.progress >= issued - kRing + 2) {
-          const int sl = issued % kRing;
+        if (issued < G && *S.progress >= issued - kSRing + 2) {
+          const int sl = issued % kSRing;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_expect_tx(S.mbar + sl, lay.bytes);
           bulk_g2s(S.slots + static_cast<size_t>(sl) * lay.bytes,
@@ -580,8 +612,8 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         }
         // complete: publish the oldest outstanding copy once it has landed
         if (done < issued) {
-          const int sl = done % kRing;
-          if (mbar_test(S.mbar + sl, (S.base_use[sl] + done / kRing) & 1)) {
+          const int sl = done % kSRing;
+          if (mbar_test(S.mbar + sl, (S.base_use[sl] + done / kSRing) & 1)) {
             S.sready[sl] = done;
             ++done;
             idle = false;
@@ -589,7 +621,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         }
         if (idle) {
           if (sg.expired()) {
-            g_flow_dbg[3] = 1000000000ull * 3 + 100000ull * s.G + done;
+            g_flow_dbg[3] = 1000000000ull * 3 + 100000ull * G + done;
             break;
           }
         } else {
@@ -602,17 +634,17 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     const long long th0 = clock64();
     long long tw_need = 0, tw_rem = 0;
     unsigned hpub[4] = {0, 0, 0, 0}, hstart[4] = {0, 0, 0, 0};
-    long long t_post = 0;
+    long long t_post = 0, t_pa = 0, t_pb = 0, t_pc = 0, t_pd = 0;
     unsigned n_spun = 0;
     int g = hid;
     int nr = 0, pw = 0;
     int64_t pb0 = 0;
-    if (g < s.G) {
+    if (g < G) {
       nr = __ldg(s.nr + g);
       pw = __ldg(s.pw + g);
       pb0 = __ldg(s.pptr + g);
     }
-    for (; g < s.G; g += nh) {
+    for (; g < G; g += nh) {
       const int sl = g % kRing;
       const int gn = g + nh;
       {
@@ -621,7 +653,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       }
       int nrn = 0, pwn = 0;
       int64_t pbn = 0;
-      if (gn < s.G) {
+      if (gn < G) {
         nrn = __ldg(s.nr + gn);
         pwn = __ldg(s.pw + gn);
         pbn = __ldg(s.pptr + gn);
@@ -640,7 +672,9 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       }
       const int32_t* cp = s.pcols + pb0 + lane;
       const double* vp = s.pvals + pb0 + lane;
-      double part = 0.0;
+      // acc = rhs - (older entries) - (chunk sums): consuming rhs first keeps
+      // its global load off the path after the last dependency wait
+      double acc = lane < nr ? rhs : 0.0;
       SpinGuard sg(abort_flag);
       if (RING && R.on) {  // entries older than the ring: remote helpers' partial sum
         if (__ldg(s.gw + g) > 0) {
@@ -648,12 +682,12 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
           while (ld_acquire(R.rflag + g) != R.tag) {
             __nanosleep(20);
             if (sg.expired()) {
-              g_flow_dbg[3] = 1000000000ull * 8 + 100000ull * s.G + g;
+              g_flow_dbg[3] = 1000000000ull * 8 + 100000ull * G + g;
               break;
             }
           }
           tw_rem += clock64() - t0;
-          part = __ldcg(R.rpsum + static_cast<int64_t>(g) * 32 + lane);
+          acc = sub_rn(acc, __ldcg(R.rpsum + static_cast<int64_t>(g) * 32 + lane));
         }
       } else if (RING) {  // entries older than the ring: global memory, once published
         const int gw = __ldg(s.gw + g);
@@ -663,7 +697,7 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
           while (*S.gprogress <= gneed) {
             __nanosleep(20);
             if (sg.expired()) {
-              g_flow_dbg[3] = 1000000000ull * 6 + 100000ull * s.G + g;
+              g_flow_dbg[3] = 1000000000ull * 6 + 100000ull * G + g;
               break;
             }
           }
@@ -680,30 +714,33 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
             double pp[PW];
 #pragma unroll
             for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], __ldcg(gx + pc[q]));
-            part = add_rn(part, tree_sum<PW>(pp));
+            acc = sub_rn(acc, tree_sum<PW>(pp));
           }
         }
       }
       // ring-list entries, oldest chunk first; each chunk waits for its own
       // newest dependency, so the next chunk's loads overlap that wait
-      const int nch = pw / PW;  // whole chunks (padded on the host)
+      // kPW-entry chunks, then the small last chunk (the newest entries)
+      const int nbig = pw > 0 ? (pw - kPL) / PW : -1;
       long long t_last = clock64();
       bool spun = false;
-      const int c0 = nch > 0 ? __ldg(s.cptr + g) : 0;
-      for (int ch = 0; ch < nch; ++ch) {
+      int seen = 0;  // last progress value observed
+      const int c0 = pw > 0 ? __ldg(s.cptr + g) : 0;
+      auto chunk = [&](auto width, int ch) {
+        constexpr int CW = decltype(width)::value;
         const int32_t* cq = cp + ch * (PW * 32);
         const double* vq = vp + ch * (PW * 32);
         const int cn = __ldg(s.cneed + c0 + ch);
-        int pc[PW];
-        double pv[PW];
+        int pc[CW];
+        double pv[CW];
 #pragma unroll
-        for (int q = 0; q < PW; ++q) {
+        for (int q = 0; q < CW; ++q) {
           pc[q] = __ldg(cq + q * 32);
           pv[q] = __ldg(vq + q * 32);
         }
         const long long t0 = clock64();
         spun = false;
-        while (*S.progress <= cn) {
+        while ((seen = *S.progress) <= cn) {
           spun = true;
           __nanosleep(g_hsleep);
           if (sg.expired()) {
@@ -713,26 +750,37 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
         }
         t_last = clock64();
         tw_need += t_last - t0;
-        double pp[PW];
+        double pp[CW];
 #pragma unroll
-        for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], xs_at(pc[q]));
-        part = add_rn(part, tree_sum<PW>(pp));
-      }
-      const double acc = lane < nr ? sub_rn(rhs, part) : 0.0;
-      // psum slot reuse: group g - kRing's psum was read by main iteration g - kRing - 1
-      while (*S.progress < g - kRing + 2) {
+        for (int q = 0; q < CW; ++q) pp[q] = mul_rn(pv[q], xs_at(pc[q]));
+        acc = sub_rn(acc, tree_sum<CW>(pp));
+      };
+      for (int ch = 0; ch < nbig; ++ch) chunk(std::integral_constant<int, PW>(), ch);
+      if (nbig >= 0) chunk(std::integral_constant<int, kPL>(), nbig);
+      if (lane >= nr) acc = 0.0;
+      const long long t_a = clock64();
+      // psum slot reuse: group g - kRing's psum was consumed before the main
+      // warp's iteration g - kRing (skip the read when already observed)
+      while (seen < g - kRing + 2 && (seen = *S.progress) < g - kRing + 2) {
         __nanosleep(20);
         if (sg.expired()) {
           g_flow_dbg[3] = 1000000ull * (blockIdx.x + 1) + 1000ull * 5 + (g % 1000);
           break;
         }
       }
+      const long long t_b = clock64();
       S.psum[sl * 32 + lane] = acc;
       __syncwarp();
+      const long long t_c = clock64();
       if (lane == 0) {
         __threadfence_block();
         S.pready[sl] = g;
       }
+      const long long t_d = clock64();
+      t_pa += t_a - t_last;
+      t_pb += t_b - t_a;
+      t_pc += t_c - t_b;
+      t_pd += t_d - t_c;
       {
         const int dist = g - *S.progress;
         ++hpub[dist <= 1 ? 0 : dist <= 3 ? 1 : dist <= 6 ? 2 : 3];
@@ -748,6 +796,10 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
       atomicAdd(&g_flow_dbg[6], static_cast<unsigned long long>(tw_rem));
       atomicAdd(&g_flow_dbg[7], static_cast<unsigned long long>(clock64() - th0));
       atomicAdd(&g_flow_dbg[16], static_cast<unsigned long long>(t_post));
+      atomicAdd(&g_flow_dbg[19], static_cast<unsigned long long>(t_pa));
+      atomicAdd(&g_flow_dbg[20], static_cast<unsigned long long>(t_pb));
+      atomicAdd(&g_flow_dbg[21], static_cast<unsigned long long>(t_pc));
+      atomicAdd(&g_flow_dbg[22], static_cast<unsigned long long>(t_pd));
       atomicAdd(&g_flow_dbg[17], static_cast<unsigned long long>(n_spun));
       for (int i = 0; i < 4; ++i) {
         atomicAdd(&g_flow_dbg[8 + i], static_cast<unsigned long long>(hpub[i]));
@@ -756,9 +808,9 @@ __device__ void flow_sweep(const DFlow& s, int n, double* smem, const double* __
     }
   }
   __syncthreads();
-  if (threadIdx.x < kRing) {
+  if (threadIdx.x < kSRing) {
     const int sl = threadIdx.x;
-    if (s.G > sl) S.base_use[sl] += (s.G - 1 - sl) / kRing + 1;
+    if (G > sl) S.base_use[sl] += (G - 1 - sl) / kSRing + 1;
   }
   __syncthreads();
 }
@@ -844,10 +896,13 @@ struct Ctx {
   double* xb;
   unsigned* abort_flag;
   unsigned sweeps[2] = {0u, 0u};  // IC(0) sweeps issued per block (same count in every CTA)
+  unsigned req[2] = {0u, 0u};     // IC(0) server requests posted per block
   int status = DSGPU_OK, failed_block = -1;
 
+  // worker CTAs only: cta / G index the workers (blockIdx.x - n_srv)
   __device__ Ctx(const Args& args, double* red_, double* sums_, double* xs)
-      : a(args), cta(blockIdx.x), G(gridDim.x), epoch(0), red(red_), sums(sums_) {
+      : a(args), cta(blockIdx.x - args.n_srv), G(gridDim.x - args.n_srv), epoch(0), red(red_),
+        sums(sums_) {
     r0 = a.row_start[cta];
     r1 = a.row_start[cta + 1];
     xf = xs;
@@ -870,13 +925,13 @@ struct Ctx {
   // grid barrier, then reduce `mask` slots of this epoch into sums[]
   __device__ bool sync_reduce(unsigned mask) {
     const long long tb0 = clock64();
-    const bool ok = grid_sync(a.bar, a.bar + 32, abort_flag);
+    const bool ok = grid_sync(a.bar, a.bar + 32, abort_flag, static_cast<unsigned>(G));
     if (threadIdx.x == 0) {
       if (cta == 0) {
         atomicAdd(&g_phase_dbg[0], static_cast<unsigned long long>(clock64() - tb0));
         atomicAdd(&g_phase_dbg[3], 1ull);
       }
-      if (cta == 2) atomicAdd(&g_phase_dbg[2], static_cast<unsigned long long>(clock64() - tb0));
+      if (cta == 1) atomicAdd(&g_phase_dbg[2], static_cast<unsigned long long>(clock64() - tb0));
     }
     if (ok) {
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -891,6 +946,47 @@ struct Ctx {
     __syncthreads();
     ++epoch;
     return ok;
+  }
+  // post an IC(0) apply of block b to its server (the lead worker thread);
+  // every worker counts the request
+  __device__ void post(int b, int op, double alpha, const Input* in) {
+    ++req[b];
+    if (cta == 0 && threadIdx.x == 0) {
+      Mailbox* m = a.mbox + b;
+      m->op = op;
+      m->alpha = alpha;
+      if (in) {
+        m->src0 = in->src0;
+        m->src1 = in->src1;
+        m->coef = in->coef;
+        m->dst = in->dst;
+      }
+      st_release(&m->req, req[b]);
+    }
+  }
+  // wait for the server's answer to the latest request of block b; <r, z>
+  __device__ double ic_result(int b) {
+    __shared__ double rz_sh;
+    __shared__ int ok_sh;
+    if (threadIdx.x == 0) {
+      Mailbox* m = a.mbox + b;
+      int ok = 1;
+      const long long t0 = clock64();
+      while (ld_acquire(&m->done) != req[b]) {
+        if (*reinterpret_cast<volatile unsigned*>(abort_flag) ||
+            clock64() - t0 > kSpinTimeoutCycles) {
+          atomicExch(abort_flag, 1u);
+          ok = 0;
+          break;
+        }
+      }
+      __threadfence();
+      rz_sh = ok ? *reinterpret_cast<volatile double*>(&m->rz) : 0.0;
+      ok_sh = ok;
+    }
+    __syncthreads();
+    if (!ok_sh) status = DSGPU_E_CUDA;
+    return rz_sh;
   }
   // rows of this CTA inside block b: [lo, hi) in global vector indices
   __device__ void block_rows(int b, int& lo, int& hi) const {
@@ -909,30 +1005,14 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
   const int tid = threadIdx.x;
   double rho_p[2] = {0.0, 0.0}, zr_p[2] = {0.0, 0.0};
   // ---- S1: r := input; z := M_b^{-1} r; x := 0 -------------------------
+  // IC(0) blocks: the block's server CTA computes r and z (requests posted
+  // here, answered at the next reduction); ring mode: remote helper CTAs
+  for (int b = 0; b < 2; ++b)
+    if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_S1, 0.0, &in);
   for (int b = 0; b < 2; ++b) {
     const DBlock& B = a.blk[b];
-    if (B.kind == DSGPU_BLOCK_PCG_IC0 && C.cta == B.ic_cta) {
-      const double* src0 = in.src0;
-      const double* src1 = in.src1;
-      const double coef = in.coef;
-      double* dst = in.dst;
-      double* r = B.r;
-      const int off = B.off;
-      const long long ti0 = clock64();
-      rho_p[b] = ic_apply<TB, RING>(
-          B,
-          [&](int row) {
-            const int i = off + row;
-            const double ri = src1 ? add_rn(src0[i], mul_rn(coef, src1[i])) : src0[i];
-            if (dst) dst[i] = ri;
-            r[row] = ri;
-            return ri;
-          },
-          C.xf, C.xb, C.red, C.abort_flag, a.launch_id, C.sweeps[b]);
-      if (threadIdx.x == 0) atomicAdd(&g_phase_dbg[C.cta == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));
-    } else if (RING && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0) {
+    if (RING && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
       ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
-    }
     if (B.kind == DSGPU_BLOCK_PCG_IC0) C.sweeps[b] += 2;
   }
   for (int b = 0; b < 2; ++b) {
@@ -981,7 +1061,8 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
       ++apps[b];
       continue;
     }
-    rho[b] = C.sums[SL_RHO0 + b];
+    rho[b] = B.kind == DSGPU_BLOCK_PCG_IC0 ? C.ic_result(b) : C.sums[SL_RHO0 + b];
+    if (C.status != DSGPU_OK) return false;
     if (rho[b] < 0.0) {  // pcg: preconditioner is not positive definite
       C.status = DSGPU_E_INDEFINITE_PRECOND;
       C.failed_block = b;
@@ -1046,25 +1127,12 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
     }
     // ---- L2: r -= alpha q; z = M^{-1} r; x += alpha p -------------------
     double rho_n[2] = {0.0, 0.0}, zr_n[2] = {0.0, 0.0};
+    for (int b = 0; b < 2; ++b)
+      if (active[b] && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_L2, alpha[b], nullptr);
     for (int b = 0; b < 2; ++b) {
       const DBlock& B = a.blk[b];
-      if (active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.cta == B.ic_cta) {
-        double* r = B.r;
-        const double* q = B.q;
-        const double na = -alpha[b];
-        const long long ti0 = clock64();
-        rho_n[b] = ic_apply<TB, RING>(
-            B,
-            [&](int row) {
-              const double ri = add_rn(r[row], mul_rn(na, q[row]));
-              r[row] = ri;
-              return ri;
-            },
-            C.xf, C.xb, C.red, C.abort_flag, a.launch_id, C.sweeps[b]);
-        if (threadIdx.x == 0) atomicAdd(&g_phase_dbg[C.cta == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));
-      } else if (RING && active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0) {
+      if (RING && active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
         ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
-      }
       if (active[b] && B.kind == DSGPU_BLOCK_PCG_IC0) C.sweeps[b] += 2;
     }
     for (int b = 0; b < 2; ++b) {
@@ -1101,7 +1169,8 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
       return false;
     for (int b = 0; b < 2; ++b) {
       if (!active[b]) continue;
-      const double rn = C.sums[SL_RHO0 + b];
+      const double rn = a.blk[b].kind == DSGPU_BLOCK_PCG_IC0 ? C.ic_result(b) : C.sums[SL_RHO0 + b];
+      if (C.status != DSGPU_OK) return false;
       if (rn < 0.0) {
         C.status = DSGPU_E_INDEFINITE_PRECOND;
         C.failed_block = b;
@@ -1127,22 +1196,105 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
   return true;
 }
 
+// IC(0) server CTA of block b: answers the workers' apply requests until told
+// to exit. Runs no MINRES code, so the sweep's registers are its own.
+template <int TB, bool RING>
+__device__ void ic_server(const Args& a, int b, double* xs, double* red) {
+  const DBlock& B = a.blk[b];
+  if (B.kind != DSGPU_BLOCK_PCG_IC0) return;
+  Mailbox* m = a.mbox + b;
+  unsigned* abort_flag = a.bar + 64;
+  __shared__ int op_sh;
+  __shared__ double al_sh, coef_sh;
+  __shared__ const double* src0_sh;
+  __shared__ const double* src1_sh;
+  __shared__ double* dst_sh;
+  if (!B.exact) flow_setup<TB>(xs, B.n, B.ffwd.ring);
+  for (unsigned seq = 1;; ++seq) {
+    if (threadIdx.x == 0) {
+      int op = IC_OP_EXIT;
+      const long long t0 = clock64();
+      for (;;) {
+        if (ld_acquire(&m->req) == seq) {
+          op = *reinterpret_cast<volatile int*>(&m->op);
+          break;
+        }
+        if (*reinterpret_cast<volatile unsigned*>(abort_flag)) break;
+        if (clock64() - t0 > 4 * kSpinTimeoutCycles) {  // workers gone: give up
+          atomicExch(abort_flag, 1u);
+          break;
+        }
+      }
+      op_sh = op;
+      al_sh = *reinterpret_cast<volatile double*>(&m->alpha);
+      src0_sh = m->src0;
+      src1_sh = m->src1;
+      coef_sh = m->coef;
+      dst_sh = m->dst;
+    }
+    __syncthreads();
+    const int op = op_sh;
+    if (op == IC_OP_EXIT) break;
+    const long long ti0 = clock64();
+    const unsigned sweep_no = 2 * (seq - 1);
+    double rz;
+    if (op == IC_OP_S1) {
+      const double* src0 = src0_sh;
+      const double* src1 = src1_sh;
+      const double coef = coef_sh;
+      double* dst = dst_sh;
+      double* r = B.r;
+      const int off = B.off;
+      rz = ic_apply<TB, RING>(
+          B,
+          [&](int row) {
+            const int i = off + row;
+            const double ri = src1 ? add_rn(src0[i], mul_rn(coef, src1[i])) : src0[i];
+            if (dst) dst[i] = ri;
+            r[row] = ri;
+            return ri;
+          },
+          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no);
+    } else {
+      double* r = B.r;
+      const double* q = B.q;
+      const double na = -al_sh;
+      rz = ic_apply<TB, RING>(
+          B,
+          [&](int row) {
+            const double ri = add_rn(r[row], mul_rn(na, q[row]));
+            r[row] = ri;
+            return ri;
+          },
+          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no);
+    }
+    __syncthreads();  // every thread's r, z (and dst) written
+    if (threadIdx.x == 0) {
+      m->rz = rz;
+      __threadfence();
+      st_release(&m->done, seq);
+      atomicAdd(&g_phase_dbg[b == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));
+    }
+  }
+}
+
 template <int TB, bool RING>
 __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
   __shared__ double sums[NSLOT];
+  if (static_cast<int>(blockIdx.x) < a.n_srv) {
+    ic_server<TB, RING>(a, blockIdx.x, xs_dyn, red);
+    return;
+  }
   Ctx C(a, red, sums, xs_dyn);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long t_kernel0 = clock64();
-  for (int b = 0; b < 2; ++b)
-    if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0 && !a.blk[b].exact && C.cta == a.blk[b].ic_cta)
-      flow_setup<TB>(xs_dyn, a.blk[b].n, a.blk[b].ffwd.ring);
   const int r0 = C.r0, r1 = C.r1;
   long long inner[2] = {0, 0}, apps[2] = {0, 0};
   int iterations = 0, converged = 0, hist_len = 0;
   double relres_m = 1.0, relres_e = 1.0;
-  const bool writer = (blockIdx.x == 0 && tid == 0);
+  const bool writer = (C.cta == 0 && tid == 0);
 
   // ---- P0: b = [f'; 0]; res = b; x = w* = aw* = 0; ||b||^2 --------------
   double* bvec = a.rbuf[0];
@@ -1324,8 +1476,14 @@ finish:
         a.p_out[a.perm_p[i - a.n_u]] = a.filter ? sub_rn(a.x[i], mul_rn(mean, 1.0)) : a.x[i];
     }
   }
-  if (threadIdx.x == 0 && blockIdx.x == 0)
+  if (threadIdx.x == 0 && C.cta == 0)
     atomicAdd(&g_phase_dbg[4], static_cast<unsigned long long>(clock64() - t_kernel0));
+  if (writer)  // release the IC(0) servers
+    for (int b = 0; b < 2; ++b)
+      if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) {
+        a.mbox[b].op = IC_OP_EXIT;
+        st_release(&a.mbox[b].req, C.req[b] + 1);
+      }
   if (writer) {
     DevReport* R = a.rep;
     R->iterations = iterations;
@@ -1364,12 +1522,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 using MinresFn = void (*)(Args);
 using IcFn = void (*)(DBlock, const double*, unsigned*, unsigned);
 MinresFn minres_for(int tb, bool ring) {
-  if (ring) return tb <= 4 ? minres_kernel<4, true> : tb <= 8 ? minres_kernel<8, true> : minres_kernel<16, true>;
-  return tb <= 4 ? minres_kernel<4, false> : tb <= 8 ? minres_kernel<8, false> : minres_kernel<16, false>;
+  if (ring) return tb <= 8 ? minres_kernel<8, true> : minres_kernel<16, true>;
+  return tb <= 8 ? minres_kernel<8, false> : minres_kernel<16, false>;
 }
 IcFn ic_for(int tb, bool ring) {
-  if (ring) return tb <= 4 ? ic_apply_kernel<4, true> : tb <= 8 ? ic_apply_kernel<8, true> : ic_apply_kernel<16, true>;
-  return tb <= 4 ? ic_apply_kernel<4, false> : tb <= 8 ? ic_apply_kernel<8, false> : ic_apply_kernel<16, false>;
+  if (ring) return tb <= 8 ? ic_apply_kernel<8, true> : ic_apply_kernel<16, true>;
+  return tb <= 8 ? ic_apply_kernel<8, false> : ic_apply_kernel<16, false>;
 }
 
 // y = M x, warp per row; na != nullptr limits each row to its first na[i] entries
@@ -1473,14 +1631,11 @@ DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
   DFlow d{};
   d.G = f.G;
   d.nr = h->upload(f.nr);
-  d.need = h->upload(f.need);
   d.cptr = h->upload(f.cptr);
   d.cneed = h->upload(f.cneed);
   d.pw = h->upload(f.pw);
   d.grows = h->upload(f.grows);
   d.pcols = h->upload(f.pcols);
-  d.acol = h->upload(f.acol);
-  d.bsrc = h->upload(f.bsrc);
   d.pptr = h->upload(f.pptr);
   d.pvals = h->upload(f.pvals);
   d.ww = h->upload(f.ww);
@@ -1494,10 +1649,6 @@ DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
   d.wptr = h->upload(f.wptr);
   d.wcols = h->upload(f.wcols);
   d.wvals = h->upload(f.wvals);
-  d.aval = h->upload(f.aval);
-  d.bval = h->upload(f.bval);
-  d.diag = h->upload(f.diag);
-  d.dinv = h->upload(f.dinv);
   return d;
 }
 
@@ -1573,6 +1724,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
     h->sms = sms;
     if (const char* env = std::getenv("DSGPU_REMOTE")) h->remote_max = std::max(0, std::atoi(env));
+    if (const char* env = std::getenv("DSGPU_NOWAIT")) {
+      const int v = std::atoi(env);
+      cudaMemcpyToSymbol(g_nowait, &v, sizeof(v));
+    }
     if (const char* env = std::getenv("DSGPU_HSLEEP")) {
       const unsigned ns = static_cast<unsigned>(std::max(0, std::atoi(env)));
       cudaMemcpyToSymbol(g_hsleep, &ns, sizeof(ns));
@@ -1623,13 +1778,16 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
                     "occupancy");
     if (rc) return rc;
     if (per_sm < 1) return fail(h, DSGPU_E_CUDA, "minres kernel cannot be resident");
-    // grid: one CTA per SM, fewer for tiny systems (barrier cost grows with CTAs)
+    // grid: IC(0) server CTAs (one per block, CTA b serves block b) + worker
+    // CTAs, one per SM, fewer for tiny systems (barrier cost grows with CTAs)
     const int64_t nnz = P.k_rp[P.n];
-    int G = static_cast<int>(std::min<int64_t>(sms, std::max<int64_t>(2, (nnz + 16383) / 16384)));
+    const int n_srv = (P.blk[0].kind == DSGPU_BLOCK_PCG_IC0 || P.blk[1].kind == DSGPU_BLOCK_PCG_IC0) ? 2 : 0;
+    const int wmax = sms - n_srv;
+    int G = static_cast<int>(std::min<int64_t>(wmax, std::max<int64_t>(2, (nnz + 16383) / 16384)));
     G = std::max(G, 2);
-    if (h->ring) G = std::min(sms, std::max(G, 2 + 2 * h->remote_max));  // room for remote helpers
-    if (const char* env = std::getenv("DSGPU_GRID")) G = std::max(2, std::min(sms, std::atoi(env)));
-    h->grid = G;
+    if (h->ring) G = std::min(wmax, std::max(G, 1 + 2 * h->remote_max));  // room for remote helpers
+    if (const char* env = std::getenv("DSGPU_GRID")) G = std::max(2, std::min(wmax, std::atoi(env)));
+    h->grid = n_srv + G;  // G = worker CTAs below
     // K-row partition balanced by nnz + per-row vector work
     h->row_start.assign(G + 1, 0);
     {
@@ -1693,9 +1851,9 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         d.gprog = h->alloc<unsigned long long>(1);
         cudaMemset(d.rflag, 0, sizeof(unsigned) * G_max);
         cudaMemset(d.gprog, 0, sizeof(unsigned long long));
-        const int R = std::min(h->remote_max, (G - 2) / 2);
+        const int R = std::min(h->remote_max, (G - 1) / 2);
         d.n_remote = R > 0 ? R : 0;
-        d.remote_cta0 = 2 + b * d.n_remote;
+        d.remote_cta0 = n_srv + 1 + b * d.n_remote;  // workers, after the lead worker
       }
       d.r = h->alloc<double>(hb.n);
       d.z = h->alloc<double>(hb.n);
@@ -1741,6 +1899,8 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     a.filter_den = P.filter_den;
     a.partial = h->alloc<double>(static_cast<size_t>(2) * NSLOT * G);
     a.bar = h->alloc<unsigned>(128);
+    a.n_srv = n_srv;
+    a.mbox = h->alloc<Mailbox>(2);
     rc = cuda_check(h, cudaMemset(a.bar, 0, 128 * sizeof(unsigned)), "cudaMemset");
     if (rc) return rc;
     h->d_rep = h->alloc<DevReport>(1);
@@ -1778,6 +1938,7 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   a.hist_cap = (d_hm && d_he) ? hist_cap : 0;
   a.launch_id = h->next_launch_id();
   int rc = cuda_check(h, cudaMemsetAsync(a.bar, 0, 128 * sizeof(unsigned), h->stream), "memset");
+  if (!rc) rc = cuda_check(h, cudaMemsetAsync(a.mbox, 0, 2 * sizeof(Mailbox), h->stream), "memset");
   if (rc) return rc;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -1980,12 +2141,12 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
   return rc;
 }
 
-int dsgpu_debug_counters(int reset, int64_t* out20) {
-  unsigned long long v[20] = {};
+int dsgpu_debug_counters(int reset, int64_t* out32) {
+  unsigned long long v[32] = {};
   cudaMemcpyFromSymbol(v, g_flow_dbg, sizeof(v));
-  for (int i = 0; i < 20; ++i) out20[i] = static_cast<int64_t>(v[i]);
+  for (int i = 0; i < 32; ++i) out32[i] = static_cast<int64_t>(v[i]);
   if (reset) {
-    const unsigned long long z[20] = {};
+    const unsigned long long z[32] = {};
     cudaMemcpyToSymbol(g_flow_dbg, z, sizeof(z));
   }
   return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;

@@ -5,7 +5,7 @@ from paper_1309_5048_b200 import host, solver
 case, k, n = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 s = host.assemble(case, k, n, seed=1234)
 g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
-cnt = np.zeros(20, np.int64)
+cnt = np.zeros(32, np.int64)
 g.L.dsgpu_debug_counters.argtypes = [C.c_int, np.ctypeslib.ndpointer(dtype=np.int64)]
 g.apply_ic0(0, np.ones(s.n_u))
 g.L.dsgpu_debug_counters(1, cnt)

@@ -3,7 +3,7 @@ sys.path.insert(0, "/root/repo")
 from paper_1309_5048_b200 import host, solver
 s = host.assemble("psi-mms", 2, int(sys.argv[1]) if len(sys.argv) > 1 else 8)
 g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
-cnt = np.zeros(20, np.int64)
+cnt = np.zeros(32, np.int64)
 g.L.dsgpu_debug_counters.argtypes = [C.c_int, np.ctypeslib.ndpointer(dtype=np.int64)]
 g.L.dsgpu_debug_counters(1, cnt)
 print("ic", g.time_kernel(1, 2), flush=True)

@@ -22,7 +22,7 @@ for (case, k, n, ringn) in cases:
         if zr is None: zr = P.ic0_solve(c(g.top.factor), r)
         z = g.apply_ic0(0, r)
         err = np.abs(z - zr).max() / np.abs(zr).max()
-        cnt = np.zeros(20, np.int64)
+        cnt = np.zeros(32, np.int64)
         g.L.dsgpu_debug_counters.argtypes = [C.c_int, np.ctypeslib.ndpointer(dtype=np.int64)]
         g.L.dsgpu_debug_counters(1, cnt)
         ms = g.time_kernel(1, 5)
