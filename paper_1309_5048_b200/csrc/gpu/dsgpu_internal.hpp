@@ -125,6 +125,9 @@ struct HostBlock {
   std::vector<int32_t> ci;
   std::vector<double> v;
   std::vector<double> dinv;      // Jacobi / Jacobi-PCG
+  std::vector<int64_t> lrp;      // IC0-PCG: the factor L (block ordering), as given
+  std::vector<int32_t> lci;
+  std::vector<double> lv;
   HostSweep fwd, bwd;            // IC0-PCG, exact column-order sweeps (bit-identical mode)
   HostFlow ffwd, fbwd;           // IC0-PCG, staged sweeps (production)
 };

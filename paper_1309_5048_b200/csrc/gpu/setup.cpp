@@ -266,7 +266,13 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
         }
       }
     }
-    if (hb.kind == DSGPU_BLOCK_PCG_IC0) build_sweeps(*facs[b], hb.fwd, hb.bwd);
+    if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
+      build_sweeps(*facs[b], hb.fwd, hb.bwd);
+      const dsgpu_csr* L = facs[b];
+      hb.lrp.assign(L->row_ptr, L->row_ptr + hb.n + 1);
+      hb.lci.assign(L->cols, L->cols + hb.lrp[hb.n]);
+      hb.lv.assign(L->vals, L->vals + hb.lrp[hb.n]);
+    }
   }
 
   P.filter = false;

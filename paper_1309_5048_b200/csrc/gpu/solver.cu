@@ -33,6 +33,7 @@
 
 #include "dsgpu_internal.hpp"
 #include "kernels.cuh"
+#include "pi.cuh"
 
 using namespace dsgpu;
 using namespace dsgpu::dev;
@@ -87,6 +88,8 @@ struct DBlock {
   unsigned* rflag;              // max(G): sweep tag once rpsum[g] is final
   unsigned long long* gprog;    // (sweep tag << 32) | groups published by the main warp
   int remote_cta0, n_remote;    // remote helper CTAs (0: none)
+  int pi;                       // 1: partitioned-inverse IC(0) apply (pi.cuh), all CTAs
+  DPi pim;
 };
 
 struct DevReport {
@@ -897,6 +900,7 @@ struct Ctx {
   unsigned* abort_flag;
   unsigned sweeps[2] = {0u, 0u};  // IC(0) sweeps issued per block (same count in every CTA)
   unsigned req[2] = {0u, 0u};     // IC(0) server requests posted per block
+  unsigned pi_par = 0u;           // partitioned-inverse applies issued (buffer-set parity)
   int status = DSGPU_OK, failed_block = -1;
 
   // worker CTAs only: cta / G index the workers (blockIdx.x - n_srv)
@@ -998,7 +1002,24 @@ struct Ctx {
 // Preconditioner application z = M^{-1} rin (BlockDiagPreconditioner::apply,
 // precond.cpp:139-148). Writes zout (length n), returns the two guard dots
 // <z_b, r_b> in zr[] (identical in all CTAs). False on error.
-template <int TB, bool RING>
+// Partitioned-inverse IC(0) apply of the active PI blocks by all worker CTAs;
+// adds each block's CTA partial of <r, z> to rho_p[b] (warp 0 of the CTA).
+template <bool PI>
+__device__ void pi_blocks(Ctx& C, const bool act[2], const PiRhs* rhs, double rho_p[2]) {
+  if constexpr (PI) {
+    const Args& a = C.a;
+    extern __shared__ double xs_dyn[];
+    double rho0 = 0.0, rho1 = 0.0;
+    pi_apply(a.blk[0].pim, a.blk[1].pim, act[0], act[1], rhs[0], rhs[1], a.blk[0].z, a.blk[1].z,
+                    C.pi_par & 1u, C.cta, C.G, xs_dyn, C.abort_flag, rho0, rho1);
+    ++C.pi_par;
+    const bool l0 = (threadIdx.x & 31) == 0;
+    if (act[0]) rho_p[0] += block_sum(l0 ? rho0 : 0.0, C.red);
+    if (act[1]) rho_p[1] += block_sum(l0 ? rho1 : 0.0, C.red);
+  }
+}
+
+template <int TB, bool RING, bool PI>
 __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
                         long long inner[2], long long apps[2]) {
   const Args& a = C.a;
@@ -1006,14 +1027,28 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
   double rho_p[2] = {0.0, 0.0}, zr_p[2] = {0.0, 0.0};
   // ---- S1: r := input; z := M_b^{-1} r; x := 0 -------------------------
   // IC(0) blocks: the block's server CTA computes r and z (requests posted
-  // here, answered at the next reduction); ring mode: remote helper CTAs
+  // here, answered at the next reduction); ring mode: remote helper CTAs.
+  // PI blocks: every CTA joins the partitioned-inverse apply; r (and the
+  // materialized input) are written after the reduction, by their owners.
   for (int b = 0; b < 2; ++b)
-    if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_S1, 0.0, &in);
+    if (!PI && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_S1, 0.0, &in);
   for (int b = 0; b < 2; ++b) {
     const DBlock& B = a.blk[b];
-    if (RING && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
+    if (!PI && RING && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
       ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
     if (B.kind == DSGPU_BLOCK_PCG_IC0) C.sweeps[b] += 2;
+  }
+  if constexpr (PI) {
+    bool act[2];
+    PiRhs rhs[2];
+    for (int b = 0; b < 2; ++b) {
+      act[b] = a.blk[b].kind == DSGPU_BLOCK_PCG_IC0;
+      rhs[b].src0 = in.src0;
+      rhs[b].src1 = in.src1;
+      rhs[b].coef = in.coef;
+      rhs[b].off = a.blk[b].off;
+    }
+    pi_blocks<PI>(C, act, rhs, rho_p);
   }
   for (int b = 0; b < 2; ++b) {
     const DBlock& B = a.blk[b];
@@ -1050,6 +1085,19 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
   C.put(SL_ZR1, zr_p[1]);
   if (!C.sync_reduce((1u << SL_RHO0) | (1u << SL_RHO1) | (1u << SL_ZR0) | (1u << SL_ZR1)))
     return false;
+  if constexpr (PI) {  // deferred: r := input (and the materialized input) for owned rows
+    for (int b = 0; b < 2; ++b) {
+      const DBlock& B = a.blk[b];
+      if (B.kind != DSGPU_BLOCK_PCG_IC0) continue;
+      int lo, hi;
+      C.block_rows(b, lo, hi);
+      for (int i = lo + tid; i < hi; i += blockDim.x) {
+        const double ri = in.at(i);
+        if (in.dst) in.dst[i] = ri;
+        B.r[i - B.off] = ri;
+      }
+    }
+  }
 
   bool active[2] = {false, false};
   double rho[2] = {0, 0}, rho0[2] = {0, 0}, beta[2] = {0, 0}, alpha[2] = {0, 0};
@@ -1061,7 +1109,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
       ++apps[b];
       continue;
     }
-    rho[b] = B.kind == DSGPU_BLOCK_PCG_IC0 ? C.ic_result(b) : C.sums[SL_RHO0 + b];
+    rho[b] = (B.kind == DSGPU_BLOCK_PCG_IC0 && !PI) ? C.ic_result(b) : C.sums[SL_RHO0 + b];
     if (C.status != DSGPU_OK) return false;
     if (rho[b] < 0.0) {  // pcg: preconditioner is not positive definite
       C.status = DSGPU_E_INDEFINITE_PRECOND;
@@ -1128,12 +1176,23 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
     // ---- L2: r -= alpha q; z = M^{-1} r; x += alpha p -------------------
     double rho_n[2] = {0.0, 0.0}, zr_n[2] = {0.0, 0.0};
     for (int b = 0; b < 2; ++b)
-      if (active[b] && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_L2, alpha[b], nullptr);
+      if (!PI && active[b] && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_L2, alpha[b], nullptr);
     for (int b = 0; b < 2; ++b) {
       const DBlock& B = a.blk[b];
-      if (RING && active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
+      if (!PI && RING && active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
         ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
       if (active[b] && B.kind == DSGPU_BLOCK_PCG_IC0) C.sweeps[b] += 2;
+    }
+    if constexpr (PI) {
+      bool act[2];
+      PiRhs rhs[2];
+      for (int b = 0; b < 2; ++b) {
+        act[b] = active[b] && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0;
+        rhs[b].r = a.blk[b].r;
+        rhs[b].q = a.blk[b].q;
+        rhs[b].na = -alpha[b];
+      }
+      pi_blocks<PI>(C, act, rhs, rho_n);
     }
     for (int b = 0; b < 2; ++b) {
       if (!active[b]) continue;
@@ -1167,9 +1226,22 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
     C.put(SL_ZR1, zr_n[1]);
     if (!C.sync_reduce((1u << SL_RHO0) | (1u << SL_RHO1) | (1u << SL_ZR0) | (1u << SL_ZR1)))
       return false;
+    if constexpr (PI) {  // deferred: r -= alpha q for owned rows
+      for (int b = 0; b < 2; ++b) {
+        const DBlock& B = a.blk[b];
+        if (!active[b] || B.kind != DSGPU_BLOCK_PCG_IC0) continue;
+        int lo, hi;
+        C.block_rows(b, lo, hi);
+        const double na = -alpha[b];
+        for (int i = lo + tid; i < hi; i += blockDim.x) {
+          const int li = i - B.off;
+          B.r[li] = add_rn(B.r[li], mul_rn(na, B.q[li]));
+        }
+      }
+    }
     for (int b = 0; b < 2; ++b) {
       if (!active[b]) continue;
-      const double rn = a.blk[b].kind == DSGPU_BLOCK_PCG_IC0 ? C.ic_result(b) : C.sums[SL_RHO0 + b];
+      const double rn = (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0 && !PI) ? C.ic_result(b) : C.sums[SL_RHO0 + b];
       if (C.status != DSGPU_OK) return false;
       if (rn < 0.0) {
         C.status = DSGPU_E_INDEFINITE_PRECOND;
@@ -1278,12 +1350,12 @@ __device__ void ic_server(const Args& a, int b, double* xs, double* red) {
   }
 }
 
-template <int TB, bool RING>
+template <int TB, bool RING, bool PI>
 __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
   __shared__ double sums[NSLOT];
-  if (static_cast<int>(blockIdx.x) < a.n_srv) {
+  if (!PI && static_cast<int>(blockIdx.x) < a.n_srv) {
     ic_server<TB, RING>(a, blockIdx.x, xs_dyn, red);
     return;
   }
@@ -1310,6 +1382,13 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
       acc += bi * bi;
     }
     C.put(SL_BB, block_sum(acc, red));
+    if (PI)  // both partitioned-inverse buffer sets start out "not yet computed"
+      for (int b = 0; b < 2; ++b)
+        if (a.blk[b].pi)
+          for (int s = 0; s < 2; ++s) {
+            unsigned long long* o = reinterpret_cast<unsigned long long*>(a.blk[b].pim.set[s]);
+            for (int k = C.cta * blockDim.x + tid; k < 4 * a.blk[b].pim.n; k += C.G * blockDim.x) o[k] = kSentinel;
+          }
   }
   if (!C.sync_reduce(1u << SL_BB)) goto finish;
   {
@@ -1320,7 +1399,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
     double* free4 = a.rbuf[2];
     double* y = a.y;
     double zr[2];
-    if (!precond<TB, RING>(C, Input{r1v, nullptr, 0.0, nullptr}, y, zr, inner, apps)) goto finish;
+    if (!precond<TB, RING, PI>(C, Input{r1v, nullptr, 0.0, nullptr}, y, zr, inner, apps)) goto finish;
     if (zr[0] < 0.0 || zr[1] < 0.0) {  // BlockDiagPreconditioner guards
       C.status = DSGPU_E_INDEFINITE_PRECOND;
       C.failed_block = zr[0] < 0.0 ? 0 : 1;
@@ -1418,7 +1497,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
       }
       const double alfa = sums[SL_ALPHA];
       // ---- precond: r2_new = spare - (alfa/beta) r2;  y = M^{-1} r2_new ----
-      if (!precond<TB, RING>(C, Input{spare, r2v, div_rn(-alfa, beta), spare}, y, zr, inner, apps))
+      if (!precond<TB, RING, PI>(C, Input{spare, r2v, div_rn(-alfa, beta), spare}, y, zr, inner, apps))
         goto finish;
       {
         double* nr1 = r2v;
@@ -1478,7 +1557,7 @@ finish:
   }
   if (threadIdx.x == 0 && C.cta == 0)
     atomicAdd(&g_phase_dbg[4], static_cast<unsigned long long>(clock64() - t_kernel0));
-  if (writer)  // release the IC(0) servers
+  if (writer && !PI)  // release the IC(0) servers
     for (int b = 0; b < 2; ++b)
       if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) {
         a.mbox[b].op = IC_OP_EXIT;
@@ -1519,11 +1598,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                      launch_id, 0u);
 }
 
+// One partitioned-inverse IC(0) apply z = (L L^T)^{-1} r of one block by all
+// CTAs (cooperative launch); the buffer set `par` must hold sentinels.
+__global__ void __launch_bounds__(kThreads, 1)
+    pi_apply_kernel(const __grid_constant__ DPi P, const double* r, double* z, unsigned par, unsigned* abort_flag) {
+  extern __shared__ double xs_dyn[];
+  PiRhs rhs;
+  rhs.src0 = r;
+  double rho0 = 0.0, rho1 = 0.0;
+  pi_apply(P, DPi{}, true, false, rhs, rhs, z, nullptr, par, blockIdx.x, gridDim.x, xs_dyn, abort_flag, rho0,
+                  rho1);
+}
+
+__global__ void fill_sentinel(double* p, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    reinterpret_cast<unsigned long long*>(p)[i] = kSentinel;
+}
+
 using MinresFn = void (*)(Args);
 using IcFn = void (*)(DBlock, const double*, unsigned*, unsigned);
-MinresFn minres_for(int tb, bool ring) {
-  if (ring) return tb <= 8 ? minres_kernel<8, true> : minres_kernel<16, true>;
-  return tb <= 8 ? minres_kernel<8, false> : minres_kernel<16, false>;
+MinresFn minres_for(int tb, bool ring, bool pi) {
+  if (pi) return minres_kernel<8, false, true>;
+  if (ring) return tb <= 8 ? minres_kernel<8, true, false> : minres_kernel<16, true, false>;
+  return tb <= 8 ? minres_kernel<8, false, false> : minres_kernel<16, false, false>;
 }
 IcFn ic_for(int tb, bool ring) {
   if (ring) return tb <= 8 ? ic_apply_kernel<8, true> : ic_apply_kernel<16, true>;
@@ -1580,6 +1678,10 @@ struct dsgpu_handle {
   int64_t nnz_k = 0, nnz_a = 0, nnz_l[2] = {0, 0}, nnz_q = 0;
   bool exact = false;
   bool ring = false;
+  bool pi = false;            // partitioned-inverse IC(0) applies (pi.cuh)
+  PiPlan pip[2];
+  int pi_cbase = 0, pi_cslot = 0;  // chain coefficient prefetch slots (doubles)
+  int pi_steps = 0;           // dependent chain steps per IC(0) apply (both sweeps)
   int tb = 4, merge = 1;
   int remote_max = 8;         // remote helper CTAs per IC block (ring mode)
   int sms = 148;
@@ -1664,6 +1766,50 @@ DSweep upload_sweep(dsgpu_handle* h, const HostSweep& s) {
   return d;
 }
 
+// Partitioned-inverse mode (pi.hpp) for the IC(0) blocks: block size = the
+// factor's lower bandwidth x DSGPU_PI_B (default 1); the pressure block is cut
+// into no more blocks than the velocity block so both chains share steps.
+// Off (staged sweeps) when DSGPU_PI=0, when the windows do not fit shared
+// memory, or when the block inverses would exceed half the free HBM.
+bool choose_pi(dsgpu_handle* h, const HostPlan& P, size_t smem_budget) {
+  if (const char* env = std::getenv("DSGPU_PI"))
+    if (std::atoi(env) == 0) return false;
+  const double mult = std::getenv("DSGPU_PI_B") ? std::atof(std::getenv("DSGPU_PI_B")) : 1.0;
+  int nb0 = 0;
+  size_t bytes = 0;
+  for (int b = 0; b < 2; ++b) {
+    h->pip[b] = PiPlan{};
+    const HostBlock& hb = P.blk[b];
+    if (hb.kind != DSGPU_BLOCK_PCG_IC0) continue;
+    const int bw = pi_bandwidth(hb.n, hb.lrp.data(), hb.lci.data());
+    int bsz = std::max(1, static_cast<int>(std::ceil(std::max(1, bw) * mult)));
+    if (b == 1 && nb0 > 0) bsz = std::max(bsz, (hb.n + nb0 - 1) / nb0);
+    h->pip[b] = pi_plan(hb.n, hb.lrp.data(), hb.lci.data(), bsz);
+    if (b == 0) nb0 = h->pip[0].nb;
+    bytes += sizeof(double) * (static_cast<size_t>(h->pip[b].n_coef) + 8ull * hb.n);
+  }
+  const size_t smem = sizeof(double) * static_cast<size_t>(h->pip[0].wmax + h->pip[1].wmax + 32);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  if (smem > smem_budget || bytes > free_b / 2) return false;
+  h->pi_steps = 2 * std::max(h->pip[0].nb, h->pip[1].nb);
+  return true;
+}
+
+// Shared memory of the PI kernels: both chain windows, then (when it fits)
+// one coefficient-prefetch slot per warp.
+size_t pi_smem(dsgpu_handle* h, size_t budget) {
+  const int win = h->pip[0].wmax + h->pip[1].wmax;
+  h->pi_cbase = (win + 31) / 32 * 32;
+  h->pi_cslot = (std::max(h->pip[0].wmax, h->pip[1].wmax) + 1) / 2 * 2;
+  size_t bytes = sizeof(double) * (static_cast<size_t>(h->pi_cbase) + static_cast<size_t>(kWarps) * h->pi_cslot);
+  if (bytes > budget) {
+    h->pi_cslot = 0;
+    bytes = sizeof(double) * static_cast<size_t>(h->pi_cbase);
+  }
+  return bytes;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1737,7 +1883,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     for (int b = 0; b < 2; ++b)
       if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0) nmax = std::max(nmax, P.blk[b].n);
     h->exact = std::getenv("DSGPU_EXACT") && std::atoi(std::getenv("DSGPU_EXACT")) != 0;
-    if (!h->exact && nmax > 0) {
+    int smem_optin_pi = 0;
+    cudaDeviceGetAttribute(&smem_optin_pi, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+    h->pi = !h->exact && nmax > 0 && choose_pi(h, P, static_cast<size_t>(smem_optin_pi) - 2048);
+    if (!h->exact && !h->pi && nmax > 0) {
       const int merge = std::getenv("DSGPU_MERGE") ? std::atoi(std::getenv("DSGPU_MERGE")) : kDefaultMerge;
       // ring mode when the full solution vector + ring would not fit shared memory
       int smem_optin0 = 0;
@@ -1754,6 +1903,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     }
     h->smem = h->exact ? static_cast<size_t>(2) * nmax * sizeof(double)
                        : FlowSmem::bytes(nmax, SlotLayout(h->tb).bytes);
+    if (h->pi) h->smem = pi_smem(h, static_cast<size_t>(smem_optin_pi) - 2048);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const size_t static_smem = 1024;
@@ -1762,18 +1912,19 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
                   "IC(0) block too large for the shared-memory dataflow sweep in this build (n=" +
                       std::to_string(nmax) + ")");
     int rc = cuda_check(h,
-                        cudaFuncSetAttribute(minres_for(h->tb, h->ring), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                        cudaFuncSetAttribute(minres_for(h->tb, h->ring, h->pi), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(h->smem)),
                         "cudaFuncSetAttribute");
     if (rc) return rc;
     rc = cuda_check(h,
-                    cudaFuncSetAttribute(ic_for(h->tb, h->ring), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(h->smem)),
+                    cudaFuncSetAttribute(h->pi ? reinterpret_cast<const void*>(pi_apply_kernel)
+                                               : reinterpret_cast<const void*>(ic_for(h->tb, h->ring)),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->smem)),
                     "cudaFuncSetAttribute");
     if (rc) return rc;
     int per_sm = 0;
     rc = cuda_check(h,
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minres_for(h->tb, h->ring), kThreads,
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minres_for(h->tb, h->ring, h->pi), kThreads,
                                                                   h->smem),
                     "occupancy");
     if (rc) return rc;
@@ -1781,10 +1932,12 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     // grid: IC(0) server CTAs (one per block, CTA b serves block b) + worker
     // CTAs, one per SM, fewer for tiny systems (barrier cost grows with CTAs)
     const int64_t nnz = P.k_rp[P.n];
-    const int n_srv = (P.blk[0].kind == DSGPU_BLOCK_PCG_IC0 || P.blk[1].kind == DSGPU_BLOCK_PCG_IC0) ? 2 : 0;
+    const int n_srv =
+        (!h->pi && (P.blk[0].kind == DSGPU_BLOCK_PCG_IC0 || P.blk[1].kind == DSGPU_BLOCK_PCG_IC0)) ? 2 : 0;
     const int wmax = sms - n_srv;
     int G = static_cast<int>(std::min<int64_t>(wmax, std::max<int64_t>(2, (nnz + 16383) / 16384)));
     G = std::max(G, 2);
+    if (h->pi) G = wmax;  // the partitioned-inverse chain wants every SM
     if (h->ring) G = std::min(wmax, std::max(G, 1 + 2 * h->remote_max));  // room for remote helpers
     if (const char* env = std::getenv("DSGPU_GRID")) G = std::max(2, std::min(wmax, std::atoi(env)));
     h->grid = n_srv + G;  // G = worker CTAs below
@@ -1830,7 +1983,23 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       }
       if (!hb.dinv.empty()) d.dinv = h->upload(hb.dinv);
       d.exact = h->exact ? 1 : 0;
-      if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
+      if (hb.kind == DSGPU_BLOCK_PCG_IC0 && h->pi) {
+        const PiPlan& pp = h->pip[b];
+        d.pi = 1;
+        d.pim.nb = pp.nb;
+        d.pim.bsz = pp.bsz;
+        d.pim.n = pp.n;
+        d.pim.wmax = pp.wmax;
+        d.pim.cbase = h->pi_cbase;
+        d.pim.cslot = h->pi_cslot;
+        d.pim.blk = h->upload(pp.blk);
+        double* coef = h->alloc<double>(static_cast<size_t>(pp.n_coef));
+        d.pim.coef = coef;
+        d.pim.set[0] = h->alloc<double>(static_cast<size_t>(4) * pp.n);
+        d.pim.set[1] = h->alloc<double>(static_cast<size_t>(4) * pp.n);
+        const std::string e = pi_fill(pp, hb.lrp.data(), hb.lci.data(), hb.lv.data(), coef, h->stream);
+        if (!e.empty()) throw std::runtime_error("partitioned-inverse setup: " + e);
+      } else if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
         if (h->exact) {
           d.fwd = upload_sweep(h, hb.fwd);
           d.bwd = upload_sweep(h, hb.bwd);
@@ -1946,7 +2115,7 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   cudaEventRecord(e0, h->stream);
   void* params[] = {&a};
   rc = cuda_check(h,
-                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_for(h->tb, h->ring)), dim3(h->grid),
+                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_for(h->tb, h->ring, h->pi)), dim3(h->grid),
                                               dim3(kThreads), params, h->smem, h->stream),
                   "cooperative launch");
   cudaEventRecord(e1, h->stream);
@@ -2058,6 +2227,15 @@ int dsgpu_apply_saddle(dsgpu_handle* h, const double* x, double* y) {
 // helper CTAs (co-resident: cooperative launch).
 static cudaError_t launch_ic(dsgpu_handle* h, DBlock B, const double* r) {
   unsigned* abort_flag = h->args.bar + 64;
+  if (B.pi) {
+    fill_sentinel<<<h->sms, 256, 0, h->stream>>>(B.pim.set[0], 4ll * B.pim.n);
+    DPi P = B.pim;
+    double* z = B.z;
+    unsigned par = 0;
+    void* params[] = {&P, &r, &z, &par, &abort_flag};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(pi_apply_kernel), dim3(h->grid), dim3(kThreads),
+                                       params, h->smem, h->stream);
+  }
   unsigned id = h->next_launch_id();
   const int R = B.n_remote > 0 ? std::min(h->sms - 1, std::max(B.n_remote, 2 * h->remote_max)) : 0;
   B.remote_cta0 = 1;

@@ -53,10 +53,39 @@ def test_saddle_apply_matches_reference(gpu, port):
     assert np.abs(y - ref).max() <= 1e-14 * np.abs(ref).max()
 
 
-def test_ic0_apply_staged_matches_reference(gpu, port):
-    """Production (staged) sweeps: same factor and operation, summation
-    reassociated inside each row -> agreement to round-off."""
+@pytest.mark.parametrize("pi_b", [None, "0.5", "1.7"])
+def test_ic0_apply_partitioned_inverse_matches_reference(gpu, port, monkeypatch, pi_b):
+    """Default mode for 2D systems: partitioned-inverse IC(0) apply (block
+    inverses of the same factor; agreement to round-off). pi_b scales the
+    block size (0.5: windows spanning two earlier blocks; 1.7: ragged last
+    block)."""
     host, solver = gpu
+    if pi_b:
+        monkeypatch.setenv("DSGPU_PI_B", pi_b)
+    d = load_golden("c1_psi_k2_n8.npz")
+    s = host.assemble("psi-mms", 2, 8)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    for b, tag in ((0, "A"), (1, "Q")):
+        z = g.apply_ic0(b, d["ic_r_" + tag])
+        ref = d["ic_z_" + tag]  # the reference's own Ic0Factor::solve output
+        assert np.abs(z - ref).max() <= 1e-12 * np.abs(ref).max()
+    s = host.assemble("psi-mms", 2, 64)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    for b, fac in ((0, g.top.factor), (1, g.bottom.factor)):
+        r = np.random.default_rng(3 + b).standard_normal(fac.n_rows)
+        z = g.apply_ic0(b, r)
+        ref = port.ic0_solve(to_oracle(fac), r)
+        assert np.abs(z - ref).max() <= 1e-12 * np.abs(ref).max()
+    sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+    check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+
+
+def test_ic0_apply_staged_matches_reference(gpu, port, monkeypatch):
+    """Staged dataflow sweeps (DSGPU_PI=0; the mode for systems whose block
+    inverses do not fit): same factor and operation, summation reassociated
+    inside each row -> agreement to round-off."""
+    host, solver = gpu
+    monkeypatch.setenv("DSGPU_PI", "0")
     d = load_golden("c1_psi_k2_n8.npz")
     s = host.assemble("psi-mms", 2, 8)
     g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
@@ -220,6 +249,7 @@ def test_ring_mode_forced_small(gpu, port, monkeypatch):
     """Ring mode (results beyond the shared-memory ring published in global
     memory) forced on a small system: same answers as the full-vector mode."""
     host, solver = gpu
+    monkeypatch.setenv("DSGPU_PI", "0")
     monkeypatch.setenv("DSGPU_RING_N", "1")
     s = host.assemble("psi-mms", 2, 16)
     g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
@@ -231,9 +261,12 @@ def test_ring_mode_forced_small(gpu, port, monkeypatch):
     check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
 
 
-def test_large_system_ring_mode(gpu, port):
-    """k'=3, 96x96 (n_u = 19,404 > shared memory): ring mode chosen by setup."""
+@pytest.mark.parametrize("pi", ["0", "1"])
+def test_large_system_ring_mode(gpu, port, monkeypatch, pi):
+    """k'=3, 96x96 (n_u = 19,404 > shared memory): ring mode chosen by setup
+    when the partitioned inverse is off; the partitioned inverse otherwise."""
     host, solver = gpu
+    monkeypatch.setenv("DSGPU_PI", pi)
     s = host.assemble("random", 3, 96, seed=1234)
     g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
     sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
