@@ -155,6 +155,12 @@ int dsgpu_debug_counters(int reset, int64_t* out32);
  * wait, CTA0 IC(0) apply, CTA2 grid-barrier wait, barriers, CTA0 kernel,
  * CTA1 IC(0) apply, 0, 0. */
 int dsgpu_debug_phases(int reset, int64_t* out8);
+/* Partitioned-inverse IC(0) apply timeline: arm != 0 arms the recorder (CTA 0
+ * and the last CTA record %globaltimer at every phase boundary of their next
+ * apply); arm == 0 reads it: out1024[s*512] = marks recorded by slot s,
+ * out1024[s*512 + 1 ..] = timestamps (ns): start, g done, per forward step
+ * (window staged, rows stored), h done, per backward step (same). */
+int dsgpu_debug_pi_trace(int arm, int64_t* out1024);
 
 #ifdef __cplusplus
 }

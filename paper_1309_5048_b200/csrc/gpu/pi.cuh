@@ -47,6 +47,46 @@ struct PiRhs {
   }
 };
 
+// Timeline diagnostics (dsgpu_debug_pi_trace): when armed, CTA 0 and the last
+// CTA record %globaltimer at every phase boundary of their next apply.
+__device__ unsigned long long g_pi_trace[2][512];
+__device__ int g_pi_trace_arm[2];
+struct PiTrace {
+  int slot = -1, k = 0;
+  __device__ __forceinline__ void init(int cta, int G) {
+    slot = cta == 0 ? 0 : (cta == G - 1 ? 1 : -1);
+    if (slot >= 0 && !*reinterpret_cast<volatile int*>(&g_pi_trace_arm[slot])) slot = -1;
+  }
+  __device__ __forceinline__ void mark() {
+    if (slot >= 0 && threadIdx.x == 0 && k < 511) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_pi_trace[slot][++k] = t;
+      g_pi_trace[slot][0] = k;
+    }
+  }
+  __device__ __forceinline__ void done() {
+    if (slot >= 0 && threadIdx.x == 0) g_pi_trace_arm[slot] = 0;
+  }
+};
+
+// Per-warp mbarriers for the chain rows' bulk copies (initialized once per
+// kernel launch by pi_prologue; parity tracked in pi_mb_phase).
+__shared__ __align__(8) uint64_t pi_mb[16];
+__shared__ unsigned pi_mb_phase[16];
+__device__ __forceinline__ unsigned pi_s32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// every thread of the CTA, once per launch before any apply
+__device__ __forceinline__ void pi_prologue() {
+  if (threadIdx.x < 16) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(pi_s32(&pi_mb[threadIdx.x])) : "memory");
+    pi_mb_phase[threadIdx.x] = 0u;
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+}
+
 __device__ __forceinline__ unsigned long long pi_ld(const double* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -158,6 +198,33 @@ __device__ __forceinline__ double pi_h_row(const DPi& P, const double* y, int ro
   return warp_sum(acc);
 }
 
+// window part of a chain row: sum_k c[k] ws[k], four independent accumulators
+// (the fp64 FMA dependency chain is the row's latency)
+__device__ __forceinline__ double pi_win(const double* c, const double* ws, int w, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int k = lane;
+  for (; k + 96 < w; k += 128) {
+    a0 = fma(c[k], ws[k], a0);
+    a1 = fma(c[k + 32], ws[k + 32], a1);
+    a2 = fma(c[k + 64], ws[k + 64], a2);
+    a3 = fma(c[k + 96], ws[k + 96], a3);
+  }
+  for (; k < w; k += 32) a0 = fma(c[k], ws[k], a0);
+  return (a0 + a1) + (a2 + a3);
+}
+__device__ __forceinline__ double pi_win_g(const double* __restrict__ c, const double* ws, int w, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int k = lane;
+  for (; k + 96 < w; k += 128) {
+    a0 = fma(__ldg(c + k), ws[k], a0);
+    a1 = fma(__ldg(c + k + 32), ws[k + 32], a1);
+    a2 = fma(__ldg(c + k + 64), ws[k + 64], a2);
+    a3 = fma(__ldg(c + k + 96), ws[k + 96], a3);
+  }
+  for (; k < w; k += 32) a0 = fma(__ldg(c + k), ws[k], a0);
+  return (a0 + a1) + (a2 + a3);
+}
+
 // ---- chain ------------------------------------------------------------------
 // Per-block view of one chain step for this CTA (scalars only: no arrays
 // indexed at run time, which would live in local memory).
@@ -184,7 +251,7 @@ __device__ __forceinline__ PiStep pi_step(const DPi& P, bool act, int t, int cta
 template <bool FWD>
 __device__ void pi_chain(const DPi& P0, const DPi& P1, bool act0, bool act1, const PiRhs& rhs0,
                          const PiRhs& rhs1, double* zc0, double* zc1, unsigned par, int cta, int G, double* ws,
-                         unsigned* ab, double& rho0, double& rho1) {
+                         unsigned* ab, double& rho0, double& rho1, PiTrace& tr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nsteps = max(act0 ? P0.nb : 0, act1 ? P1.nb : 0);
   constexpr int kIn = FWD ? 1 : 3, kBase = FWD ? 0 : 2;
@@ -192,9 +259,10 @@ __device__ void pi_chain(const DPi& P0, const DPi& P1, bool act0, bool act1, con
     const PiStep S0 = pi_step<FWD>(P0, act0, t, cta, G);
     const PiStep S1 = pi_step<FWD>(P1, act1, t, cta, G);
     const int nj0 = S0.hi - S0.lo, nj = nj0 + S1.hi - S1.lo;
-    // prefetch this warp's first row: coefficients (cp.async into its shared-
-    // memory slot) and base value, both before waiting for the window
-    double bse = 0.0;
+    // prefetch this warp's first row, before waiting for the window: its
+    // coefficients (one bulk copy into the warp's shared-memory slot) and
+    // its base value
+    unsigned long long bse_raw = 0ull;
     double* cs = ws + P0.cbase + warp * P0.cslot;
     const bool pre = warp < nj && P0.cslot > 0;
     if (warp < nj) {
@@ -203,22 +271,28 @@ __device__ void pi_chain(const DPi& P0, const DPi& P1, bool act0, bool act1, con
       const int row = q ? S1.lo + warp - nj0 : S0.lo + warp;
       const int w = q ? S1.wl : S0.wl;
       const PiBlk& B = P.blk[q ? S1.i : S0.i];
-      const double* cr = P.coef + (FWD ? B.f : B.h) + static_cast<int64_t>(row - B.s) * w;
-      if (pre) {
-        for (int k = lane; k < w; k += 32) {
-          const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(cs + k));
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(cr + k) : "memory");
+      if (lane == 0) {
+        if (pre && w > 0) {
+          const unsigned bytes = static_cast<unsigned>(pi_ldw(w)) * 8u;
+          const double* cr = P.coef + (FWD ? B.f : B.h) + static_cast<int64_t>(row - B.s) * pi_ldw(w);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pi_s32(&pi_mb[warp])),
+                       "r"(bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  pi_s32(cs)),
+              "l"(cr), "r"(bytes), "r"(pi_s32(&pi_mb[warp]))
+              : "memory");
         }
+        bse_raw = pi_ld(P.set[par] + kBase * P.n + row);  // checked after the stage
       }
-      if (lane == 0) bse = pi_wait(P.set[par] + kBase * P.n + row, ab);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
     // stage the windows: block 0 at ws[0, wl0), block 1 at ws[wl0, wl0 + wl1)
     __syncthreads();  // the previous step's readers of ws are done
     if (S0.wl > 0) pi_stage(ws, P0.set[par] + kIn * P0.n + S0.wlo, S0.wl, ab);
     if (S1.wl > 0) pi_stage(ws + S0.wl, P1.set[par] + kIn * P1.n + S1.wlo, S1.wl, ab);
-    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    tr.mark();
     for (int j = warp; j < nj; j += nw) {
       const bool q = j >= nj0;
       const DPi& P = q ? P1 : P0;
@@ -226,16 +300,29 @@ __device__ void pi_chain(const DPi& P0, const DPi& P1, bool act0, bool act1, con
       const int w = q ? S1.wl : S0.wl;
       const PiBlk& B = P.blk[q ? S1.i : S0.i];
       const double* wsb = ws + (q ? S0.wl : 0);
-      double acc = 0.0;
+      double acc;
       if (j == warp && pre) {
-        for (int k = lane; k < w; k += 32) acc = fma(cs[k], wsb[k], acc);
+        if (w > 0) {  // wait for the bulk copy of the row
+          const unsigned ph = pi_mb_phase[warp];
+          unsigned ok = 0;
+          while (!ok)
+            asm volatile(
+                "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                : "=r"(ok)
+                : "r"(pi_s32(&pi_mb[warp])), "r"(ph)
+                : "memory");
+          __syncwarp();
+          if (lane == 0) pi_mb_phase[warp] = ph ^ 1u;
+        }
+        acc = pi_win(cs, wsb, w, lane);
       } else {
-        const double* cr = P.coef + (FWD ? B.f : B.h) + static_cast<int64_t>(row - B.s) * w;
-        for (int k = lane; k < w; k += 32) acc = fma(__ldg(cr + k), wsb[k], acc);
+        acc = pi_win_g(P.coef + (FWD ? B.f : B.h) + static_cast<int64_t>(row - B.s) * pi_ldw(w), wsb, w, lane);
       }
       acc = warp_sum(acc);
       if (lane == 0) {
-        const double base = j == warp ? bse : pi_wait(P.set[par] + kBase * P.n + row, ab);
+        const double base = (j == warp && bse_raw != kSentinel)
+                                ? __longlong_as_double(static_cast<long long>(bse_raw))
+                                : pi_wait(P.set[par] + kBase * P.n + row, ab);
         const double v = add_rn(base, acc);
         pi_st(P.set[par] + kIn * P.n + row, v);
         if (!FWD) {
@@ -249,6 +336,7 @@ __device__ void pi_chain(const DPi& P0, const DPi& P1, bool act0, bool act1, con
         }
       }
     }
+    tr.mark();
   }
 }
 
@@ -264,6 +352,9 @@ __device__ void pi_apply(const DPi& P0, const DPi& P1, bool act0, bool act1, con
                          unsigned* ab, double& rho0, double& rho1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int gw = cta * nw + warp, gws = G * nw;
+  PiTrace tr;
+  tr.init(cta, G);
+  tr.mark();
   // reset the other buffer set (the next apply's) of every PI block, active
   // or not: the parity advances for both blocks on every apply
   if (P0.n) pi_reset(P0, par ^ 1u, cta, G);
@@ -278,7 +369,8 @@ __device__ void pi_apply(const DPi& P0, const DPi& P1, bool act0, bool act1, con
       const double v = pi_g_row(P1, rhs1, row, lane);
       if (lane == 0) pi_st(P1.set[par] + row, v);
     }
-  pi_chain<true>(P0, P1, act0, act1, rhs0, rhs1, zc0, zc1, par, cta, G, ws, ab, rho0, rho1);
+  tr.mark();
+  pi_chain<true>(P0, P1, act0, act1, rhs0, rhs1, zc0, zc1, par, cta, G, ws, ab, rho0, rho1, tr);
   if (act0)
     for (int row = gw; row < P0.n; row += gws) {
       const double v = pi_h_row(P0, P0.set[par] + P0.n, row, lane, ab);
@@ -289,7 +381,9 @@ __device__ void pi_apply(const DPi& P0, const DPi& P1, bool act0, bool act1, con
       const double v = pi_h_row(P1, P1.set[par] + P1.n, row, lane, ab);
       if (lane == 0) pi_st(P1.set[par] + 2 * P1.n + row, v);
     }
-  pi_chain<false>(P0, P1, act0, act1, rhs0, rhs1, zc0, zc1, par, cta, G, ws, ab, rho0, rho1);
+  tr.mark();
+  pi_chain<false>(P0, P1, act0, act1, rhs0, rhs1, zc0, zc1, par, cta, G, ws, ab, rho0, rho1, tr);
+  tr.done();
 }
 
 }  // namespace dev

@@ -25,9 +25,12 @@ struct PiBlk {
   int32_t c, v;    // forward window [c, s); backward window [e, v)
   int64_t dinv;    // D_i^{-1}, row-major b_i x b_i (lower triangle used), offset in doubles
   int64_t dinvt;   // D_i^{-T}, row-major b_i x b_i (upper triangle used)
-  int64_t f;       // F_i = -D_i^{-1} E_i, row-major b_i x (s - c)
-  int64_t h;       // H_i = -D_i^{-T} G_i^T, row-major b_i x (v - e)
+  int64_t f;       // F_i = -D_i^{-1} E_i, row-major b_i x (s - c), row stride pi_ld(s - c)
+  int64_t h;       // H_i = -D_i^{-T} G_i^T, row-major b_i x (v - e), row stride pi_ld(v - e)
 };
+
+// F/H row stride: even, so every row starts 16-byte aligned (one bulk copy)
+inline constexpr int pi_ldw(int w) { return (w + 1) & ~1; }
 
 struct PiPlan {
   int n = 0, bsz = 0, nb = 0;

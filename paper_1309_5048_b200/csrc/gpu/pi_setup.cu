@@ -40,14 +40,15 @@ PiPlan pi_plan(int n, const int64_t* lrp, const int32_t* lci, int bsz) {
       if (rowmin[r] < B.e) v = r + 1;
     B.v = v;
     const int64_t b = B.e - B.s;
+    auto even = [](int64_t x) { return (x + 1) & ~int64_t{1}; };
     B.dinv = off;
-    off += b * b;
+    off = even(off + b * b);
     B.dinvt = off;
-    off += b * b;
+    off = even(off + b * b);
     B.f = off;
-    off += b * (B.s - B.c);
+    off = even(off + b * pi_ldw(B.s - B.c));
     B.h = off;
-    off += b * (B.v - B.e);
+    off = even(off + b * pi_ldw(B.v - B.e));
     P.wmax = std::max(P.wmax, std::max(B.s - B.c, B.v - B.e));
   }
   P.n_coef = off;
@@ -128,6 +129,7 @@ std::string pi_fill(const PiPlan& P, const int64_t* lrp, const int32_t* lci, con
     ck(cudaMemcpyAsync(d_rp, lrp, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st), "pi: H2D");
     ck(cudaMemcpyAsync(d_ci, lci, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st), "pi: H2D");
     ck(cudaMemcpyAsync(d_v, lv, sizeof(double) * nnz, cudaMemcpyHostToDevice, st), "pi: H2D");
+    ck(cudaMemsetAsync(d_coef, 0, sizeof(double) * P.n_coef, st), "pi: memset");
     cbk(cublasCreate(&S.cb), "cublasCreate");
     cbk(cublasSetStream(S.cb, st), "cublasSetStream");
     cbk(cublasSetMathMode(S.cb, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");
@@ -152,14 +154,14 @@ std::string pi_fill(const PiPlan& P, const int64_t* lrp, const int32_t* lci, con
         cbk(cublasDtrsm(S.cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, bi, w1,
                         &mone, D, bi, E, bi),
             "trsm F");
-        cbk(cublasDgeam(S.cb, CUBLAS_OP_T, CUBLAS_OP_N, w1, bi, &one, E, bi, &zero, E, w1, d_coef + B.f, w1),
+        cbk(cublasDgeam(S.cb, CUBLAS_OP_T, CUBLAS_OP_N, w1, bi, &one, E, bi, &zero, E, w1, d_coef + B.f, pi_ldw(w1)),
             "geam F");
       }
       if (w2) {
         cbk(cublasDtrsm(S.cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, bi, w2,
                         &mone, D, bi, Gt, bi),
             "trsm H");
-        cbk(cublasDgeam(S.cb, CUBLAS_OP_T, CUBLAS_OP_N, w2, bi, &one, Gt, bi, &zero, Gt, w2, d_coef + B.h, w2),
+        cbk(cublasDgeam(S.cb, CUBLAS_OP_T, CUBLAS_OP_N, w2, bi, &one, Gt, bi, &zero, Gt, w2, d_coef + B.h, pi_ldw(w2)),
             "geam H");
       }
     }

@@ -1359,6 +1359,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
     ic_server<TB, RING>(a, blockIdx.x, xs_dyn, red);
     return;
   }
+  if (PI) pi_prologue();
   Ctx C(a, red, sums, xs_dyn);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long t_kernel0 = clock64();
@@ -1603,6 +1604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void __launch_bounds__(kThreads, 1)
     pi_apply_kernel(const __grid_constant__ DPi P, const double* r, double* z, unsigned par, unsigned* abort_flag) {
   extern __shared__ double xs_dyn[];
+  pi_prologue();
   PiRhs rhs;
   rhs.src0 = r;
   double rho0 = 0.0, rho1 = 0.0;
@@ -1767,14 +1769,14 @@ DSweep upload_sweep(dsgpu_handle* h, const HostSweep& s) {
 }
 
 // Partitioned-inverse mode (pi.hpp) for the IC(0) blocks: block size = the
-// factor's lower bandwidth x DSGPU_PI_B (default 1); the pressure block is cut
+// factor's lower bandwidth x DSGPU_PI_B (default 1.5, measured best on C2); the pressure block is cut
 // into no more blocks than the velocity block so both chains share steps.
 // Off (staged sweeps) when DSGPU_PI=0, when the windows do not fit shared
 // memory, or when the block inverses would exceed half the free HBM.
 bool choose_pi(dsgpu_handle* h, const HostPlan& P, size_t smem_budget) {
   if (const char* env = std::getenv("DSGPU_PI"))
     if (std::atoi(env) == 0) return false;
-  const double mult = std::getenv("DSGPU_PI_B") ? std::atof(std::getenv("DSGPU_PI_B")) : 1.0;
+  const double mult = std::getenv("DSGPU_PI_B") ? std::atof(std::getenv("DSGPU_PI_B")) : 1.5;
   int nb0 = 0;
   size_t bytes = 0;
   for (int b = 0; b < 2; ++b) {
@@ -2337,6 +2339,20 @@ int dsgpu_debug_phases(int reset, int64_t* out8) {
   if (reset) {
     const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_phase_dbg, z, sizeof(z));
+  }
+  return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
+}
+
+int dsgpu_debug_pi_trace(int arm, int64_t* out1024) {
+  if (arm) {
+    const unsigned long long z[2][512] = {};
+    const int on[2] = {1, 1};
+    cudaMemcpyToSymbol(g_pi_trace, z, sizeof(z));
+    cudaMemcpyToSymbol(g_pi_trace_arm, on, sizeof(on));
+  } else {
+    static unsigned long long v[2][512];
+    cudaMemcpyFromSymbol(v, g_pi_trace, sizeof(v));
+    for (int i = 0; i < 1024; ++i) out1024[i] = static_cast<int64_t>(v[i / 512][i % 512]);
   }
   return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
 }
