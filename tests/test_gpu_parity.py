@@ -271,3 +271,50 @@ def test_large_system_ring_mode(gpu, port, monkeypatch, pi):
     g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
     sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
     check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+
+
+# C3 stagnates near 4e-7 in the reference (relaxed inner CG makes the block
+# preconditioner vary between applications), so both sides run to the same
+# iteration cap and parity is parity of the iterates at that count.
+FULL = {
+    "c3": ("c3_rand_k3_n256.npz",
+           dict(case="random", k_prime=3, n_elem=256, dim=2, seed=1234, max_iter=150)),
+    "c4": ("c4_psi3d_k2_n32.npz",
+           dict(case="psi-mms", k_prime=2, n_elem=32, dim=3, seed=0, max_iter=400)),
+}
+
+
+@pytest.mark.parametrize("cfg", sorted(FULL))
+def test_full_size_config_vs_reference(gpu, cfg):
+    """BASELINE configs 3 (2D k'=3 256^2, U[-1,1] seed 1234) and 4 (3D 32^3
+    psi-MMS) at FULL size against the reference's own solve of the identical
+    system (tests/golden/make_golden_large.py): rel-L2 <= 1e-8, outer
+    iterations +-2, inner means close, the Euclidean residual history within
+    1e-8 relative, convergence (C4: final residual <= 1e-8) or the same capped
+    non-convergence (C3), and the true residual ||b - K x|| / ||b|| through the
+    device saddle apply agreeing with the recurrence."""
+    host, solver = gpu
+    name, kw = FULL[cfg]
+    g = load_golden(name)
+    s = host.assemble(kw["case"], kw["k_prime"], kw["n_elem"], dim=kw["dim"], seed=kw["seed"])
+    assert [s.n_u, s.n_p, s.A.nnz, s.B.nnz, s.Q.nnz] == g["sizes"].tolist()
+    gs = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    sol = gs.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1,
+                                                max_iter=kw["max_iter"]))
+    x = np.concatenate([sol.u, sol.p])
+    xr = np.concatenate([g["u"], g["p"]])
+    rel = np.linalg.norm(x - xr) / np.linalg.norm(xr)
+    assert rel <= 1e-8, rel
+    assert abs(sol.report.iterations - int(g["meta"][0])) <= 2, (sol.report.iterations, g["meta"])
+    assert abs(sol.report.mean_inner_top - g["meta"][2]) < 0.2
+    assert abs(sol.report.mean_inner_bottom - g["meta"][3]) < 0.2
+    he, hr = sol.report.euclid_history, g["he"]
+    m = min(len(he), len(hr))
+    assert np.all(np.abs(he[:m] - hr[:m]) <= 1e-8 * hr[:m])
+    assert sol.report.converged == bool(g["meta"][1])
+    if sol.report.converged:
+        assert sol.report.relres_e <= 1e-8
+    b = np.concatenate([s.f, np.zeros(s.n_p)])
+    true = np.linalg.norm(b - gs.apply(x)) / np.linalg.norm(b)
+    assert abs(true - sol.report.relres_e) <= 1e-3 * sol.report.relres_e + 1e-12
+    gs.close()

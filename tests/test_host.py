@@ -98,3 +98,18 @@ def test_errors():
         host.ic0(CsrMatrix(2, 2, np.array([0, 1, 2], np.int64), np.array([0, 1], np.int32),
                            np.array([1.0, -1.0])))
     assert e.value.row == 1
+
+
+def test_full_size_golden_systems_match_native_assembly_sizes():
+    """The C3/C4 golden fixtures (reference solves, make_golden_large.py) were
+    produced on systems of exactly SURVEY.md §8(d)'s structural sizes."""
+    import numpy as np
+    from conftest import GOLDEN
+    import os
+    exp = {"c3_rand_k3_n256.npz": [133644, 67081, 16713212, 7391304, 3243601],
+           "c4_psi3d_k2_n32.npz": [114444, 39304, 53944848, 15492096, 4410944]}
+    for name, sizes in exp.items():
+        g = np.load(os.path.join(GOLDEN, name))
+        assert g["sizes"].tolist() == sizes
+        assert len(g["u"]) == sizes[0] and len(g["p"]) == sizes[1]
+        assert np.all(np.isfinite(g["u"])) and np.all(np.isfinite(g["p"]))
