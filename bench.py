@@ -41,6 +41,15 @@ WORKLOADS = {
     "c1": dict(case="psi-mms", k=2, n=16, dim=2, seed=0, strategy="IC0-PCG(A)+Diag(Q)",
                outer=1e-8, inners=(1e-1,),
                label="C1: 2D k'=2 16x16 psi-MMS, IC0-PCG(A)+Diag(Q), outer 1e-8, inner 1e-1"),
+    # C3 stagnates near 4e-7 in the reference too (variable relaxed preconditioner):
+    # capped at 150 outer iterations (tests/golden/make_golden_large.py)
+    "c3": dict(case="random", k=3, n=256, dim=2, seed=1234, strategy="IC0-PCG(A,Q)",
+               outer=1e-8, inners=(1e-1,), max_iter=150, cpu_max_iter=20,
+               label="C3: 2D k'=3 256x256 U[-1,1] seed 1234, IC0-PCG(A,Q), outer 1e-8 (cap 150), "
+                     "inner 1e-1"),
+    "c4": dict(case="psi-mms", k=2, n=32, dim=3, seed=0, strategy="IC0-PCG(A,Q)",
+               outer=1e-8, inners=(1e-1,), cpu_max_iter=12,
+               label="C4: 3D k'=2 32^3 psi-MMS, IC0-PCG(A,Q), outer 1e-8, inner 1e-1"),
 }
 METRIC = "MINRES outer iterations/s (time-to-solution of the BASELINE C2 solve pair)"
 
@@ -61,15 +70,20 @@ def measured_peak():
 
 
 def measured_traffic(label: str):
-    """DRAM bytes (read + write) of the dominant kernel per step, from the
-    committed ncu --set full capture of tools/minres_profile.py (both launches
-    of one step summed), or None when no capture matches this workload."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_minres_traffic.json")) as fh:
-            t = json.load(fh)
-        return float(t["dram_bytes_per_step"]) if t.get("workload") == label else None
-    except Exception:
-        return None
+    """DRAM bytes (read + write) of the dominant kernel per step, from a
+    committed ncu capture of tools/minres_profile.py (profiles/
+    r01_minres_traffic*.json; all launches of one step summed), or None when
+    no capture matches this workload."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_minres_traffic*.json"))):
+        try:
+            with open(path) as fh:
+                t = json.load(fh)
+            if t.get("workload") == label:
+                return float(t["dram_bytes_per_step"])
+        except Exception:
+            continue
+    return None
 
 
 class ClockSampler:
@@ -112,6 +126,20 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)[:80]}
 
 
+def reduce_over_ranks(dist, device, ms: float, units: float):
+    """Whole-job timing of one replica per rank: (max over ranks of the
+    device-timed ms, sum over ranks of the units processed). With no process
+    group (N = 1) the inputs pass through. Collective: every rank calls it."""
+    if dist is None:
+        return ms, units
+    import torch
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    u = torch.tensor([units], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
 def algorithmic_bytes(info: dict, rep, outer_iters: int) -> float:
     """SURVEY.md §8(d) algorithmic bytes of one solve with the counted work:
     outer_iters saddle SpMVs + MINRES vector passes, and for each block
@@ -143,7 +171,8 @@ def run_ours(args, world, rank, local):
     g = solver.GpuStokesSolver(s, W["strategy"], device=local)
     setup_s = time.perf_counter() - t0
     info = g.info()
-    opts = [solver.SolverOptions(outer_tol=W["outer"], inner_tol=t) for t in W["inners"]]
+    opts = [solver.SolverOptions(outer_tol=W["outer"], inner_tol=t,
+                                 max_iter=W.get("max_iter", 20000)) for t in W["inners"]]
     dev = torch.device("cuda", local)
     d_f = torch.from_numpy(s.f).to(dev)
     d_u = torch.empty(s.n_u, dtype=torch.float64, device=dev)
@@ -175,13 +204,11 @@ def run_ours(args, world, rank, local):
             iters += sum(r.iterations for r in reps)
             launches += sum(r.gpu_launches for r in reps)
             last = reps
+    dev_ms, job_iters = reduce_over_ranks(dist, dev, dev_ms, iters)
     if dist:
-        t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
         dist.barrier()
     ms_per_step = dev_ms / args.steps
-    value = world * iters / (dev_ms * 1e-3)
+    value = job_iters / (dev_ms * 1e-3)
 
     # ---- e2e: host buffers through the C ABI (pinned), wall clock ---------
     f_pin = torch.from_numpy(s.f.copy()).pin_memory()
@@ -199,11 +226,8 @@ def run_ours(args, world, rank, local):
             e2e_iters += sol.report.iterations
         torch.cuda.synchronize()
         e2e_s += time.perf_counter() - t1
-    if dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * e2e_iters / e2e_s
+    e2e_ms, job_e2e_iters = reduce_over_ranks(dist, dev, e2e_s * 1e3, e2e_iters)
+    e2e_value = job_e2e_iters / (e2e_ms * 1e-3)
 
     # ---- roofline of the dominant kernel (the persistent MINRES kernel) ----
     peak, peak_kind = measured_peak()
@@ -272,35 +296,52 @@ def run_ours(args, world, rank, local):
     return result
 
 
+def cpu_runner(W):
+    """run(inner_tol, max_iter) -> result dict of the reference solve of the
+    workload on this host: oracle/_ref (the unmodified reference; its own
+    assembly in 2D, the native 3D blocks through ref_from_csr since the
+    reference has no 3D code) or, when it is not built, the C restatement."""
+    from oracle import CSR, RefLib, ref_available
+    from paper_1309_5048_b200 import host
+    c = lambda m: CSR(m.n_rows, m.n_cols, m.row_ptr, m.cols, m.vals)  # noqa: E731
+    if ref_available():
+        R = RefLib()
+        if W["dim"] == 2:
+            rs = R.assemble(W["case"], W["k"], W["n"], seed=W["seed"])
+        else:
+            s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
+            rs = R.from_csr(c(s.A), c(s.B), c(s.Q), s.f, nu=s.nu)
+        return (lambda t, mi: rs.solve(W["strategy"], W["outer"], t, max_iter=mi)), "reference"
+    from oracle import PortLib
+    P = PortLib()
+    s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
+    return (lambda t, mi: P.solve_stokes(c(s.A), c(s.B), c(s.Bt), c(s.Q_nu), s.f, W["strategy"],
+                                         W["outer"], t, max_iter=mi, Q_filter=c(s.Q))), "port"
+
+
+def cpu_sample_note(W, reps):
+    cap = W.get("cpu_max_iter")
+    what = (f"the first {cap} outer iterations of each solve" if cap else
+            f"the {len(W['inners'])}-solve step")
+    return (f"{reps} x {what} (MINRES time only, setup excluded; the reference solver is "
+            "single-threaded)")
+
+
 def cpu_baseline(args, W):
     """The reference (oracle/_ref) on this host's cores, bounded sample."""
     try:
-        from oracle import RefLib, ref_available
-        if not ref_available():
-            from oracle import CSR, PortLib
-            from paper_1309_5048_b200 import host
-            P = PortLib()
-            s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
-            c = lambda m: CSR(m.n_rows, m.n_cols, m.row_ptr, m.cols, m.vals)  # noqa: E731
-            kind = "port"
-            run = lambda t: P.solve_stokes(c(s.A), c(s.B), c(s.Bt), c(s.Q_nu), s.f, W["strategy"],  # noqa: E731
-                                           W["outer"], t, Q_filter=c(s.Q))
-        else:
-            R = RefLib()
-            rs = R.assemble(W["case"], W["k"], W["n"], seed=W["seed"])
-            kind = "reference"
-            run = lambda t: rs.solve(W["strategy"], W["outer"], t)  # noqa: E731
+        run, kind = cpu_runner(W)
+        cap = W.get("cpu_max_iter", W.get("max_iter", 20000))
         iters, secs, reps = 0, 0.0, 0
         t_start = time.perf_counter()
         while reps < 3 and time.perf_counter() - t_start < args.cpu_budget_s:
             for t in W["inners"]:
-                r = run(t)
+                r = run(t, cap)
                 iters += r["iterations"]
                 secs += r["wall_seconds"]
             reps += 1
         return {"value": iters / secs, "unit": "iter/s", "cores": 1, "kind": kind,
-                "sample": f"{reps} x the {len(W['inners'])}-solve step (MINRES time only, "
-                          "setup excluded; the reference solver is single-threaded)"}
+                "sample": cpu_sample_note(W, reps)}
     except Exception as e:
         return {"value": None, "unit": "iter/s", "cores": 1, "kind": "reference",
                 "sample": f"unavailable: {str(e)[:100]}"}
@@ -310,28 +351,15 @@ def run_reference(args, world, rank):
     if rank != 0:
         return None
     W = WORKLOADS[args.workload]
-    from oracle import RefLib, ref_available
-    if ref_available():
-        R = RefLib()
-        rs = R.assemble(W["case"], W["k"], W["n"], seed=W["seed"])
-        run = lambda t: rs.solve(W["strategy"], W["outer"], t)  # noqa: E731
-        kind = "reference"
-    else:
-        from oracle import CSR, PortLib
-        from paper_1309_5048_b200 import host
-        P = PortLib()
-        s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
-        c = lambda m: CSR(m.n_rows, m.n_cols, m.row_ptr, m.cols, m.vals)  # noqa: E731
-        run = lambda t: P.solve_stokes(c(s.A), c(s.B), c(s.Bt), c(s.Q_nu), s.f, W["strategy"],  # noqa: E731
-                                       W["outer"], t, Q_filter=c(s.Q))
-        kind = "port"
+    run, kind = cpu_runner(W)
+    cap = W.get("cpu_max_iter", W.get("max_iter", 20000))
     for _ in range(args.warmup):
         for t in W["inners"][:1]:
-            run(t)
+            run(t, cap)
     iters, secs = 0, 0.0
     for _ in range(args.steps):
         for t in W["inners"]:
-            r = run(t)
+            r = run(t, cap)
             iters += r["iterations"]
             secs += r["wall_seconds"]
     value = iters / secs
@@ -341,7 +369,7 @@ def run_reference(args, world, rank):
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": W["label"], "parallelism": "1 host core (serial reference)"},
            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": kind,
-                            "sample": f"{args.steps} steps of the full workload (MINRES time)"},
+                            "sample": cpu_sample_note(W, args.steps)},
            "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

@@ -630,16 +630,33 @@ static void flow_stats(const HostFlow& f, const char* name) {
 
 // Staged plans for every IC(0) block with one shared B capacity; lowers the
 // merge factor until the B entries fit kTBMax. Returns the capacity used.
+// Host memory: at most one DepRows (~16 B per factor entry) is alive at a
+// time -- a first pass only measures the B capacity, the second rebuilds each
+// direction's rows and turns them into its flow -- and each exact column-order
+// sweep (only needed by DSGPU_EXACT, which does not come here) is released once
+// its flow exists. At 96^3 (717M factor entries) this is the difference
+// between fitting the GPU box's host memory and not.
 int build_block_flows(HostPlan& P, int merge, int* merge_used, size_t smem_budget, int force_ring_n) {
+  auto rows_of = [](const HostSweep& s, int M) {
+    DepRows r = rows_from_sweep(s);
+    if (M > 1) return merge_levels(r, M);
+    return r;  // moved: no copy when M <= 1
+  };
+  auto release = [](HostSweep& s) {  // keep n, n_groups, n_levels
+    std::vector<int64_t>().swap(s.gptr);
+    std::vector<int32_t>().swap(s.gwidth);
+    std::vector<int32_t>().swap(s.grows);
+    std::vector<int32_t>().swap(s.cols);
+    std::vector<double>().swap(s.vals);
+    std::vector<double>().swap(s.diag);
+  };
   for (int M = std::max(1, merge);; M = M > 1 ? M / 2 : 0) {
     if (M == 0) throw std::invalid_argument("flow sweep: dependency fan-in too large");
-    DepRows rows[2][2];
     int need = 1;
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 2 && need <= kTBMax; ++b) {
       if (P.blk[b].kind != DSGPU_BLOCK_PCG_IC0) continue;
-      rows[b][0] = merge_levels(rows_from_sweep(P.blk[b].fwd), M);
-      rows[b][1] = merge_levels(rows_from_sweep(P.blk[b].bwd), M);
-      need = std::max({need, flow_b_needed(rows[b][0]), flow_b_needed(rows[b][1])});
+      need = std::max(need, flow_b_needed(rows_of(P.blk[b].fwd, M)));
+      if (need <= kTBMax) need = std::max(need, flow_b_needed(rows_of(P.blk[b].bwd, M)));
     }
     if (need > kTBMax) continue;
     const int tb = need <= 8 ? 8 : 16;
@@ -653,8 +670,10 @@ int build_block_flows(HostPlan& P, int merge, int* merge_used, size_t smem_budge
         ring = 1;
     for (int b = 0; b < 2; ++b) {
       if (P.blk[b].kind != DSGPU_BLOCK_PCG_IC0) continue;
-      build_flow(rows[b][0], tb, ring, P.blk[b].ffwd);
-      build_flow(rows[b][1], tb, ring, P.blk[b].fbwd);
+      build_flow(rows_of(P.blk[b].fwd, M), tb, ring, P.blk[b].ffwd);
+      release(P.blk[b].fwd);
+      build_flow(rows_of(P.blk[b].bwd, M), tb, ring, P.blk[b].fbwd);
+      release(P.blk[b].bwd);
       P.blk[b].ffwd.merge = P.blk[b].fbwd.merge = M;
       flow_stats(P.blk[b].ffwd, b == 0 ? "A fwd" : "Q fwd");
       flow_stats(P.blk[b].fbwd, b == 0 ? "A bwd" : "Q bwd");

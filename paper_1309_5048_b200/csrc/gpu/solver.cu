@@ -307,6 +307,8 @@ __device__ unsigned g_hsleep = 20;
 // timing experiments only (DSGPU_NOWAIT=1): the main warp does not wait for
 // the co-mains (results are wrong); isolates the main warp's own loop cost
 __device__ int g_nowait = 0;
+__device__ int g_coplace = 0;
+constexpr int kDefaultCoplace = 0;  // co-main warp placement (flow_sweep), DSGPU_COPLACE
 // phase diagnostics of the persistent kernel: [0] CTA0 cycles in grid barriers,
 // [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
@@ -418,11 +420,18 @@ __device__ void flow_sweep(const DFlow& s_in, int n, double* smem, const double*
   // SM sub-partition, nearly idle); co-mains = the kCo warps before main (other
   // sub-partition); helpers = the remaining warps off main's sub-partition.
   constexpr int kCo = 2;  // co-main warps (round-robin over groups)
+  // g_coplace != 0: the co-mains sit on main's own sub-partition (warps main-8,
+  // main-12, otherwise idle) instead of competing with helpers for issue slots
   const int mainw = nw - 1, prodw = nw - 5;
-  const int cid = warp < mainw && warp >= mainw - kCo ? mainw - 1 - warp : -1;
+  const bool coplace = g_coplace != 0 && nw >= 13;
+  auto co_index = [&](int w) {
+    if (coplace) return w == mainw - 8 ? 0 : (w == mainw - 12 ? 1 : -1);
+    return w < mainw && w >= mainw - kCo ? mainw - 1 - w : -1;
+  };
+  const int cid = co_index(warp);
   int hid = -1, nh = 0;
   for (int w = 0; w < nw; ++w)
-    if (w != mainw && !(w < mainw && w >= mainw - kCo) && (w & 3) != (mainw & 3)) {
+    if (w != mainw && co_index(w) < 0 && (w & 3) != (mainw & 3)) {
       if (w == warp) hid = nh;
       ++nh;
     }
@@ -1772,17 +1781,35 @@ DSweep upload_sweep(dsgpu_handle* h, const HostSweep& s) {
 // factor's lower bandwidth x DSGPU_PI_B (default 1.5, measured best on C2); the pressure block is cut
 // into no more blocks than the velocity block so both chains share steps.
 // Off (staged sweeps) when DSGPU_PI=0, when the windows do not fit shared
-// memory, or when the block inverses would exceed half the free HBM.
+// memory, when the block inverses would exceed half the free HBM, or when the
+// cost model below predicts the staged sweeps to be competitive. DSGPU_PI=1
+// skips the cost model.
+//
+// Cost model (B200, measured: profiles/r01_configs_c3_c4.jsonl). A PI apply
+// streams every coefficient once (both blocks' chains run together) and pays
+// a short latency per chain step; a staged sweep pays per dependency level
+// and the two blocks' sweeps run concurrently on their server CTAs:
+//   t_pi     = 8 n_coef / 5.5 TB/s + 1.3 us x steps
+//   t_staged = 0.6 us x max_b (levels_fwd + levels_bwd)
+// PI is chosen when t_pi < 0.7 t_staged: C2 (51 MB of coefficients, 2,048
+// levels), C3 (16 GB, 11,032 levels: PI 3.1 ms vs staged 8.6 ms per apply);
+// not C4 (3D, lower bandwidth 23k: 80 GB of coefficients, 14 ms per apply
+// vs 14.5 ms staged, and the staged solve is 1.4x faster end to end).
 bool choose_pi(dsgpu_handle* h, const HostPlan& P, size_t smem_budget) {
-  if (const char* env = std::getenv("DSGPU_PI"))
+  bool force = false;
+  if (const char* env = std::getenv("DSGPU_PI")) {
     if (std::atoi(env) == 0) return false;
+    force = true;
+  }
   const double mult = std::getenv("DSGPU_PI_B") ? std::atof(std::getenv("DSGPU_PI_B")) : 1.5;
   int nb0 = 0;
   size_t bytes = 0;
+  double staged_levels = 0.0;
   for (int b = 0; b < 2; ++b) {
     h->pip[b] = PiPlan{};
     const HostBlock& hb = P.blk[b];
     if (hb.kind != DSGPU_BLOCK_PCG_IC0) continue;
+    staged_levels = std::max(staged_levels, static_cast<double>(hb.fwd.n_levels + hb.bwd.n_levels));
     const int bw = pi_bandwidth(hb.n, hb.lrp.data(), hb.lci.data());
     int bsz = std::max(1, static_cast<int>(std::ceil(std::max(1, bw) * mult)));
     if (b == 1 && nb0 > 0) bsz = std::max(bsz, (hb.n + nb0 - 1) / nb0);
@@ -1794,7 +1821,12 @@ bool choose_pi(dsgpu_handle* h, const HostPlan& P, size_t smem_budget) {
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   if (smem > smem_budget || bytes > free_b / 2) return false;
-  h->pi_steps = 2 * std::max(h->pip[0].nb, h->pip[1].nb);
+  const int steps = 2 * std::max(h->pip[0].nb, h->pip[1].nb);
+  const double coef_bytes = 8.0 * static_cast<double>(h->pip[0].n_coef + h->pip[1].n_coef);
+  const double t_pi = coef_bytes / 5.5e12 + 1.3e-6 * steps;
+  const double t_staged = 0.6e-6 * staged_levels;
+  if (!force && !(t_pi < 0.7 * t_staged)) return false;
+  h->pi_steps = steps;
   return true;
 }
 
@@ -1875,6 +1907,11 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     if (const char* env = std::getenv("DSGPU_NOWAIT")) {
       const int v = std::atoi(env);
       cudaMemcpyToSymbol(g_nowait, &v, sizeof(v));
+    }
+    {
+      const char* env = std::getenv("DSGPU_COPLACE");
+      const int v = env ? std::atoi(env) : kDefaultCoplace;
+      cudaMemcpyToSymbol(g_coplace, &v, sizeof(v));
     }
     if (const char* env = std::getenv("DSGPU_HSLEEP")) {
       const unsigned ns = static_cast<unsigned>(std::max(0, std::atoi(env)));
@@ -2043,14 +2080,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       h->nnz_a = s;
     }
     for (int b = 0; b < 2; ++b)
-      h->nnz_l[b] = P.blk[b].kind == DSGPU_BLOCK_PCG_IC0
-                        ? static_cast<int64_t>(P.blk[b].fwd.diag.size()) +
-                              [&] {
-                                int64_t c = 0;
-                                for (auto x : P.blk[b].fwd.cols) c += x >= 0;
-                                return c;
-                              }()
-                        : 0;
+      h->nnz_l[b] = P.blk[b].kind == DSGPU_BLOCK_PCG_IC0 ? P.blk[b].lrp.back() : 0;
     h->nnz_q = P.blk[1].rp.empty() ? 0 : P.blk[1].rp.back();
     a.perm_u = h->upload(P.blk[0].perm);
     a.perm_p = h->upload(P.blk[1].perm);

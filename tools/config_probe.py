@@ -1,6 +1,6 @@
 """Solve BASELINE configs C3 / C4 on the GPU and record timings + parity.
 
-  python tools/config_probe.py c3 [c4 ...]  [--modes pi,staged]
+  python tools/config_probe.py c3 [c4 ...]  [--modes=auto,1,0]
 
 Per config and IC(0) apply mode (DSGPU_PI=1 partitioned inverse / 0 staged
 sweeps): native assembly + host setup time, device setup time, two solves
@@ -29,6 +29,10 @@ CFG = {
     "k3n128": dict(case="random", k=3, n=128, dim=2, seed=1234, outer=1e-8, inner=1e-1,
                    golden=None),
     "3d16": dict(case="psi-mms", k=2, n=16, dim=3, seed=0, outer=1e-8, inner=1e-1, golden=None),
+    # C5 data (U[-1,1] seed 42, outer 1e-6) at growing 3D sizes, and C5 itself
+    "c5_48": dict(case="random", k=2, n=48, dim=3, seed=42, outer=1e-6, inner=1e-1, golden=None),
+    "c5_64": dict(case="random", k=2, n=64, dim=3, seed=42, outer=1e-6, inner=1e-1, golden=None),
+    "c5": dict(case="random", k=2, n=96, dim=3, seed=42, outer=1e-6, inner=1e-1, golden=None),
 }
 
 
@@ -36,10 +40,34 @@ T0 = time.time()
 
 
 def log(msg):
-    print(f"[{time.time() - T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+    import resource
+    rss = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20
+    print(f"[{time.time() - T0:7.1f}s rss {rss:6.1f} GB] {msg}", file=sys.stderr, flush=True)
+
+
+def memguard(min_avail_gb: float):
+    """Exit the process (not the box) before the host runs out of memory: poll
+    MemAvailable and _exit(3) below the threshold (C5-size setups)."""
+    import threading
+
+    def watch():
+        while True:
+            with open("/proc/meminfo") as fh:
+                for line in fh:
+                    if line.startswith("MemAvailable:"):
+                        avail = int(line.split()[1]) / 2**20
+                        break
+            if avail < min_avail_gb:
+                log(f"memguard: MemAvailable {avail:.1f} GB < {min_avail_gb} GB, exiting")
+                os._exit(3)
+            time.sleep(0.1)
+
+    threading.Thread(target=watch, daemon=True).start()
 
 
 def main():
+    if os.environ.get("PROBE_MEMGUARD_GB"):
+        memguard(float(os.environ["PROBE_MEMGUARD_GB"]))
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     modes = ["1", "0"]
     for a in sys.argv[1:]:
@@ -61,7 +89,10 @@ def main():
         if c["golden"] and os.path.exists(os.path.join(ROOT, "tests", "golden", c["golden"])):
             gold = np.load(os.path.join(ROOT, "tests", "golden", c["golden"]))
         for mode in modes:
-            os.environ["DSGPU_PI"] = mode
+            if mode == "auto":  # the setup's own choice (cost model)
+                os.environ.pop("DSGPU_PI", None)
+            else:
+                os.environ["DSGPU_PI"] = mode
             out = dict(cfg=tag, pi=mode, n_u=s.n_u, n_p=s.n_p, assemble_s=round(t_asm, 2),
                        host_setup_s=round(t_host, 2))
             try:

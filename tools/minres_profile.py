@@ -9,7 +9,8 @@ from paper_1309_5048_b200 import host, solver
 W = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
 g = solver.GpuStokesSolver(s, W["strategy"])
-opts = [solver.SolverOptions(outer_tol=W["outer"], inner_tol=t) for t in W["inners"]]
+opts = [solver.SolverOptions(outer_tol=W["outer"], inner_tol=t, max_iter=W.get("max_iter", 20000))
+        for t in W["inners"]]
 for step in range(2):
     for o in opts:
         sol = g.solve(s.f, o, history=False)
