@@ -307,8 +307,6 @@ __device__ unsigned g_hsleep = 20;
 // timing experiments only (DSGPU_NOWAIT=1): the main warp does not wait for
 // the co-mains (results are wrong); isolates the main warp's own loop cost
 __device__ int g_nowait = 0;
-__device__ int g_coplace = 0;
-constexpr int kDefaultCoplace = 0;  // co-main warp placement (flow_sweep), DSGPU_COPLACE
 // phase diagnostics of the persistent kernel: [0] CTA0 cycles in grid barriers,
 // [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
@@ -420,18 +418,11 @@ __device__ void flow_sweep(const DFlow& s_in, int n, double* smem, const double*
   // SM sub-partition, nearly idle); co-mains = the kCo warps before main (other
   // sub-partition); helpers = the remaining warps off main's sub-partition.
   constexpr int kCo = 2;  // co-main warps (round-robin over groups)
-  // g_coplace != 0: the co-mains sit on main's own sub-partition (warps main-8,
-  // main-12, otherwise idle) instead of competing with helpers for issue slots
   const int mainw = nw - 1, prodw = nw - 5;
-  const bool coplace = g_coplace != 0 && nw >= 13;
-  auto co_index = [&](int w) {
-    if (coplace) return w == mainw - 8 ? 0 : (w == mainw - 12 ? 1 : -1);
-    return w < mainw && w >= mainw - kCo ? mainw - 1 - w : -1;
-  };
-  const int cid = co_index(warp);
+  const int cid = warp < mainw && warp >= mainw - kCo ? mainw - 1 - warp : -1;
   int hid = -1, nh = 0;
   for (int w = 0; w < nw; ++w)
-    if (w != mainw && co_index(w) < 0 && (w & 3) != (mainw & 3)) {
+    if (w != mainw && !(w < mainw && w >= mainw - kCo) && (w & 3) != (mainw & 3)) {
       if (w == warp) hid = nh;
       ++nh;
     }
@@ -1777,57 +1768,74 @@ DSweep upload_sweep(dsgpu_handle* h, const HostSweep& s) {
   return d;
 }
 
-// Partitioned-inverse mode (pi.hpp) for the IC(0) blocks: block size = the
-// factor's lower bandwidth x DSGPU_PI_B (default 1.5, measured best on C2); the pressure block is cut
-// into no more blocks than the velocity block so both chains share steps.
-// Off (staged sweeps) when DSGPU_PI=0, when the windows do not fit shared
-// memory, when the block inverses would exceed half the free HBM, or when the
-// cost model below predicts the staged sweeps to be competitive. DSGPU_PI=1
-// skips the cost model.
+// Partitioned-inverse mode (pi.hpp) for the IC(0) blocks. Block size = the
+// factor's lower bandwidth x m, with m the candidate (0.5, 1, 1.5; DSGPU_PI_B
+// fixes it) of least modelled apply time; the pressure block is cut into no
+// more blocks than the velocity block so both chains share steps. Off (staged
+// sweeps) when DSGPU_PI=0, when the windows do not fit shared memory, when the
+// block inverses would exceed half the free HBM, or when the cost model
+// predicts the staged sweeps to be competitive. DSGPU_PI=1 skips the model.
 //
-// Cost model (B200, measured: profiles/r01_configs_c3_c4.jsonl). A PI apply
-// streams every coefficient once (both blocks' chains run together) and pays
-// a short latency per chain step; a staged sweep pays per dependency level
-// and the two blocks' sweeps run concurrently on their server CTAs:
-//   t_pi     = 8 n_coef / 5.5 TB/s + 1.3 us x steps
+// Cost model (B200, measured: profiles/r01_configs_c3_c4.jsonl,
+// r01_knobs_c3_pib.jsonl, r01_ic_ncu_c3_c4.md). A PI apply streams every
+// coefficient once (both blocks' chains run together, 3.9 TB/s measured by
+// ncu at C3) and pays a latency per chain step; a staged sweep pays per
+// dependency level and the two blocks' sweeps run concurrently:
+//   t_pi     = 8 n_coef / 3.9 TB/s + 2 us x steps
 //   t_staged = 0.6 us x max_b (levels_fwd + levels_bwd)
-// PI is chosen when t_pi < 0.7 t_staged: C2 (51 MB of coefficients, 2,048
-// levels), C3 (16 GB, 11,032 levels: PI 3.1 ms vs staged 8.6 ms per apply);
-// not C4 (3D, lower bandwidth 23k: 80 GB of coefficients, 14 ms per apply
-// vs 14.5 ms staged, and the staged solve is 1.4x faster end to end).
+// PI when t_pi < 0.7 t_staged: C2 (m = 1.5: 58 steps, latency-bound), C3
+// (m = 0.5: 2.0 ms per velocity apply vs 3.1 ms at m = 1.5 and 8.6 ms
+// staged); not C4/C5 (3D, lower bandwidth 23k+: tens of GB of block inverses;
+// C4 PI 14 ms per apply vs 14.5 ms staged, staged solve 1.4x faster).
 bool choose_pi(dsgpu_handle* h, const HostPlan& P, size_t smem_budget) {
   bool force = false;
   if (const char* env = std::getenv("DSGPU_PI")) {
     if (std::atoi(env) == 0) return false;
     force = true;
   }
-  const double mult = std::getenv("DSGPU_PI_B") ? std::atof(std::getenv("DSGPU_PI_B")) : 1.5;
-  int nb0 = 0;
-  size_t bytes = 0;
+  std::vector<double> mults = {0.5, 1.0, 1.5};
+  if (const char* env = std::getenv("DSGPU_PI_B")) mults = {std::atof(env)};
   double staged_levels = 0.0;
+  int bw[2] = {0, 0};
   for (int b = 0; b < 2; ++b) {
-    h->pip[b] = PiPlan{};
     const HostBlock& hb = P.blk[b];
     if (hb.kind != DSGPU_BLOCK_PCG_IC0) continue;
     staged_levels = std::max(staged_levels, static_cast<double>(hb.fwd.n_levels + hb.bwd.n_levels));
-    const int bw = pi_bandwidth(hb.n, hb.lrp.data(), hb.lci.data());
-    int bsz = std::max(1, static_cast<int>(std::ceil(std::max(1, bw) * mult)));
-    if (b == 1 && nb0 > 0) bsz = std::max(bsz, (hb.n + nb0 - 1) / nb0);
-    h->pip[b] = pi_plan(hb.n, hb.lrp.data(), hb.lci.data(), bsz);
-    if (b == 0) nb0 = h->pip[0].nb;
-    bytes += sizeof(double) * (static_cast<size_t>(h->pip[b].n_coef) + 8ull * hb.n);
+    bw[b] = pi_bandwidth(hb.n, hb.lrp.data(), hb.lci.data());
   }
-  const size_t smem = sizeof(double) * static_cast<size_t>(h->pip[0].wmax + h->pip[1].wmax + 32);
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  if (smem > smem_budget || bytes > free_b / 2) return false;
-  const int steps = 2 * std::max(h->pip[0].nb, h->pip[1].nb);
-  const double coef_bytes = 8.0 * static_cast<double>(h->pip[0].n_coef + h->pip[1].n_coef);
-  const double t_pi = coef_bytes / 5.5e12 + 1.3e-6 * steps;
+  double best = 0.0;
+  bool found = false;
+  for (const double mult : mults) {
+    PiPlan pp[2];
+    int nb0 = 0;
+    size_t bytes = 0;
+    for (int b = 0; b < 2; ++b) {
+      const HostBlock& hb = P.blk[b];
+      if (hb.kind != DSGPU_BLOCK_PCG_IC0) continue;
+      int bsz = std::max(1, static_cast<int>(std::ceil(std::max(1, bw[b]) * mult)));
+      if (b == 1 && nb0 > 0) bsz = std::max(bsz, (hb.n + nb0 - 1) / nb0);
+      pp[b] = pi_plan(hb.n, hb.lrp.data(), hb.lci.data(), bsz);
+      if (b == 0) nb0 = pp[0].nb;
+      bytes += sizeof(double) * (static_cast<size_t>(pp[b].n_coef) + 8ull * hb.n);
+    }
+    const size_t smem = sizeof(double) * static_cast<size_t>(pp[0].wmax + pp[1].wmax + 32);
+    if (smem > smem_budget || bytes > free_b / 2) continue;
+    const int steps = 2 * std::max(pp[0].nb, pp[1].nb);
+    const double coef_bytes = 8.0 * static_cast<double>(pp[0].n_coef + pp[1].n_coef);
+    const double t_pi = coef_bytes / 3.9e12 + 2e-6 * steps;
+    if (!found || t_pi < best) {
+      found = true;
+      best = t_pi;
+      h->pip[0] = pp[0];
+      h->pip[1] = pp[1];
+      h->pi_steps = steps;
+    }
+  }
+  if (!found) return false;
   const double t_staged = 0.6e-6 * staged_levels;
-  if (!force && !(t_pi < 0.7 * t_staged)) return false;
-  h->pi_steps = steps;
-  return true;
+  return force || best < 0.7 * t_staged;
 }
 
 // Shared memory of the PI kernels: both chain windows, then (when it fits)
@@ -1907,11 +1915,6 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     if (const char* env = std::getenv("DSGPU_NOWAIT")) {
       const int v = std::atoi(env);
       cudaMemcpyToSymbol(g_nowait, &v, sizeof(v));
-    }
-    {
-      const char* env = std::getenv("DSGPU_COPLACE");
-      const int v = env ? std::atoi(env) : kDefaultCoplace;
-      cudaMemcpyToSymbol(g_coplace, &v, sizeof(v));
     }
     if (const char* env = std::getenv("DSGPU_HSLEEP")) {
       const unsigned ns = static_cast<unsigned>(std::max(0, std::atoi(env)));
