@@ -62,6 +62,8 @@ constexpr int kTA = 16, kRing = 16, kSRing = 8, kFlowD = 7;
 // last kXRing groups' results live in a shared-memory ring, older ones in
 // global memory (published every kFenceEvery groups after a fence).
 constexpr int kXRing = 64, kFenceEvery = 8;
+// remote helpers: warps sharing one group's older-than-ring list (power of 2)
+constexpr int kRSplit = 4;
 // Supported per-lane B capacities (templates); the plan picks the smallest that fits.
 constexpr int kTBMax = 16;
 constexpr int kPW = 16;  // helper prefix-list chunk (entries per lane)

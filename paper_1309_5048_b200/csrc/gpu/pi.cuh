@@ -347,7 +347,7 @@ __device__ __forceinline__ void pi_reset(const DPi& P, unsigned set, int cta, in
 
 // Full apply for the active blocks (every thread of every CTA). rho0/rho1:
 // this warp's partial <r, z> (lane 0), to be reduced by the caller.
-__device__ void pi_apply(const DPi& P0, const DPi& P1, bool act0, bool act1, const PiRhs& rhs0,
+__device__ __forceinline__ void pi_apply(const DPi& P0, const DPi& P1, bool act0, bool act1, const PiRhs& rhs0,
                          const PiRhs& rhs1, double* zc0, double* zc1, unsigned par, int cta, int G, double* ws,
                          unsigned* ab, double& rho0, double& rho1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;

@@ -67,6 +67,7 @@ struct DFlow {
   const int64_t* gptr;
   const double* gvals;
   const int32_t *cptr, *cneed;  // prefix-list chunks: newest dependency group of each
+  int rsplit;                   // remote helpers: warps per group's older-than-ring list (<= kRSplit)
 };
 
 struct DBlock {
@@ -84,8 +85,8 @@ struct DBlock {
   double* bb;                   // materialized right-hand side (staged mode), n + 1
   // ring mode: partial sums of the entries older than the ring are computed by
   // "remote" helper CTAs and handed over through global memory
-  double* rpsum;                // max(G) * 32
-  unsigned* rflag;              // max(G): sweep tag once rpsum[g] is final
+  double* rpsum;                // max(G) * kRSplit * 32
+  unsigned* rflag;              // max(G) * kRSplit: sweep tag once rpsum[g][part] is final
   unsigned long long* gprog;    // (sweep tag << 32) | groups published by the main warp
   int remote_cta0, n_remote;    // remote helper CTAs (0: none)
   int pi;                       // 1: partitioned-inverse IC(0) apply (pi.cuh), all CTAs
@@ -346,17 +347,23 @@ __device__ void flow_remote(const DFlow& s, int n, const double* __restrict__ gx
   constexpr int PW = 16;
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int wid = rank * nw + (threadIdx.x >> 5), W = nranks * nw;
-  for (int g = wid; g < s.G; g += W) {
+  // task t = (group g, part): kRSplit consecutive warps share one group's list
+  // (chunks part, part + kRSplit, ...) so its partial sum is ready kRSplit x
+  // sooner; each part publishes its own slot and flag
+  const int S = s.rsplit;
+  for (int t = wid; t < s.G * S; t += W) {
+    const int g = t / S, part = t - g * S;
     const int gw = __ldg(s.gw + g);
     if (gw == 0) continue;
     const int gneed = __ldg(s.gneed + g);
     const int64_t gb = __ldg(s.gptr + g);
     const unsigned need = static_cast<unsigned>(gneed + 1);
-    double part = 0.0;
+    double acc = 0.0;
     SpinGuard sg(abort_flag);
-    const int32_t* gc = s.gcols + gb + lane;
-    const double* gv = s.gvals + gb + lane;
-    for (int k0 = 0; k0 < gw; k0 += PW, gc += PW * 32, gv += PW * 32) {
+    const int32_t* gc = s.gcols + gb + part * PW * 32 + lane;
+    const double* gv = s.gvals + gb + part * PW * 32 + lane;
+    bool waited = false;
+    for (int k0 = part * PW; k0 < gw; k0 += S * PW, gc += S * PW * 32, gv += S * PW * 32) {
       int pc[PW];
       double pv[PW];
 #pragma unroll
@@ -364,7 +371,8 @@ __device__ void flow_remote(const DFlow& s, int n, const double* __restrict__ gx
         pc[q] = __ldg(gc + q * 32);
         pv[q] = __ldg(gv + q * 32);
       }
-      if (k0 == 0)
+      if (!waited) {
+        waited = true;
         for (;;) {  // the tag must match: stale words of other sweeps never count
           const unsigned long long v = ld_acquire_u64(R.gprog);
           if (static_cast<unsigned>(v >> 32) == R.tag && static_cast<unsigned>(v) >= need) break;
@@ -374,15 +382,16 @@ __device__ void flow_remote(const DFlow& s, int n, const double* __restrict__ gx
             break;
           }
         }
+      }
       double pp[PW];
 #pragma unroll
       for (int q = 0; q < PW; ++q) pp[q] = mul_rn(pv[q], __ldcg(gx + pc[q]));
-      part = add_rn(part, tree_sum<PW>(pp));
+      acc = add_rn(acc, tree_sum<PW>(pp));
     }
-    __stcg(R.rpsum + static_cast<int64_t>(g) * 32 + lane, part);
+    __stcg(R.rpsum + static_cast<int64_t>(t) * 32 + lane, acc);
     __threadfence();
     __syncwarp();
-    if (lane == 0) st_release(R.rflag + g, R.tag);
+    if (lane == 0) st_release(R.rflag + t, R.tag);
   }
 }
 
@@ -682,15 +691,23 @@ __device__ void flow_sweep(const DFlow& s_in, int n, double* smem, const double*
       if (RING && R.on) {  // entries older than the ring: remote helpers' partial sum
         if (__ldg(s.gw + g) > 0) {
           const long long t0 = clock64();
-          while (ld_acquire(R.rflag + g) != R.tag) {
-            __nanosleep(20);
-            if (sg.expired()) {
-              g_flow_dbg[3] = 1000000000ull * 8 + 100000ull * G + g;
-              break;
+          double rp[kRSplit];
+#pragma unroll
+          for (int q = 0; q < kRSplit; ++q) {
+            rp[q] = 0.0;
+            if (q < s.rsplit) {
+              while (ld_acquire(R.rflag + g * s.rsplit + q) != R.tag) {
+                __nanosleep(20);
+                if (sg.expired()) {
+                  g_flow_dbg[3] = 1000000000ull * 8 + 100000ull * G + g;
+                  break;
+                }
+              }
+              rp[q] = __ldcg(R.rpsum + (static_cast<int64_t>(g) * s.rsplit + q) * 32 + lane);
             }
           }
           tw_rem += clock64() - t0;
-          acc = sub_rn(acc, __ldcg(R.rpsum + static_cast<int64_t>(g) * 32 + lane));
+          acc = sub_rn(acc, tree_sum<kRSplit>(rp));
         }
       } else if (RING) {  // entries older than the ring: global memory, once published
         const int gw = __ldg(s.gw + g);
@@ -1034,8 +1051,9 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
     if (!PI && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_S1, 0.0, &in);
   for (int b = 0; b < 2; ++b) {
     const DBlock& B = a.blk[b];
-    if (!PI && RING && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
-      ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
+    if constexpr (!PI && RING)
+      if (B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
+        ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
     if (B.kind == DSGPU_BLOCK_PCG_IC0) C.sweeps[b] += 2;
   }
   if constexpr (PI) {
@@ -1179,8 +1197,9 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
       if (!PI && active[b] && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_L2, alpha[b], nullptr);
     for (int b = 0; b < 2; ++b) {
       const DBlock& B = a.blk[b];
-      if (!PI && RING && active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
-        ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
+      if constexpr (!PI && RING)
+        if (active[b] && B.kind == DSGPU_BLOCK_PCG_IC0 && C.remote_rank(b) >= 0)
+          ic_apply_remote(B, C.remote_rank(b), C.abort_flag, a.launch_id, C.sweeps[b]);
       if (active[b] && B.kind == DSGPU_BLOCK_PCG_IC0) C.sweeps[b] += 2;
     }
     if constexpr (PI) {
@@ -1355,9 +1374,11 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
   __shared__ double sums[NSLOT];
-  if (!PI && static_cast<int>(blockIdx.x) < a.n_srv) {
-    ic_server<TB, RING>(a, blockIdx.x, xs_dyn, red);
-    return;
+  if constexpr (!PI) {  // (the PI variant must not even instantiate the sweeps)
+    if (static_cast<int>(blockIdx.x) < a.n_srv) {
+      ic_server<TB, RING>(a, blockIdx.x, xs_dyn, red);
+      return;
+    }
   }
   if (PI) pi_prologue();
   Ctx C(a, red, sums, xs_dyn);
@@ -1753,6 +1774,14 @@ DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
   d.wptr = h->upload(f.wptr);
   d.wcols = h->upload(f.wcols);
   d.wvals = h->upload(f.wvals);
+  // remote split: lists of >= 4 chunks per group on average get kRSplit warps,
+  // short ones 1 (a split only adds flags to wait on); DSGPU_RSPLIT overrides
+  double chunks = 0.0;
+  for (const int32_t w : f.gw) chunks += w / 16.0;
+  chunks /= std::max(1, f.G);
+  d.rsplit = chunks >= 4.0 ? kRSplit : 1;
+  if (const char* env = std::getenv("DSGPU_RSPLIT"))
+    d.rsplit = std::min(kRSplit, std::max(1, std::atoi(env)));
   return d;
 }
 
@@ -2057,10 +2086,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       if (hb.kind == DSGPU_BLOCK_PCG_IC0 && !h->exact && hb.ffwd.ring) {
         // remote helpers: CTAs [2 + b R, 2 + (b+1) R) of the persistent kernel
         const int G_max = std::max(hb.ffwd.G, hb.fbwd.G);
-        d.rpsum = h->alloc<double>(static_cast<size_t>(G_max) * 32);
-        d.rflag = h->alloc<unsigned>(G_max);
+        d.rpsum = h->alloc<double>(static_cast<size_t>(G_max) * kRSplit * 32);
+        d.rflag = h->alloc<unsigned>(static_cast<size_t>(G_max) * kRSplit);
         d.gprog = h->alloc<unsigned long long>(1);
-        cudaMemset(d.rflag, 0, sizeof(unsigned) * G_max);
+        cudaMemset(d.rflag, 0, sizeof(unsigned) * G_max * kRSplit);
         cudaMemset(d.gprog, 0, sizeof(unsigned long long));
         const int R = std::min(h->remote_max, (G - 1) / 2);
         d.n_remote = R > 0 ? R : 0;
