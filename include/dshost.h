@@ -28,7 +28,8 @@ enum {
   DSHOST_OK = 0,
   DSHOST_E_INVALID = 3,   /* std::invalid_argument in the reference */
   DSHOST_E_BREAKDOWN = 6, /* FactorBreakdown (proj/include/divstokes/cholesky.hpp:13-19) */
-  DSHOST_E_INTERNAL = 7
+  DSHOST_E_INTERNAL = 7,
+  DSHOST_E_RUNTIME = 8    /* std::runtime_error in the reference (I/O, file format) */
 };
 
 /* case ids: BASELINE psi-MMS forcing, lid-driven cavity (2D), seeded
@@ -64,6 +65,23 @@ int64_t dshost_lower_nnz(int n, const int64_t* row_ptr, const int32_t* cols);
 /* ic0: L arrays sized n+1 / dshost_lower_nnz; *bad_row = breakdown row. */
 int dshost_ic0(int n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
                int64_t* l_row_ptr, int32_t* l_cols, double* l_vals, int* bad_row);
+
+/* ---- Matrix Market wire format (proj/src/csr.cpp:126-175) ------------- */
+/* write_matrix_market: the reference's dump format byte for byte (header,
+ * size line, 1-based "i j v" lines at 17 significant digits; symmetric =
+ * lower triangle only). */
+int dshost_write_matrix_market(const char* path, int n_rows, int n_cols, const int64_t* row_ptr,
+                               const int32_t* cols, const double* vals, int symmetric);
+/* read_matrix_market: the CSR the reference's reader builds (symmetric
+ * entries mirrored, duplicates summed, csr_from_triplets ordering). Errors:
+ * DSHOST_E_RUNTIME (cannot open, bad header / type / size line, truncated
+ * entry list), DSHOST_E_INVALID (index out of range). */
+typedef struct dshost_csr dshost_csr;
+int dshost_read_matrix_market(const char* path, dshost_csr** out);
+/* Borrowed pointers into the matrix (valid until dshost_csr_free). */
+int dshost_csr_view(const dshost_csr* m, int* n_rows, int* n_cols, const int64_t** row_ptr,
+                    const int32_t** cols, const double** vals);
+void dshost_csr_free(dshost_csr* m);
 
 #ifdef __cplusplus
 }

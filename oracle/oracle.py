@@ -102,6 +102,12 @@ class RefLib:
                                 C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_char_p, C.c_int]
         L.ref_spmv.argtypes = [C.c_int, C.c_int, _i64p, _i32p, _dp, _dp, _dp]
         L.ref_rcm.argtypes = [C.c_int, _i64p, _i32p, _i32p, C.c_char_p, C.c_int]
+        L.ref_write_mm.argtypes = [C.c_int, C.c_int, _i64p, _i32p, _dp, C.c_char_p, C.c_int,
+                                   C.c_char_p, C.c_int]
+        L.ref_read_mm.restype = C.c_void_p
+        L.ref_read_mm.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int64), C.c_char_p, C.c_int]
+        L.ref_mm_take.argtypes = [C.c_void_p, _i64p, _i32p, _dp]
         L.ref_bandwidth.argtypes = [C.c_int, _i64p, _i32p]
         L.ref_bandwidth.restype = C.c_int
         L.ref_permute.argtypes = [C.c_int, _i64p, _i32p, _dp, _i32p, _i64p, _i32p, _dp,
@@ -145,6 +151,27 @@ class RefLib:
         if rc:
             raise ValueError(err.value.decode())
         return perm
+
+    def write_matrix_market(self, A: CSR, path: str, symmetric: bool = False) -> None:
+        """The reference's write_matrix_market (csr.cpp:126-142)."""
+        err = C.create_string_buffer(256)
+        rc = self.L.ref_write_mm(A.n_rows, A.n_cols, A.rp, A.ci, A.v, path.encode(), int(symmetric),
+                                 err, 256)
+        if rc:
+            raise RuntimeError(err.value.decode())
+
+    def read_matrix_market(self, path: str) -> CSR:
+        """The reference's read_matrix_market (csr.cpp:144-175)."""
+        nr, nc, nnz = C.c_int(), C.c_int(), C.c_int64()
+        err = C.create_string_buffer(256)
+        h = self.L.ref_read_mm(path.encode(), C.byref(nr), C.byref(nc), C.byref(nnz), err, 256)
+        if not h:
+            raise RuntimeError(err.value.decode())
+        rp = np.zeros(nr.value + 1, np.int64)
+        ci = np.zeros(nnz.value, np.int32)
+        v = np.zeros(nnz.value)
+        self.L.ref_mm_take(h, rp, ci, v)
+        return CSR(nr.value, nc.value, rp, ci, v)
 
     def bandwidth(self, A: CSR) -> int:
         return self.L.ref_bandwidth(A.n_rows, A.rp, A.ci)

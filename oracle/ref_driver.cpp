@@ -418,4 +418,35 @@ int ref_minres_csr(int n, const int64_t* rp, const int32_t* ci, const double* v,
   });
 }
 
+// ---- Matrix Market wire format (csr.cpp:126-175), for the dump / load
+// parity of the framework's reader and writer ---------------------------
+
+int ref_write_mm(int n_rows, int n_cols, const int64_t* rp, const int32_t* ci, const double* v,
+                 const char* path, int symmetric, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    write_matrix_market(csr_from_arrays(n_rows, n_cols, rp, ci, v), path, symmetric != 0);
+  });
+}
+
+// Two calls: ref_read_mm returns the matrix (heap) and its sizes; ref_mm_take
+// copies it out and frees it.
+void* ref_read_mm(const char* path, int* n_rows, int* n_cols, int64_t* nnz, char* err, int errlen) {
+  CsrMatrix* out = nullptr;
+  const int rc = guarded(err, errlen, [&] {
+    out = new CsrMatrix(read_matrix_market(path));
+    *n_rows = out->n_rows;
+    *n_cols = out->n_cols;
+    *nnz = static_cast<int64_t>(out->cols.size());
+  });
+  return rc ? nullptr : out;
+}
+
+void ref_mm_take(void* m, int64_t* rp, int32_t* ci, double* v) {
+  auto* a = static_cast<CsrMatrix*>(m);
+  std::copy(a->row_ptr.begin(), a->row_ptr.end(), rp);
+  std::copy(a->cols.begin(), a->cols.end(), ci);
+  std::copy(a->vals.begin(), a->vals.end(), v);
+  delete a;
+}
+
 }  // extern "C"

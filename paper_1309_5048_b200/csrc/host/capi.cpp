@@ -10,6 +10,9 @@
 struct dshost_system {
   dshost::System sys;
 };
+struct dshost_csr {
+  dshost::Csr m;
+};
 
 namespace {
 thread_local std::string g_err;
@@ -28,6 +31,9 @@ int guard(F&& f) {
   } catch (const std::domain_error& e) {
     g_err = e.what();
     return DSHOST_E_INVALID;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return DSHOST_E_RUNTIME;
   } catch (const std::exception& e) {
     g_err = e.what();
     return DSHOST_E_INTERNAL;
@@ -133,5 +139,38 @@ int dshost_ic0(int n, const int64_t* row_ptr, const int32_t* cols, const double*
     }
   });
 }
+
+int dshost_write_matrix_market(const char* path, int n_rows, int n_cols, const int64_t* row_ptr,
+                               const int32_t* cols, const double* vals, int symmetric) {
+  return guard([&] {
+    if (!path || n_rows < 0 || n_cols < 0 || !row_ptr) throw std::invalid_argument("write_matrix_market: bad input");
+    dshost::write_matrix_market(view(n_rows, n_cols, row_ptr, cols, vals), path, symmetric != 0);
+  });
+}
+
+int dshost_read_matrix_market(const char* path, dshost_csr** out) {
+  *out = nullptr;
+  return guard([&] {
+    if (!path) throw std::invalid_argument("read_matrix_market: null path");
+    auto* m = new dshost_csr{dshost::read_matrix_market(path)};
+    *out = m;
+  });
+}
+
+int dshost_csr_view(const dshost_csr* m, int* n_rows, int* n_cols, const int64_t** row_ptr,
+                    const int32_t** cols, const double** vals) {
+  if (!m) {
+    g_err = "dshost_csr_view: null matrix";
+    return DSHOST_E_INVALID;
+  }
+  *n_rows = m->m.n_rows;
+  *n_cols = m->m.n_cols;
+  *row_ptr = m->m.rp.data();
+  *cols = m->m.ci.data();
+  *vals = m->m.v.data();
+  return DSHOST_OK;
+}
+
+void dshost_csr_free(dshost_csr* m) { delete m; }
 
 }  // extern "C"

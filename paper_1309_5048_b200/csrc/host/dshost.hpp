@@ -71,6 +71,9 @@ Csr transpose(const Csr& a);
 bool pattern_symmetric(const Csr& a);
 std::vector<int32_t> rcm_permutation(const Csr& a);  // throws on nonsymmetric pattern
 Csr permute_symmetric(const Csr& a, const std::vector<int32_t>& perm);
+// Matrix Market dump / load (proj/src/csr.cpp:126-175), mmio.cpp
+void write_matrix_market(const Csr& a, const std::string& path, bool symmetric);
+Csr read_matrix_market(const std::string& path);
 // IC(0) of a; throws ic0_breakdown{row} or std::invalid_argument (missing diagonal)
 struct Ic0Breakdown {
   int row;

@@ -104,6 +104,13 @@ def _host():
         L.dshost_lower_nnz.restype = C.c_int64
         L.dshost_ic0.argtypes = [C.c_int, _i64p, _i32p, _dp, _i64p, _i32p, _dp,
                                  C.POINTER(C.c_int)]
+        L.dshost_write_matrix_market.argtypes = [C.c_char_p, C.c_int, C.c_int, _i64p, _i32p, _dp,
+                                                 C.c_int]
+        L.dshost_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        L.dshost_csr_view.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                      C.POINTER(C.c_void_p)]
+        L.dshost_csr_free.argtypes = [C.c_void_p]
         L._typed = True
     return L
 
@@ -176,3 +183,73 @@ def ic0(a: CsrMatrix) -> CsrMatrix:
 __all__ = ["CsrMatrix", "StokesSystem", "FactorBreakdown", "assemble", "rcm_permutation",
            "permute_symmetric", "ic0", "CASES"]
 _ = os
+
+
+# ---- Matrix Market wire format (proj/src/csr.cpp:126-175) -----------------
+DSHOST_E_INVALID, DSHOST_E_RUNTIME = 3, 8
+
+
+def _raise(L, rc: int):
+    msg = _err(L)
+    if rc == DSHOST_E_INVALID:
+        raise ValueError(msg)  # std::invalid_argument in the reference
+    raise RuntimeError(msg)    # std::runtime_error (I/O, file format)
+
+
+def write_matrix_market(a: CsrMatrix, path: str, symmetric: bool = False) -> None:
+    """The reference's dump format (write_matrix_market, csr.cpp:126-142),
+    byte for byte; symmetric writes the lower triangle only."""
+    L = _host()
+    rc = L.dshost_write_matrix_market(str(path).encode(), a.n_rows, a.n_cols,
+                                      np.ascontiguousarray(a.row_ptr, np.int64),
+                                      np.ascontiguousarray(a.cols, np.int32),
+                                      np.ascontiguousarray(a.vals, np.float64), int(symmetric))
+    if rc:
+        _raise(L, rc)
+
+
+def read_matrix_market(path: str) -> CsrMatrix:
+    """The CSR the reference's read_matrix_market (csr.cpp:144-175) builds."""
+    L = _host()
+    h = C.c_void_p()
+    rc = L.dshost_read_matrix_market(str(path).encode(), C.byref(h))
+    if rc:
+        _raise(L, rc)
+    try:
+        nr, nc = C.c_int(), C.c_int()
+        rp, ci, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        L.dshost_csr_view(h, C.byref(nr), C.byref(nc), C.byref(rp), C.byref(ci), C.byref(v))
+        row_ptr = np.ctypeslib.as_array(C.cast(rp, C.POINTER(C.c_int64)), (nr.value + 1,)).copy()
+        k = int(row_ptr[-1])
+        cols = np.ctypeslib.as_array(C.cast(ci, C.POINTER(C.c_int32)), (max(k, 1),))[:k].copy()
+        vals = np.ctypeslib.as_array(C.cast(v, C.POINTER(C.c_double)), (max(k, 1),))[:k].copy()
+    finally:
+        L.dshost_csr_free(h)
+    return CsrMatrix(nr.value, nc.value, row_ptr, cols, vals)
+
+
+def transpose(a: CsrMatrix) -> CsrMatrix:
+    """CsrMatrix::transposed: rows of the result keep the source row order."""
+    rows = np.repeat(np.arange(a.n_rows, dtype=np.int32), np.diff(a.row_ptr))
+    order = np.argsort(a.cols, kind="stable")
+    rp = np.zeros(a.n_cols + 1, np.int64)
+    np.cumsum(np.bincount(a.cols, minlength=a.n_cols), out=rp[1:])
+    return CsrMatrix(a.n_cols, a.n_rows, rp, rows[order].astype(np.int32), a.vals[order].copy())
+
+
+def system_from_matrix_market(a_path: str, b_path: str, q_path: str, f: np.ndarray,
+                              nu: float = 1.0, dim: int = 2,
+                              has_constant_pressure_kernel: bool = True) -> StokesSystem:
+    """A StokesSystem from the reference's --dump-matrices files
+    (runner.cpp:223-229: A, B, Q) and a velocity right-hand side, completed
+    like assemble_stokes (assembly.cpp:350-355): Bt = B^T, Q_nu = Q / (2 nu)."""
+    A, B, Q = read_matrix_market(a_path), read_matrix_market(b_path), read_matrix_market(q_path)
+    if A.n_rows != A.n_cols or Q.n_rows != Q.n_cols or B.n_rows != Q.n_rows or B.n_cols != A.n_rows:
+        raise ValueError("system_from_matrix_market: inconsistent block dimensions")
+    f = np.ascontiguousarray(f, np.float64)
+    if f.shape != (A.n_rows,):
+        raise ValueError("system_from_matrix_market: f must have n_u entries")
+    scale = 1.0 / (2.0 * nu)
+    Q_nu = CsrMatrix(Q.n_rows, Q.n_cols, Q.row_ptr.copy(), Q.cols.copy(), Q.vals * scale)
+    return StokesSystem(A, B, transpose(B), Q, Q_nu, f=f.copy(), nu=nu, dim=dim,
+                        has_constant_pressure_kernel=has_constant_pressure_kernel)
