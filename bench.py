@@ -249,6 +249,12 @@ def run_ours(args, world, rank, local):
                             "levels": info["levels_fwd_A"] + info["levels_bwd_A"],
                             "us_per_level": ic_ms * 1e3 / (info["levels_fwd_A"] + info["levels_bwd_A"])},
         }
+        # fused MINRES vector pass + ||res|| reduction, stand-alone at C5's n
+        # (3,735,956 rows, 359 MB per pass: HBM-resident, unlike C2's vectors)
+        n5 = 3735956
+        vec_ms, _ = solver.time_vector_update(n5, reps=20, device=local)
+        kernels["minres_vector_pass_c5_n"] = {"ms": vec_ms, "rows": n5,
+                                              "GB/s": 96.0 * n5 / (vec_ms * 1e-3) / 1e9}
     except Exception as e:
         kernels = {"error": str(e)[:100]}
 

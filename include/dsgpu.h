@@ -131,6 +131,16 @@ int dsgpu_apply_block_matrix(dsgpu_handle* h, int block, const double* x, double
  * which = 0 saddle SpMV, 1 IC(0) apply (top), 2 IC(0) apply (bottom),
  * 3 block-0 SpMV. Returns mean ms per launch in *ms. */
 int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms);
+/* Roofline probe of the fused MINRES vector pass (the persistent kernel's
+ * minres_update_row + ||res||^2 block reduction, solvers.cpp:93-101) as a
+ * stand-alone kernel on `device` over n rows of synthetic data (no handle):
+ * v[i] = (i%97)/100, av = (i%89)/50 - 1/2, w1 = (i%83) 3e-3, w2 = (i%79) 4e-3,
+ * aw1 = (i%73) 5e-3, aw2 = (i%71) 6e-3, x = (i%67) 7e-3,
+ * res = (i%61) 8e-3 - 1/5; oldeps = 1/4, delta = 1/2, gamma = 3/2, phi = 1e-3.
+ * Runs 1 + reps launches (x, res updated in place each launch), returns the
+ * mean ms of the last reps in *ms and ||res||^2 after the last launch in
+ * *res2 (sum of the per-CTA partials). 96 bytes per row per launch. */
+int dsgpu_time_vector_update(int device, int64_t n, int reps, double* ms, double* res2);
 
 /* Sizes of the device-resident problem (for roofline accounting):
  * info[0..11] = n_u, n_p, nnz_K, nnz_Aperm, nnz_L_A, nnz_L_Q, nnz_Qperm,

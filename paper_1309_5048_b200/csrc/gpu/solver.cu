@@ -1369,6 +1369,24 @@ __device__ void ic_server(const Args& a, int b, double* xs, double* red) {
   }
 }
 
+// MINRES vector recurrences of one row (solvers.cpp:93-101, one fused pass):
+// w = (v - oldeps w1 - delta w2) / gamma and the same for aw = K w; x += phi w;
+// res -= phi aw. Returns res_i^2 (the caller's ||res|| reduction). Rounds like
+// the reference's scalar C++ (explicit mul/add/div, no FMA contraction).
+__device__ __forceinline__ double minres_update_row(int i, const double* v, const double* av, const double* w1,
+                                                    const double* w2, const double* aw1, const double* aw2,
+                                                    double* wn, double* awn, double* x, double* res,
+                                                    double oldeps, double delta, double gamma, double phi) {
+  const double wv = div_rn(sub_rn(sub_rn(v[i], mul_rn(oldeps, w1[i])), mul_rn(delta, w2[i])), gamma);
+  const double awv = div_rn(sub_rn(sub_rn(av[i], mul_rn(oldeps, aw1[i])), mul_rn(delta, aw2[i])), gamma);
+  wn[i] = wv;
+  awn[i] = awv;
+  x[i] = add_rn(x[i], mul_rn(phi, wv));
+  const double rv = add_rn(res[i], mul_rn(-phi, awv));
+  res[i] = rv;
+  return rv * rv;
+}
+
 template <int TB, bool RING, bool PI>
 __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
   extern __shared__ double xs_dyn[];
@@ -1462,17 +1480,9 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
         const double* aw2 = a.aw[iw];
         double* awn = a.aw[nw];
         wi = nw;
-        for (int i = r0 + tid; i < r1; i += blockDim.x) {
-          const double wv = div_rn(sub_rn(sub_rn(a.v[i], mul_rn(oldeps, w1[i])), mul_rn(delta, w2[i])), gamma);
-          const double awv =
-              div_rn(sub_rn(sub_rn(a.av[i], mul_rn(oldeps, aw1[i])), mul_rn(delta, aw2[i])), gamma);
-          wn[i] = wv;
-          awn[i] = awv;
-          a.x[i] = add_rn(a.x[i], mul_rn(phi, wv));
-          const double rv = add_rn(a.res[i], mul_rn(-phi, awv));
-          a.res[i] = rv;
-          acc_res += rv * rv;
-        }
+        for (int i = r0 + tid; i < r1; i += blockDim.x)
+          acc_res += minres_update_row(i, a.v, a.av, w1, w2, aw1, aw2, wn, awn, a.x, a.res, oldeps, delta,
+                                       gamma, phi);
         C.put(SL_RES, block_sum(acc_res, red));
       }
       if (do_spmv) {
@@ -1662,6 +1672,23 @@ __global__ void spmv_kernel(int n_rows, const int64_t* rp, const int32_t* ci, co
   for (int64_t k = s + lane; k < e; k += 32) acc = fma(v[k], x[ci[k]], acc);
   acc = warp_sum(acc);
   if (lane == 0) y[row] = acc;
+}
+
+// Stand-alone form of the persistent kernel's fused MINRES vector pass (the
+// roofline measurement of part (3)/(4) of the hot path): minres_update_row over
+// all rows + the ||res||^2 warp-shuffle / block reduction, one partial per CTA.
+// 12 vectors streamed once: 8 reads + 4 writes = 96 bytes per row.
+__global__ void __launch_bounds__(kThreads) minres_vec_kernel(int n, const double* v, const double* av,
+                                                              const double* w1, const double* w2,
+                                                              const double* aw1, const double* aw2, double* wn,
+                                                              double* awn, double* x, double* res,
+                                                              double* partial) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    acc += minres_update_row(i, v, av, w1, w2, aw1, aw2, wn, awn, x, res, 0.25, 0.5, 1.5, 1e-3);
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
 }
 
 __global__ void gather_kernel(int n, const int32_t* perm, const double* src, double* dst) {
@@ -2381,6 +2408,72 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
   cudaEventDestroy(e1);
   *ms = t / reps;
   return rc;
+}
+
+namespace {
+__global__ void vec_init_kernel(int n, double* v, double* av, double* w1, double* w2, double* aw1, double* aw2,
+                                double* x, double* res) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    v[i] = (i % 97) / 100.0;
+    av[i] = (i % 89) / 50.0 - 0.5;
+    w1[i] = (i % 83) * 3e-3;
+    w2[i] = (i % 79) * 4e-3;
+    aw1[i] = (i % 73) * 5e-3;
+    aw2[i] = (i % 71) * 6e-3;
+    x[i] = (i % 67) * 7e-3;
+    res[i] = (i % 61) * 8e-3 - 0.2;
+  }
+}
+}  // namespace
+
+int dsgpu_time_vector_update(int device, int64_t n64, int reps, double* ms, double* res2) {
+  if (n64 < 1 || n64 > (1ll << 30) || reps < 1 || !ms || !res2) {
+    g_err = "dsgpu_time_vector_update: bad arguments";
+    return DSGPU_E_BAD_INPUT;
+  }
+  const int n = static_cast<int>(n64);
+  if (cudaSetDevice(device) != cudaSuccess) {
+    g_err = "dsgpu_time_vector_update: cudaSetDevice failed";
+    return DSGPU_E_CUDA;
+  }
+  int sms = 0, per_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minres_vec_kernel, kThreads, 0);
+  const int grid = std::max(1, sms * std::max(1, per_sm));
+  double* buf = nullptr;
+  const size_t nn = static_cast<size_t>(n);
+  if (cudaMalloc(&buf, sizeof(double) * (10 * nn + grid)) != cudaSuccess) {
+    g_err = "dsgpu_time_vector_update: cudaMalloc failed";
+    return DSGPU_E_CUDA;
+  }
+  double *v = buf, *av = v + nn, *w1 = av + nn, *w2 = w1 + nn, *aw1 = w2 + nn, *aw2 = aw1 + nn, *wn = aw2 + nn,
+         *awn = wn + nn, *x = awn + nn, *res = x + nn, *partial = res + nn;
+  vec_init_kernel<<<grid, 256>>>(n, v, av, w1, w2, aw1, aw2, x, res);
+  minres_vec_kernel<<<grid, kThreads>>>(n, v, av, w1, w2, aw1, aw2, wn, awn, x, res, partial);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r)
+    minres_vec_kernel<<<grid, kThreads>>>(n, v, av, w1, w2, aw1, aw2, wn, awn, x, res, partial);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float t = 0.0f;
+  cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  std::vector<double> hp(grid);
+  if (e == cudaSuccess) e = cudaMemcpy(hp.data(), partial, sizeof(double) * grid, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  if (e != cudaSuccess) {
+    g_err = std::string("dsgpu_time_vector_update: ") + cudaGetErrorString(e);
+    return DSGPU_E_CUDA;
+  }
+  double sum = 0.0;
+  for (const double p : hp) sum += p;
+  *ms = t / reps;
+  *res2 = sum;
+  return DSGPU_OK;
 }
 
 int dsgpu_debug_counters(int reset, int64_t* out32) {

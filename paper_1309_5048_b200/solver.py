@@ -85,6 +85,8 @@ def _lib():
         L.dsgpu_apply_ic0.argtypes = [vp, ip, _dp, _dp]
         L.dsgpu_apply_block_matrix.argtypes = [vp, ip, _dp, _dp]
         L.dsgpu_time_kernel.argtypes = [vp, ip, ip, C.POINTER(C.c_double)]
+        L.dsgpu_time_vector_update.argtypes = [ip, C.c_int64, ip, C.POINTER(C.c_double),
+                                               C.POINTER(C.c_double)]
         L.dsgpu_info.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")]
         L._typed = True
     return L
@@ -301,3 +303,15 @@ def solve_stokes(system: host.StokesSystem, strategy: str,
 
 __all__ = ["SolverOptions", "SolveReport", "StokesSolution", "GpuStokesSolver", "solve_stokes",
            "strategy_names", "STRATEGIES", "PreconditionerError", "prepare_block", "BlockSetup"]
+
+
+def time_vector_update(n: int, reps: int = 20, device: int = 0):
+    """Stand-alone roofline probe of the fused MINRES vector pass
+    (dsgpu_time_vector_update): (mean ms per launch, ||res||^2 after 1 + reps
+    launches). 96 bytes per row per launch."""
+    L = _lib()
+    ms, res2 = C.c_double(0.0), C.c_double(0.0)
+    rc = L.dsgpu_time_vector_update(device, n, reps, C.byref(ms), C.byref(res2))
+    if rc != 0:
+        raise RuntimeError(f"dsgpu_time_vector_update failed ({rc}): {L.dsgpu_last_error(None).decode()}")
+    return ms.value, res2.value

@@ -53,12 +53,12 @@ def test_saddle_apply_matches_reference(gpu, port):
     assert np.abs(y - ref).max() <= 1e-14 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("pi_b", [None, "0.5", "1.7"])
+@pytest.mark.parametrize("pi_b", [None, "0.5", "1.7", "3.0"])
 def test_ic0_apply_partitioned_inverse_matches_reference(gpu, port, monkeypatch, pi_b):
     """Default mode for 2D systems: partitioned-inverse IC(0) apply (block
     inverses of the same factor; agreement to round-off). pi_b scales the
     block size (0.5: windows spanning two earlier blocks; 1.7: ragged last
-    block)."""
+    block; 3.0: windows shorter than the block)."""
     host, solver = gpu
     if pi_b:
         monkeypatch.setenv("DSGPU_PI_B", pi_b)
@@ -354,3 +354,44 @@ def test_c5_full_size_properties(gpu):
     hm = r.residual_history
     assert np.all(hm[1:] <= hm[:-1] * (1 + 1e-10))
     g.close()
+
+
+def vector_update_reference(n, launches):
+    """numpy restatement of minres_update_row (solvers.cpp:93-101) on the
+    probe's synthetic data (include/dsgpu.h, dsgpu_time_vector_update)."""
+    i = np.arange(n)
+    v, av = (i % 97) / 100.0, (i % 89) / 50.0 - 0.5
+    w1, w2, aw1, aw2 = (i % 83) * 3e-3, (i % 79) * 4e-3, (i % 73) * 5e-3, (i % 71) * 6e-3
+    res = (i % 61) * 8e-3 - 0.2
+    oldeps, delta, gamma, phi = 0.25, 0.5, 1.5, 1e-3
+    aw = ((av - oldeps * aw1) - delta * aw2) / gamma
+    for _ in range(launches):
+        res = res + (-phi) * aw
+    return float(np.dot(res, res))
+
+
+@pytest.mark.parametrize("n", [1, 1000, 300007])
+def test_fused_vector_update_kernel(gpu, n):
+    """The stand-alone fused MINRES vector pass (same device function as the
+    persistent kernel) and its ||res||^2 reduction against numpy."""
+    _, solver = gpu
+    ms, res2 = solver.time_vector_update(n, reps=3)
+    ref = vector_update_reference(n, 4)
+    assert ms > 0.0
+    assert abs(res2 - ref) <= 1e-12 * abs(ref)
+
+
+def test_solve_from_reference_matrix_market_dump(gpu, port):
+    """Drop-in path for a system the reference dumped (--dump-matrices,
+    runner.cpp:223-229): A/B/Q read from its Matrix Market files, solved on the
+    GPU, against the oracle on the same blocks."""
+    import os
+    from conftest import GOLDEN
+    host, solver = gpu
+    mm = os.path.join(GOLDEN, "mm")
+    s = host.system_from_matrix_market(os.path.join(mm, "A_psi_k2_h3.mtx"), os.path.join(mm, "B_psi_k2_h3.mtx"),
+                                       os.path.join(mm, "Q_psi_k2_h3.mtx"),
+                                       np.load(os.path.join(mm, "f_psi_k2_h3.npy")))
+    for strategy in ("IC0-PCG(A,Q)", "IC0-PCG(A)+Diag(Q)"):
+        sol = solver.solve_stokes(s, strategy, solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+        check_parity(sol, reference_solve(port, s, strategy, 1e-8, 1e-1), 1e-8)
