@@ -23,7 +23,7 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from config_probe import CFG  # noqa: E402
 
 KNOBS = ("DSGPU_PI", "DSGPU_PI_B", "DSGPU_REMOTE", "DSGPU_MERGE", "DSGPU_HSLEEP", "DSGPU_FLOWD",
-         "DSGPU_GRID", "DSGPU_NOWAIT", "DSGPU_RING_N")
+         "DSGPU_GRID", "DSGPU_NOWAIT", "DSGPU_RING_N", "DSGPU_PI_G", "DSGPU_PI_DIRECT")
 
 
 def main():
