@@ -26,6 +26,7 @@ CFG = {
     "c4": dict(case="psi-mms", k=2, n=32, dim=3, seed=0, outer=1e-8, inner=1e-1,
                golden="c4_psi3d_k2_n32.npz", max_iter=400),
     "c2": dict(case="psi-mms", k=2, n=64, dim=2, seed=0, outer=1e-8, inner=1e-1, golden=None),
+    "c2x": dict(case="psi-mms", k=2, n=64, dim=2, seed=0, outer=1e-8, inner=1e-8, golden=None),
     "k3n128": dict(case="random", k=3, n=128, dim=2, seed=1234, outer=1e-8, inner=1e-1,
                    golden=None),
     "3d16": dict(case="psi-mms", k=2, n=16, dim=3, seed=0, outer=1e-8, inner=1e-1, golden=None),
