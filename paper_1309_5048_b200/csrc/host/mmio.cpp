@@ -74,6 +74,10 @@ struct Scan {
     char* q = nullptr;
     out = std::strtod(p, &q);
     if (q == p) return false;
+    // the reference's stream extraction takes decimal numbers only (no hex
+    // floats, inf or nan): stop where it would
+    for (const char* c = p; c < q; ++c)
+      if (!((*c >= '0' && *c <= '9') || *c == '+' || *c == '-' || *c == '.' || *c == 'e' || *c == 'E')) return false;
     p = q;
     return true;
   }

@@ -103,6 +103,7 @@ BAD = {
                  "unsupported qualifier hermitian"),
     "size.mtx": ("%%MatrixMarket matrix coordinate real general\n2 x 1\n", "bad size line"),
     "trunc.mtx": ("%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1\n2 2\n", "truncated entry list"),
+    "nan.mtx": ("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 nan\n", "truncated entry list"),
 }
 
 
