@@ -38,6 +38,7 @@ enum {
   DSGPU_E_BAD_INPUT = 3,          /* std::invalid_argument */
   DSGPU_E_CUDA = 4,               /* CUDA failure: dsgpu_last_error() */
   DSGPU_E_NONPOS_DIAG = 5,        /* Jacobi block: nonpositive diagonal (std::domain_error) */
+  DSGPU_E_FACTOR_BREAKDOWN = 6,   /* IC(0): nonpositive pivot (FactorBreakdown, cholesky.hpp:13-19) */
   DSGPU_E_UNSUPPORTED = 7         /* size beyond this build's limits */
 };
 
@@ -141,6 +142,21 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms);
  * mean ms of the last reps in *ms and ||res||^2 after the last launch in
  * *res2 (sum of the per-CTA partials). 96 bytes per row per launch. */
 int dsgpu_time_vector_update(int device, int64_t n, int reps, double* ms, double* res2);
+
+/* ---- host-setup on the device --------------- */
+/* IC(0) factor of a symmetric CSR matrix on `device`, bit-identical to the
+ * reference's ic0 (proj/src/cholesky.cpp:84-134): level-scheduled rows (one
+ * launch per level of L's dependency DAG, one warp per row), each row's
+ * entries in the reference's order with explicitly rounded arithmetic.
+ * Outputs (host, caller-allocated): l_row_ptr[n+1], l_cols / l_vals sized
+ * nnz(lower(A)) incl. the diagonal. Errors: DSGPU_E_BAD_INPUT (structurally
+ * missing diagonal, std::invalid_argument), DSGPU_E_FACTOR_BREAKDOWN with the
+ * first failing row in *bad_row. *n_levels = DAG depth, *device_ms = time of
+ * the level launches (CUDA events). Message: dsgpu_ic0_last_error(). */
+int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                     int64_t* l_row_ptr, int32_t* l_cols, double* l_vals, int* bad_row, int* n_levels,
+                     double* device_ms);
+const char* dsgpu_ic0_last_error(void);
 
 /* Sizes of the device-resident problem (for roofline accounting):
  * info[0..11] = n_u, n_p, nnz_K, nnz_Aperm, nnz_L_A, nnz_L_Q, nnz_Qperm,

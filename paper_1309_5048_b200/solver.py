@@ -24,11 +24,14 @@ from . import host
 from ._lib import load_gpu
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_i64 = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_i32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 
 BLOCK_JACOBI, BLOCK_PCG_JACOBI, BLOCK_PCG_IC0 = 0, 1, 2
 STOP_PRECONDITIONED, STOP_EUCLIDEAN = 0, 1
 DSGPU_OK, E_INDEFINITE, E_NEG_CURVATURE, E_BAD_INPUT, E_CUDA, E_NONPOS_DIAG, E_UNSUPPORTED = (
     0, 1, 2, 3, 4, 5, 7)
+E_FACTOR_BREAKDOWN = 6
 
 # strategy -> (top block, bottom block); precond.cpp:161-193 plus the
 # "IC0-PCG(A)+Diag(Q)" composition BASELINE config 1 asks for
@@ -87,6 +90,9 @@ def _lib():
         L.dsgpu_time_kernel.argtypes = [vp, ip, ip, C.POINTER(C.c_double)]
         L.dsgpu_time_vector_update.argtypes = [ip, C.c_int64, ip, C.POINTER(C.c_double),
                                                C.POINTER(C.c_double)]
+        L.dsgpu_ic0_factor.argtypes = [ip, ip, _i64, _i32, _dp, _i64, _i32, _dp, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        L.dsgpu_ic0_last_error.restype = C.c_char_p
         L.dsgpu_info.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")]
         L._typed = True
     return L
@@ -154,13 +160,42 @@ class BlockSetup:
     factor: host.CsrMatrix | None = None
 
 
-def prepare_block(m: host.CsrMatrix, kind: int) -> BlockSetup:
-    """PcgBlock ctor, precond.cpp:59-73: for IC(0) blocks rcm -> permute -> ic0."""
+def prepare_block(m: host.CsrMatrix, kind: int, ic0_on_gpu: bool = False) -> BlockSetup:
+    """PcgBlock ctor, precond.cpp:59-73: for IC(0) blocks rcm -> permute -> ic0
+    (ic0_on_gpu: the factor from ic0_factor_gpu, bit-identical)."""
     if kind != BLOCK_PCG_IC0:
         return BlockSetup(kind)
     perm = host.rcm_permutation(m)
-    factor = host.ic0(host.permute_symmetric(m, perm))
+    pm = host.permute_symmetric(m, perm)
+    factor = ic0_factor_gpu(pm)[0] if ic0_on_gpu else host.ic0(pm)
     return BlockSetup(kind, perm, factor)
+
+
+def ic0_factor_gpu(a: host.CsrMatrix, device: int = 0):
+    """IC(0) factor of a symmetric CSR matrix on the device, bit-identical to
+    the reference's ic0 (cholesky.cpp:84-134; dsgpu_ic0_factor). Returns
+    (L, {"levels": DAG depth, "device_ms": level-launch time}). Raises
+    host.FactorBreakdown (first failing row) or ValueError like host.ic0."""
+    L = _lib()
+    n = a.n_rows
+    rows = np.repeat(np.arange(n), np.diff(a.row_ptr))
+    lnnz = int(np.count_nonzero(a.cols <= rows))
+    rp = np.zeros(n + 1, np.int64)
+    ci = np.zeros(max(lnnz, 1), np.int32)
+    v = np.zeros(max(lnnz, 1))
+    bad, lev, ms = C.c_int(-1), C.c_int(0), C.c_double(0.0)
+    rc = L.dsgpu_ic0_factor(device, n, np.ascontiguousarray(a.row_ptr, np.int64),
+                            np.ascontiguousarray(a.cols, np.int32), np.ascontiguousarray(a.vals, np.float64),
+                            rp, ci, v, C.byref(bad), C.byref(lev), C.byref(ms))
+    msg = L.dsgpu_ic0_last_error().decode()
+    if rc == E_FACTOR_BREAKDOWN:
+        raise host.FactorBreakdown(msg, bad.value)
+    if rc in (E_BAD_INPUT, E_UNSUPPORTED):
+        raise ValueError(msg)
+    if rc:
+        raise RuntimeError(f"dsgpu_ic0_factor failed ({rc}): {msg}")
+    return (host.CsrMatrix(n, n, rp, ci[:lnnz].copy(), v[:lnnz].copy()),
+            {"levels": lev.value, "device_ms": ms.value})
 
 
 class GpuStokesSolver:

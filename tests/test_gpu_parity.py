@@ -395,3 +395,69 @@ def test_solve_from_reference_matrix_market_dump(gpu, port):
     for strategy in ("IC0-PCG(A,Q)", "IC0-PCG(A)+Diag(Q)"):
         sol = solver.solve_stokes(s, strategy, solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
         check_parity(sol, reference_solve(port, s, strategy, 1e-8, 1e-1), 1e-8)
+
+
+# ---- IC(0) factorization on the device -----------
+
+def _same_csr(a, rp, ci, v):
+    return (np.array_equal(a.row_ptr, rp) and np.array_equal(a.cols, ci)
+            and np.array_equal(a.vals.view(np.int64), np.asarray(v).view(np.int64)))
+
+
+def test_ic0_factor_gpu_bit_identical_to_reference_fixture(gpu):
+    """The device factor of RCM(A) / RCM(Q_nu) equals the reference's own
+    ic0 output stored in the golden fixture, bit for bit."""
+    host, solver = gpu
+    d = load_golden("c1_psi_k2_n8.npz")
+    s = host.assemble("psi-mms", 2, 8)
+    for m, tag in ((s.A, "A"), (s.Q_nu, "Q")):
+        perm = host.rcm_permutation(m)
+        L, info = solver.ic0_factor_gpu(host.permute_symmetric(m, perm))
+        ref = golden_csr(d, "L_" + tag)
+        assert _same_csr(L, ref.rp, ref.ci, ref.v), tag
+        assert info["levels"] > 1
+
+
+@pytest.mark.parametrize("case,k,n,dim", [("psi-mms", 2, 64, 2), ("random", 3, 16, 2), ("cavity", 2, 16, 2),
+                                          ("psi-mms", 2, 6, 3)])
+def test_ic0_factor_gpu_bit_identical_to_host(gpu, case, k, n, dim):
+    """Against the native host ic0 (itself bit-identical to the reference,
+    tests/test_host.py) on BASELINE-shaped systems, 2D and 3D."""
+    host, solver = gpu
+    s = host.assemble(case, k, n, dim=dim, seed=1234)
+    for m in (s.A, s.Q_nu):
+        pm = host.permute_symmetric(m, host.rcm_permutation(m))
+        L, _ = solver.ic0_factor_gpu(pm)
+        H = host.ic0(pm)
+        assert _same_csr(L, H.row_ptr, H.cols, H.vals)
+
+
+def test_ic0_factor_gpu_errors(gpu):
+    """FactorBreakdown at the reference's first failing row; a structurally
+    missing diagonal is std::invalid_argument (cholesky.cpp:109-111,128)."""
+    host, solver = gpu
+    d = np.array([[4.0, 1.0, 0.0, 0.0], [1.0, 4.0, 3.0, 0.0], [0.0, 3.0, 1.0, 1.0], [0.0, 0.0, 1.0, 4.0]])
+    rows, cols = np.nonzero(d)
+    rp = np.zeros(5, np.int64)
+    np.cumsum(np.bincount(rows, minlength=4), out=rp[1:])
+    m = host.CsrMatrix(4, 4, rp, cols.astype(np.int32), d[rows, cols])
+    with pytest.raises(host.FactorBreakdown) as e_host:
+        host.ic0(m)
+    with pytest.raises(host.FactorBreakdown) as e_gpu:
+        solver.ic0_factor_gpu(m)
+    assert e_gpu.value.row == e_host.value.row == 2
+    nodiag = host.CsrMatrix(2, 2, np.array([0, 1, 2], np.int64), np.array([0, 0], np.int32), np.array([1.0, 0.5]))
+    with pytest.raises(ValueError, match="missing diagonal"):
+        solver.ic0_factor_gpu(nodiag)
+
+
+def test_solve_with_device_factor_matches_reference(gpu, port):
+    """The whole preconditioner setup with the device factor feeds the same
+    solve (prepare_block(ic0_on_gpu=True))."""
+    host, solver = gpu
+    s = host.assemble("psi-mms", 2, 16)
+    top = solver.prepare_block(s.A, solver.BLOCK_PCG_IC0, ic0_on_gpu=True)
+    bot = solver.prepare_block(s.Q_nu, solver.BLOCK_PCG_IC0, ic0_on_gpu=True)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)", top=top, bottom=bot)
+    sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+    check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
