@@ -11,9 +11,13 @@
 // entries before it) and every subtraction is applied in the reference's
 // order with explicitly rounded mul / sub / div / sqrt (no FMA), so the result
 // is the reference's factor bit for bit. The 32 lanes parallelize the merge:
-// each lane takes one entry of row j and binary-searches its column among the
-// finished entries of row i (staged in shared memory); the matched products
-// are then subtracted in column order through warp shuffles.
+// each lane takes one entry of row j and finds its column's position in row i
+// through a per-warp column -> position map in global memory (n ints per row
+// of the widest level, set at the row's start, cleared at its end); the
+// matched products are compacted into shared memory and subtracted in column
+// order by one sequential chain.
+// Row j's entries and their map lookups do not depend on row i's results, so
+// the next entry's are loaded while the current one is reduced.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,9 +34,59 @@ thread_local std::string g_ic0_err;
 
 constexpr int kWarpsPerBlock = 4;
 
+// Row j's entries (without its diagonal) of one pass: U chunks of 32, the
+// column's position in row i (pos map), the value. Prefetched one entry ahead.
+struct RowChunk {
+  static constexpr int U = 8;
+  int col[U], pos[U];
+  double val[U];
+};
+
+__device__ __forceinline__ void load_chunk(RowChunk& r, const int32_t* __restrict__ ci, const double* v,
+                                           const int* __restrict__ pos, int64_t b, int64_t e, int pmax, int lane) {
+#pragma unroll
+  for (int u = 0; u < RowChunk::U; ++u) {
+    const int64_t q = b + u * 32 + lane;
+    r.col[u] = q < e ? __ldg(ci + q) : -1;
+    r.val[u] = q < e ? v[q] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < RowChunk::U; ++u)
+    r.pos[u] = (r.col[u] >= 0 && r.col[u] <= pmax) ? pos[r.col[u]] : -1;
+}
+
+// s -= the matched products of one pass, in column (= chunk, then lane)
+// order: the hits are compacted into the warp's shared buffer (ballot + popc
+// rank), then every lane runs the same sequential subtraction chain from it
+// (loads independent of s, one dependent fp64 subtract per product).
+// Returns true when the pass reached past row i's prefix (nothing more can match).
+__device__ __forceinline__ bool apply_chunk(const RowChunk& r, const double* sval, int t, int pmax, double& s,
+                                            double* buf, int lane) {
+  int cnt = 0;
+  bool done = false;
+  const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+  for (int u = 0; u < RowChunk::U; ++u) {
+    const bool hit = r.pos[u] >= 0 && r.pos[u] < t;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (hit) buf[cnt + __popc(m & below)] = __dmul_rn(sval[r.pos[u]], r.val[u]);
+    cnt += __popc(m);
+    const int last = __shfl_sync(0xffffffffu, r.col[u], 31);
+    if (last < 0 || last >= pmax) {
+      done = true;
+      break;
+    }
+  }
+  __syncwarp();
+  for (int k = 0; k < cnt; ++k) s = __dsub_rn(s, buf[k]);
+  __syncwarp();  // buf is reused by the next pass
+  return done;
+}
+
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     ic0_level_kernel(const int32_t* __restrict__ rows, int nrows, const int64_t* __restrict__ rp,
-                     const int32_t* __restrict__ ci, double* v, int maxlen, int* bad) {
+                     const int32_t* __restrict__ ci, double* v, int maxlen, int* pos_maps, int64_t map_len,
+                     int* bad) {
   extern __shared__ unsigned char smem[];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int w = blockIdx.x * kWarpsPerBlock + wl;
@@ -40,58 +94,53 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   int32_t* scol = reinterpret_cast<int32_t*>(smem) + static_cast<size_t>(wl) * maxlen;
   double* sval = reinterpret_cast<double*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 4 +
                                            static_cast<size_t>(wl) * maxlen * 8);
+  double* buf = reinterpret_cast<double*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 12) +
+                static_cast<size_t>(wl) * RowChunk::U * 32;
+  int* pos = pos_maps + static_cast<int64_t>(w) * map_len;  // this warp's column -> position map (all -1)
   const int i = rows[w];
   const int64_t ib = rp[i], ie = rp[i + 1];
   const int len = static_cast<int>(ie - ib);
   for (int k = lane; k < len; k += 32) {
-    scol[k] = ci[ib + k];
+    const int c = ci[ib + k];
+    scol[k] = c;
     sval[k] = v[ib + k];
+    if (k < len - 1) pos[c] = k;
   }
   __syncwarp();
+  const int pfull = len >= 2 ? scol[len - 2] : -1;  // largest off-diagonal column of row i
+  RowChunk cur, nxt;
+  if (len >= 2) {
+    const int j0 = scol[0];
+    load_chunk(cur, ci, v, pos, rp[j0], rp[j0 + 1] - 1, pfull, lane);
+  }
   for (int t = 0; t < len - 1; ++t) {  // entry ku = ib + t, column j < i
     const int j = scol[t];
-    double s = sval[t];
     const int64_t jb = rp[j], je = rp[j + 1] - 1;  // row j without its diagonal
-    const int pmax = t > 0 ? scol[t - 1] : -1;     // largest column of row i's finished prefix
-    for (int64_t c0 = jb; t > 0 && c0 < je; c0 += 32) {
-      const int64_t q = c0 + lane;
-      int col = -1;
-      double vj = 0.0;
-      if (q < je) {
-        col = ci[q];
-        vj = v[q];
-      }
-      // col among row i's finished entries [0, t) (sorted ascending)
-      int lo = 0, hi = t;
-      if (col >= 0)
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (scol[mid] < col)
-            lo = mid + 1;
-          else
-            hi = mid;
-        }
-      const bool hit = col >= 0 && lo < t && scol[lo] == col;
-      const double prod = hit ? __dmul_rn(sval[lo], vj) : 0.0;
-      unsigned m = __ballot_sync(0xffffffffu, hit);
-      while (m) {  // the merge's order: ascending column = lane order
-        const int l = __ffs(m) - 1;
-        m &= m - 1;
-        s = __dsub_rn(s, __shfl_sync(0xffffffffu, prod, l));
-      }
-      // row j's columns ascend: once past row i's prefix nothing can match
-      const int last = __shfl_sync(0xffffffffu, col, 31);
-      if (last < 0 || last >= pmax) break;
+    if (t + 1 < len - 1) {  // prefetch the next entry's row (static data)
+      const int j1 = scol[t + 1];
+      load_chunk(nxt, ci, v, pos, rp[j1], rp[j1 + 1] - 1, pfull, lane);
     }
-    const double lij = __ddiv_rn(s, v[rp[j + 1] - 1]);  // L_jj is final (earlier level)
+    double s = sval[t];
+    const int pmax = t > 0 ? scol[t - 1] : -1;  // largest column of row i's finished prefix
+    if (t > 0 && !apply_chunk(cur, sval, t, pmax, s, buf, lane)) {
+      // rows longer than one pass: the rest, synchronously
+      for (int64_t b = jb + RowChunk::U * 32; b < je; b += RowChunk::U * 32) {
+        RowChunk more;
+        load_chunk(more, ci, v, pos, b, je, pfull, lane);
+        if (apply_chunk(more, sval, t, pmax, s, buf, lane)) break;
+      }
+    }
+    const double lij = __ddiv_rn(s, v[je]);  // L_jj is final (earlier level)
     if (lane == 0) {
       sval[t] = lij;
       v[ib + t] = lij;
     }
     __syncwarp();
+    cur = nxt;
   }
   double d = sval[len - 1];
   for (int k = 0; k < len - 1; ++k) d = __dsub_rn(d, __dmul_rn(sval[k], sval[k]));
+  for (int k = lane; k < len - 1; k += 32) pos[scol[k]] = -1;  // leave the map clean
   if (lane == 0) {
     if (!(d > 0.0)) atomicMin(bad, i);
     v[ie - 1] = __dsqrt_rn(d);
@@ -150,12 +199,17 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   std::vector<int64_t> lstart(nlev + 1, 0);
   for (int i = 0; i < n; ++i) ++lstart[level[i] + 1];
   for (int l = 0; l < nlev; ++l) lstart[l + 1] += lstart[l];
+  int maxw = 1;  // widest level: one column-position map (n ints) per row of it
+  for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, static_cast<int>(lstart[l + 1] - lstart[l]));
   std::vector<int32_t> order(n);
   {
     std::vector<int64_t> fill(lstart.begin(), lstart.end() - 1);
     for (int i = 0; i < n; ++i) order[fill[level[i]]++] = i;
   }
-  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * maxlen * 12;
+  // 4-byte columns and 8-byte values of maxlen entries per warp: keep the
+  // product buffers behind them 8-byte aligned
+  maxlen = (maxlen + 1) / 2 * 2;
+  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * (maxlen * 12 + RowChunk::U * 32 * 8);
   if (cudaSetDevice(device) != cudaSuccess) return fail(DSGPU_E_CUDA, "ic0: cudaSetDevice failed");
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
@@ -168,6 +222,7 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   int32_t *d_ci = nullptr, *d_rows = nullptr;
   double* d_v = nullptr;
   int* d_bad = nullptr;
+  int* d_pos = nullptr;
   cudaStream_t st = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   auto cleanup = [&]() {
@@ -176,6 +231,7 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
     cudaFree(d_rows);
     cudaFree(d_v);
     cudaFree(d_bad);
+    cudaFree(d_pos);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (st) cudaStreamDestroy(st);
@@ -184,7 +240,9 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   if (cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)) != cudaSuccess ||
       cudaMalloc(&d_ci, sizeof(int32_t) * nnz) != cudaSuccess ||
       cudaMalloc(&d_rows, sizeof(int32_t) * n) != cudaSuccess || cudaMalloc(&d_v, sizeof(double) * nnz) != cudaSuccess ||
-      cudaMalloc(&d_bad, sizeof(int)) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaMalloc(&d_bad, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&d_pos, sizeof(int) * static_cast<size_t>(maxw) * n) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
     cleanup();
     return fail(DSGPU_E_CUDA, "ic0: device allocation failed");
   }
@@ -193,6 +251,7 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   cudaMemcpyAsync(d_v, l_vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(d_rows, order.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(d_bad, &big, sizeof(int), cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(d_pos, 0xFF, sizeof(int) * static_cast<size_t>(maxw) * n, st);  // all -1
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, st);
@@ -200,7 +259,7 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
     const int cnt = static_cast<int>(lstart[l + 1] - lstart[l]);
     const int grid = (cnt + kWarpsPerBlock - 1) / kWarpsPerBlock;
     ic0_level_kernel<<<grid, kWarpsPerBlock * 32, smem, st>>>(d_rows + lstart[l], cnt, d_rp, d_ci, d_v, maxlen,
-                                                              d_bad);
+                                                              d_pos, static_cast<int64_t>(n), d_bad);
   }
   cudaEventRecord(e1, st);
   int bad = big;
