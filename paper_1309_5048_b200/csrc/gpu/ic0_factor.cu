@@ -17,7 +17,7 @@
 // matched products are compacted into shared memory and subtracted in column
 // order by one sequential chain.
 // Row j's entries and their map lookups do not depend on row i's results, so
-// the next entry's are loaded while the current one is reduced.
+// the next two entries' are loaded while the current one is reduced.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -55,6 +55,21 @@ __device__ __forceinline__ void load_chunk(RowChunk& r, const int32_t* __restric
     r.pos[u] = (r.col[u] >= 0 && r.col[u] <= pmax) ? pos[r.col[u]] : -1;
 }
 
+// s - p[0] - p[1] - ... in order; the loads are batched ahead of the
+// dependent subtractions.
+__device__ __forceinline__ double sub_chain(double s, const double* p, int cnt) {
+  int k = 0;
+  for (; k + 8 <= cnt; k += 8) {
+    double b[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) b[q] = p[k + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = __dsub_rn(s, b[q]);
+  }
+  for (; k < cnt; ++k) s = __dsub_rn(s, p[k]);
+  return s;
+}
+
 // s -= the matched products of one pass, in column (= chunk, then lane)
 // order: the hits are compacted into the warp's shared buffer (ballot + popc
 // rank), then every lane runs the same sequential subtraction chain from it
@@ -78,7 +93,7 @@ __device__ __forceinline__ bool apply_chunk(const RowChunk& r, const double* sva
     }
   }
   __syncwarp();
-  for (int k = 0; k < cnt; ++k) s = __dsub_rn(s, buf[k]);
+  s = sub_chain(s, buf, cnt);
   __syncwarp();  // buf is reused by the next pass
   return done;
 }
@@ -94,7 +109,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   int32_t* scol = reinterpret_cast<int32_t*>(smem) + static_cast<size_t>(wl) * maxlen;
   double* sval = reinterpret_cast<double*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 4 +
                                            static_cast<size_t>(wl) * maxlen * 8);
-  double* buf = reinterpret_cast<double*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 12) +
+  // per entry of row i: row j's range and its final diagonal L_jj
+  int64_t* sjb = reinterpret_cast<int64_t*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 12) +
+                 static_cast<size_t>(wl) * maxlen * 3;
+  int64_t* sje = sjb + maxlen;
+  double* sdg = reinterpret_cast<double*>(sje + maxlen);
+  double* buf = reinterpret_cast<double*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 36) +
                 static_cast<size_t>(wl) * RowChunk::U * 32;
   int* pos = pos_maps + static_cast<int64_t>(w) * map_len;  // this warp's column -> position map (all -1)
   const int i = rows[w];
@@ -104,22 +124,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const int c = ci[ib + k];
     scol[k] = c;
     sval[k] = v[ib + k];
-    if (k < len - 1) pos[c] = k;
+    if (k < len - 1) {
+      pos[c] = k;
+      const int64_t b = rp[c], e = rp[c + 1] - 1;
+      sjb[k] = b;
+      sje[k] = e;
+      sdg[k] = v[e];  // row c is at an earlier level: final
+    }
   }
   __syncwarp();
   const int pfull = len >= 2 ? scol[len - 2] : -1;  // largest off-diagonal column of row i
-  RowChunk cur, nxt;
-  if (len >= 2) {
-    const int j0 = scol[0];
-    load_chunk(cur, ci, v, pos, rp[j0], rp[j0 + 1] - 1, pfull, lane);
-  }
+  RowChunk cur, nxt, nx2;  // entries t, t+1, t+2 (two-deep prefetch of static data)
+  if (len >= 2) load_chunk(cur, ci, v, pos, sjb[0], sje[0], pfull, lane);
+  if (len >= 3) load_chunk(nxt, ci, v, pos, sjb[1], sje[1], pfull, lane);
   for (int t = 0; t < len - 1; ++t) {  // entry ku = ib + t, column j < i
-    const int j = scol[t];
-    const int64_t jb = rp[j], je = rp[j + 1] - 1;  // row j without its diagonal
-    if (t + 1 < len - 1) {  // prefetch the next entry's row (static data)
-      const int j1 = scol[t + 1];
-      load_chunk(nxt, ci, v, pos, rp[j1], rp[j1 + 1] - 1, pfull, lane);
-    }
+    const int64_t jb = sjb[t], je = sje[t];  // row j = scol[t] without its diagonal
+    if (t + 2 < len - 1) load_chunk(nx2, ci, v, pos, sjb[t + 2], sje[t + 2], pfull, lane);
     double s = sval[t];
     const int pmax = t > 0 ? scol[t - 1] : -1;  // largest column of row i's finished prefix
     if (t > 0 && !apply_chunk(cur, sval, t, pmax, s, buf, lane)) {
@@ -130,16 +150,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         if (apply_chunk(more, sval, t, pmax, s, buf, lane)) break;
       }
     }
-    const double lij = __ddiv_rn(s, v[je]);  // L_jj is final (earlier level)
+    const double lij = __ddiv_rn(s, sdg[t]);  // L_jj is final (earlier level)
     if (lane == 0) {
       sval[t] = lij;
       v[ib + t] = lij;
     }
     __syncwarp();
     cur = nxt;
+    nxt = nx2;
   }
-  double d = sval[len - 1];
-  for (int k = 0; k < len - 1; ++k) d = __dsub_rn(d, __dmul_rn(sval[k], sval[k]));
+  for (int k = lane; k < len - 1; k += 32) sjb[k] = __double_as_longlong(__dmul_rn(sval[k], sval[k]));
+  __syncwarp();
+  const double d = sub_chain(sval[len - 1], reinterpret_cast<const double*>(sjb), len - 1);
   for (int k = lane; k < len - 1; k += 32) pos[scol[k]] = -1;  // leave the map clean
   if (lane == 0) {
     if (!(d > 0.0)) atomicMin(bad, i);
@@ -209,7 +231,7 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   // 4-byte columns and 8-byte values of maxlen entries per warp: keep the
   // product buffers behind them 8-byte aligned
   maxlen = (maxlen + 1) / 2 * 2;
-  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * (maxlen * 12 + RowChunk::U * 32 * 8);
+  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * (maxlen * 36 + RowChunk::U * 32 * 8);
   if (cudaSetDevice(device) != cudaSuccess) return fail(DSGPU_E_CUDA, "ic0: cudaSetDevice failed");
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
