@@ -1,6 +1,6 @@
 """Solve BASELINE configs C3 / C4 on the GPU and record timings + parity.
 
-  python tools/config_probe.py c3 [c4 ...]  [--modes=auto,1,0]
+  python tools/config_probe.py c3 [c4 ...]  [--modes=auto,1,0] [--ic0-gpu]
 
 Per config and IC(0) apply mode (DSGPU_PI=1 partitioned inverse / 0 staged
 sweeps): native assembly + host setup time, device setup time, two solves
@@ -82,8 +82,9 @@ def main():
         t_asm = time.time() - t0
         log(f"{tag}: assembled n_u={s.n_u} n_p={s.n_p}")
         t0 = time.time()
-        top = solver.prepare_block(s.A, solver.BLOCK_PCG_IC0)
-        bot = solver.prepare_block(s.Q_nu, solver.BLOCK_PCG_IC0)
+        ic0_gpu = "--ic0-gpu" in sys.argv  # factor on the device (dsgpu_ic0_factor, bit-identical)
+        top = solver.prepare_block(s.A, solver.BLOCK_PCG_IC0, ic0_on_gpu=ic0_gpu)
+        bot = solver.prepare_block(s.Q_nu, solver.BLOCK_PCG_IC0, ic0_on_gpu=ic0_gpu)
         t_host = time.time() - t0
         log(f"{tag}: host setup (RCM, permute, IC0) {t_host:.1f}s")
         gold = None
@@ -95,7 +96,7 @@ def main():
             else:
                 os.environ["DSGPU_PI"] = mode
             out = dict(cfg=tag, pi=mode, n_u=s.n_u, n_p=s.n_p, assemble_s=round(t_asm, 2),
-                       host_setup_s=round(t_host, 2))
+                       host_setup_s=round(t_host, 2), ic0_on_gpu=ic0_gpu)
             try:
                 t0 = time.time()
                 g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)", top=top, bottom=bot)
