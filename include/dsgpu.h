@@ -145,9 +145,10 @@ int dsgpu_time_vector_update(int device, int64_t n, int reps, double* ms, double
 
 /* ---- host-setup on the device --------------- */
 /* IC(0) factor of a symmetric CSR matrix on `device`, bit-identical to the
- * reference's ic0 (proj/src/cholesky.cpp:84-134): level-scheduled rows (one
- * launch per level of L's dependency DAG, one warp per row), each row's
- * entries in the reference's order with explicitly rounded arithmetic.
+ * reference's ic0 (proj/src/cholesky.cpp:84-134): one warp per row, each
+ * row's entries in the reference's order with explicitly rounded arithmetic;
+ * a persistent dataflow kernel where entry (i, j) waits only for row j's
+ * completion flag (DSGPU_IC0_FLOW=0: one launch per level of L's DAG).
  * Outputs (host, caller-allocated): l_row_ptr[n+1], l_cols / l_vals sized
  * nnz(lower(A)) incl. the diagonal. Errors: DSGPU_E_BAD_INPUT (structurally
  * missing diagonal, std::invalid_argument), DSGPU_E_FACTOR_BREAKDOWN with the

@@ -1,5 +1,7 @@
 // IC(0) factorization on the device, bit-identical
-// to the reference's ic0 (proj/src/cholesky.cpp:84-134).
+// to the reference's ic0 (proj/src/cholesky.cpp:84-134). Two schedules of the
+// same per-row work: a barrier-free dataflow kernel (default, below) and
+// level-scheduled launches (DSGPU_IC0_FLOW=0).
 //
 // The reference walks rows in order; inside row i, entry (i, j) is
 //   s = A_ij - sum_{c < j, c in row i and row j} L_ic L_jc   (merge order = c ascending)
@@ -22,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -169,6 +172,129 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
+// ---- dataflow variant: no level barriers ----------------------------------
+// A persistent grid of warps walks the rows in order (warp w: rows w, w + W,
+// ...). Entry (i, j) waits only for row j's completion flag (st.release by
+// the warp that finished it, ld.acquire here), so a row processes its entries
+// on old rows at once and stalls only on its most recent dependencies. All
+// warps are co-resident and each walks its rows in increasing order, so the
+// smallest unfinished row can always progress.
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+  int x;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+  return x;
+}
+__device__ __forceinline__ void st_release_i32(int* p, int x) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+
+__device__ __forceinline__ void load_chunk_cg(RowChunk& r, const int32_t* __restrict__ ci, const double* v,
+                                              const int* __restrict__ pos, int64_t b, int64_t e, int pmax,
+                                              int lane) {
+#pragma unroll
+  for (int u = 0; u < RowChunk::U; ++u) {
+    const int64_t q = b + u * 32 + lane;
+    r.col[u] = q < e ? __ldg(ci + q) : -1;
+    r.val[u] = q < e ? __ldcg(v + q) : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < RowChunk::U; ++u)
+    r.pos[u] = (r.col[u] >= 0 && r.col[u] <= pmax) ? pos[r.col[u]] : -1;
+}
+
+// spin until row j is final; false on timeout (abort flag set)
+__device__ __forceinline__ bool wait_row(const int* done, int j, int* abort_flag) {
+  if (ld_acquire_i32(done + j)) return true;
+  const long long t0 = clock64();
+  while (!ld_acquire_i32(done + j)) {
+    __nanosleep(32);
+    if (*reinterpret_cast<volatile int*>(abort_flag)) return false;
+    if (clock64() - t0 > 20000000000ll) {  // ~10 s: report instead of hanging the GPU
+      atomicExch(abort_flag, 1);
+      return false;
+    }
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    ic0_flow_kernel(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, double* v, int maxlen,
+                    int* pos_maps, int* done, int* bad, int* abort_flag) {
+  extern __shared__ unsigned char smem[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int w = blockIdx.x * kWarpsPerBlock + wl, W = gridDim.x * kWarpsPerBlock;
+  int32_t* scol = reinterpret_cast<int32_t*>(smem) + static_cast<size_t>(wl) * maxlen;
+  double* sval = reinterpret_cast<double*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 4 +
+                                           static_cast<size_t>(wl) * maxlen * 8);
+  int64_t* sjb = reinterpret_cast<int64_t*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 12) +
+                 static_cast<size_t>(wl) * maxlen * 3;
+  int64_t* sje = sjb + maxlen;
+  double* buf = reinterpret_cast<double*>(smem + static_cast<size_t>(kWarpsPerBlock) * maxlen * 36) +
+                static_cast<size_t>(wl) * RowChunk::U * 32;
+  int* pos = pos_maps + static_cast<int64_t>(w) * n;
+  for (int i = w; i < n; i += W) {
+    const int64_t ib = rp[i], ie = rp[i + 1];
+    const int len = static_cast<int>(ie - ib);
+    for (int k = lane; k < len; k += 32) {
+      const int c = ci[ib + k];
+      scol[k] = c;
+      sval[k] = v[ib + k];  // A's values: only this warp writes row i
+      if (k < len - 1) {
+        pos[c] = k;
+        sjb[k] = rp[c];
+        sje[k] = rp[c + 1] - 1;
+      }
+    }
+    __syncwarp();
+    const int pfull = len >= 2 ? scol[len - 2] : -1;
+    bool ok = true;
+    RowChunk cur, nxt;
+    bool cur_ok = false, nxt_ok = false;  // chunk loaded after its row was seen final
+    if (len >= 2 && ld_acquire_i32(done + scol[0])) {
+      load_chunk_cg(cur, ci, v, pos, sjb[0], sje[0], pfull, lane);
+      cur_ok = true;
+    }
+    for (int t = 0; t < len - 1; ++t) {
+      const int j = scol[t];
+      if (t + 1 < len - 1) {
+        nxt_ok = ld_acquire_i32(done + scol[t + 1]) != 0;
+        if (nxt_ok) load_chunk_cg(nxt, ci, v, pos, sjb[t + 1], sje[t + 1], pfull, lane);
+      }
+      ok = ok && wait_row(done, j, abort_flag);
+      if (!cur_ok) load_chunk_cg(cur, ci, v, pos, sjb[t], sje[t], pfull, lane);
+      const int64_t jb = sjb[t], je = sje[t];
+      double s = sval[t];
+      const int pmax = t > 0 ? scol[t - 1] : -1;
+      if (t > 0 && !apply_chunk(cur, sval, t, pmax, s, buf, lane)) {
+        for (int64_t b = jb + RowChunk::U * 32; b < je; b += RowChunk::U * 32) {
+          RowChunk more;
+          load_chunk_cg(more, ci, v, pos, b, je, pfull, lane);
+          if (apply_chunk(more, sval, t, pmax, s, buf, lane)) break;
+        }
+      }
+      const double lij = __ddiv_rn(s, __ldcg(v + je));  // L_jj: row j is final
+      if (lane == 0) {
+        sval[t] = lij;
+        v[ib + t] = lij;
+      }
+      __syncwarp();
+      cur = nxt;
+      cur_ok = nxt_ok;
+    }
+    for (int k = lane; k < len - 1; k += 32) sjb[k] = __double_as_longlong(__dmul_rn(sval[k], sval[k]));
+    __syncwarp();
+    const double d = sub_chain(sval[len - 1], reinterpret_cast<const double*>(sjb), len - 1);
+    for (int k = lane; k < len - 1; k += 32) pos[scol[k]] = -1;
+    if (lane == 0) {
+      if (!(d > 0.0) || !ok) atomicMin(bad, i);
+      v[ie - 1] = __dsqrt_rn(d);
+      __threadfence();
+      st_release_i32(done + i, 1);
+    }
+    __syncwarp();
+  }
+}
+
 int fail(int code, const std::string& msg) {
   g_ic0_err = msg;
   return code;
@@ -223,6 +349,10 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   for (int l = 0; l < nlev; ++l) lstart[l + 1] += lstart[l];
   int maxw = 1;  // widest level: one column-position map (n ints) per row of it
   for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, static_cast<int>(lstart[l + 1] - lstart[l]));
+  // dataflow grid: up to 2,368 warps, maps capped at 8 GB
+  const int maxw_flow = static_cast<int>(std::max<int64_t>(
+      kWarpsPerBlock, std::min<int64_t>(2368, (8ll << 30) / (4ll * std::max(n, 1)))));
+  maxw = std::max(maxw, maxw_flow);
   std::vector<int32_t> order(n);
   {
     std::vector<int64_t> fill(lstart.begin(), lstart.end() - 1);
@@ -276,22 +406,49 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   cudaMemsetAsync(d_pos, 0xFF, sizeof(int) * static_cast<size_t>(maxw) * n, st);  // all -1
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  // the barrier-free dataflow kernel by default; DSGPU_IC0_FLOW=0: level-scheduled launches
+  const bool flow = !(std::getenv("DSGPU_IC0_FLOW") && std::atoi(std::getenv("DSGPU_IC0_FLOW")) == 0);
+  int flow_grid = 0;
+  int* d_done = nullptr;
+  int* d_abort = nullptr;
+  if (flow) {
+    int per_sm = 0, sms = 0;
+    cudaFuncSetAttribute(ic0_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ic0_flow_kernel, kWarpsPerBlock * 32, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    flow_grid = std::max(1, std::min(per_sm * sms, (maxw_flow + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    if (cudaMalloc(&d_done, sizeof(int) * n) != cudaSuccess || cudaMalloc(&d_abort, sizeof(int)) != cudaSuccess) {
+      cudaFree(d_done);
+      cudaFree(d_abort);
+      cleanup();
+      return fail(DSGPU_E_CUDA, "ic0: device allocation failed");
+    }
+    cudaMemsetAsync(d_done, 0, sizeof(int) * n, st);
+    cudaMemsetAsync(d_abort, 0, sizeof(int), st);
+  }
   cudaEventRecord(e0, st);
-  for (int l = 0; l < nlev; ++l) {
+  if (flow)
+    ic0_flow_kernel<<<flow_grid, kWarpsPerBlock * 32, smem, st>>>(n, d_rp, d_ci, d_v, maxlen, d_pos, d_done, d_bad,
+                                                                  d_abort);
+  for (int l = 0; !flow && l < nlev; ++l) {
     const int cnt = static_cast<int>(lstart[l + 1] - lstart[l]);
     const int grid = (cnt + kWarpsPerBlock - 1) / kWarpsPerBlock;
     ic0_level_kernel<<<grid, kWarpsPerBlock * 32, smem, st>>>(d_rows + lstart[l], cnt, d_rp, d_ci, d_v, maxlen,
                                                               d_pos, static_cast<int64_t>(n), d_bad);
   }
   cudaEventRecord(e1, st);
-  int bad = big;
+  int bad = big, aborted = 0;
+  if (flow) cudaMemcpyAsync(&aborted, d_abort, sizeof(int), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(l_vals, d_v, sizeof(double) * nnz, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st);
   const cudaError_t e = cudaStreamSynchronize(st);
   float ms = 0.0f;
   if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+  cudaFree(d_done);
+  cudaFree(d_abort);
   cleanup();
   if (e != cudaSuccess) return fail(DSGPU_E_CUDA, std::string("ic0: ") + cudaGetErrorString(e));
+  if (aborted) return fail(DSGPU_E_CUDA, "ic0: dataflow wait timed out");
   if (device_ms) *device_ms = ms;
   if (bad != big) {
     if (bad_row) *bad_row = bad;

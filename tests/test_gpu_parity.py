@@ -418,12 +418,15 @@ def test_ic0_factor_gpu_bit_identical_to_reference_fixture(gpu):
         assert info["levels"] > 1
 
 
+@pytest.mark.parametrize("flow", ["0", "1"])
 @pytest.mark.parametrize("case,k,n,dim", [("psi-mms", 2, 64, 2), ("random", 3, 16, 2), ("cavity", 2, 16, 2),
                                           ("psi-mms", 2, 6, 3)])
-def test_ic0_factor_gpu_bit_identical_to_host(gpu, case, k, n, dim):
+def test_ic0_factor_gpu_bit_identical_to_host(gpu, monkeypatch, case, k, n, dim, flow):
     """Against the native host ic0 (itself bit-identical to the reference,
-    tests/test_host.py) on BASELINE-shaped systems, 2D and 3D."""
+    tests/test_host.py) on BASELINE-shaped systems, 2D and 3D; flow = 1 runs
+    the barrier-free dataflow kernel instead of level-scheduled launches."""
     host, solver = gpu
+    monkeypatch.setenv("DSGPU_IC0_FLOW", flow)
     s = host.assemble(case, k, n, dim=dim, seed=1234)
     for m in (s.A, s.Q_nu):
         pm = host.permute_symmetric(m, host.rcm_permutation(m))

@@ -25,15 +25,19 @@ def main():
         t0 = time.time()
         H = host.ic0(pm)
         t_host = time.time() - t0
-        solver.ic0_factor_gpu(pm)  # warm-up (module load, first launches)
-        t0 = time.time()
-        L, info = solver.ic0_factor_gpu(pm)
-        t_gpu = time.time() - t0
-        same = (np.array_equal(L.row_ptr, H.row_ptr) and np.array_equal(L.cols, H.cols)
-                and np.array_equal(L.vals.view(np.int64), H.vals.view(np.int64)))
-        print(json.dumps(dict(cfg=tag, n=pm.n_rows, nnz_L=int(L.row_ptr[-1]), levels=info["levels"],
-                              host_ic0_s=round(t_host, 3), gpu_call_s=round(t_gpu, 3),
-                              gpu_levels_ms=round(info["device_ms"], 2), bit_identical=bool(same))), flush=True)
+        for flow in os.environ.get("IC0_PROBE_MODES", "1").split(","):
+            os.environ["DSGPU_IC0_FLOW"] = flow
+            solver.ic0_factor_gpu(pm)  # warm-up (module load, first launches)
+            t0 = time.time()
+            L, info = solver.ic0_factor_gpu(pm)
+            t_gpu = time.time() - t0
+            same = (np.array_equal(L.row_ptr, H.row_ptr) and np.array_equal(L.cols, H.cols)
+                    and np.array_equal(L.vals.view(np.int64), H.vals.view(np.int64)))
+            print(json.dumps(dict(cfg=tag, kernel="dataflow" if flow == "1" else "levels", n=pm.n_rows,
+                                  nnz_L=int(L.row_ptr[-1]), levels=info["levels"],
+                                  host_ic0_s=round(t_host, 3), gpu_call_s=round(t_gpu, 3),
+                                  gpu_device_ms=round(info["device_ms"], 2), bit_identical=bool(same))),
+                  flush=True)
 
 
 if __name__ == "__main__":
