@@ -349,9 +349,11 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   for (int l = 0; l < nlev; ++l) lstart[l + 1] += lstart[l];
   int maxw = 1;  // widest level: one column-position map (n ints) per row of it
   for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, static_cast<int>(lstart[l + 1] - lstart[l]));
-  // dataflow grid: up to 2,368 warps, maps capped at 8 GB
-  const int maxw_flow = static_cast<int>(std::max<int64_t>(
-      kWarpsPerBlock, std::min<int64_t>(2368, (8ll << 30) / (4ll * std::max(n, 1)))));
+  // dataflow grid: up to 2,368 warps (whole CTAs), maps capped at 8 GB;
+  // DSGPU_IC0_MAX_WARPS lowers the cap (tests)
+  int64_t cap_w = std::min<int64_t>(2368, (8ll << 30) / (4ll * std::max(n, 1)));
+  if (const char* env = std::getenv("DSGPU_IC0_MAX_WARPS")) cap_w = std::min<int64_t>(cap_w, std::atoll(env));
+  const int maxw_flow = static_cast<int>(std::max<int64_t>(kWarpsPerBlock, cap_w / kWarpsPerBlock * kWarpsPerBlock));
   maxw = std::max(maxw, maxw_flow);
   std::vector<int32_t> order(n);
   {
@@ -416,7 +418,7 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
     cudaFuncSetAttribute(ic0_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ic0_flow_kernel, kWarpsPerBlock * 32, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    flow_grid = std::max(1, std::min(per_sm * sms, (maxw_flow + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    flow_grid = std::max(1, std::min(per_sm * sms, maxw_flow / kWarpsPerBlock));  // W <= maps allocated
     if (cudaMalloc(&d_done, sizeof(int) * n) != cudaSuccess || cudaMalloc(&d_abort, sizeof(int)) != cudaSuccess) {
       cudaFree(d_done);
       cudaFree(d_abort);

@@ -435,6 +435,20 @@ def test_ic0_factor_gpu_bit_identical_to_host(gpu, monkeypatch, case, k, n, dim,
         assert _same_csr(L, H.row_ptr, H.cols, H.vals)
 
 
+@pytest.mark.parametrize("max_warps", ["4", "37", "101"])
+def test_ic0_factor_gpu_dataflow_small_grids(gpu, monkeypatch, max_warps):
+    """The dataflow schedule with few warps (each walks many rows; the cap is
+    rounded down to whole CTAs so every warp owns a position map)."""
+    host, solver = gpu
+    monkeypatch.setenv("DSGPU_IC0_MAX_WARPS", max_warps)
+    s = host.assemble("psi-mms", 2, 6, dim=3)
+    for m in (s.A, s.Q_nu):
+        pm = host.permute_symmetric(m, host.rcm_permutation(m))
+        L, _ = solver.ic0_factor_gpu(pm)
+        H = host.ic0(pm)
+        assert _same_csr(L, H.row_ptr, H.cols, H.vals)
+
+
 def test_ic0_factor_gpu_errors(gpu):
     """FactorBreakdown at the reference's first failing row; a structurally
     missing diagonal is std::invalid_argument (cholesky.cpp:109-111,128)."""
