@@ -164,6 +164,15 @@ const char* dsgpu_ic0_last_error(void);
  * levels_fwd_A, levels_bwd_A, levels_fwd_Q, levels_bwd_Q, grid_ctas. */
 int dsgpu_info(const dsgpu_handle* h, int64_t* info);
 
+/* Blocked-sweep plan check (no device): builds the blocked-sweep plan of the
+ * factor L (as dsgpu_setup does) and evaluates it on the host in the plan's own
+ * arithmetic order, z = (L L^T)^{-1} r. A test hook for the plan's structure
+ * and coefficients, never used by a solve. stats8 (nullable): groups, factor
+ * entries in dense blocks / mid lists / far lists (forward sweep), widest mid
+ * and far list, padded mid and far list entries. */
+int dsgpu_debug_bsweep_host(int n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                            const double* r, double* z, int64_t* stats8);
+
 /* Process-wide sweep diagnostics (summed since the last reset), out32:
  * [0] main-warp cycles, [1] main cycles waiting, [2] groups, [3] abort code,
  * [4] main cycles waiting for static slot data, [5] helper cycles waiting for

@@ -101,6 +101,14 @@ class RefLib:
         L.ref_solve.argtypes = [C.c_void_p, C.c_char_p, C.c_double, C.c_double, C.c_int,
                                 C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_char_p, C.c_int]
         L.ref_spmv.argtypes = [C.c_int, C.c_int, _i64p, _i32p, _dp, _dp, _dp]
+        if hasattr(L, "ref_precond_make"):
+            L.ref_precond_make.restype = C.c_void_p
+            L.ref_precond_make.argtypes = [C.c_void_p, C.c_char_p, C.c_double,
+                                           C.POINTER(C.c_double), C.c_char_p, C.c_int]
+            L.ref_precond_free.argtypes = [C.c_void_p]
+            L.ref_solve_with.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_int,
+                                         C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_char_p,
+                                         C.c_int]
         L.ref_rcm.argtypes = [C.c_int, _i64p, _i32p, _i32p, C.c_char_p, C.c_int]
         L.ref_write_mm.argtypes = [C.c_int, C.c_int, _i64p, _i32p, _dp, C.c_char_p, C.c_int,
                                    C.c_char_p, C.c_int]
@@ -293,6 +301,46 @@ class RefSystem:
         return dict(u=u, p=p, iterations=int(rep[0]), converged=bool(rep[1]),
                     wall_seconds=rep[2], mean_inner_top=rep[3], mean_inner_bottom=rep[4],
                     setup_seconds=rep[5], residual_history=hm[:n], euclid_history=he[:n])
+
+
+class RefPrecond:
+    """make_strategy once (precond.cpp:161-193), many solve_stokes(system, precond, options)."""
+
+    def __init__(self, system: RefSystem, strategy: str, inner_tol: float):
+        self.system, self.inner_tol = system, inner_tol
+        err = C.create_string_buffer(512)
+        t = C.c_double(0.0)
+        self.h = system.lib.L.ref_precond_make(C.c_void_p(system.h), strategy.encode(), inner_tol,
+                                               C.byref(t), err, 512)
+        if not self.h:
+            raise RuntimeError(err.value.decode())
+        self.setup_seconds = t.value
+
+    def close(self):
+        if self.h:
+            self.system.lib.L.ref_precond_free(C.c_void_p(self.h))
+            self.h = None
+
+    def solve(self, outer_tol: float, max_iter: int = 20000, euclid: bool = True):
+        s = self.system
+        u = np.zeros(s.n_u)
+        p = np.zeros(s.n_p)
+        rep = np.zeros(7)
+        cap = max_iter + 1
+        hm = np.zeros(cap)
+        he = np.zeros(cap)
+        err = C.create_string_buffer(512)
+        rc = s.lib.L.ref_solve_with(C.c_void_p(s.h), C.c_void_p(self.h), outer_tol, self.inner_tol,
+                                    max_iter, int(euclid), u, p, rep, hm, he, cap, err, 512)
+        if rc:
+            e = RuntimeError(err.value.decode())
+            e.code = rc  # type: ignore[attr-defined]
+            raise e
+        n = min(int(rep[6]), cap)
+        return dict(u=u, p=p, iterations=int(rep[0]), converged=bool(rep[1]),
+                    wall_seconds=rep[2], mean_inner_top=rep[3], mean_inner_bottom=rep[4],
+                    setup_seconds=self.setup_seconds, residual_history=hm[:n],
+                    euclid_history=he[:n])
 
 
 class _OrCsr(C.Structure):

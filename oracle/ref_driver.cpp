@@ -302,6 +302,61 @@ int ref_solve(ref_system* s, const char* strategy, double outer_tol, double inne
   });
 }
 
+// ---- a preconditioner kept across solves ---------------------------------
+// make_strategy (proj/src/precond.cpp:161-193) once, then any number of
+// solve_stokes(system, precond, options) calls (precond.cpp:245-290): at 96^3
+// the reference's RCM + permute + ic0 is ~15 minutes, so the bounded
+// (max_iter = k) and the full C5 solves share it. The block counters are
+// cumulative in the reference; the per-call inner means are counter deltas.
+struct ref_precond {
+  BlockDiagPreconditioner p;
+};
+
+ref_precond* ref_precond_make(ref_system* s, const char* strategy, double inner_tol,
+                              double* setup_seconds, char* err, int errlen) {
+  ref_precond* out = nullptr;
+  const int rc = guarded(err, errlen, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    auto* h = new ref_precond{make_strategy(strategy, s->sys, inner_tol)};
+    *setup_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    out = h;
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+void ref_precond_free(ref_precond* h) { delete h; }
+
+int ref_solve_with(ref_system* s, ref_precond* h, double outer_tol, double inner_tol,
+                   int max_iter, int stop_euclid, double* u, double* p, double* report7,
+                   double* hist_m, double* hist_e, int hist_cap, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    SolverOptions opt;
+    opt.outer_tol = outer_tol;
+    opt.inner_tol = inner_tol;
+    opt.max_iter = max_iter;
+    opt.stop = stop_euclid ? MinresStop::euclidean : MinresStop::preconditioned;
+    const long it0 = h->p.top->inner_iterations(), ap0 = h->p.top->applications();
+    const long ib0 = h->p.bottom->inner_iterations(), ab0 = h->p.bottom->applications();
+    const StokesSolution sol = solve_stokes(s->sys, h->p, opt);
+    std::memcpy(u, sol.u.data(), sizeof(double) * sol.u.size());
+    std::memcpy(p, sol.p.data(), sizeof(double) * sol.p.size());
+    const long at = h->p.top->applications() - ap0, ab = h->p.bottom->applications() - ab0;
+    report7[0] = sol.report.iterations;
+    report7[1] = sol.report.converged ? 1.0 : 0.0;
+    report7[2] = sol.report.wall_seconds;
+    report7[3] = at > 0 ? static_cast<double>(h->p.top->inner_iterations() - it0) / at : 0.0;
+    report7[4] = ab > 0 ? static_cast<double>(h->p.bottom->inner_iterations() - ib0) / ab : 0.0;
+    report7[5] = 0.0;
+    const int len = static_cast<int>(sol.report.residual_history.size());
+    report7[6] = len;
+    for (int i = 0; i < len && i < hist_cap; ++i) {
+      if (hist_m) hist_m[i] = sol.report.residual_history[i];
+      if (hist_e) hist_e[i] = sol.report.euclid_history[i];
+    }
+  });
+}
+
 // ---- solver-layer primitives -------------------------------------------
 
 void ref_spmv(int n_rows, int n_cols, const int64_t* rp, const int32_t* ci, const double* v,

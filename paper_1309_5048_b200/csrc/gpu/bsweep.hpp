@@ -1,0 +1,105 @@
+// Blocked triangular sweep ("block sweep"): the production form of the IC(0)
+// forward / backward solves (reference Ic0Factor::solve,
+// proj/src/cholesky.cpp:136-152) on B200.
+//
+// The rows of the (RCM-ordered) factor are cut into groups of kBsB = 16
+// CONSECUTIVE rows (not dependency levels). With D_g the 16 x 16 diagonal
+// block of group g and E_{g,h} its coupling to group h < g,
+//
+//   y_g = D_g^{-1} ( r_g - sum_{h<g} E_{g,h} y_h )
+//       = T_g ( r_g - sum_{h < g-K} E_{g,h} y_h )  -  sum_{k=1..K} F_{g,k} y_{g-k},
+//
+// T_g = D_g^{-1} and F_{g,k} = D_g^{-1} E_{g,g-k} formed once at setup as
+// DENSE 16 x 16 blocks (the factor is quasi-dense next to its diagonal: at
+// 32^3 a row has 12 of its 235 entries within the previous 32 rows). The
+// sequential chain is then one dense 16 x 16 product per group, done by ONE
+// warp out of shared memory, instead of one step per dependency level
+// (32^3: 7,153 groups vs 10,715 levels of 10.7 rows).
+//
+// Roles (one "sweep CTA" per triangular solve, plus far-worker CTAs):
+//   * MAIN warp: y_g = c_g - sum_k F_{g,k} y_{g-k}; lane (r, h) owns row r and
+//     columns 8h..8h+7 of each block (two lanes per row, combined by one
+//     shuffle). y_{g-1} is broadcast through the shared-memory y ring.
+//   * CO-MAIN warps (kBsNC, round-robin over groups): c_g = T_g (r_g - far_g
+//     - mid_g): the "mid" entries (groups g-R .. g-K-1) are gathered from the y
+//     ring; the "far" partial sums come from the far workers.
+//   * PRODUCER lane: TMA bulk copies of each group's dense blocks (F_1..F_K,
+//     T) into a shared-memory slot ring.
+//   * PUBLISHER warp: copies finished groups from the y ring to the result
+//     vector in global memory and publishes the progress counter (fence +
+//     release), so the main warp never touches global memory.
+//   * FAR WORKERS (warps of other CTAs): for each group the partial sums of
+//     the entries older than the ring (col group < g-R), gathered from the
+//     published result vector; they run far ahead of the main warp and stream
+//     ~85 % of the factor at HBM/L2 speed on as many SMs as needed.
+// The backward solve is the same sweep on the reversed ordering (row p of the
+// sweep = row n-1-p of the factor; L^T's rows are L's columns).
+//
+// Arithmetic: T_g and F_{g,k} are formed in long double and rounded once; the
+// sweep itself is fp64. The result is the same operator (L L^T)^{-1} applied
+// with a different association (measured agreement with the reference's
+// Ic0Factor::solve: see tests/test_gpu_parity.py); the exact column-order
+// sweep stays available behind DSGPU_EXACT=1.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "dsgpu.h"
+
+namespace dsgpu {
+
+constexpr int kBsB = 16;     // rows per group
+constexpr int kBsK = 3;      // dense pre-multiplied coupling blocks on the main warp
+constexpr int kBsR = 32;     // y ring depth in groups; older entries are "far"
+constexpr int kBsNC = 4;     // co-main warps
+constexpr int kBsRC = 8;     // c ring (co-main -> main), groups
+constexpr int kBsMC = 4;     // mid-list chunk (entries per lane)
+constexpr int kBsFC = 8;     // far-list chunk (entries per lane)
+constexpr int kBsBlock = kBsB * kBsB * 8;              // bytes of one dense block
+constexpr int kBsSlotBytes = (kBsK + 1) * kBsBlock;    // F_1..F_K, T
+constexpr int kBsZero = kBsR * kBsB * 8;               // byte offset of the ring's zero slot
+
+// Lane-unit layouts. A dense block: lane l = (row r = l & 15, half h = l >> 4)
+// owns columns 8h..8h+7 as four 16-byte units; unit q of lane l sits at byte
+// ((q * 32) + l) * 16 (conflict-free 128-bit shared loads). Sparse lists: entry
+// k of lane l at int32 index ((k / 4) * 32 + l) * 4 + k % 4 and double index
+// ((k / 2) * 32 + l) * 2 + k % 2 from the group's base (coalesced 128-bit loads).
+inline int64_t bs_i32_at(int k, int l) { return (static_cast<int64_t>(k >> 2) * 32 + l) * 4 + (k & 3); }
+inline int64_t bs_f64_at(int k, int l) { return (static_cast<int64_t>(k >> 1) * 32 + l) * 2 + (k & 1); }
+
+struct HostBSweep {
+  int n = 0, G = 0, dir = 0;        // dir 0: forward (L), 1: backward (L^T, reversed ordering)
+  std::vector<uint8_t> slots;        // G * kBsSlotBytes
+  std::vector<int32_t> mw, ms;       // mid list: width (multiple of kBsMC), leading entries that only
+                                     //   need groups <= g-K-3 (multiple of kBsMC)
+  std::vector<int64_t> mptr;         // G + 1, element offset of the group's lists (width * 32 each)
+  std::vector<int32_t> mcols;        // byte offsets into the y ring (pad: kBsZero)
+  std::vector<double> mvals;
+  std::vector<int32_t> fw;           // far list: width (multiple of kBsFC; 0 = none)
+  std::vector<int64_t> fptr;         // G + 1
+  std::vector<int32_t> fcols;        // rows of the result vector (original ordering; pad: n, x[n] = 0)
+  std::vector<double> fvals;
+  std::vector<int32_t> fcptr;        // G + 1: first chunk of the group in fneed
+  std::vector<int32_t> fneed;        // per chunk: newest group it depends on (-1: none)
+  int64_t nnz_dense = 0, nnz_mid = 0, nnz_far = 0;  // factor entries by class (statistics)
+};
+
+// Builds both sweeps of the factor L (lower triangular CSR, columns ascending,
+// diagonal last in each row, as Ic0Factor::lower). Throws std::invalid_argument.
+void build_bsweeps(const dsgpu_csr& L, HostBSweep& fwd, HostBSweep& bwd);
+
+// CPU evaluation of one sweep plan (tests: the plan against the plain
+// substitution): x = T^{-1} rhs in the sweep's own arithmetic order.
+void bsweep_host_apply(const HostBSweep& s, const double* rhs, double* x);
+
+// Shared memory of the sweep CTA with a slot ring of `ns` slots.
+inline size_t bs_smem_bytes(int ns) {
+  return static_cast<size_t>(kBsZero) + 128            // y ring + zero slot
+         + kBsRC * kBsB * 8                             // c ring
+         + static_cast<size_t>(ns) * kBsSlotBytes       // dense-block slots
+         + static_cast<size_t>(ns) * 8                  // mbarriers
+         + (2 * ns + kBsRC + 8) * 4 + 128;              // sready, base_use, aready, progress words
+}
+
+}  // namespace dsgpu

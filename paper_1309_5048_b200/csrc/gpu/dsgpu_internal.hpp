@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "bsweep.hpp"
 #include "dsgpu.h"
 
 namespace dsgpu {
@@ -131,7 +132,8 @@ struct HostBlock {
   std::vector<int32_t> lci;
   std::vector<double> lv;
   HostSweep fwd, bwd;            // IC0-PCG, exact column-order sweeps (bit-identical mode)
-  HostFlow ffwd, fbwd;           // IC0-PCG, staged sweeps (production)
+  HostFlow ffwd, fbwd;           // IC0-PCG, staged level sweeps
+  HostBSweep bfwd, bbwd;         // IC0-PCG, blocked sweeps (production, bsweep.hpp)
 };
 
 struct HostPlan {
@@ -148,11 +150,13 @@ struct HostPlan {
   double filter_den = 0.0;
 };
 
-// Throws std::invalid_argument / std::domain_error on bad input.
+// Throws std::invalid_argument / std::domain_error on bad input. blocked != 0:
+// the IC(0) blocks get blocked sweeps (bsweep.hpp); otherwise the level-grouped
+// exact sweeps plus a copy of the factor (staged / partitioned-inverse modes).
 void build_plan(HostPlan& plan, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu_csr* Bt,
                 const dsgpu_csr* Q_nu, int top_kind, const int32_t* perm_A, const dsgpu_csr* L_A,
                 int bottom_kind, const int32_t* perm_Q, const dsgpu_csr* L_Q,
-                const dsgpu_csr* Q_filter);
+                const dsgpu_csr* Q_filter, int blocked);
 
 void build_sweeps(const dsgpu_csr& L, HostSweep& fwd, HostSweep& bwd);
 DepRows rows_from_sweep(const HostSweep& s);

@@ -154,7 +154,7 @@ void build_sweeps(const dsgpu_csr& L, HostSweep& fwd, HostSweep& bwd) {
 void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu_csr* Bt,
                 const dsgpu_csr* Q_nu, int top_kind, const int32_t* perm_A, const dsgpu_csr* L_A,
                 int bottom_kind, const int32_t* perm_Q, const dsgpu_csr* L_Q,
-                const dsgpu_csr* Q_filter) {
+                const dsgpu_csr* Q_filter, int blocked) {
   if (!A || !B || !Bt || !Q_nu) throw std::invalid_argument("dsgpu_setup: null block");
   const int n_u = A->n_rows, n_p = Q_nu->n_rows;
   if (n_u <= 0 || n_p <= 0) throw std::invalid_argument("dsgpu_setup: empty system");
@@ -266,7 +266,9 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
         }
       }
     }
-    if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
+    if (hb.kind == DSGPU_BLOCK_PCG_IC0 && blocked) {
+      build_bsweeps(*facs[b], hb.bfwd, hb.bbwd);
+    } else if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
       build_sweeps(*facs[b], hb.fwd, hb.bwd);
       const dsgpu_csr* L = facs[b];
       hb.lrp.assign(L->row_ptr, L->row_ptr + hb.n + 1);

@@ -34,6 +34,7 @@
 #include "dsgpu_internal.hpp"
 #include "kernels.cuh"
 #include "pi.cuh"
+#include "bsweep.cuh"
 
 using namespace dsgpu;
 using namespace dsgpu::dev;
@@ -91,6 +92,11 @@ struct DBlock {
   int remote_cta0, n_remote;    // remote helper CTAs (0: none)
   int pi;                       // 1: partitioned-inverse IC(0) apply (pi.cuh), all CTAs
   DPi pim;
+  // blocked sweeps (bsweep.cuh): remote_cta0 / n_remote name the far-worker CTAs
+  int bs, bs_ns;                // 1: blocked sweeps; slot-ring depth
+  DBSweep bfwd, bbwd;
+  double* fpsum;                // max(G) * 16 far partial sums
+  unsigned* fflag;              // max(G)
 };
 
 struct DevReport {
@@ -212,35 +218,6 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
   double out;
   asm volatile("mov.b64 %0, {%1,%2};" : "=d"(out) : "r"(rlo), "r"(rhi));
   return out;
-}
-
-// ---- mbarrier / bulk-copy (TMA) helpers -----------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* mb, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_test(uint64_t* mb, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
-      : "=r"(ok)
-      : "r"(smem_u32(mb)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mb) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(mb))
-      : "memory");
 }
 
 // Shared-memory workspace of one staged sweep: xs[n+1] | ring of kSRing static
@@ -859,7 +836,16 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
   for (int i = threadIdx.x; i < B.n; i += blockDim.x) bb[i] = rhs(i);
   __syncthreads();
   double* y = B.y;
-  if (RING) {
+  if constexpr (TB == 0) {
+    // blocked sweeps (bsweep.cuh): results go to global memory (y, then z)
+    const int workers = B.n_remote * static_cast<int>(blockDim.x >> 5);
+    bsweep<kBsK>(B.bfwd, xf, B.bs_ns, bb, y,
+                 BsFar{B.fpsum, B.fflag, B.gprog, sweep_tag(launch_id, sweep_no), workers}, abort_flag);
+    bsweep<kBsK>(B.bbwd, xf, B.bs_ns, y, z,
+                 BsFar{B.fpsum, B.fflag, B.gprog, sweep_tag(launch_id, sweep_no + 1), workers}, abort_flag);
+    for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += r[i] * z[i];
+    return block_sum(rz, red);
+  } else if constexpr (RING) {
     // results go straight to global memory (y, then z)
     const int on = B.n_remote > 0;
     flow_sweep<TB, true>(B.ffwd, B.n, xf, bb, y,
@@ -870,23 +856,31 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
                          abort_flag);
     for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += r[i] * z[i];
     return block_sum(rz, red);
+  } else {
+    const FlowRemote none{nullptr, nullptr, nullptr, 0u, 0};
+    flow_sweep<TB, false>(B.ffwd, B.n, xf, bb, nullptr, none, abort_flag);
+    for (int i = threadIdx.x; i < B.n; i += blockDim.x) y[i] = xf[i];
+    __syncthreads();
+    flow_sweep<TB, false>(B.fbwd, B.n, xf, y, nullptr, none, abort_flag);
+    for (int i = threadIdx.x; i < B.n; i += blockDim.x) {
+      const double zi = xf[i];
+      z[i] = zi;
+      rz += r[i] * zi;
+    }
+    return block_sum(rz, red);
   }
-  const FlowRemote none{nullptr, nullptr, nullptr, 0u, 0};
-  flow_sweep<TB, false>(B.ffwd, B.n, xf, bb, nullptr, none, abort_flag);
-  for (int i = threadIdx.x; i < B.n; i += blockDim.x) y[i] = xf[i];
-  __syncthreads();
-  flow_sweep<TB, false>(B.fbwd, B.n, xf, y, nullptr, none, abort_flag);
-  for (int i = threadIdx.x; i < B.n; i += blockDim.x) {
-    const double zi = xf[i];
-    z[i] = zi;
-    rz += r[i] * zi;
-  }
-  return block_sum(rz, red);
 }
 
 // What a remote helper CTA does while the IC CTA runs one IC(0) apply.
 __device__ void ic_apply_remote(const DBlock& B, int rank, unsigned* abort_flag, unsigned launch_id,
                                 unsigned sweep_no) {
+  if (B.bs) {  // far workers of the blocked sweeps: every warp of this CTA
+    const int nw = blockDim.x >> 5, W = B.n_remote * nw, wid = rank * nw + (threadIdx.x >> 5);
+    bs_far(B.bfwd, B.y, BsFar{B.fpsum, B.fflag, B.gprog, sweep_tag(launch_id, sweep_no), W}, wid, W, abort_flag);
+    bs_far(B.bbwd, B.z, BsFar{B.fpsum, B.fflag, B.gprog, sweep_tag(launch_id, sweep_no + 1), W}, wid, W,
+           abort_flag);
+    return;
+  }
   flow_remote(B.ffwd, B.n, B.y,
               FlowRemote{B.rpsum, B.rflag, B.gprog, sweep_tag(launch_id, sweep_no), 1}, rank,
               B.n_remote, abort_flag);
@@ -1300,7 +1294,11 @@ __device__ void ic_server(const Args& a, int b, double* xs, double* red) {
   __shared__ const double* src0_sh;
   __shared__ const double* src1_sh;
   __shared__ double* dst_sh;
-  if (!B.exact) flow_setup<TB>(xs, B.n, B.ffwd.ring);
+  if constexpr (TB == 0) {
+    if (!B.exact) bs_setup(xs, B.bs_ns);
+  } else {
+    if (!B.exact) flow_setup<TB>(xs, B.n, B.ffwd.ring);
+  }
   for (unsigned seq = 1;; ++seq) {
     if (threadIdx.x == 0) {
       int op = IC_OP_EXIT;
@@ -1625,7 +1623,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     ic_apply_remote(B, blockIdx.x - 1, abort_flag, launch_id, 0u);
     return;
   }
-  if (!B.exact) flow_setup<TB>(xs_dyn, B.n, B.ffwd.ring);
+  if constexpr (TB == 0) {
+    if (!B.exact) bs_setup(xs_dyn, B.bs_ns);
+  } else {
+    if (!B.exact) flow_setup<TB>(xs_dyn, B.n, B.ffwd.ring);
+  }
   ic_apply<TB, RING>(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag,
                      launch_id, 0u);
 }
@@ -1652,11 +1654,13 @@ __global__ void fill_sentinel(double* p, int64_t n) {
 using MinresFn = void (*)(Args);
 using IcFn = void (*)(DBlock, const double*, unsigned*, unsigned);
 MinresFn minres_for(int tb, bool ring, bool pi) {
+  if (tb == 0) return minres_kernel<0, true, false>;  // blocked sweeps
   if (pi) return minres_kernel<8, false, true>;
   if (ring) return tb <= 8 ? minres_kernel<8, true, false> : minres_kernel<16, true, false>;
   return tb <= 8 ? minres_kernel<8, false, false> : minres_kernel<16, false, false>;
 }
 IcFn ic_for(int tb, bool ring) {
+  if (tb == 0) return ic_apply_kernel<0, true>;  // blocked sweeps
   if (ring) return tb <= 8 ? ic_apply_kernel<8, true> : ic_apply_kernel<16, true>;
   return tb <= 8 ? ic_apply_kernel<8, false> : ic_apply_kernel<16, false>;
 }
@@ -1729,6 +1733,9 @@ struct dsgpu_handle {
   bool exact = false;
   bool ring = false;
   bool pi = false;            // partitioned-inverse IC(0) applies (pi.cuh)
+  bool bs = false;            // blocked sweeps (bsweep.cuh): the default IC(0) apply
+  int bs_ns = 12;             // dense-block slot ring depth
+  int far_ctas[2] = {0, 0};   // far-worker CTAs per IC block
   PiPlan pip[2];
   int pi_cbase = 0, pi_cslot = 0;  // chain coefficient prefetch slots (doubles)
   int pi_steps = 0;           // dependent chain steps per IC(0) apply (both sweeps)
@@ -1810,6 +1817,44 @@ DFlow upload_flow(dsgpu_handle* h, const HostFlow& f) {
   if (const char* env = std::getenv("DSGPU_RSPLIT"))
     d.rsplit = std::min(kRSplit, std::max(1, std::atoi(env)));
   return d;
+}
+
+DBSweep upload_bsweep(dsgpu_handle* h, HostBSweep& s) {
+  DBSweep d{};
+  d.n = s.n;
+  d.G = s.G;
+  d.dir = s.dir;
+  d.slots = h->upload(s.slots);
+  d.mw = h->upload(s.mw);
+  d.ms = h->upload(s.ms);
+  d.mptr = h->upload(s.mptr);
+  d.mcols = h->upload(s.mcols);
+  d.mvals = h->upload(s.mvals);
+  d.fw = h->upload(s.fw);
+  d.fptr = h->upload(s.fptr);
+  d.fcols = h->upload(s.fcols);
+  d.fvals = h->upload(s.fvals);
+  d.fcptr = h->upload(s.fcptr);
+  d.fneed = h->upload(s.fneed);
+  // the device copy is the plan from here on (96^3: 13 GB of lists per sweep)
+  std::vector<uint8_t>().swap(s.slots);
+  std::vector<int32_t>().swap(s.mcols);
+  std::vector<double>().swap(s.mvals);
+  std::vector<int32_t>().swap(s.fcols);
+  std::vector<double>().swap(s.fvals);
+  return d;
+}
+
+// Dynamic shared memory limit of a kernel: raised once to the device maximum
+// (the attribute belongs to the function, not to a handle: a per-handle value
+// would be lowered by the next, smaller system's setup).
+cudaError_t raise_smem_limit(const void* fn, int smem_optin) {
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  const int want = smem_optin - static_cast<int>(fa.sharedSizeBytes);
+  if (fa.maxDynamicSharedSizeBytes >= want) return cudaSuccess;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
 }
 
 DSweep upload_sweep(dsgpu_handle* h, const HostSweep& s) {
@@ -1954,15 +1999,26 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
   cudaSetDevice(h->device);
   h->free_all();
   h->plan = HostPlan{};
+  for (auto& l : h->levels) l = 0;
+  // IC(0) apply mode: blocked sweeps unless DSGPU_SWEEP=legacy (or one of the
+  // legacy knobs DSGPU_PI / DSGPU_EXACT is set): staged level sweeps or the
+  // partitioned inverse by the cost model, or the exact column-order sweeps
+  h->exact = std::getenv("DSGPU_EXACT") && std::atoi(std::getenv("DSGPU_EXACT")) != 0;
+  {
+    const char* sw = std::getenv("DSGPU_SWEEP");
+    h->bs = !h->exact && (sw ? std::string(sw) == "bs" : std::getenv("DSGPU_PI") == nullptr);
+  }
   try {
     build_plan(h->plan, A, B, Bt, Q_nu, top_kind, perm_A, L_A, bottom_kind, perm_Q, L_Q,
-               Q_filter);
+               Q_filter, h->bs ? 1 : 0);
   } catch (const std::domain_error& e) {
     return fail(h, DSGPU_E_NONPOS_DIAG, e.what());
   } catch (const std::exception& e) {
     return fail(h, DSGPU_E_BAD_INPUT, e.what());
   }
   HostPlan& P = h->plan;
+  const int64_t L_nnz[2] = {(top_kind == DSGPU_BLOCK_PCG_IC0 && L_A) ? L_A->row_ptr[L_A->n_rows] : 0,
+                            (bottom_kind == DSGPU_BLOCK_PCG_IC0 && L_Q) ? L_Q->row_ptr[L_Q->n_rows] : 0};
   try {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
@@ -1980,11 +2036,18 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     int nmax = 0;
     for (int b = 0; b < 2; ++b)
       if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0) nmax = std::max(nmax, P.blk[b].n);
-    h->exact = std::getenv("DSGPU_EXACT") && std::atoi(std::getenv("DSGPU_EXACT")) != 0;
     int smem_optin_pi = 0;
     cudaDeviceGetAttribute(&smem_optin_pi, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
-    h->pi = !h->exact && nmax > 0 && choose_pi(h, P, static_cast<size_t>(smem_optin_pi) - 2048);
-    if (!h->exact && !h->pi && nmax > 0) {
+    h->pi = !h->exact && !h->bs && nmax > 0 && choose_pi(h, P, static_cast<size_t>(smem_optin_pi) - 2048);
+    h->ring = false;
+    h->tb = 4;
+    if (h->bs && nmax == 0) h->bs = false;  // no IC(0) block: nothing to sweep
+    if (h->bs) {
+      h->tb = 0;  // selects the blocked-sweep kernels (minres_for / ic_for)
+      h->ring = true;
+      if (const char* env = std::getenv("DSGPU_BS_SLOTS")) h->bs_ns = std::max(kBsK + 2, std::atoi(env));
+    }
+    if (!h->exact && !h->pi && !h->bs && nmax > 0) {
       const int merge = std::getenv("DSGPU_MERGE") ? std::atoi(std::getenv("DSGPU_MERGE")) : kDefaultMerge;
       // ring mode when the full solution vector + ring would not fit shared memory
       int smem_optin0 = 0;
@@ -2002,6 +2065,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     h->smem = h->exact ? static_cast<size_t>(2) * nmax * sizeof(double)
                        : FlowSmem::bytes(nmax, SlotLayout(h->tb).bytes);
     if (h->pi) h->smem = pi_smem(h, static_cast<size_t>(smem_optin_pi) - 2048);
+    if (h->bs) h->smem = bs_smem_bytes(h->bs_ns);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const size_t static_smem = 1024;
@@ -2009,15 +2073,13 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       return fail(h, DSGPU_E_UNSUPPORTED,
                   "IC(0) block too large for the shared-memory dataflow sweep in this build (n=" +
                       std::to_string(nmax) + ")");
-    int rc = cuda_check(h,
-                        cudaFuncSetAttribute(minres_for(h->tb, h->ring, h->pi), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(h->smem)),
+    int rc = cuda_check(h, raise_smem_limit(reinterpret_cast<const void*>(minres_for(h->tb, h->ring, h->pi)), smem_optin),
                         "cudaFuncSetAttribute");
     if (rc) return rc;
     rc = cuda_check(h,
-                    cudaFuncSetAttribute(h->pi ? reinterpret_cast<const void*>(pi_apply_kernel)
-                                               : reinterpret_cast<const void*>(ic_for(h->tb, h->ring)),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->smem)),
+                    raise_smem_limit(h->pi ? reinterpret_cast<const void*>(pi_apply_kernel)
+                                           : reinterpret_cast<const void*>(ic_for(h->tb, h->ring)),
+                                     smem_optin),
                     "cudaFuncSetAttribute");
     if (rc) return rc;
     int per_sm = 0;
@@ -2036,8 +2098,25 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     int G = static_cast<int>(std::min<int64_t>(wmax, std::max<int64_t>(2, (nnz + 16383) / 16384)));
     G = std::max(G, 2);
     if (h->pi) G = wmax;  // the partitioned-inverse chain wants every SM
-    if (h->ring) G = std::min(wmax, std::max(G, 1 + 2 * h->remote_max));  // room for remote helpers
+    if (h->ring && !h->bs) G = std::min(wmax, std::max(G, 1 + 2 * h->remote_max));  // room for remote helpers
     if (const char* env = std::getenv("DSGPU_GRID")) G = std::max(2, std::min(wmax, std::atoi(env)));
+    if (h->bs) {
+      // far-worker CTAs of the blocked sweeps: workers 1.. of the grid (worker 0
+      // posts the requests), split between the blocks; a block without far
+      // entries (everything within the y ring) needs none
+      int want[2] = {32, 8};
+      if (const char* env = std::getenv("DSGPU_FAR_A")) want[0] = std::max(0, std::atoi(env));
+      if (const char* env = std::getenv("DSGPU_FAR_Q")) want[1] = std::max(0, std::atoi(env));
+      for (int b = 0; b < 2; ++b)
+        if (P.blk[b].kind != DSGPU_BLOCK_PCG_IC0 || P.blk[b].bfwd.nnz_far + P.blk[b].bbwd.nnz_far == 0) want[b] = 0;
+      if (!std::getenv("DSGPU_GRID")) G = std::min(wmax, std::max(G, 1 + want[0] + want[1]));
+      while (want[0] + want[1] > G - 1) {  // small grids: shrink the larger share first
+        int& w = want[0] >= want[1] ? want[0] : want[1];
+        --w;
+      }
+      h->far_ctas[0] = want[0];
+      h->far_ctas[1] = want[1];
+    }
     h->grid = n_srv + G;  // G = worker CTAs below
     // K-row partition balanced by nnz + per-row vector work
     h->row_start.assign(G + 1, 0);
@@ -2097,6 +2176,25 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         d.pim.set[1] = h->alloc<double>(static_cast<size_t>(4) * pp.n);
         const std::string e = pi_fill(pp, hb.lrp.data(), hb.lci.data(), hb.lv.data(), coef, h->stream);
         if (!e.empty()) throw std::runtime_error("partitioned-inverse setup: " + e);
+      } else if (hb.kind == DSGPU_BLOCK_PCG_IC0 && h->bs) {
+        d.bs = 1;
+        d.bs_ns = h->bs_ns;
+        const int G_max = std::max(hb.bfwd.G, hb.bbwd.G);
+        h->levels[2 * b] = hb.bfwd.G;
+        h->levels[2 * b + 1] = hb.bbwd.G;
+        d.bfwd = upload_bsweep(h, hb.bfwd);
+        d.bbwd = upload_bsweep(h, hb.bbwd);
+        d.y = h->alloc<double>(hb.n + 1);
+        d.bb = h->alloc<double>(hb.n + 1);
+        cudaMemset(d.y, 0, sizeof(double) * (hb.n + 1));
+        cudaMemset(d.bb, 0, sizeof(double) * (hb.n + 1));
+        d.fpsum = h->alloc<double>(static_cast<size_t>(G_max) * kBsB);
+        d.fflag = h->alloc<unsigned>(static_cast<size_t>(G_max));
+        d.gprog = h->alloc<unsigned long long>(1);
+        cudaMemset(d.fflag, 0, sizeof(unsigned) * G_max);
+        cudaMemset(d.gprog, 0, sizeof(unsigned long long));
+        d.n_remote = h->far_ctas[b];
+        d.remote_cta0 = 1 + (b == 1 ? h->far_ctas[0] : 0);  // worker units (Ctx::remote_rank)
       } else if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
         if (h->exact) {
           d.fwd = upload_sweep(h, hb.fwd);
@@ -2123,15 +2221,18 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         d.remote_cta0 = n_srv + 1 + b * d.n_remote;  // workers, after the lead worker
       }
       d.r = h->alloc<double>(hb.n);
-      d.z = h->alloc<double>(hb.n);
+      d.z = h->alloc<double>(hb.n + 1);  // z[n] = 0: the padding column of the far lists
+      cudaMemset(d.z, 0, sizeof(double) * (hb.n + 1));
       d.q = h->alloc<double>(hb.n);
       d.p0 = h->alloc<double>(hb.n);
       d.p1 = h->alloc<double>(hb.n);
     }
-    h->levels[0] = P.blk[0].fwd.n_levels;
-    h->levels[1] = P.blk[0].bwd.n_levels;
-    h->levels[2] = P.blk[1].fwd.n_levels;
-    h->levels[3] = P.blk[1].bwd.n_levels;
+    if (!h->bs) {
+      h->levels[0] = P.blk[0].fwd.n_levels;
+      h->levels[1] = P.blk[0].bwd.n_levels;
+      h->levels[2] = P.blk[1].fwd.n_levels;
+      h->levels[3] = P.blk[1].bwd.n_levels;
+    }
     h->nnz_k = nnz;
     {
       int64_t s = 0;
@@ -2139,7 +2240,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       h->nnz_a = s;
     }
     for (int b = 0; b < 2; ++b)
-      h->nnz_l[b] = P.blk[b].kind == DSGPU_BLOCK_PCG_IC0 ? P.blk[b].lrp.back() : 0;
+      h->nnz_l[b] = P.blk[b].kind == DSGPU_BLOCK_PCG_IC0 ? L_nnz[b] : 0;
     h->nnz_q = P.blk[1].rp.empty() ? 0 : P.blk[1].rp.back();
     a.perm_u = h->upload(P.blk[0].perm);
     a.perm_p = h->upload(P.blk[1].perm);
@@ -2328,7 +2429,8 @@ static cudaError_t launch_ic(dsgpu_handle* h, DBlock B, const double* r) {
                                        params, h->smem, h->stream);
   }
   unsigned id = h->next_launch_id();
-  const int R = B.n_remote > 0 ? std::min(h->sms - 1, std::max(B.n_remote, 2 * h->remote_max)) : 0;
+  const int R = B.bs ? std::min(h->sms - 1, B.n_remote)
+                     : (B.n_remote > 0 ? std::min(h->sms - 1, std::max(B.n_remote, 2 * h->remote_max)) : 0);
   B.remote_cta0 = 1;
   B.n_remote = R;
   if (R == 0) {

@@ -15,6 +15,8 @@ with k = ones (the identity map's kernel), as SURVEY.md §8(c) prescribes.
   c3_rand_k3_n256.npz  C3: 2D k'=3 256x256, f_u ~ U[-1,1] seed 1234, IC0-PCG(A,Q),
                        outer 1e-8, inner 1e-1
   c4_psi3d_k2_n32.npz  C4: 3D k'=2 32^3 psi-MMS, IC0-PCG(A,Q), outer 1e-8, inner 1e-1
+  c5data_rand3d_k2_n48.npz  C5's data at 48^3: f_u ~ U[-1,1] seed 42, outer 1e-6, inner 1e-1
+                       (u, p stored as float64; 490k unknowns)
 
 C3 does not reach 1e-8 in the reference: with the relaxed (1e-1) inner CG the
 block preconditioner varies between applications and MINRES stagnates near
@@ -45,6 +47,10 @@ CASES = {
                outer=1e-8, inner=1e-1, max_iter=150),
     "c4": dict(file="c4_psi3d_k2_n32.npz", case="psi-mms", k=2, n=32, dim=3, seed=0,
                outer=1e-8, inner=1e-1, max_iter=400),
+    # C5's data (3D k'=2, f_u ~ U[-1,1] seed 42, outer 1e-6) at 48^3: the
+    # largest C5-shaped system whose reference solve fits the -m gpu budget
+    "c5_48": dict(file="c5data_rand3d_k2_n48.npz", case="random", k=2, n=48, dim=3, seed=42,
+                  outer=1e-6, inner=1e-1, max_iter=400),
 }
 
 

@@ -329,6 +329,39 @@ def test_c5_data_small_vs_reference(gpu, port):
     check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-6, 1e-1), 1e-6)
 
 
+def test_c5_data_48_vs_reference(gpu):
+    """BASELINE config 5's data (3D k'=2, f_u ~ U[-1,1] seed 42, outer 1e-6,
+    inner 1e-1) at 48^3 (492,500 unknowns, nnz(L_A) 90.5M, ring-mode sweeps with
+    remote helpers) against the reference's own solve of the identical system
+    (tests/golden/make_golden_large.py c5_48): rel-L2 <= 1e-8, outer iterations
+    +-2, inner means, the Euclidean residual history, convergence to 1e-6, and
+    the true residual through the device saddle apply. The preconditioner setup
+    uses the device IC(0) factor (bit-identical to the reference's)."""
+    host, solver = gpu
+    g = load_golden("c5data_rand3d_k2_n48.npz")
+    s = host.assemble("random", 2, 48, dim=3, seed=42)
+    assert [s.n_u, s.n_p, s.A.nnz, s.B.nnz, s.Q.nnz] == g["sizes"].tolist()
+    top = solver.prepare_block(s.A, solver.BLOCK_PCG_IC0, ic0_on_gpu=True)
+    bot = solver.prepare_block(s.Q_nu, solver.BLOCK_PCG_IC0, ic0_on_gpu=True)
+    gs = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)", top=top, bottom=bot)
+    sol = gs.solve(options=solver.SolverOptions(outer_tol=1e-6, inner_tol=1e-1, max_iter=400))
+    x = np.concatenate([sol.u, sol.p])
+    xr = np.concatenate([g["u"], g["p"]])
+    rel = np.linalg.norm(x - xr) / np.linalg.norm(xr)
+    assert rel <= 1e-8, rel
+    assert abs(sol.report.iterations - int(g["meta"][0])) <= 2, (sol.report.iterations, g["meta"])
+    assert abs(sol.report.mean_inner_top - g["meta"][2]) < 0.2
+    assert abs(sol.report.mean_inner_bottom - g["meta"][3]) < 0.2
+    he, hr = sol.report.euclid_history, g["he"]
+    m = min(len(he), len(hr))
+    assert np.all(np.abs(he[:m] - hr[:m]) <= 1e-8 * hr[:m])
+    assert sol.report.converged and sol.report.relres_e <= 1e-6
+    b = np.concatenate([s.f, np.zeros(s.n_p)])
+    true = np.linalg.norm(b - gs.apply(x)) / np.linalg.norm(b)
+    assert abs(true - sol.report.relres_e) <= 1e-3 * sol.report.relres_e + 1e-12
+    gs.close()
+
+
 @pytest.mark.skipif(not __import__("os").environ.get("DSGPU_TEST_C5"),
                     reason="C5 at full size: ~20 min of host setup and ~150 GB host RAM; "
                            "set DSGPU_TEST_C5=1")
