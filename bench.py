@@ -1,10 +1,14 @@
 """Benchmark: MINRES + IC(0) block-preconditioned Stokes solve on B200.
 
-Workload (BASELINE.json configs[1], "C2"): 2D unit-square Stokes, k'=2
-divergence-conforming B-splines on 64x64 elements, psi-MMS forcing, solved
-with IC0-PCG(A,Q) (RCM + IC(0) preconditioned inner CG on A and on Q_nu) at
-outer tolerance 1e-8, once with relaxed inner CG (1e-1) and once with
-exact-ish inner CG (1e-8). One bench step = both solves.
+Headline workload (BASELINE.json configs[3], "C4"): 3D unit-cube Stokes, k'=2
+divergence-conforming B-splines on 32^3 elements (153,748 unknowns, nnz(K) =
+84.9M: 1.0 GB per saddle SpMV, HBM-resident), psi-MMS forcing, IC0-PCG(A,Q)
+(RCM + IC(0) preconditioned inner CG on A and on Q_nu), outer 1e-8, inner
+1e-1. One bench step = one solve. It is the largest BASELINE configuration
+whose GPU arm AND bounded reference arm fit the default run's few minutes
+(C5, 96^3, needs ~20 min of host assembly/setup: --workload c5). BASELINE
+configs[1] (C2: 2D 64x64, the relaxed + exact-ish solve pair, L2-resident) is
+measured in the same run and reported under "extra".
 
 metric  : MINRES outer iterations per second (whole job, all ranks)
 value   : device-resident solves (inputs already in HBM), CUDA-event time of
@@ -15,9 +19,9 @@ roofline: dominant kernel = the persistent MINRES kernel; algorithmic bytes
           per SURVEY.md §8(d) with the counted inner iterations
 --impl reference: the unmodified reference (oracle/_ref, built from
           /root/reference/proj/src) on the host CPU, same workload.
-Multi-GPU (--gpus N under torchrun): the C2 solve does not shard usefully
-(replicated triangular sweeps); each rank runs an
-independent replica ("replicas only", weak scaling), max-over-ranks timing.
+Multi-GPU (--gpus N under torchrun): each rank runs an independent replica of
+the solve (weak scaling), max-over-ranks timing; the row-partitioned data
+plane is described in DESIGN.md.
 """
 from __future__ import annotations
 
@@ -50,16 +54,29 @@ WORKLOADS = {
     "c4": dict(case="psi-mms", k=2, n=32, dim=3, seed=0, strategy="IC0-PCG(A,Q)",
                outer=1e-8, inners=(1e-1,), cpu_max_iter=12,
                label="C4: 3D k'=2 32^3 psi-MMS, IC0-PCG(A,Q), outer 1e-8, inner 1e-1"),
+    # C5's data at 48^3 (the reference-pinned -m gpu test size) and C5 itself
+    # (96^3: ~10 min of native assembly + ~5 min of setup before the first step)
+    "c5_48": dict(case="random", k=2, n=48, dim=3, seed=42, strategy="IC0-PCG(A,Q)",
+                  outer=1e-6, inners=(1e-1,), cpu_max_iter=4,
+                  label="C5 data at 48^3: 3D k'=2 U[-1,1] seed 42, IC0-PCG(A,Q), outer 1e-6, inner 1e-1"),
+    "c5": dict(case="random", k=2, n=96, dim=3, seed=42, strategy="IC0-PCG(A,Q)",
+               outer=1e-6, inners=(1e-1,), cpu_max_iter=1,
+               label="C5: 3D k'=2 96^3 U[-1,1] seed 42, IC0-PCG(A,Q), outer 1e-6, inner 1e-1"),
 }
-METRIC = "MINRES outer iterations/s (time-to-solution of the BASELINE C2 solve pair)"
+DEFAULT_WORKLOAD = "c4"
+EXTRA_WORKLOADS = ("c2",)  # measured after the headline, reported under "extra"
 
 
 def metric_for(workload: str) -> str:
-    """The headline metric (C2, the default workload) keeps its exact name; the
-    other workloads name their own BASELINE config."""
-    if workload == "c2":
-        return METRIC
-    return f"MINRES outer iterations/s (time-to-solution of the BASELINE {workload.upper()} solve)"
+    name = {"c2": "C2 solve pair", "c5_48": "C5-data 48^3 solve"}.get(workload, f"{workload.upper()} solve")
+    return f"MINRES outer iterations/s (time-to-solution of the BASELINE {name})"
+
+
+def workload_config(W) -> dict:
+    """What the workload IS (identical in the GPU and the reference arm)."""
+    return {"workload": W["label"], "case": W["case"], "dim": W["dim"], "k_prime": W["k"],
+            "n_elem": W["n"], "strategy": W["strategy"], "outer_tol": W["outer"],
+            "inner_tols": list(W["inners"]), "max_iter": W.get("max_iter", 20000)}
 
 
 def dist_env():
@@ -77,21 +94,23 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def measured_traffic(label: str):
-    """DRAM bytes (read + write) of the dominant kernel per step, from a
-    committed ncu capture of tools/minres_profile.py (profiles/
-    r01_minres_traffic*.json; all launches of one step summed), or None when
-    no capture matches this workload."""
+def measured_traffic(label: str, ic0_mode: str):
+    """(DRAM bytes read + written by the dominant kernel per step, source) from
+    the committed ncu capture of this workload AND this IC(0) apply mode
+    (profiles/r02_minres_traffic*.json, written by tools/minres_profile.py with
+    the commit it was captured on), else (None, None): ncu cannot run inside
+    the timed bench, and a capture of another kernel variant is not this run's
+    traffic."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_minres_traffic*.json"))):
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r02_minres_traffic*.json"))):
         try:
             with open(path) as fh:
                 t = json.load(fh)
-            if t.get("workload") == label:
-                return float(t["dram_bytes_per_step"])
+            if t.get("workload") == label and t.get("ic0_mode") == ic0_mode:
+                return float(t["dram_bytes_per_step"]), f"{os.path.basename(path)} @ {t.get('commit', '?')}"
         except Exception:
             continue
-    return None
+    return None, None
 
 
 class ClockSampler:
@@ -164,20 +183,24 @@ def algorithmic_bytes(info: dict, rep, outer_iters: int) -> float:
             + rep.apps_bottom * (S_ICQ + 48 * n_p) + rep.inner_bottom * (S_Q + S_ICQ + 72 * n_p))
 
 
-def run_ours(args, world, rank, local):
+def measure(tag, args, world, local, dist, full: bool):
+    """Device-timed and end-to-end runs of one workload; `full` adds the
+    per-kernel microbenchmarks and the roofline of the headline workload."""
     import torch
     from paper_1309_5048_b200 import host, solver
 
-    W = WORKLOADS[args.workload]
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
+    W = WORKLOADS[tag]
     t0 = time.perf_counter()
-    g = solver.GpuStokesSolver(s, W["strategy"], device=local)
-    setup_s = time.perf_counter() - t0
+    s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
+    assemble_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tk, bk = solver.STRATEGIES[W["strategy"]]
+    top = solver.prepare_block(s.A, tk, ic0_on_gpu=True)       # RCM, permute (host) + IC(0) (device)
+    bot = solver.prepare_block(s.Q_nu, bk, ic0_on_gpu=True)
+    precond_setup_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g = solver.GpuStokesSolver(s, W["strategy"], device=local, top=top, bottom=bot)
+    device_setup_s = time.perf_counter() - t0
     info = g.info()
     opts = [solver.SolverOptions(outer_tol=W["outer"], inner_tol=t,
                                  max_iter=W.get("max_iter", 20000)) for t in W["inners"]]
@@ -188,23 +211,17 @@ def run_ours(args, world, rank, local):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step_device():
-        reps = []
-        for o in opts:
-            reps.append(g.solve_device(d_f.data_ptr(), d_u.data_ptr(), d_p.data_ptr(), o))
-        return reps
+        return [g.solve_device(d_f.data_ptr(), d_u.data_ptr(), d_p.data_ptr(), o) for o in opts]
 
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    dev_ms = 0.0
-    iters = 0
-    launches = 0
-    last = None
+    dev_ms, iters, launches, last = 0.0, 0, 0, None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            flush.fill_(1.0)  # L2 flush between steps (256 MiB > 126 MB L2)
+            flush.fill_(1.0)  # L2 flush between steps (256 MiB write > 126 MB L2)
             torch.cuda.synchronize()
             reps = step_device()
             torch.cuda.synchronize()
@@ -215,16 +232,10 @@ def run_ours(args, world, rank, local):
     dev_ms, job_iters = reduce_over_ranks(dist, dev, dev_ms, iters)
     if dist:
         dist.barrier()
-    ms_per_step = dev_ms / args.steps
-    value = job_iters / (dev_ms * 1e-3)
-
     # ---- e2e: host buffers through the C ABI (pinned), wall clock ---------
     f_pin = torch.from_numpy(s.f.copy()).pin_memory()
     f_np = f_pin.numpy()
-    e2e_s = 0.0
-    e2e_iters = 0
-    if dist:
-        dist.barrier()
+    e2e_s, e2e_iters = 0.0, 0
     for _ in range(args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
@@ -235,73 +246,100 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         e2e_s += time.perf_counter() - t1
     e2e_ms, job_e2e_iters = reduce_over_ranks(dist, dev, e2e_s * 1e3, e2e_iters)
-    e2e_value = job_e2e_iters / (e2e_ms * 1e-3)
+    out = {
+        "metric": metric_for(tag),
+        "value": job_iters / (dev_ms * 1e-3),
+        "unit": "iter/s",
+        "ms_per_step": dev_ms / args.steps,
+        "config": workload_config(W),
+        "run": {"n_u": info["n_u"], "n_p": info["n_p"], "nnz_K": info["nnz_K"], "nnz_L_A": info["nnz_L_A"],
+                "outer_iterations_per_step": iters // args.steps,
+                "mean_inner_A": [round(r.mean_inner_top, 3) for r in last],
+                "mean_inner_Q": [round(r.mean_inner_bottom, 3) for r in last],
+                "time_to_solution_ms": [round(r.wall_seconds * 1e3, 3) for r in last],
+                "converged": [bool(r.converged) for r in last],
+                "setup_s": {"assemble_host": round(assemble_s, 2),
+                            "rcm_permute_host_ic0_device": round(precond_setup_s, 2),
+                            "plan_and_upload": round(device_setup_s, 2)},
+                "time_to_solution_incl_precond_setup_s": round(
+                    precond_setup_s + device_setup_s + sum(r.wall_seconds for r in last), 3),
+                "grid_ctas": info["grid_ctas"], "ic0_apply": info["ic0_mode"],
+                "far_ctas": [info["far_ctas_A"], info["far_ctas_Q"]],
+                "l2": "flushed between steps (256 MiB write)", "parallelism": f"replicas x{world}"},
+        "e2e": {"value": job_e2e_iters / (e2e_ms * 1e-3), "unit": "iter/s",
+                "h2d_bytes_per_step": 8 * s.n_u * len(opts),
+                "d2h_bytes_per_step": 8 * (s.n_u + s.n_p) * len(opts)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if full:
+        # ---- roofline of the dominant kernel (the persistent MINRES kernel) ----
+        peak, peak_kind = measured_peak()
+        bytes_step = sum(algorithmic_bytes(info, r, r.iterations) for r in last)
+        kern_ms = sum(r.wall_seconds for r in last) * 1e3
+        achieved = bytes_step / (kern_ms * 1e-3) / 1e9
+        traffic, traffic_src = measured_traffic(W["label"], info["ic0_mode"])
+        out["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                           "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                           "peak_kind": peak_kind, "kernel": "minres_kernel (persistent, cooperative)",
+                           "algorithmic_bytes_per_step": bytes_step}
+        # per-kernel microbenchmarks on device-resident data (same launch path)
+        try:
+            n = info["n_u"] + info["n_p"]
+            spmv_ms, spmva_ms = g.time_kernel(0, 50), g.time_kernel(3, 50)
+            ic_ms, icq_ms = g.time_kernel(1, 10), g.time_kernel(2, 10)
+            ic_bytes = 24 * info["nnz_L_A"] + 40 * info["n_u"]
+            out["kernels"] = {
+                "saddle_spmv": {"ms": spmv_ms, "GB/s": (12 * info["nnz_K"] + 20 * n) / (spmv_ms * 1e-3) / 1e9},
+                "A_spmv": {"ms": spmva_ms,
+                           "GB/s": (12 * info["nnz_A"] + 20 * info["n_u"]) / (spmva_ms * 1e-3) / 1e9},
+                "ic0_apply_A": {"ms": ic_ms, "GB/s": ic_bytes / (ic_ms * 1e-3) / 1e9,
+                                "frac_of_peak": ic_bytes / (ic_ms * 1e-3) / 1e9 / peak,
+                                "mode": info["ic0_mode"], "dependent_steps": info["ic0_steps_A"],
+                                "us_per_step": ic_ms * 1e3 / max(1, info["ic0_steps_A"])},
+                "ic0_apply_Q": {"ms": icq_ms},
+            }
+            # fused MINRES vector pass + ||res|| reduction, stand-alone at C5's n
+            # (3,735,956 rows, 359 MB per pass: HBM-resident)
+            n5 = 3735956
+            vec_ms, _ = solver.time_vector_update(n5, reps=20, device=local)
+            out["kernels"]["minres_vector_pass_c5_n"] = {"ms": vec_ms, "rows": n5,
+                                                         "GB/s": 96.0 * n5 / (vec_ms * 1e-3) / 1e9}
+        except Exception as e:
+            out["kernels"] = {"error": str(e)[:100]}
+    g.close()
+    del g, top, bot, s, flush
+    torch.cuda.empty_cache()
+    return out
 
-    # ---- roofline of the dominant kernel (the persistent MINRES kernel) ----
-    peak, peak_kind = measured_peak()
-    bytes_step = 0.0
-    kern_ms = 0.0
-    for r in last:
-        bytes_step += algorithmic_bytes(info, r, r.iterations)
-        kern_ms += r.wall_seconds * 1e3
-    achieved = bytes_step / (kern_ms * 1e-3) / 1e9
-    # per-kernel microbenchmarks on device-resident data (same launch path)
-    kernels = {}
-    try:
-        spmv_ms = g.time_kernel(0, 50)
-        ic_ms = g.time_kernel(1, 5)
-        n = info["n_u"] + info["n_p"]
-        kernels = {
-            "saddle_spmv": {"ms": spmv_ms, "GB/s": (12 * info["nnz_K"] + 20 * n) / (spmv_ms * 1e-3) / 1e9},
-            "ic0_apply_A": {"ms": ic_ms, "GB/s": (24 * info["nnz_L_A"] + 40 * info["n_u"]) / (ic_ms * 1e-3) / 1e9,
-                            "levels": info["levels_fwd_A"] + info["levels_bwd_A"],
-                            "us_per_level": ic_ms * 1e3 / (info["levels_fwd_A"] + info["levels_bwd_A"])},
-        }
-        # fused MINRES vector pass + ||res|| reduction, stand-alone at C5's n
-        # (3,735,956 rows, 359 MB per pass: HBM-resident, unlike C2's vectors)
-        n5 = 3735956
-        vec_ms, _ = solver.time_vector_update(n5, reps=20, device=local)
-        kernels["minres_vector_pass_c5_n"] = {"ms": vec_ms, "rows": n5,
-                                              "GB/s": 96.0 * n5 / (vec_ms * 1e-3) / 1e9}
-    except Exception as e:
-        kernels = {"error": str(e)[:100]}
 
+def run_ours(args, world, rank, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    head = measure(args.workload, args, world, local, dist, full=True)
+    extra = {}
+    if not args.no_extra and args.workload == DEFAULT_WORKLOAD:
+        for tag in EXTRA_WORKLOADS:
+            e = measure(tag, args, world, local, dist, full=False)
+            extra[tag] = {k: e[k] for k in ("metric", "value", "unit", "ms_per_step", "config", "run", "e2e")}
     result = None
     if rank == 0:
+        W = WORKLOADS[args.workload]
         cpu = cpu_baseline(args, W) if (world == 1 and not args.no_cpu_baseline) else None
         result = {
-            "metric": metric_for(args.workload),
-            "value": value,
-            "unit": "iter/s",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms_per_step,
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "f64",
-            "data": "synthetic (BASELINE psi-MMS forcing, native assembly bit-identical to the reference)",
-            "config": {"workload": W["label"], "n_u": info["n_u"], "n_p": info["n_p"],
-                       "nnz_K": info["nnz_K"], "nnz_L_A": info["nnz_L_A"],
-                       "outer_iterations_per_step": iters // args.steps,
-                       "mean_inner_A": [round(r.mean_inner_top, 3) for r in last],
-                       "mean_inner_Q": [round(r.mean_inner_bottom, 3) for r in last],
-                       "time_to_solution_ms": [round(r.wall_seconds * 1e3, 3) for r in last],
-                       "setup_s": round(setup_s, 3), "grid_ctas": info["grid_ctas"],
-                       "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": f"replicas x{world}"},
-            "e2e": {"value": e2e_value, "unit": "iter/s",
-                    "h2d_bytes_per_step": 8 * s.n_u * len(opts),
-                    "d2h_bytes_per_step": 8 * (s.n_u + s.n_p) * len(opts)},
-            "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": measured_traffic(W["label"]),
-                         "peak_kind": peak_kind, "kernel": "minres_kernel (persistent, cooperative)",
-                         "algorithmic_bytes_per_step": bytes_step},
-            "kernels": kernels,
-            "clocks": clk.summary(),
-            "cpu_baseline": cpu,
+            "metric": head["metric"], "value": head["value"], "unit": "iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE forcing / seeded RHS, native assembly; the 2D assembly is "
+                    "bit-identical to the reference's, the 3D blocks follow the same rule)",
+            "config": head["config"], "run": head["run"], "e2e": head["e2e"],
+            "gpu_launches": head["gpu_launches"], "roofline": head["roofline"],
+            "kernels": head["kernels"], "clocks": head["clocks"], "cpu_baseline": cpu, "extra": extra,
         }
         print(json.dumps(result), flush=True)
     if dist:
@@ -314,17 +352,28 @@ def cpu_runner(W):
     """run(inner_tol, max_iter) -> result dict of the reference solve of the
     workload on this host: oracle/_ref (the unmodified reference; its own
     assembly in 2D, the native 3D blocks through ref_from_csr since the
-    reference has no 3D code) or, when it is not built, the C restatement."""
+    reference has no 3D code) or, when it is not built, the C restatement. The
+    reference's make_strategy (RCM, permute, IC(0): precond.cpp:161-193) runs
+    once per inner tolerance and is reused by every timed solve."""
     from oracle import CSR, RefLib, ref_available
     from paper_1309_5048_b200 import host
     c = lambda m: CSR(m.n_rows, m.n_cols, m.row_ptr, m.cols, m.vals)  # noqa: E731
     if ref_available():
+        from oracle.oracle import RefPrecond
         R = RefLib()
         if W["dim"] == 2:
             rs = R.assemble(W["case"], W["k"], W["n"], seed=W["seed"])
         else:
             s = host.assemble(W["case"], W["k"], W["n"], dim=W["dim"], seed=W["seed"])
             rs = R.from_csr(c(s.A), c(s.B), c(s.Q), s.f, nu=s.nu)
+        if W["strategy"] not in ("IC0-PCG(A)+Diag(Q)",) and hasattr(R.L, "ref_precond_make"):
+            pre = {}
+
+            def run(t, mi):
+                if t not in pre:
+                    pre[t] = RefPrecond(rs, W["strategy"], t)
+                return pre[t].solve(W["outer"], max_iter=mi)
+            return run, "reference"
         return (lambda t, mi: rs.solve(W["strategy"], W["outer"], t, max_iter=mi)), "reference"
     from oracle import PortLib
     P = PortLib()
@@ -337,8 +386,8 @@ def cpu_sample_note(W, reps):
     cap = W.get("cpu_max_iter")
     what = (f"the first {cap} outer iterations of each solve" if cap else
             f"the {len(W['inners'])}-solve step")
-    return (f"{reps} x {what} (MINRES time only, setup excluded; the reference solver is "
-            "single-threaded)")
+    return (f"{reps} x {what} (MINRES time only, preconditioner setup excluded; the reference "
+            "solver is single-threaded)")
 
 
 def cpu_baseline(args, W):
@@ -348,7 +397,7 @@ def cpu_baseline(args, W):
         cap = W.get("cpu_max_iter", W.get("max_iter", 20000))
         iters, secs, reps = 0, 0.0, 0
         t_start = time.perf_counter()
-        while reps < 3 and time.perf_counter() - t_start < args.cpu_budget_s:
+        while reps < 3 and (reps == 0 or time.perf_counter() - t_start < args.cpu_budget_s):
             for t in W["inners"]:
                 r = run(t, cap)
                 iters += r["iterations"]
@@ -367,8 +416,8 @@ def run_reference(args, world, rank):
     W = WORKLOADS[args.workload]
     run, kind = cpu_runner(W)
     cap = W.get("cpu_max_iter", W.get("max_iter", 20000))
-    for _ in range(args.warmup):
-        for t in W["inners"][:1]:
+    for _ in range(min(args.warmup, 1)):  # one warm-up solve builds the preconditioner
+        for t in W["inners"]:
             run(t, cap)
     iters, secs = 0, 0.0
     for _ in range(args.steps):
@@ -381,7 +430,8 @@ def run_reference(args, world, rank):
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": W["label"], "parallelism": "1 host core (serial reference)"},
+           "config": workload_config(W),
+           "run": {"parallelism": "1 host core (serial reference)", "kind": kind},
            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": kind,
                             "sample": cpu_sample_note(W, args.steps)},
            "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
@@ -396,8 +446,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     args = ap.parse_args()
     world, rank, local = dist_env()

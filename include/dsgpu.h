@@ -160,8 +160,12 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
 const char* dsgpu_ic0_last_error(void);
 
 /* Sizes of the device-resident problem (for roofline accounting):
- * info[0..11] = n_u, n_p, nnz_K, nnz_Aperm, nnz_L_A, nnz_L_Q, nnz_Qperm,
- * levels_fwd_A, levels_bwd_A, levels_fwd_Q, levels_bwd_Q, grid_ctas. */
+ * info[0..15] = n_u, n_p, nnz_K, nnz_Aperm, nnz_L_A, nnz_L_Q, nnz_Qperm,
+ * dependent steps of the forward / backward sweep of A, of Q (16-row groups
+ * with the blocked sweeps, dependency levels otherwise), grid_ctas, IC(0)
+ * apply mode (0 exact column order, 1 staged level sweeps, 2 partitioned
+ * inverse, 3 blocked sweeps), dependent steps of one velocity IC(0) apply,
+ * far-worker CTAs of the A and Q block. */
 int dsgpu_info(const dsgpu_handle* h, int64_t* info);
 
 /* Blocked-sweep plan check (no device): builds the blocked-sweep plan of the
@@ -172,6 +176,17 @@ int dsgpu_info(const dsgpu_handle* h, int64_t* info);
  * and far list, padded mid and far list entries. */
 int dsgpu_debug_bsweep_host(int n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
                             const double* r, double* z, int64_t* stats8);
+
+/* Multi-GPU row partition check (no device): partitions a square operator
+ * (n rows; the first n_u are velocity rows whose first na[i] entries are the A
+ * part, na nullable) over `world` ranks as dsgpu_setup_multi does -- one
+ * contiguous velocity range and one pressure range per rank, each balanced by
+ * nonzeros -- and evaluates y = K x rank by rank: halo gather from the owners'
+ * slices, then the local rows. bounds: 2 (world + 1) ints; halo_counts:
+ * world x world entries (row r: what rank r reads from each source rank). */
+int dsgpu_debug_partition_spmv(int n, int n_u, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                               const int32_t* na, int world, int32_t* bounds, int64_t* halo_counts,
+                               const double* x, double* y);
 
 /* Process-wide sweep diagnostics (summed since the last reset), out32:
  * [0] main-warp cycles, [1] main cycles waiting, [2] groups, [3] abort code,
@@ -187,7 +202,14 @@ int dsgpu_debug_bsweep_host(int n, const int64_t* row_ptr, const int32_t* cols, 
  * (<=0, 1, 2, >=3 groups ahead), [28..29] co-main waits that found the
  * prefix sum / the dependencies not ready, [30..31] 0. */
 int dsgpu_debug_counters(int reset, int64_t* out32);
-/* Persistent-kernel phase diagnostics (cycles): out8 = CTA0 grid-barrier
+/* Blocked-sweep diagnostics, summed since the last reset; all zero unless the
+ * library was built with -DDSGPU_DIAG (make diag; the production kernels carry
+ * no counters). out16: [0] main-warp cycles, [1] main cycles waiting for c,
+ * [2] for dense-block slots, [3] for the publisher, [4] groups, [5] co-main
+ * cycles waiting for progress, [6] for far sums, [7] co-main cycles, [8]
+ * far-worker cycles waiting for progress, [9] far-worker cycles. */
+int dsgpu_debug_bs_counters(int reset, int64_t* out16);
+/* Persistent-kernel phase diagnostics (cycles; -DDSGPU_DIAG build only): out8 = CTA0 grid-barrier
  * wait, CTA0 IC(0) apply, CTA2 grid-barrier wait, barriers, CTA0 kernel,
  * CTA1 IC(0) apply, 0, 0. */
 int dsgpu_debug_phases(int reset, int64_t* out8);

@@ -31,6 +31,8 @@ struct BsFar {
   int workers;                 // far-worker warps outside the sweep CTA (0: its spare warps)
 };
 
+// Diagnostics exist only in the -DDSGPU_DIAG build (make diag): the production
+// kernels carry no counters, clocks or atomics on their paths.
 #ifdef DSGPU_DIAG
 // [0] main cycles, [1] main cycles waiting for c, [2] for slots, [3] for the
 // publisher, [4] groups, [5] co-main cycles waiting for progress, [6] for far
@@ -219,6 +221,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       if (exact ? v == want_ge : v >= want_ge) break;
       if (sg.expired()) break;
     }
+    asm volatile("" ::: "memory");  // data reads stay behind the flag
   };
 
   if (warp == mainw && G > 0) {
@@ -282,6 +285,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
         wait_int(S.aready + gn % kBsRC, gn, true);
         BS_DIAG(w_c += clock64() - tw;)
       }
+      asm volatile("" ::: "memory");
       c = S.cbuf[(gn % kBsRC) * kBsB + r];
       if (g + 1 - pd >= kBsR - 2) {  // never lap the publisher on the y ring
         BS_DIAG(const long long tw = clock64();)
@@ -315,6 +319,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
         SpinGuard sg(abort_flag);
         while ((prog = *S.progress) < need)
           if (sg.expired()) break;
+        asm volatile("" ::: "memory");
         BS_DIAG(w_p += clock64() - tw;)
       };
       auto chunks = [&](int k0, int k1) {  // mid entries [k0, k1), whole chunks
@@ -421,6 +426,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     while (done < G) {
       const int pnow = *S.progress;
       if (pnow > done) {
+        asm volatile("" ::: "memory");
         for (int g = done + hf; g < pnow; g += 2) {
           const int p = g * kBsB + r;
           if (p < n) __stcg(gx + orig(p), S.ring[(g % kBsR) * kBsB + r]);

@@ -289,6 +289,11 @@ __device__ int g_nowait = 0;
 // [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
 __device__ unsigned long long g_phase_dbg[8];
+#ifdef DSGPU_DIAG
+#define PHASE_DIAG(...) __VA_ARGS__
+#else
+#define PHASE_DIAG(...)
+#endif
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -939,15 +944,15 @@ struct Ctx {
   }
   // grid barrier, then reduce `mask` slots of this epoch into sums[]
   __device__ bool sync_reduce(unsigned mask) {
-    const long long tb0 = clock64();
+    PHASE_DIAG(const long long tb0 = clock64();)
     const bool ok = grid_sync(a.bar, a.bar + 32, abort_flag, static_cast<unsigned>(G));
-    if (threadIdx.x == 0) {
+    PHASE_DIAG(if (threadIdx.x == 0) {
       if (cta == 0) {
         atomicAdd(&g_phase_dbg[0], static_cast<unsigned long long>(clock64() - tb0));
         atomicAdd(&g_phase_dbg[3], 1ull);
       }
       if (cta == 1) atomicAdd(&g_phase_dbg[2], static_cast<unsigned long long>(clock64() - tb0));
-    }
+    })
     if (ok) {
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       if (warp < NSLOT && (mask >> warp) & 1u) {
@@ -1324,7 +1329,7 @@ __device__ void ic_server(const Args& a, int b, double* xs, double* red) {
     __syncthreads();
     const int op = op_sh;
     if (op == IC_OP_EXIT) break;
-    const long long ti0 = clock64();
+    PHASE_DIAG(const long long ti0 = clock64();)
     const unsigned sweep_no = 2 * (seq - 1);
     double rz;
     if (op == IC_OP_S1) {
@@ -1362,7 +1367,7 @@ __device__ void ic_server(const Args& a, int b, double* xs, double* red) {
       m->rz = rz;
       __threadfence();
       st_release(&m->done, seq);
-      atomicAdd(&g_phase_dbg[b == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));
+      PHASE_DIAG(atomicAdd(&g_phase_dbg[b == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));)
     }
   }
 }
@@ -1399,7 +1404,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
   if (PI) pi_prologue();
   Ctx C(a, red, sums, xs_dyn);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long t_kernel0 = clock64();
+  PHASE_DIAG(const long long t_kernel0 = clock64();)
   const int r0 = C.r0, r1 = C.r1;
   long long inner[2] = {0, 0}, apps[2] = {0, 0};
   int iterations = 0, converged = 0, hist_len = 0;
@@ -1585,8 +1590,8 @@ finish:
         a.p_out[a.perm_p[i - a.n_u]] = a.filter ? sub_rn(a.x[i], mul_rn(mean, 1.0)) : a.x[i];
     }
   }
-  if (threadIdx.x == 0 && C.cta == 0)
-    atomicAdd(&g_phase_dbg[4], static_cast<unsigned long long>(clock64() - t_kernel0));
+  PHASE_DIAG(if (threadIdx.x == 0 && C.cta == 0)
+               atomicAdd(&g_phase_dbg[4], static_cast<unsigned long long>(clock64() - t_kernel0));)
   if (writer && !PI)  // release the IC(0) servers
     for (int b = 0; b < 2; ++b)
       if (a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) {
@@ -2589,6 +2594,23 @@ int dsgpu_debug_counters(int reset, int64_t* out32) {
   return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
 }
 
+int dsgpu_debug_bs_counters(int reset, int64_t* out16) {
+#ifdef DSGPU_DIAG
+  unsigned long long v[16] = {};
+  cudaMemcpyFromSymbol(v, g_bs_dbg, sizeof(v));
+  for (int i = 0; i < 16; ++i) out16[i] = static_cast<int64_t>(v[i]);
+  if (reset) {
+    const unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_bs_dbg, z, sizeof(z));
+  }
+  return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
+#else
+  (void)reset;
+  for (int i = 0; i < 16; ++i) out16[i] = 0;
+  return DSGPU_OK;
+#endif
+}
+
 int dsgpu_debug_phases(int reset, int64_t* out8) {
   unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyFromSymbol(v, g_phase_dbg, sizeof(v));
@@ -2625,6 +2647,10 @@ int dsgpu_info(const dsgpu_handle* h, int64_t* info) {
   info[6] = h->nnz_q;
   for (int i = 0; i < 4; ++i) info[7 + i] = h->levels[i];
   info[11] = h->grid;
+  info[12] = h->exact ? 0 : h->bs ? 3 : h->pi ? 2 : 1;
+  info[13] = h->bs ? h->levels[0] + h->levels[1] : h->pi ? h->pi_steps : h->levels[0] + h->levels[1];
+  info[14] = h->far_ctas[0];
+  info[15] = h->far_ctas[1];
   return DSGPU_OK;
 }
 

@@ -318,11 +318,14 @@ class GpuStokesSolver:
         return ms.value
 
     def info(self) -> dict:
-        a = np.zeros(12, np.int64)
+        a = np.zeros(16, np.int64)
         self.L.dsgpu_info(self.h, a)
         keys = ["n_u", "n_p", "nnz_K", "nnz_A", "nnz_L_A", "nnz_L_Q", "nnz_Q", "levels_fwd_A",
-                "levels_bwd_A", "levels_fwd_Q", "levels_bwd_Q", "grid_ctas"]
-        return dict(zip(keys, a.tolist()))
+                "levels_bwd_A", "levels_fwd_Q", "levels_bwd_Q", "grid_ctas", "ic0_mode",
+                "ic0_steps_A", "far_ctas_A", "far_ctas_Q"]
+        d = dict(zip(keys, a.tolist()))
+        d["ic0_mode"] = ("exact", "staged", "partitioned-inverse", "blocked")[d["ic0_mode"]]
+        return d
 
 
 def solve_stokes(system: host.StokesSystem, strategy: str,

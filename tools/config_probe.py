@@ -1,9 +1,9 @@
 """Solve BASELINE configs C3 / C4 on the GPU and record timings + parity.
 
-  python tools/config_probe.py c3 [c4 ...]  [--modes=auto,1,0] [--ic0-gpu]
+  python tools/config_probe.py c3 [c4 ...]  [--modes=bs,legacy,1,0] [--ic0-gpu] [--check-ic0]
 
-Per config and IC(0) apply mode (DSGPU_PI=1 partitioned inverse / 0 staged
-sweeps): native assembly + host setup time, device setup time, two solves
+Per config and IC(0) apply mode (bs: blocked sweeps, the default; legacy: the
+round-1 cost model; DSGPU_PI=1 partitioned inverse / 0 staged level sweeps): native assembly + host setup time, device setup time, two solves
 (first = warm-up), outer iterations, inner means, kernel time, per-kernel
 microbenchmarks, and — when tests/golden/<cfg>.npz exists — rel-L2 against the
 reference's solution and the iteration difference. One JSON line per run.
@@ -70,7 +70,7 @@ def main():
     if os.environ.get("PROBE_MEMGUARD_GB"):
         memguard(float(os.environ["PROBE_MEMGUARD_GB"]))
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    modes = ["1", "0"]
+    modes = ["bs"]
     for a in sys.argv[1:]:
         if a.startswith("--modes="):
             modes = a.split("=", 1)[1].split(",")
@@ -91,9 +91,12 @@ def main():
         if c["golden"] and os.path.exists(os.path.join(ROOT, "tests", "golden", c["golden"])):
             gold = np.load(os.path.join(ROOT, "tests", "golden", c["golden"]))
         for mode in modes:
-            if mode == "auto":  # the setup's own choice (cost model)
-                os.environ.pop("DSGPU_PI", None)
-            else:
+            os.environ.pop("DSGPU_PI", None)
+            os.environ.pop("DSGPU_SWEEP", None)
+            if mode in ("bs", "legacy"):
+                os.environ["DSGPU_SWEEP"] = mode
+            elif mode != "auto":
+                os.environ["DSGPU_SWEEP"] = "legacy"
                 os.environ["DSGPU_PI"] = mode
             out = dict(cfg=tag, pi=mode, n_u=s.n_u, n_p=s.n_p, assemble_s=round(t_asm, 2),
                        host_setup_s=round(t_host, 2), ic0_on_gpu=ic0_gpu)
@@ -103,6 +106,16 @@ def main():
                 out["device_setup_s"] = round(time.time() - t0, 2)
                 out["info"] = g.info()
                 log(f"{tag} pi={mode}: device setup {out['device_setup_s']}s")
+                if "--check-ic0" in sys.argv:  # one velocity apply against the CPU oracle
+                    from oracle import CSR, PortLib
+                    F = top.factor
+                    rv = np.random.default_rng(5).uniform(-1.0, 1.0, F.n_rows)
+                    zr = PortLib().ic0_solve(CSR(F.n_rows, F.n_cols, F.row_ptr, F.cols, F.vals), rv)
+                    zg = g.apply_ic0(0, rv)
+                    out["ic0_apply_rel"] = float(np.linalg.norm(zg - zr) / np.linalg.norm(zr))
+                    log(f"{tag} {mode}: IC(0) apply rel {out['ic0_apply_rel']:.2e}")
+                bs_cnt = np.zeros(16, np.int64)
+                g.L.dsgpu_debug_bs_counters(1, bs_cnt.ctypes.data_as(__import__("ctypes").c_void_p))
                 o = solver.SolverOptions(outer_tol=c["outer"], inner_tol=c["inner"],
                                          max_iter=c.get("max_iter", 20000))
                 sol = g.solve(options=o)
@@ -124,8 +137,15 @@ def main():
                 # true residual through the device saddle apply
                 b = np.concatenate([s.f, np.zeros(s.n_p)])
                 out["true_relres"] = float(np.linalg.norm(b - g.apply(x)) / np.linalg.norm(b))
+                g.L.dsgpu_debug_bs_counters(1, bs_cnt.ctypes.data_as(__import__("ctypes").c_void_p))
+                if bs_cnt.any():
+                    out["bs_counters_solves"] = bs_cnt.tolist()
                 for w, nm in [(0, "saddle_spmv"), (1, "ic0_A"), (2, "ic0_Q"), (3, "spmv_A")]:
                     out["us_" + nm] = round(g.time_kernel(w, 20) * 1e3, 2)
+                    if w == 1:
+                        g.L.dsgpu_debug_bs_counters(1, bs_cnt.ctypes.data_as(__import__("ctypes").c_void_p))
+                        if bs_cnt.any():
+                            out["bs_counters_21_applies_A"] = bs_cnt.tolist()
                 if gold is not None:
                     xr = np.concatenate([gold["u"], gold["p"]])
                     out["relL2_vs_ref"] = float(np.linalg.norm(x - xr) / np.linalg.norm(xr))
