@@ -140,10 +140,14 @@ struct HostPlan {
   int n_u = 0, n_p = 0, n = 0;
   // K' = diag(P_A,P_Q) K diag(P_A,P_Q)^T: velocity rows = [A' | Bt'] (A'
   // entries first, k_na per row), pressure rows = [B'].
+  // 128-bit-load layout: every row part ([A'], [Bt'], [B']) is padded to a
+  // multiple of 4 entries (pad: the row's own column, value 0), so k_rp / k_na
+  // count padded entries; nnz_* keep the true counts.
   std::vector<int64_t> k_rp;
   std::vector<int32_t> k_ci;
   std::vector<double> k_v;
   std::vector<int32_t> k_na;
+  int64_t nnz_k = 0, nnz_a = 0, nnz_q = 0;
   HostBlock blk[2];
   bool filter = false;
   std::vector<double> qk;  // Q 1 in the pressure block ordering

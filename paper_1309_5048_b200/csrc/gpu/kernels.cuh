@@ -44,6 +44,35 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
+// ---- CSR SpMV with 128-bit loads --------------------------------------------
+// Device operators are stored with every row (the velocity rows of K': each of
+// the two parts [A' | Bt']) padded to a multiple of 4 entries (pad: the row's
+// own column, value 0), so a row starts on a 16-byte boundary of both the
+// int32 column array and the f64 value array. L lanes (8, 16 or 32, chosen per
+// operator from its mean row length) cooperate on a row: lane `sub` reads
+// entries 4 sub .. 4 sub + 3 as one int4 + two double2 and strides 4 L. The
+// matrix is streamed (evict-first); the gathered vector stays cached.
+template <class X>
+__device__ __forceinline__ double row_partial(const int32_t* ci, const double* v, int len, int sub, int L, X xf) {
+  const int4* cp = reinterpret_cast<const int4*>(ci) + sub;
+  const double2* vp = reinterpret_cast<const double2*>(v) + 2 * sub;
+  double a0 = 0.0, a1 = 0.0;
+  for (int k = 4 * sub; k < len; k += 4 * L, cp += L, vp += 2 * L) {
+    const int4 c = __ldcs(cp);
+    const double2 p = __ldcs(vp), q = __ldcs(vp + 1);
+    a0 = fma(p.x, xf(c.x), a0);
+    a1 = fma(p.y, xf(c.y), a1);
+    a0 = fma(q.x, xf(c.z), a0);
+    a1 = fma(q.y, xf(c.w), a1);
+  }
+  return a0 + a1;
+}
+// sum over the L lanes of a row group (L a power of two <= 32); all 32 lanes call it
+__device__ __forceinline__ double group_sum(double v, int L) {
+  for (int o = L >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

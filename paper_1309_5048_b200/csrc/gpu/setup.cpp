@@ -191,18 +191,22 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
     inv[b] = inverse(hb.perm, hb.n, b == 0 ? "perm_A" : "perm_Q");
   }
 
-  // K' rows
+  // K' rows, each part padded to a multiple of 4 entries (128-bit loads)
+  auto pad4 = [](int64_t len) { return (len + 3) / 4 * 4; };
   P.k_rp.assign(P.n + 1, 0);
   P.k_na.assign(n_u, 0);
   for (int r = 0; r < n_u; ++r) {
     const int o = P.blk[0].perm[r];
-    P.k_na[r] = static_cast<int32_t>(A->row_ptr[o + 1] - A->row_ptr[o]);
-    P.k_rp[r + 1] = P.k_rp[r] + P.k_na[r] + (Bt->row_ptr[o + 1] - Bt->row_ptr[o]);
+    P.k_na[r] = static_cast<int32_t>(pad4(A->row_ptr[o + 1] - A->row_ptr[o]));
+    P.k_rp[r + 1] = P.k_rp[r] + P.k_na[r] + pad4(Bt->row_ptr[o + 1] - Bt->row_ptr[o]);
   }
   for (int r = 0; r < n_p; ++r) {
     const int o = P.blk[1].perm[r];
-    P.k_rp[n_u + r + 1] = P.k_rp[n_u + r] + (B->row_ptr[o + 1] - B->row_ptr[o]);
+    P.k_rp[n_u + r + 1] = P.k_rp[n_u + r] + pad4(B->row_ptr[o + 1] - B->row_ptr[o]);
   }
+  P.nnz_a = A->row_ptr[n_u];
+  P.nnz_k = A->row_ptr[n_u] + Bt->row_ptr[n_u] + B->row_ptr[n_p];
+  P.nnz_q = Q_nu->row_ptr[n_p];
   P.k_ci.resize(P.k_rp[P.n]);
   P.k_v.resize(P.k_rp[P.n]);
 #pragma omp parallel
@@ -220,6 +224,10 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
         for (const auto& e : row) {
           P.k_ci[at] = e.first;
           P.k_v[at++] = e.second;
+        }
+        for (; at % 4 != 0; ++at) {  // pad (row starts are multiples of 4)
+          P.k_ci[at] = r;
+          P.k_v[at] = 0.0;
         }
       };
       if (r < n_u) {
@@ -248,7 +256,7 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
       // permuted Q_nu operator for the pressure PCG
       hb.rp.assign(hb.n + 1, 0);
       for (int r = 0; r < hb.n; ++r)
-        hb.rp[r + 1] = hb.rp[r] + (m->row_ptr[hb.perm[r] + 1] - m->row_ptr[hb.perm[r]]);
+        hb.rp[r + 1] = hb.rp[r] + pad4(m->row_ptr[hb.perm[r] + 1] - m->row_ptr[hb.perm[r]]);
       hb.ci.resize(hb.rp[hb.n]);
       hb.v.resize(hb.rp[hb.n]);
       std::vector<std::pair<int32_t, double>> row;
@@ -263,6 +271,10 @@ void build_plan(HostPlan& P, const dsgpu_csr* A, const dsgpu_csr* B, const dsgpu
         for (const auto& e : row) {
           hb.ci[at] = e.first;
           hb.v[at++] = e.second;
+        }
+        for (; at < hb.rp[r + 1]; ++at) {
+          hb.ci[at] = r;
+          hb.v[at] = 0.0;
         }
       }
     }

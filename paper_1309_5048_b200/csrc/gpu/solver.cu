@@ -76,7 +76,8 @@ struct DBlock {
   const int64_t* rp;  // operator rows (block ordering)
   const int32_t* ci;
   const double* v;
-  const int32_t* na;  // top block: A-part length of each K row (nullptr: full row)
+  const int32_t* na;  // top block: (padded) A-part length of each K row (nullptr: full row)
+  int lanes;          // lanes per row of the block SpMV (row_partial)
   const double* dinv;
   DSweep fwd, bwd;    // exact column-order sweeps (bit-identical mode)
   DFlow ffwd, fbwd;   // staged sweeps (production)
@@ -127,6 +128,7 @@ struct Args {
   const int32_t* k_ci;
   const double* k_v;
   const int32_t* row_start;  // G + 1
+  int k_lanes;               // lanes per row of the saddle SpMV (row_partial)
   DBlock blk[2];
   const double* f_in;        // n_u, original order
   const int32_t* perm_u;     // block ordering -> original
@@ -1156,18 +1158,22 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
         const double bt = beta[b];
         const bool first = k == 0;
         double acc_k = 0.0;
-        for (int i = lo + warp; i < hi; i += kWarps) {
+        const int L = B.lanes, sub = lane & (L - 1), ng = kWarps * (32 / L);
+        const int gid = warp * (32 / L) + lane / L;
+        for (int base = lo; base < hi; base += ng) {
+          const int i = base + gid;
+          const bool ok = i < hi;
           const int li = i - B.off;
-          const int64_t s = B.rp[li];
-          const int64_t e = B.na ? s + B.na[li] : B.rp[li + 1];
           double acc = 0.0;
-          for (int64_t kk = s + lane; kk < e; kk += 32) {
-            const int j = B.ci[kk];
-            const double pj = first ? z[j] : add_rn(z[j], mul_rn(bt, po[j]));
-            acc = fma(B.v[kk], pj, acc);
+          if (ok) {
+            const int64_t s = B.rp[li];
+            const int len = B.na ? B.na[li] : static_cast<int>(B.rp[li + 1] - s);
+            acc = row_partial(B.ci + s, B.v + s, len, sub, L, [&](int j) {
+              return first ? z[j] : add_rn(z[j], mul_rn(bt, po[j]));
+            });
           }
-          acc = warp_sum(acc);
-          if (lane == 0) {
+          acc = group_sum(acc, L);
+          if (ok && sub == 0) {
             const double pi = first ? z[li] : add_rn(z[li], mul_rn(bt, po[li]));
             pn[li] = pi;
             B.q[li] = acc;
@@ -1493,13 +1499,19 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
         const double c1 = it >= 2 ? div_rn(-beta, oldb) : 0.0;
         for (int i = r0 + tid; i < r1; i += blockDim.x) a.v[i] = mul_rn(s, y[i]);
         __syncthreads();  // old av consumed above before the new av is written
-        for (int i = r0 + warp; i < r1; i += kWarps) {
-          const int64_t ks = a.k_rp[i], ke = a.k_rp[i + 1];
+        const int L = a.k_lanes, sub = lane & (L - 1), ng = kWarps * (32 / L);
+        const int gid = warp * (32 / L) + lane / L;
+        for (int base = r0; base < r1; base += ng) {
+          const int i = base + gid;
+          const bool ok = i < r1;
           double acc = 0.0;
-          for (int64_t kk = ks + lane; kk < ke; kk += 32)
-            acc = fma(a.k_v[kk], mul_rn(s, y[a.k_ci[kk]]), acc);
-          acc = warp_sum(acc);
-          if (lane == 0) {
+          if (ok) {
+            const int64_t ks = a.k_rp[i];
+            acc = row_partial(a.k_ci + ks, a.k_v + ks, static_cast<int>(a.k_rp[i + 1] - ks), sub, L,
+                              [&](int j) { return mul_rn(s, y[j]); });
+          }
+          acc = group_sum(acc, L);
+          if (ok && sub == 0) {
             a.av[i] = acc;
             const double t = it >= 2 ? add_rn(acc, mul_rn(c1, r1v[i])) : acc;
             spare[i] = t;
@@ -1671,16 +1683,24 @@ IcFn ic_for(int tb, bool ring) {
 }
 
 // y = M x, warp per row; na != nullptr limits each row to its first na[i] entries
+// (padded rows, L lanes per row: row_partial in kernels.cuh; launch with
+// spmv_grid(n_rows, L) CTAs of 256 threads)
 __global__ void spmv_kernel(int n_rows, const int64_t* rp, const int32_t* ci, const double* v,
-                            const int32_t* na, const double* x, double* y) {
-  const int lane = threadIdx.x & 31;
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= n_rows) return;
-  const int64_t s = rp[row], e = na ? s + na[row] : rp[row + 1];
+                            const int32_t* na, const double* x, double* y, int L) {
+  const int lane = threadIdx.x & 31, sub = lane & (L - 1);
+  const int row = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L);
+  const bool ok = row < n_rows;
   double acc = 0.0;
-  for (int64_t k = s + lane; k < e; k += 32) acc = fma(v[k], x[ci[k]], acc);
-  acc = warp_sum(acc);
-  if (lane == 0) y[row] = acc;
+  if (ok) {
+    const int64_t s = rp[row];
+    const int len = na ? na[row] : static_cast<int>(rp[row + 1] - s);
+    acc = row_partial(ci + s, v + s, len, sub, L, [&](int j) { return x[j]; });
+  }
+  acc = group_sum(acc, L);
+  if (ok && sub == 0) y[row] = acc;
+}
+inline unsigned spmv_grid(int n_rows, int L) {
+  return static_cast<unsigned>((static_cast<int64_t>(n_rows) * L + 255) / 256);
 }
 
 // Stand-alone form of the persistent kernel's fused MINRES vector pass (the
@@ -2096,7 +2116,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     if (per_sm < 1) return fail(h, DSGPU_E_CUDA, "minres kernel cannot be resident");
     // grid: IC(0) server CTAs (one per block, CTA b serves block b) + worker
     // CTAs, one per SM, fewer for tiny systems (barrier cost grows with CTAs)
-    const int64_t nnz = P.k_rp[P.n];
+    const int64_t nnz = P.nnz_k;
     const int n_srv =
         (!h->pi && (P.blk[0].kind == DSGPU_BLOCK_PCG_IC0 || P.blk[1].kind == DSGPU_BLOCK_PCG_IC0)) ? 2 : 0;
     const int wmax = sms - n_srv;
@@ -2144,6 +2164,12 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     a.k_ci = h->upload(P.k_ci);
     a.k_v = h->upload(P.k_v);
     a.row_start = h->upload(h->row_start);
+    auto lanes_for = [](double mean_row) { return mean_row >= 96.0 ? 32 : mean_row >= 40.0 ? 16 : 8; };
+    a.k_lanes = lanes_for(static_cast<double>(P.k_rp[P.n]) / P.n);
+    if (const char* env = std::getenv("DSGPU_SPMV_LANES")) {
+      const int L = std::atoi(env);
+      if (L == 8 || L == 16 || L == 32) a.k_lanes = L;
+    }
     const int32_t* d_na = h->upload(P.k_na);
     for (int b = 0; b < 2; ++b) {
       HostBlock& hb = P.blk[b];
@@ -2157,11 +2183,17 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         d.ci = a.k_ci;
         d.v = a.k_v;
         d.na = d_na;
+        {
+          double sum = 0.0;
+          for (int i = 0; i < P.n_u; ++i) sum += P.k_na[i];
+          d.lanes = lanes_for(sum / std::max(1, P.n_u));
+        }
       } else if (hb.kind != DSGPU_BLOCK_JACOBI) {
         d.rp = h->upload(hb.rp);
         d.ci = h->upload(hb.ci);
         d.v = h->upload(hb.v);
         d.na = nullptr;
+        d.lanes = lanes_for(static_cast<double>(hb.rp[hb.n]) / std::max(1, hb.n));
       }
       if (!hb.dinv.empty()) d.dinv = h->upload(hb.dinv);
       d.exact = h->exact ? 1 : 0;
@@ -2239,14 +2271,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       h->levels[3] = P.blk[1].bwd.n_levels;
     }
     h->nnz_k = nnz;
-    {
-      int64_t s = 0;
-      for (int i = 0; i < P.n_u; ++i) s += P.k_na[i];
-      h->nnz_a = s;
-    }
+    h->nnz_a = P.nnz_a;
     for (int b = 0; b < 2; ++b)
       h->nnz_l[b] = P.blk[b].kind == DSGPU_BLOCK_PCG_IC0 ? L_nnz[b] : 0;
-    h->nnz_q = P.blk[1].rp.empty() ? 0 : P.blk[1].rp.back();
+    h->nnz_q = P.blk[1].rp.empty() ? 0 : P.nnz_q;
     a.perm_u = h->upload(P.blk[0].perm);
     a.perm_p = h->upload(P.blk[1].perm);
     a.x = h->alloc<double>(P.n);
@@ -2413,7 +2441,7 @@ int dsgpu_apply_saddle(dsgpu_handle* h, const double* x, double* y) {
   // to RCM basis: x'[i] = x[perm_u[i]] / x'[n_u+i] = x[n_u + perm_p[i]]
   gather_kernel<<<(P.n_u + 255) / 256, 256, 0, h->stream>>>(P.n_u, a.perm_u, d0, d1);
   gather_kernel<<<(P.n_p + 255) / 256, 256, 0, h->stream>>>(P.n_p, a.perm_p, d0 + P.n_u, d1 + P.n_u);
-  spmv_kernel<<<(P.n * 32 + 255) / 256, 256, 0, h->stream>>>(P.n, a.k_rp, a.k_ci, a.k_v, nullptr, d1, d2);
+  spmv_kernel<<<spmv_grid(P.n, a.k_lanes), 256, 0, h->stream>>>(P.n, a.k_rp, a.k_ci, a.k_v, nullptr, d1, d2, a.k_lanes);
   scatter_kernel<<<(P.n_u + 255) / 256, 256, 0, h->stream>>>(P.n_u, a.perm_u, d2, d0);
   scatter_kernel<<<(P.n_p + 255) / 256, 256, 0, h->stream>>>(P.n_p, a.perm_p, d2 + P.n_u, d0 + P.n_u);
   cudaMemcpyAsync(y, d0, sizeof(double) * P.n, cudaMemcpyDeviceToHost, h->stream);
@@ -2473,7 +2501,7 @@ int dsgpu_apply_block_matrix(dsgpu_handle* h, int block, const double* x, double
   const DBlock& B = h->args.blk[block];
   double *d0 = h->d_tmp[0], *d1 = h->d_tmp[1];
   cudaMemcpyAsync(d0, x, sizeof(double) * B.n, cudaMemcpyHostToDevice, h->stream);
-  spmv_kernel<<<(B.n * 32 + 255) / 256, 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1);
+  spmv_kernel<<<spmv_grid(B.n, B.lanes), 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1, B.lanes);
   cudaMemcpyAsync(y, d1, sizeof(double) * B.n, cudaMemcpyDeviceToHost, h->stream);
   return cuda_check(h, cudaStreamSynchronize(h->stream), "apply_block_matrix");
 }
@@ -2488,7 +2516,7 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
   cudaMemsetAsync(a.bar, 0, 128 * sizeof(unsigned), h->stream);
   auto launch = [&]() {
     if (which == 0) {
-      spmv_kernel<<<(P.n * 32 + 255) / 256, 256, 0, h->stream>>>(P.n, a.k_rp, a.k_ci, a.k_v, nullptr, d0, d1);
+      spmv_kernel<<<spmv_grid(P.n, a.k_lanes), 256, 0, h->stream>>>(P.n, a.k_rp, a.k_ci, a.k_v, nullptr, d0, d1, a.k_lanes);
     } else if (which == 1 || which == 2) {
       DBlock B = a.blk[which - 1];
       B.r = d0;
@@ -2496,7 +2524,7 @@ int dsgpu_time_kernel(dsgpu_handle* h, int which, int reps, double* ms) {
       launch_ic(h, B, d0);
     } else {
       const DBlock& B = a.blk[0];
-      spmv_kernel<<<(B.n * 32 + 255) / 256, 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1);
+      spmv_kernel<<<spmv_grid(B.n, B.lanes), 256, 0, h->stream>>>(B.n, B.rp, B.ci, B.v, B.na, d0, d1, B.lanes);
     }
   };
   if ((which == 1 || which == 2) && a.blk[which - 1].kind != DSGPU_BLOCK_PCG_IC0)
