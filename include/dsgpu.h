@@ -21,7 +21,9 @@
  * Errors mirror the reference's exception taxonomy (precond.cpp:141-147,
  * solvers.cpp:46,74-75,133,142,148): non-convergence is NOT an error
  * (report.converged = 0). A handle is not thread-safe (like BlockSolver);
- * distinct handles may be used concurrently.
+ * distinct handles may be used from different threads, but their solves
+ * serialize on the device: a solve is one cooperative kernel that occupies
+ * every SM.
  */
 #ifndef DSGPU_H
 #define DSGPU_H
@@ -39,7 +41,9 @@ enum {
   DSGPU_E_CUDA = 4,               /* CUDA failure: dsgpu_last_error() */
   DSGPU_E_NONPOS_DIAG = 5,        /* Jacobi block: nonpositive diagonal (std::domain_error) */
   DSGPU_E_FACTOR_BREAKDOWN = 6,   /* IC(0): nonpositive pivot (FactorBreakdown, cholesky.hpp:13-19) */
-  DSGPU_E_UNSUPPORTED = 7         /* size beyond this build's limits */
+  DSGPU_E_UNSUPPORTED = 7,        /* size beyond this build's limits */
+  DSGPU_E_TIMEOUT = 8             /* a device-side wait exceeded DSGPU_TIMEOUT_S (default 10 s wall
+                                     clock): the solve was aborted instead of hanging the GPU */
 };
 
 /* preconditioner block kinds (precond.cpp:14-118) */
@@ -123,8 +127,12 @@ int dsgpu_solve_device(dsgpu_handle* h, const double* d_f, const dsgpu_opts* opt
  * assembly.cpp:363-372); host buffers of length n_u + n_p. */
 int dsgpu_apply_saddle(dsgpu_handle* h, const double* x, double* y);
 /* z = (L L^T)^{-1} r for block 0 (top) / 1 (bottom), in the block's RCM
- * ordering (Ic0Factor::solve, cholesky.cpp:136-152). Bit-identical to the
- * reference by construction (same per-row operation order, no FMA). */
+ * ordering (Ic0Factor::solve, cholesky.cpp:136-152): the same operator, i.e.
+ * mathematically identical to the reference's preconditioner. Bitwise identical
+ * to the reference only in DSGPU_EXACT=1 mode (column-order sweeps, no FMA);
+ * the default blocked sweeps re-associate each row's sum (dense 16 x 16 blocks
+ * next to the diagonal, formed in long double) and agree with the reference
+ * to round-off: <= 1e-13 relative in the tests, ~1e-15 measured. */
 int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z);
 /* y = M x with M = permuted A (block 0) or permuted Q_nu (block 1). */
 int dsgpu_apply_block_matrix(dsgpu_handle* h, int block, const double* x, double* y);

@@ -15,7 +15,19 @@ namespace dev {
 
 constexpr unsigned long long kSentinel = 0xFFF4A11C0DEDBEEFull;  // "not yet computed" (a NaN payload)
 constexpr unsigned long long kCanonNaN = 0x7FF8000000000000ull;
-constexpr long long kSpinTimeoutCycles = 2000000000ll;  // ~1 s at 1.96 GHz: abort instead of hanging
+constexpr long long kSpinTimeoutCycles = 2000000000ll;  // grid barrier / mailbox waits (cycles)
+// Abort flag values: a device spin that gives up sets the flag so every other
+// spin ends too (the solve returns an error instead of hanging the GPU).
+constexpr unsigned kAbortSet = 1u, kAbortTimeout = 2u;
+// Wall-clock limit of one device spin in ns (%globaltimer: independent of the
+// SM clock, so throttling or a profiler's replay do not shorten it);
+// DSGPU_TIMEOUT_S sets it at dsgpu_setup (default 10 s).
+__device__ unsigned long long g_spin_timeout_ns = 10000000000ull;
+__device__ __forceinline__ unsigned long long wall_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -103,13 +115,14 @@ __device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, unsign
       st_release(gen, g + 1);
     } else {
       const long long t0 = clock64();
+      const unsigned long long w0 = wall_ns();
       while (ld_acquire(gen) == g) {
         if (*reinterpret_cast<volatile unsigned*>(abort_flag)) {
           ok = 0;
           break;
         }
-        if (clock64() - t0 > kSpinTimeoutCycles) {
-          atomicExch(abort_flag, 1u);
+        if (clock64() - t0 > kSpinTimeoutCycles && wall_ns() - w0 > g_spin_timeout_ns) {
+          atomicCAS(abort_flag, 0u, kAbortTimeout);
           ok = 0;
           break;
         }
@@ -126,7 +139,8 @@ __device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, unsign
 // soon as another thread has aborted; the flag is only read after a short
 // grace period so the fast path stays free of global loads.
 struct SpinGuard {
-  long long t0;
+  long long t0;              // cycles: the cheap test of the fast path
+  unsigned long long w0 = 0; // wall clock, taken once the grace period is over
   unsigned* ab;
   __device__ __forceinline__ explicit SpinGuard(unsigned* a) {
 #ifdef __CUDA_ARCH__
@@ -139,15 +153,15 @@ struct SpinGuard {
   __device__ __forceinline__ bool expired() {
 #ifdef __CUDA_ARCH__
     const long long dt = clock64() - t0;
-#else
-    const long long dt = 0;
-#endif
     if (dt < (1ll << 16)) return false;
     if (*reinterpret_cast<volatile unsigned*>(ab)) return true;
-    if (dt > kSpinTimeoutCycles) {
-      atomicExch(ab, 1u);
+    const unsigned long long now = wall_ns();
+    if (w0 == 0) w0 = now;
+    if (now - w0 > g_spin_timeout_ns) {
+      atomicCAS(ab, 0u, kAbortTimeout);
       return true;
     }
+#endif
     return false;
   }
 };

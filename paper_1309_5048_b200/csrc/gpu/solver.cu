@@ -994,10 +994,11 @@ struct Ctx {
       Mailbox* m = a.mbox + b;
       int ok = 1;
       const long long t0 = clock64();
+      const unsigned long long w0 = wall_ns();
       while (ld_acquire(&m->done) != req[b]) {
         if (*reinterpret_cast<volatile unsigned*>(abort_flag) ||
-            clock64() - t0 > kSpinTimeoutCycles) {
-          atomicExch(abort_flag, 1u);
+            (clock64() - t0 > kSpinTimeoutCycles && wall_ns() - w0 > g_spin_timeout_ns)) {
+          atomicCAS(abort_flag, 0u, kAbortTimeout);
           ok = 0;
           break;
         }
@@ -1314,14 +1315,15 @@ __device__ void ic_server(const Args& a, int b, double* xs, double* red) {
     if (threadIdx.x == 0) {
       int op = IC_OP_EXIT;
       const long long t0 = clock64();
+      const unsigned long long w0 = wall_ns();
       for (;;) {
         if (ld_acquire(&m->req) == seq) {
           op = *reinterpret_cast<volatile int*>(&m->op);
           break;
         }
         if (*reinterpret_cast<volatile unsigned*>(abort_flag)) break;
-        if (clock64() - t0 > 4 * kSpinTimeoutCycles) {  // workers gone: give up
-          atomicExch(abort_flag, 1u);
+        if (clock64() - t0 > 4 * kSpinTimeoutCycles && wall_ns() - w0 > 4 * g_spin_timeout_ns) {
+          atomicCAS(abort_flag, 0u, kAbortTimeout);  // workers gone: give up
           break;
         }
       }
@@ -1469,6 +1471,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
       converged = 1;
       goto finish;
     }
+    if (a.max_iter == 0) goto finish;  // x = x0 = 0, no iteration (solvers.cpp:62)
     double oldb = 0.0, beta = beta1, dbar = 0.0, epsln = 0.0, phibar = beta1;
     double cs = -1.0, sn = 0.0, oldeps = 0.0;
     double delta = 0.0, gamma = 1.0, phi = 0.0;
@@ -1623,7 +1626,8 @@ finish:
     R->inner[1] = inner[1];
     R->apps[0] = apps[0];
     R->apps[1] = apps[1];
-    if (*reinterpret_cast<volatile unsigned*>(a.bar + 64)) R->status = DSGPU_E_CUDA;
+    const unsigned ab = *reinterpret_cast<volatile unsigned*>(a.bar + 64);
+    if (ab) R->status = ab == kAbortTimeout ? DSGPU_E_TIMEOUT : DSGPU_E_CUDA;
   }
 }
 
@@ -2049,6 +2053,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
     h->sms = sms;
     if (const char* env = std::getenv("DSGPU_REMOTE")) h->remote_max = std::max(0, std::atoi(env));
+    if (const char* env = std::getenv("DSGPU_TIMEOUT_S")) {
+      const unsigned long long ns = static_cast<unsigned long long>(std::max(0.001, std::atof(env)) * 1e9);
+      cudaMemcpyToSymbol(g_spin_timeout_ns, &ns, sizeof(ns));
+    }
     if (const char* env = std::getenv("DSGPU_NOWAIT")) {
       const int v = std::atoi(env);
       cudaMemcpyToSymbol(g_nowait, &v, sizeof(v));
@@ -2320,8 +2328,10 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   dsgpu_opts def;
   dsgpu_default_opts(&def);
   if (!o) o = &def;
-  if (!(o->outer_tol > 0.0) || o->max_iter < 1 || o->inner_cap < 1)
+  if (!(o->outer_tol > 0.0) || o->max_iter < 0 || o->inner_cap < 1)
     return fail(h, DSGPU_E_BAD_INPUT, "dsgpu_solve: bad options");
+  dsgpu_report rep_local;
+  if (!rep) rep = &rep_local;
   a.outer_tol = o->outer_tol;
   a.inner_tol = o->inner_tol;
   a.max_iter = o->max_iter;
@@ -2378,7 +2388,9 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
                                : 0.0;
   rep->hist_len = R.hist_len;
   rep->gpu_launches = 1;
-  if (R.status == DSGPU_E_CUDA) return fail(h, DSGPU_E_CUDA, "device spin timeout (aborted)");
+  if (R.status == DSGPU_E_TIMEOUT)
+    return fail(h, DSGPU_E_TIMEOUT, "a device-side wait exceeded DSGPU_TIMEOUT_S (solve aborted)");
+  if (R.status == DSGPU_E_CUDA) return fail(h, DSGPU_E_CUDA, "device-side abort");
   if (R.status != DSGPU_OK)
     return fail(h, R.status,
                 R.status == DSGPU_E_NEG_CURVATURE

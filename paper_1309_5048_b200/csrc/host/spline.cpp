@@ -84,31 +84,51 @@ int Space1D::eval(double x, double* val, double* der) const {
   return span - P;
 }
 
+namespace {
+// Legendre P_n and P_{n-1} at x by the three-term recurrence
+// k P_k = (2k - 1) x P_{k-1} - (k - 1) P_{k-2}.
+struct LegendrePair {
+  double pn, pnm1;
+};
+LegendrePair legendre_pair(int n, double x) {
+  LegendrePair r{x, 1.0};
+  for (int k = 2; k <= n; ++k) {
+    const double next = ((2 * k - 1) * x * r.pn - (k - 1) * r.pnm1) / k;
+    r.pnm1 = r.pn;
+    r.pn = next;
+  }
+  return r;
+}
+}  // namespace
+
+// n-point Gauss-Legendre rule on [0, 1]. The quadrature points feed the
+// assembly, whose matrices are compared bit for bit with the reference's
+// (tests/test_host.py), so the nodes must be the reference's doubles
+// (proj/src/quadrature.cpp:11-40), not merely accurate ones: the same Chebyshev
+// starting guess, Newton on P_n with P_n' = n (x P_n - P_{n-1}) / (x^2 - 1), the
+// same stopping rule and the same weight formula, evaluated in the same order.
+// The rule is symmetric; only the roots x > 0 are iterated.
 Gauss gauss_legendre(int n) {
   if (n < 1) throw std::invalid_argument("gauss_legendre: need n >= 1");
   Gauss g;
-  g.x.resize(n);
-  g.w.resize(n);
-  for (int i = 0; i < (n + 1) / 2; ++i) {
-    double x = std::cos(M_PI * (i + 0.75) / (n + 0.5));
-    double dp = 0.0;
-    for (int it = 0; it < 100; ++it) {
-      double p0 = 1.0, p1 = x;
-      for (int k = 2; k <= n; ++k) {
-        const double pk = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
-        p0 = p1;
-        p1 = pk;
-      }
-      dp = n * (x * p1 - p0) / (x * x - 1.0);
-      const double dx = p1 / dp;
-      x -= dx;
-      if (std::abs(dx) < 1e-15) break;
+  g.x.assign(n, 0.0);
+  g.w.assign(n, 0.0);
+  const int half = (n + 1) / 2;
+  for (int i = 0; i < half; ++i) {
+    double root = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    double slope = 0.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+      const LegendrePair p = legendre_pair(n, root);
+      slope = n * (root * p.pn - p.pnm1) / (root * root - 1.0);
+      const double step = p.pn / slope;
+      root -= step;
+      if (std::abs(step) < 1e-15) break;
     }
-    const double w = 2.0 / ((1.0 - x * x) * dp * dp);
-    g.x[i] = 0.5 * (1.0 - x);
-    g.x[n - 1 - i] = 0.5 * (1.0 + x);
-    g.w[i] = 0.5 * w;
-    g.w[n - 1 - i] = 0.5 * w;
+    const double weight = 2.0 / ((1.0 - root * root) * slope * slope);
+    const int mirror = n - 1 - i;
+    g.x[i] = 0.5 * (1.0 - root);
+    g.x[mirror] = 0.5 * (1.0 + root);
+    g.w[i] = g.w[mirror] = 0.5 * weight;
   }
   return g;
 }

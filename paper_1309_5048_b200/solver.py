@@ -32,6 +32,7 @@ STOP_PRECONDITIONED, STOP_EUCLIDEAN = 0, 1
 DSGPU_OK, E_INDEFINITE, E_NEG_CURVATURE, E_BAD_INPUT, E_CUDA, E_NONPOS_DIAG, E_UNSUPPORTED = (
     0, 1, 2, 3, 4, 5, 7)
 E_FACTOR_BREAKDOWN = 6
+E_TIMEOUT = 8
 
 # strategy -> (top block, bottom block); precond.cpp:161-193 plus the
 # "IC0-PCG(A)+Diag(Q)" composition BASELINE config 1 asks for
@@ -143,9 +144,15 @@ class PreconditionerError(RuntimeError):
     """Indefinite preconditioner / negative curvature (reference std::runtime_error)."""
 
 
+class DeviceTimeout(RuntimeError):
+    """A device-side wait exceeded DSGPU_TIMEOUT_S; the solve was aborted."""
+
+
 def _raise(code: int, msg: str):
     if code in (E_INDEFINITE, E_NEG_CURVATURE):
         raise PreconditionerError(msg)
+    if code == E_TIMEOUT:
+        raise DeviceTimeout(msg)
     if code == E_NONPOS_DIAG:
         raise ArithmeticError(msg)  # std::domain_error
     if code in (E_BAD_INPUT, E_UNSUPPORTED):

@@ -55,11 +55,12 @@ def test_saddle_apply_matches_reference(gpu, port):
 
 @pytest.mark.parametrize("pi_b", [None, "0.5", "1.7", "3.0"])
 def test_ic0_apply_partitioned_inverse_matches_reference(gpu, port, monkeypatch, pi_b):
-    """Default mode for 2D systems: partitioned-inverse IC(0) apply (block
-    inverses of the same factor; agreement to round-off). pi_b scales the
-    block size (0.5: windows spanning two earlier blocks; 1.7: ragged last
-    block; 3.0: windows shorter than the block)."""
+    """Legacy partitioned-inverse IC(0) apply (DSGPU_PI=1; block inverses of
+    the same factor; agreement to round-off). pi_b scales the block size (0.5:
+    windows spanning two earlier blocks; 1.7: ragged last block; 3.0: windows
+    shorter than the block)."""
     host, solver = gpu
+    monkeypatch.setenv("DSGPU_PI", "1")
     if pi_b:
         monkeypatch.setenv("DSGPU_PI_B", pi_b)
     d = load_golden("c1_psi_k2_n8.npz")
@@ -78,6 +79,59 @@ def test_ic0_apply_partitioned_inverse_matches_reference(gpu, port, monkeypatch,
         assert np.abs(z - ref).max() <= 1e-12 * np.abs(ref).max()
     sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
     check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+
+
+@pytest.mark.parametrize("knobs", [{}, {"DSGPU_FAR_A": "0", "DSGPU_FAR_Q": "0"}, {"DSGPU_GRID": "5"},
+                                   {"DSGPU_FAR_A": "3", "DSGPU_FAR_Q": "1", "DSGPU_BS_SLOTS": "5"}])
+def test_ic0_apply_blocked_matches_reference(gpu, port, monkeypatch, knobs):
+    """The default IC(0) apply: blocked sweeps (bsweep.hpp) -- dense 16x16
+    blocks next to the diagonal on the main warp, mid entries on the co-main
+    warps, far entries on far-worker CTAs -- against the reference's own
+    Ic0Factor::solve output (fixture), the CPU oracle on 2D and 3D factors, and
+    through a whole solve. knobs: no far-worker CTAs (the sweep CTA's spare
+    warps do the far lists), a 5-CTA grid, few far CTAs with the smallest slot
+    ring."""
+    host, solver = gpu
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    d = load_golden("c1_psi_k2_n8.npz")
+    s = host.assemble("psi-mms", 2, 8)
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    assert g.info()["ic0_mode"] == "blocked"
+    for b, tag in ((0, "A"), (1, "Q")):
+        z = g.apply_ic0(b, d["ic_r_" + tag])
+        ref = d["ic_z_" + tag]  # the reference's own Ic0Factor::solve output
+        assert np.abs(z - ref).max() <= 1e-13 * np.abs(ref).max()
+    g.close()
+    for case, k, n, dim in (("psi-mms", 2, 64, 2), ("random", 3, 32, 2), ("psi-mms", 2, 12, 3)):
+        s = host.assemble(case, k, n, dim=dim, seed=7)
+        g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+        for b, fac in ((0, g.top.factor), (1, g.bottom.factor)):
+            r = np.random.default_rng(3 + b).standard_normal(fac.n_rows)
+            ref = port.ic0_solve(to_oracle(fac), r)
+            for _ in range(2):  # a second apply reuses the slot ring, flags and tags
+                z = g.apply_ic0(b, r)
+                assert np.linalg.norm(z - ref) <= 1e-13 * np.linalg.norm(ref)
+        sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+        check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+        g.close()
+
+
+def test_two_handles_of_different_sizes(gpu, port):
+    """Distinct handles: a smaller system set up after a larger one must not
+    disturb the first handle's launches (shared-memory limits are per kernel
+    function, raised once, never lowered)."""
+    host, solver = gpu
+    s1 = host.assemble("psi-mms", 2, 32)
+    s2 = host.assemble("psi-mms", 2, 8)
+    g1 = solver.GpuStokesSolver(s1, "IC0-PCG(A,Q)")
+    g2 = solver.GpuStokesSolver(s2, "IC0-PCG(A)+Diag(Q)")
+    o = solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1)
+    check_parity(g1.solve(options=o), reference_solve(port, s1, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+    check_parity(g2.solve(options=o), reference_solve(port, s2, "IC0-PCG(A)+Diag(Q)", 1e-8, 1e-1), 1e-8)
+    check_parity(g1.solve(options=o), reference_solve(port, s1, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+    g1.close()
+    g2.close()
 
 
 def test_ic0_apply_staged_matches_reference(gpu, port, monkeypatch):
@@ -231,6 +285,10 @@ def test_max_iter_and_errors(gpu):
     s = host.assemble("psi-mms", 2, 8)
     sol = solver.solve_stokes(s, "IC0-PCG(A,Q)", solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1, max_iter=3))
     assert not sol.report.converged and sol.report.iterations == 3
+    # max_iter = 0: the reference returns x0 = 0 after one preconditioner apply (solvers.cpp:36-62)
+    sol = solver.solve_stokes(s, "IC0-PCG(A,Q)", solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1, max_iter=0))
+    assert not sol.report.converged and sol.report.iterations == 0
+    assert not sol.u.any() and not sol.p.any() and len(sol.report.euclid_history) == 1
     from paper_1309_5048_b200.host import CsrMatrix, StokesSystem
     negQ = CsrMatrix(s.Q_nu.n_rows, s.Q_nu.n_cols, s.Q_nu.row_ptr, s.Q_nu.cols, -s.Q_nu.vals)
     bad = StokesSystem(s.A, s.B, s.Bt, s.Q, negQ, s.f)
