@@ -59,6 +59,7 @@ struct BsSmem {
   double* ring;             // kBsR groups x 16 results, then the zero slot
   double* cbuf;             // kBsRC x 16 (co-main -> main)
   uint8_t* slots;           // ns x kBsSlotBytes
+  uint8_t* stage;           // kBsNC x 2 x kBsStageBytes: co-main mid-list staging
   uint64_t* mbar;           // ns
   volatile int* sready;     // ns: group whose blocks have landed in the slot
   int* base_use;            // ns: completed mbarrier phases before this sweep
@@ -76,6 +77,8 @@ struct BsSmem {
     p += kBsRC * kBsB * 8;
     slots = p;
     p += static_cast<size_t>(ns) * kBsSlotBytes;
+    stage = p;
+    p += static_cast<size_t>(kBsNC) * 2 * kBsStageBytes;
     mbar = reinterpret_cast<uint64_t*>(p);
     p += static_cast<size_t>(ns) * 8;
     sready = reinterpret_cast<volatile int*>(p);
@@ -305,14 +308,39 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     // ---- co-main: c_h = T_h (rhs_h - far_h - mid_h) ---------------------------
     BS_DIAG(const long long t0 = clock64(); long long w_p = 0, w_f = 0;)
     const uint8_t* ringb = reinterpret_cast<const uint8_t*>(S.ring);
+    uint8_t* const stage0 = S.stage + static_cast<size_t>(cid) * 2 * kBsStageBytes;
+    // stage the first min(mw, kBsStage) mid entries of group h (this lane's
+    // 16-byte units, lane-private: no cross-lane synchronization needed)
+    auto stage_group = [&](int h, int buf) {
+      if (h < G) {
+        const int mw = min(__ldg(s.mw + h), kBsStage);
+        const int64_t mb = __ldg(s.mptr + h);
+        const int4* cp = reinterpret_cast<const int4*>(s.mcols + mb) + lane;
+        const double2* vp = reinterpret_cast<const double2*>(s.mvals + mb) + lane;
+        const unsigned dst = smem_u32(stage0 + static_cast<size_t>(buf) * kBsStageBytes) + lane * 16;
+        for (int c = 0; c < mw / kBsMC; ++c) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536), "l"(cp + c * 32) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536 + 512), "l"(vp + 2 * c * 32)
+                       : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536 + 1024),
+                       "l"(vp + (2 * c + 1) * 32)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     int prog = 0;  // last progress value seen
-    for (int h = cid; h < G; h += kBsNC) {
+    stage_group(cid, 0);
+    int buf = 0;
+    for (int h = cid; h < G; h += kBsNC, buf ^= 1) {
+      stage_group(h + kBsNC, buf ^ 1);
       const int p = h * kBsB + r;
       double acc = (hf == 0 && p < n) ? __ldcg(rhs + orig(p)) : 0.0;
       const int mw = __ldg(s.mw + h), ms = __ldg(s.ms + h), fw = __ldg(s.fw + h);
       const int64_t mb = __ldg(s.mptr + h);
       const int4* cp = reinterpret_cast<const int4*>(s.mcols + mb) + lane;
       const double2* vp = reinterpret_cast<const double2*>(s.mvals + mb) + lane;
+      const uint8_t* sbuf = stage0 + static_cast<size_t>(buf) * kBsStageBytes + lane * 16;
       auto wait_progress = [&](int need) {
         if (prog >= need) return;
         BS_DIAG(const long long tw = clock64();)
@@ -322,11 +350,28 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
         asm volatile("" ::: "memory");
         BS_DIAG(w_p += clock64() - tw;)
       };
+      auto use = [&](const int4 cc, const double2 va, const double2 vb) {
+        const double x0 = *reinterpret_cast<const double*>(ringb + cc.x);
+        const double x1 = *reinterpret_cast<const double*>(ringb + cc.y);
+        const double x2 = *reinterpret_cast<const double*>(ringb + cc.z);
+        const double x3 = *reinterpret_cast<const double*>(ringb + cc.w);
+        double pa = va.x * x0, pb = vb.x * x2;
+        pa = fma(va.y, x1, pa);
+        pb = fma(vb.y, x3, pb);
+        acc -= pa + pb;
+      };
       auto chunks = [&](int k0, int k1) {  // mid entries [k0, k1), whole chunks
-        if (k0 >= k1) return;
-        int4 cc = __ldcs(cp + (k0 / 4) * 32);
-        double2 va = __ldcs(vp + (k0 / 2) * 32), vb = __ldcs(vp + (k0 / 2 + 1) * 32);
-        for (int k = k0; k < k1; k += kBsMC) {
+        int k = k0;
+        for (; k < k1 && k < kBsStage; k += kBsMC) {  // staged part
+          const uint8_t* q = sbuf + (k / kBsMC) * 1536;
+          use(*reinterpret_cast<const int4*>(q), *reinterpret_cast<const double2*>(q + 512),
+              *reinterpret_cast<const double2*>(q + 1024));
+        }
+        if (k >= k1) return;
+        // lists wider than the staging buffer (the few groups at the ends of the ordering)
+        int4 cc = __ldcs(cp + (k / 4) * 32);
+        double2 va = __ldcs(vp + (k / 2) * 32), vb = __ldcs(vp + (k / 2 + 1) * 32);
+        for (; k < k1; k += kBsMC) {
           int4 nc = cc;
           double2 na = va, nb = vb;
           if (k + kBsMC < k1) {
@@ -334,19 +379,14 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
             na = __ldcs(vp + (k / 2 + 2) * 32);
             nb = __ldcs(vp + (k / 2 + 3) * 32);
           }
-          const double x0 = *reinterpret_cast<const double*>(ringb + cc.x);
-          const double x1 = *reinterpret_cast<const double*>(ringb + cc.y);
-          const double x2 = *reinterpret_cast<const double*>(ringb + cc.z);
-          const double x3 = *reinterpret_cast<const double*>(ringb + cc.w);
-          double pa = va.x * x0, pb = vb.x * x2;
-          pa = fma(va.y, x1, pa);
-          pb = fma(vb.y, x3, pb);
-          acc -= pa + pb;
+          use(cc, va, vb);
           cc = nc;
           va = na;
           vb = nb;
         }
       };
+      // this group's staged list has landed (all but the newest commit group)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
       // entries that only need groups <= h-K-3
       wait_progress(h - K - 2);
       chunks(0, ms);
@@ -384,6 +424,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
         S.aready[h % kBsRC] = h;
       }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     BS_DIAG(if (lane == 0) {
       atomicAdd(&g_bs_dbg[5], static_cast<unsigned long long>(w_p));
       atomicAdd(&g_bs_dbg[6], static_cast<unsigned long long>(w_f));

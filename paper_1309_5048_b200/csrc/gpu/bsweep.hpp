@@ -22,7 +22,9 @@
 //     shuffle). y_{g-1} is broadcast through the shared-memory y ring.
 //   * CO-MAIN warps (kBsNC, round-robin over groups): c_g = T_g (r_g - far_g
 //     - mid_g): the "mid" entries (groups g-R .. g-K-1) are gathered from the y
-//     ring; the "far" partial sums come from the far workers.
+//     ring; the "far" partial sums come from the far workers. Each co-main
+//     stages its NEXT group's mid list in shared memory with cp.async while it
+//     works on the current one, so the lists' HBM latency is off its path.
 //   * PRODUCER lane: TMA bulk copies of each group's dense blocks (F_1..F_K,
 //     T) into a shared-memory slot ring.
 //   * PUBLISHER warp: copies finished groups from the y ring to the result
@@ -56,6 +58,8 @@ constexpr int kBsNC = 4;     // co-main warps
 constexpr int kBsRC = 8;     // c ring (co-main -> main), groups
 constexpr int kBsMC = 4;     // mid-list chunk (entries per lane)
 constexpr int kBsFC = 8;     // far-list chunk (entries per lane)
+constexpr int kBsStage = 32;  // mid-list entries per lane staged ahead in shared memory (cp.async)
+constexpr int kBsStageBytes = kBsStage / kBsMC * 3 * 512;  // per buffer: chunks x (int4 + 2 double2) x 32 lanes
 constexpr int kBsBlock = kBsB * kBsB * 8;              // bytes of one dense block
 constexpr int kBsSlotBytes = (kBsK + 1) * kBsBlock;    // F_1..F_K, T
 constexpr int kBsZero = kBsR * kBsB * 8;               // byte offset of the ring's zero slot
@@ -98,6 +102,7 @@ inline size_t bs_smem_bytes(int ns) {
   return static_cast<size_t>(kBsZero) + 128            // y ring + zero slot
          + kBsRC * kBsB * 8                             // c ring
          + static_cast<size_t>(ns) * kBsSlotBytes       // dense-block slots
+         + static_cast<size_t>(kBsNC) * 2 * kBsStageBytes  // co-main mid-list staging (double-buffered)
          + static_cast<size_t>(ns) * 8                  // mbarriers
          + (2 * ns + kBsRC + 8) * 4 + 128;              // sready, base_use, aready, progress words
 }
