@@ -421,30 +421,53 @@ def test_c5_data_48_vs_reference(gpu):
 
 
 @pytest.mark.skipif(not __import__("os").environ.get("DSGPU_TEST_C5"),
-                    reason="C5 at full size: ~20 min of host setup and ~150 GB host RAM; "
-                           "set DSGPU_TEST_C5=1")
-def test_c5_full_size_properties(gpu):
+                    reason="C5 at full size: ~12 min of host assembly/setup and ~100 GB host RAM; "
+                           "set DSGPU_TEST_C5=1 (last recorded run: profiles/r02_c5_pin.md)")
+def test_c5_full_size_vs_reference(gpu):
     """BASELINE config 5 (3D k'=2 96^3, 3.7M unknowns, nnz(K) 2.24e9 > 2^31) at
-    full size. The reference needs hours here, so parity is by size-independent
-    properties: convergence to 1e-6, the recurrence residual equal to the true
-    residual ||b - K x|| / ||b|| (device saddle apply), the M^-1-norm residual
-    history non-increasing (a MINRES invariant), and the structural sizes of
-    SURVEY.md §8(d)."""
+    full size against the reference's own solve of the identical system, run
+    once on the GPU box's host (tests/golden/make_golden_c5.py; 1,077 s of
+    MINRES on one core): outer iterations +-2, inner means, the Euclidean
+    residual history, ||u|| and ||p||, a strided 4,096-entry sample of the
+    solution, samples of one saddle apply and one IC(0) apply -- plus the
+    size-independent properties (true residual = recurrence residual, the
+    M^-1-norm history non-increasing) and the structural sizes of SURVEY.md §8(d)."""
     host, solver = gpu
+    g = load_golden("c5_rand3d_k2_n96_full.npz")
+    gb = load_golden("c5_rand3d_k2_n96_bounded.npz")
     s = host.assemble("random", 2, 96, dim=3, seed=42)
-    assert (s.n_u, s.n_p, s.A.nnz, s.B.nnz, s.Q.nnz) == (
-        2794764, 941192, 1432223760, 404794368, 113379904)
-    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
-    sol = g.solve(options=solver.SolverOptions(outer_tol=1e-6, inner_tol=1e-1))
-    r = sol.report
+    assert [s.n_u, s.n_p, s.A.nnz, s.B.nnz, s.Q.nnz] == g["sizes"].tolist() == [
+        2794764, 941192, 1432223760, 404794368, 113379904]
+    top = solver.prepare_block(s.A, solver.BLOCK_PCG_IC0, ic0_on_gpu=True)
+    bot = solver.prepare_block(s.Q_nu, solver.BLOCK_PCG_IC0, ic0_on_gpu=True)
+    gs = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)", top=top, bottom=bot)
+    sample = g["sample"]
+    rng = np.random.default_rng(int(g["probe_seed"][0]))
+    xv = rng.uniform(-1.0, 1.0, s.n_u + s.n_p)
+    rv = rng.uniform(-1.0, 1.0, s.n_u)
+    ya = gs.apply(xv)[sample]
+    assert np.linalg.norm(ya - g["apply_sample"]) <= 1e-13 * np.linalg.norm(g["apply_sample"])
+    zi = gs.apply_ic0(0, rv)[sample[sample < s.n_u]]
+    assert np.linalg.norm(zi - g["ic_sample"]) <= 1e-12 * np.linalg.norm(g["ic_sample"])
+    for gold, mi in ((gb, 5), (g, 20000)):
+        sol = gs.solve(options=solver.SolverOptions(outer_tol=1e-6, inner_tol=1e-1, max_iter=mi))
+        r = sol.report
+        x = np.concatenate([sol.u, sol.p])
+        assert abs(r.iterations - int(gold["meta"][0])) <= 2
+        assert abs(r.mean_inner_top - gold["meta"][2]) < 0.2 and abs(r.mean_inner_bottom - gold["meta"][3]) < 0.2
+        he, hr = r.euclid_history, gold["he"]
+        m = min(len(he), len(hr))
+        assert np.all(np.abs(he[:m] - hr[:m]) <= 1e-8 * hr[:m])
+        assert np.linalg.norm(x[sample] - gold["x_sample"]) <= 1e-8 * np.linalg.norm(gold["x_sample"])
+        assert abs(np.linalg.norm(sol.u) - gold["norms"][0]) <= 1e-9 * gold["norms"][0]
+        assert abs(np.linalg.norm(sol.p) - gold["norms"][1]) <= 1e-9 * gold["norms"][1]
     assert r.converged and r.relres_e <= 1e-6
-    x = np.concatenate([sol.u, sol.p])
     b = np.concatenate([s.f, np.zeros(s.n_p)])
-    true = np.linalg.norm(b - g.apply(x)) / np.linalg.norm(b)
+    true = np.linalg.norm(b - gs.apply(x)) / np.linalg.norm(b)
     assert abs(true - r.relres_e) <= 1e-3 * r.relres_e
     hm = r.residual_history
     assert np.all(hm[1:] <= hm[:-1] * (1 + 1e-10))
-    g.close()
+    gs.close()
 
 
 def vector_update_reference(n, launches):
