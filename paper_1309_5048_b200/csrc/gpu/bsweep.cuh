@@ -22,14 +22,27 @@ struct DBSweep {
   const int32_t *fcptr, *fneed;
 };
 
-// Global hand-off state of one sweep (shared by a block's two sweeps: tags differ).
+// Global hand-off state of one sweep (shared by a block's two sweeps: tags
+// differ). Cross-SM hand-offs carry NO fence and NO flag: every double travels
+// as one 16-byte unit {low word, tag, high word, tag} (two self-validating
+// 8-byte halves, like NCCL's LL protocol), and the consumer polls the data
+// itself until both tags are the sweep's. Measured on B200 (tools/bs_lab.cu):
+// 175 cycles per hop, against 2,260 for data + __threadfence + release flag.
 struct BsFar {
-  double* fpsum;               // [G][16] far partial sum of every row
-  unsigned* fflag;             // [G] sweep tag once fpsum[g] is final
-  unsigned long long* gprog;   // (sweep tag << 32) | groups published in the result vector
-  unsigned tag;
-  int workers;                 // far-worker warps outside the sweep CTA (0: its spare warps)
+  uint4* gt;       // [n + 1] tagged copy of the result vector (what the far workers gather)
+  uint4* fps;      // [G][16] tagged far partial sum of every row
+  unsigned tag;    // unique per sweep (launch id | sweep number)
+  int workers;     // far-worker warps outside the sweep CTA (0: its spare warps)
 };
+
+__device__ __forceinline__ uint4 bs_pack(double v, unsigned tag) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return make_uint4(static_cast<unsigned>(b), tag, static_cast<unsigned>(b >> 32), tag);
+}
+__device__ __forceinline__ bool bs_valid(const uint4& w, unsigned tag) { return w.y == tag && w.w == tag; }
+__device__ __forceinline__ double bs_value(const uint4& w) {
+  return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(w.z) << 32) | w.x));
+}
 
 // Diagnostics exist only in the -DDSGPU_DIAG build (make diag): the production
 // kernels carry no counters, clocks or atomics on their paths.
@@ -43,14 +56,6 @@ __device__ unsigned long long g_bs_dbg[16];
 #define BS_DIAG(...)
 #endif
 
-__device__ __forceinline__ unsigned long long bs_ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void bs_st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ double bs_shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ double bs_shfl_xor16(double v) { return __shfl_xor_sync(0xffffffffu, v, 16); }
 
@@ -103,23 +108,23 @@ __device__ void bs_setup(double* smem, int ns) {
 }
 
 // Far workers: for every group the partial sums of its far entries, gathered
-// from the published part of the result vector gx. wid / W: this warp among
-// the far-worker warps.
-__device__ void bs_far(const DBSweep& s, const double* __restrict__ gx, BsFar F, int wid, int W,
-                       unsigned* abort_flag) {
+// from the tagged result vector F.gt as the publisher fills it. A gathered
+// entry that does not carry this sweep's tag yet is simply read again (lists
+// are oldest-first, so only the last chunk of a list ever waits). wid / W: this
+// warp among the far-worker warps.
+__device__ void bs_far(const DBSweep& s, BsFar F, int wid, int W, unsigned* abort_flag) {
   const int lane = threadIdx.x & 31;
-  unsigned seen = 0;
+  const uint4* __restrict__ gt = F.gt;
+  const unsigned tag = F.tag;
   BS_DIAG(long long t_begin = clock64(); long long t_wait = 0;)
   for (int g = wid; g < s.G; g += W) {
     const int fw = __ldg(s.fw + g);
     if (fw == 0) continue;
     const int64_t base = __ldg(s.fptr + g);
-    const int32_t* need = s.fneed + __ldg(s.fcptr + g);
     const int4* cp = reinterpret_cast<const int4*>(s.fcols + base) + lane;
     const double2* vp = reinterpret_cast<const double2*>(s.fvals + base) + lane;
     const int nch = fw / kBsFC;
     double acc = 0.0;
-    SpinGuard sg(abort_flag);
     int4 ca = __ldcs(cp), cb = __ldcs(cp + 32);
     double2 v0 = __ldcs(vp), v1 = __ldcs(vp + 32), v2 = __ldcs(vp + 64), v3 = __ldcs(vp + 96);
     for (int c = 0; c < nch; ++c) {
@@ -134,29 +139,35 @@ __device__ void bs_far(const DBSweep& s, const double* __restrict__ gx, BsFar F,
         n2 = __ldcs(vp + (4 * c + 6) * 32);
         n3 = __ldcs(vp + (4 * c + 7) * 32);
       }
-      const unsigned nd = static_cast<unsigned>(__ldg(need + c) + 1);
-      if (seen < nd) {
+      uint4 w0 = __ldcg(gt + ca.x), w1 = __ldcg(gt + ca.y), w2 = __ldcg(gt + ca.z), w3 = __ldcg(gt + ca.w);
+      uint4 w4 = __ldcg(gt + cb.x), w5 = __ldcg(gt + cb.y), w6 = __ldcg(gt + cb.z), w7 = __ldcg(gt + cb.w);
+      auto all_valid = [&]() {
+        return bs_valid(w0, tag) && bs_valid(w1, tag) && bs_valid(w2, tag) && bs_valid(w3, tag) &&
+               bs_valid(w4, tag) && bs_valid(w5, tag) && bs_valid(w6, tag) && bs_valid(w7, tag);
+      };
+      if (!all_valid()) {
         BS_DIAG(const long long tw = clock64();)
-        for (;;) {  // the tag must match: progress words of other sweeps never count
-          const unsigned long long v = bs_ld_acquire_u64(F.gprog);
-          unsigned ns_sleep = 500;
-          if (static_cast<unsigned>(v >> 32) == F.tag) {
-            seen = static_cast<unsigned>(v);
-            if (seen >= nd) break;
-            ns_sleep = min(4000u, (nd - seen) * 48u);  // ~half the expected wait
-          }
+        SpinGuard sg(abort_flag);
+        unsigned ns_sleep = 100;
+        do {
           __nanosleep(ns_sleep);
-          if (sg.expired()) break;
-        }
+          ns_sleep = min(2000u, ns_sleep * 2);
+          w0 = __ldcg(gt + ca.x);
+          w1 = __ldcg(gt + ca.y);
+          w2 = __ldcg(gt + ca.z);
+          w3 = __ldcg(gt + ca.w);
+          w4 = __ldcg(gt + cb.x);
+          w5 = __ldcg(gt + cb.y);
+          w6 = __ldcg(gt + cb.z);
+          w7 = __ldcg(gt + cb.w);
+        } while (!all_valid() && !sg.expired());
         BS_DIAG(t_wait += clock64() - tw;)
       }
-      const double x0 = __ldcg(gx + ca.x), x1 = __ldcg(gx + ca.y), x2 = __ldcg(gx + ca.z), x3 = __ldcg(gx + ca.w);
-      const double x4 = __ldcg(gx + cb.x), x5 = __ldcg(gx + cb.y), x6 = __ldcg(gx + cb.z), x7 = __ldcg(gx + cb.w);
-      double p0 = v0.x * x0, p1 = v1.x * x2, p2 = v2.x * x4, p3 = v3.x * x6;
-      p0 = fma(v0.y, x1, p0);
-      p1 = fma(v1.y, x3, p1);
-      p2 = fma(v2.y, x5, p2);
-      p3 = fma(v3.y, x7, p3);
+      double p0 = v0.x * bs_value(w0), p1 = v1.x * bs_value(w2), p2 = v2.x * bs_value(w4), p3 = v3.x * bs_value(w6);
+      p0 = fma(v0.y, bs_value(w1), p0);
+      p1 = fma(v1.y, bs_value(w3), p1);
+      p2 = fma(v2.y, bs_value(w5), p2);
+      p3 = fma(v3.y, bs_value(w7), p3);
       acc += (p0 + p1) + (p2 + p3);
       ca = na;
       cb = nb;
@@ -166,10 +177,7 @@ __device__ void bs_far(const DBSweep& s, const double* __restrict__ gx, BsFar F,
       v3 = n3;
     }
     acc += bs_shfl_xor16(acc);
-    if (lane < kBsB) __stcg(F.fpsum + static_cast<int64_t>(g) * kBsB + lane, acc);
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(F.fflag + g, F.tag);
+    if (lane < kBsB) __stcg(F.fps + static_cast<int64_t>(g) * kBsB + lane, bs_pack(acc, tag));
   }
   BS_DIAG(if (lane == 0) {
     atomicAdd(&g_bs_dbg[8], static_cast<unsigned long long>(t_wait));
@@ -178,12 +186,12 @@ __device__ void bs_far(const DBSweep& s, const double* __restrict__ gx, BsFar F,
 }
 
 // One blocked sweep by every thread of the sweep CTA: gx = T^{-1} rhs (both in
-// the factor's ordering; gx has n + 1 entries, gx[n] = 0). Returns after a CTA
-// barrier with the result complete in global memory.
+// the factor's ordering). Returns after a CTA barrier with the result complete
+// in global memory (plain in gx, tagged in F.gt).
 template <int K>
 __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* __restrict__ rhs, double* gx,
                        BsFar F, unsigned* abort_flag) {
-  static_assert(K >= 1 && K <= 4 && K == kBsK, "dense coupling depth");
+  static_assert(K == 3 && K == kBsK, "the main loop is written for three dense coupling blocks");
   const DBSweep s = s_in;
   const int G = s.G, n = s.n;
   BsSmem S(smem, ns);
@@ -205,9 +213,8 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     for (int i = 0; i < kBsNC; ++i)
       if (warp == cw[i]) cid = i;
   }
-  auto slot_of = [&](int g) { return S.slots + static_cast<size_t>(g % ns) * kBsSlotBytes; };
   auto orig = [&](int p) { return s.dir ? n - 1 - p : p; };
-  // row `row` (this lane's half) of dense block `block` of the slot
+  // this lane's half row (8 doubles) of dense block `block` of a slot
   auto ld_block = [&](const uint8_t* slot, int block, double* out) {
     const double2* p = reinterpret_cast<const double2*>(slot + block * kBsBlock) + lane;
 #pragma unroll
@@ -217,32 +224,43 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       out[2 * q + 1] = t.y;
     }
   };
-  auto wait_int = [&](volatile int* p, int want_ge, bool exact) {
+  auto wait_eq = [&](volatile int* p, int want) {
     SpinGuard sg(abort_flag);
-    for (;;) {
-      const int v = *p;
-      if (exact ? v == want_ge : v >= want_ge) break;
+    while (*p != want)
       if (sg.expired()) break;
-    }
-    asm volatile("" ::: "memory");  // data reads stay behind the flag
   };
 
   if (warp == mainw && G > 0) {
+    // ---- main: y_g = c_g - (F_1^g y_{g-1} + F_2^g y_{g-2} + F_3^g y_{g-3}) ------
+    // One step per group. Everything except the first line of a step is kept
+    // off the dependent chain: the coupling rows and c of the NEXT step are
+    // loaded while the chain's latencies pass (straight-line code, no barrier
+    // inside a step except the __syncwarp that publishes y), and F_2 / F_3 of
+    // later groups are applied to y_{g-1} right after the chain.
     BS_DIAG(const long long t0 = clock64(); long long w_c = 0, w_s = 0, w_p = 0;)
-    double Q[K > 1 ? K - 1 : 1];
-#pragma unroll
-    for (int k = 0; k < (K > 1 ? K - 1 : 1); ++k) Q[k] = 0.0;
-    for (int k = 0; k < K; ++k) wait_int(S.sready + (k < G ? k : G - 1) % ns, k < G ? k : G - 1, true);
-    double f1[8];
-    ld_block(slot_of(0), 0, f1);
-    wait_int(S.aready + 0, 0, true);
+    const uint8_t* const ringb = reinterpret_cast<const uint8_t*>(S.ring);
+    for (int k = 0; k < K; ++k) {
+      const int gk = k < G ? k : G - 1;
+      wait_eq(S.sready + gk % ns, gk);
+    }
+    wait_eq(S.aready + 0, 0);
+    asm volatile("" ::: "memory");
+    // slot cursors: s1 = slot of group g (+1: g+1, +2: g+2); advanced without a modulo
+    int s1 = 0, s2 = (1 < G ? 1 : 0) % ns, s3 = (2 < G ? 2 : G - 1) % ns;
+    auto slot_at = [&](int sl) { return S.slots + static_cast<size_t>(sl) * kBsSlotBytes; };
+    double f1[8], f2[8], f3[8];
+    ld_block(slot_at(s1), 0, f1);  // F_1 of group 0
+    ld_block(slot_at(s2), 1, f2);  // F_2 of group 1
+    ld_block(slot_at(s3), 2, f3);  // F_3 of group 2
     double c = S.cbuf[r];
+    double q0 = 0.0, q1 = 0.0;  // partial sums of groups g (terms k = 2, 3) and g + 1 (term k = 3)
     int pd = 0;
+    int yoff = (kBsR - 1) * 128 + hf * 64;  // ring bytes of y_{g-1}, this lane's half
+    int woff = r * 8;                       // ring bytes of y_g, this lane's row
     for (int g = 0; g < G; ++g) {
-      // ---- the critical chain: y_g = c_g - (Q + F_1 y_{g-1}) ----------------
-      const double2* yp =
-          reinterpret_cast<const double2*>(reinterpret_cast<const uint8_t*>(S.ring) + ((g + kBsR - 1) % kBsR) * 128 + hf * 64);
+      const double2* yp = reinterpret_cast<const double2*>(ringb + yoff);
       const double2 y0 = yp[0], y1 = yp[1], y2 = yp[2], y3 = yp[3];
+      // the chain
       double pa = f1[0] * y0.x, pb = f1[4] * y2.x;
       pa = fma(f1[1], y0.y, pa);
       pb = fma(f1[5], y2.y, pb);
@@ -250,51 +268,64 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       pb = fma(f1[6], y3.x, pb);
       pa = fma(f1[3], y1.y, pa);
       pb = fma(f1[7], y3.y, pb);
-      double t = pa + pb;
-      if (K > 1) t += Q[0];
+      double t = (pa + pb) + q0;
       t += bs_shfl_xor16(t);
       const double y = c - t;
-      if (hf == 0) S.ring[(g % kBsR) * kBsB + r] = y;
+      if (hf == 0) *reinterpret_cast<double*>(const_cast<uint8_t*>(ringb) + woff) = y;
+      // F_2 of group g+1 and F_3 of group g+2 on y_{g-1} (fills the chain's bubbles)
+      double ua = f2[0] * y0.x, ub = f2[4] * y2.x, va = f3[0] * y0.x, vb = f3[4] * y2.x;
+      ua = fma(f2[1], y0.y, ua);
+      ub = fma(f2[5], y2.y, ub);
+      va = fma(f3[1], y0.y, va);
+      vb = fma(f3[5], y2.y, vb);
+      ua = fma(f2[2], y1.x, ua);
+      ub = fma(f2[6], y3.x, ub);
+      va = fma(f3[2], y1.x, va);
+      vb = fma(f3[6], y3.x, vb);
+      ua = fma(f2[3], y1.y, ua);
+      ub = fma(f2[7], y3.y, ub);
+      va = fma(f3[3], y1.y, va);
+      vb = fma(f3[7], y3.y, vb);
+      q0 = q1 + (ua + ub);
+      q1 = va + vb;
       __syncwarp();
       if (lane == 0) *S.progress = g + 1;
-      // ---- off the chain: flags of the next step, future partial sums -------
-      const int gn = g + 1 < G ? g + 1 : G - 1;
-      const int gs = g + K < G ? g + K : G - 1;
-      const int fa = S.aready[gn % kBsRC];
-      const int fs = S.sready[gs % ns];
-      if (g + 1 - pd >= kBsR - 2) pd = *S.pubdone;
-#pragma unroll
-      for (int k = 2; k <= K; ++k) {
-        const int gk = g + k - 1 < G ? g + k - 1 : G - 1;
-        double fk[8];
-        ld_block(slot_of(gk), k - 1, fk);
-        double qa = fk[0] * y0.x, qb = fk[4] * y2.x;
-        qa = fma(fk[1], y0.y, qa);
-        qb = fma(fk[5], y2.y, qb);
-        qa = fma(fk[2], y1.x, qa);
-        qb = fma(fk[6], y3.x, qb);
-        qa = fma(fk[3], y1.y, qa);
-        qb = fma(fk[7], y3.y, qb);
-        Q[k - 2] = (k < K ? Q[k - 1] : 0.0) + (qa + qb);
+      // ---- the next step's operands --------------------------------------------
+      const int gn = g + 1 < G ? g + 1 : G - 1;  // clamped: the last steps reload the last slot
+      const int gs = g + K < G ? g + K : G - 1;  // newest group whose slot the next step touches
+      if (g + 1 < G) {
+        s1 = s2;
+        s2 = s3;
       }
+      if (g + 3 < G) s3 = s3 + 1 == ns ? 0 : s3 + 1;
+      const int fa = S.aready[gn & (kBsRC - 1)];
+      const int fs = S.sready[s3];
       if (fs != gs) {
         BS_DIAG(const long long tw = clock64();)
-        wait_int(S.sready + gs % ns, gs, true);
+        wait_eq(S.sready + s3, gs);
         BS_DIAG(w_s += clock64() - tw;)
       }
-      ld_block(slot_of(gn), 0, f1);
+      ld_block(slot_at(s1), 0, f1);
+      ld_block(slot_at(s2), 1, f2);
+      ld_block(slot_at(s3), 2, f3);
       if (fa != gn) {
         BS_DIAG(const long long tw = clock64();)
-        wait_int(S.aready + gn % kBsRC, gn, true);
+        wait_eq(S.aready + (gn & (kBsRC - 1)), gn);
         BS_DIAG(w_c += clock64() - tw;)
       }
       asm volatile("" ::: "memory");
-      c = S.cbuf[(gn % kBsRC) * kBsB + r];
+      c = S.cbuf[(gn & (kBsRC - 1)) * kBsB + r];
+      yoff = woff - r * 8 + hf * 64;
+      woff = woff + 128 == kBsZero + r * 8 ? r * 8 : woff + 128;
       if (g + 1 - pd >= kBsR - 2) {  // never lap the publisher on the y ring
-        BS_DIAG(const long long tw = clock64();)
-        wait_int(S.pubdone, g + 1 - (kBsR - 3), false);
         pd = *S.pubdone;
-        BS_DIAG(w_p += clock64() - tw;)
+        if (g + 1 - pd >= kBsR - 2) {
+          BS_DIAG(const long long tw = clock64();)
+          SpinGuard sg(abort_flag);
+          while ((pd = *S.pubdone) < g + 1 - (kBsR - 3))
+            if (sg.expired()) break;
+          BS_DIAG(w_p += clock64() - tw;)
+        }
       }
     }
     BS_DIAG(if (lane == 0) {
@@ -306,40 +337,63 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     })
   } else if (cid >= 0) {
     // ---- co-main: c_h = T_h (rhs_h - far_h - mid_h) ---------------------------
+    // A three-deep pipeline over this warp's groups h, h + NC, h + 2 NC: list
+    // sizes two groups ahead, mid-list staging (cp.async) and the right-hand
+    // side one group ahead, so no global-memory latency sits on a group's path.
     BS_DIAG(const long long t0 = clock64(); long long w_p = 0, w_f = 0;)
     const uint8_t* ringb = reinterpret_cast<const uint8_t*>(S.ring);
     uint8_t* const stage0 = S.stage + static_cast<size_t>(cid) * 2 * kBsStageBytes;
-    // stage the first min(mw, kBsStage) mid entries of group h (this lane's
-    // 16-byte units, lane-private: no cross-lane synchronization needed)
-    auto stage_group = [&](int h, int buf) {
+    struct Meta {
+      int mw, ms, fw;
+      int64_t mb;
+    };
+    auto load_meta = [&](int h) {
+      Meta m{0, 0, 0, 0};
       if (h < G) {
-        const int mw = min(__ldg(s.mw + h), kBsStage);
-        const int64_t mb = __ldg(s.mptr + h);
-        const int4* cp = reinterpret_cast<const int4*>(s.mcols + mb) + lane;
-        const double2* vp = reinterpret_cast<const double2*>(s.mvals + mb) + lane;
-        const unsigned dst = smem_u32(stage0 + static_cast<size_t>(buf) * kBsStageBytes) + lane * 16;
-        for (int c = 0; c < mw / kBsMC; ++c) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536), "l"(cp + c * 32) : "memory");
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536 + 512), "l"(vp + 2 * c * 32)
-                       : "memory");
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536 + 1024),
-                       "l"(vp + (2 * c + 1) * 32)
-                       : "memory");
-        }
+        m.mw = __ldg(s.mw + h);
+        m.ms = __ldg(s.ms + h);
+        m.fw = __ldg(s.fw + h);
+        m.mb = __ldg(s.mptr + h);
+      }
+      return m;
+    };
+    // stage the first min(mw, kBsStage) mid entries of a group (lane-private units)
+    auto stage_group = [&](const Meta& m, int buf) {
+      const int mw = min(m.mw, kBsStage);
+      const int4* cp = reinterpret_cast<const int4*>(s.mcols + m.mb) + lane;
+      const double2* vp = reinterpret_cast<const double2*>(s.mvals + m.mb) + lane;
+      const unsigned dst = smem_u32(stage0 + static_cast<size_t>(buf) * kBsStageBytes) + lane * 16;
+      for (int c = 0; c < mw / kBsMC; ++c) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536), "l"(cp + c * 32) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536 + 512), "l"(vp + 2 * c * 32)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536 + 1024),
+                     "l"(vp + (2 * c + 1) * 32)
+                     : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    auto load_rhs = [&](int h) {
+      const int p = h * kBsB + r;
+      return (hf == 0 && p < n) ? __ldcg(rhs + orig(p)) : 0.0;
+    };
     int prog = 0;  // last progress value seen
-    stage_group(cid, 0);
+    Meta m0 = load_meta(cid), m1 = load_meta(cid + kBsNC);
+    stage_group(m0, 0);
+    double rhs0 = load_rhs(cid);
     int buf = 0;
     for (int h = cid; h < G; h += kBsNC, buf ^= 1) {
-      stage_group(h + kBsNC, buf ^ 1);
-      const int p = h * kBsB + r;
-      double acc = (hf == 0 && p < n) ? __ldcg(rhs + orig(p)) : 0.0;
-      const int mw = __ldg(s.mw + h), ms = __ldg(s.ms + h), fw = __ldg(s.fw + h);
-      const int64_t mb = __ldg(s.mptr + h);
-      const int4* cp = reinterpret_cast<const int4*>(s.mcols + mb) + lane;
-      const double2* vp = reinterpret_cast<const double2*>(s.mvals + mb) + lane;
+      const Meta m2 = load_meta(h + 2 * kBsNC);
+      stage_group(m1, buf ^ 1);
+      const double rhs1 = load_rhs(h + kBsNC);
+      // the far partial sum of this lane's row: the load is the poll
+      const uint4* fp = F.fps + static_cast<int64_t>(h) * kBsB + r;
+      uint4 fw0 = make_uint4(0u, 0u, 0u, 0u);
+      if (m0.fw > 0 && hf == 0) fw0 = __ldcg(fp);
+      double acc = rhs0;
+      const int mw = m0.mw, ms = m0.ms;
+      const int4* cp = reinterpret_cast<const int4*>(s.mcols + m0.mb) + lane;
+      const double2* vp = reinterpret_cast<const double2*>(s.mvals + m0.mb) + lane;
       const uint8_t* sbuf = stage0 + static_cast<size_t>(buf) * kBsStageBytes + lane * 16;
       auto wait_progress = [&](int need) {
         if (prog >= need) return;
@@ -390,24 +444,27 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       // entries that only need groups <= h-K-3
       wait_progress(h - K - 2);
       chunks(0, ms);
-      if (fw > 0) {  // far partial sum of this lane's row
-        BS_DIAG(const long long tw = clock64();)
-        SpinGuard sg(abort_flag);
-        while (ld_acquire(F.fflag + h) != F.tag) {
-          __nanosleep(40);
-          if (sg.expired()) break;
+      if (m0.fw > 0 && hf == 0) {
+        if (!bs_valid(fw0, F.tag)) {
+          BS_DIAG(const long long tw = clock64();)
+          SpinGuard sg(abort_flag);
+          do {
+            fw0 = __ldcg(fp);
+          } while (!bs_valid(fw0, F.tag) && !sg.expired());
+          BS_DIAG(w_f += clock64() - tw;)
         }
-        BS_DIAG(w_f += clock64() - tw;)
-        if (hf == 0) acc -= __ldcg(F.fpsum + static_cast<int64_t>(h) * kBsB + r);
+        acc -= bs_value(fw0);
       }
       // the newest mid entries need group h-K-1
       wait_progress(h - K);
       chunks(ms, mw);
       const double t = acc + bs_shfl_xor16(acc);
       // c = T t: this lane's half of row r; t_m lives in lane m
-      if (S.sready[h % ns] != h) wait_int(S.sready + h % ns, h, true);
+      const int sl = h % ns;
+      if (S.sready[sl] != h) wait_eq(S.sready + sl, h);
+      asm volatile("" ::: "memory");
       double tr[8];
-      ld_block(slot_of(h), K, tr);
+      ld_block(S.slots + static_cast<size_t>(sl) * kBsSlotBytes, K, tr);
       double ca = 0.0, cb = 0.0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -417,12 +474,15 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       double cv = ca + cb;
       cv += bs_shfl_xor16(cv);
       wait_progress(h - kBsRC + 1);  // the c ring slot is free
-      if (hf == 0) S.cbuf[(h % kBsRC) * kBsB + r] = cv;
+      if (hf == 0) S.cbuf[(h & (kBsRC - 1)) * kBsB + r] = cv;
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
-        S.aready[h % kBsRC] = h;
+        S.aready[h & (kBsRC - 1)] = h;
       }
+      m0 = m1;
+      m1 = m2;
+      rhs0 = rhs1;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     BS_DIAG(if (lane == 0) {
@@ -432,24 +492,24 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     })
   } else if (warp == prodw) {
     if (lane == 0) {
-      int issued = 0, done = 0;
+      int issued = 0, done = 0, isl = 0, dsl = 0;
       SpinGuard sg(abort_flag);
       while (done < G) {
         bool idle = true;
         if (issued < G && *S.progress >= issued - ns + 1) {
-          const int sl = issued % ns;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_expect_tx(S.mbar + sl, kBsSlotBytes);
-          bulk_g2s(S.slots + static_cast<size_t>(sl) * kBsSlotBytes,
-                   s.slots + static_cast<size_t>(issued) * kBsSlotBytes, kBsSlotBytes, S.mbar + sl);
+          mbar_expect_tx(S.mbar + isl, kBsSlotBytes);
+          bulk_g2s(S.slots + static_cast<size_t>(isl) * kBsSlotBytes,
+                   s.slots + static_cast<size_t>(issued) * kBsSlotBytes, kBsSlotBytes, S.mbar + isl);
           ++issued;
+          isl = isl + 1 == ns ? 0 : isl + 1;
           idle = false;
         }
         if (done < issued) {
-          const int sl = done % ns;
-          if (mbar_poll(S.mbar + sl, (S.base_use[sl] + done / ns) & 1)) {
-            S.sready[sl] = done;
+          if (mbar_poll(S.mbar + dsl, (S.base_use[dsl] + done / ns) & 1)) {
+            S.sready[dsl] = done;
             ++done;
+            dsl = dsl + 1 == ns ? 0 : dsl + 1;
             idle = false;
           }
         }
@@ -461,7 +521,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       }
     }
   } else if (warp == pubw) {
-    // ---- publisher: y ring -> result vector, then the progress word ----------
+    // ---- publisher: y ring -> the result vector (plain and tagged) -------------
     int done = 0;
     SpinGuard sg(abort_flag);
     while (done < G) {
@@ -470,14 +530,15 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
         asm volatile("" ::: "memory");
         for (int g = done + hf; g < pnow; g += 2) {
           const int p = g * kBsB + r;
-          if (p < n) __stcg(gx + orig(p), S.ring[(g % kBsR) * kBsB + r]);
+          if (p < n) {
+            const double v = S.ring[(g & (kBsR - 1)) * kBsB + r];
+            const int o = orig(p);
+            __stcg(F.gt + o, bs_pack(v, F.tag));
+            __stcg(gx + o, v);
+          }
         }
-        __threadfence();
         __syncwarp();
-        if (lane == 0) {
-          bs_st_release_u64(F.gprog, (static_cast<unsigned long long>(F.tag) << 32) | static_cast<unsigned>(pnow));
-          *S.pubdone = pnow;
-        }
+        if (lane == 0) *S.pubdone = pnow;
         done = pnow;
         sg.t0 = clock64();
       } else if (sg.expired()) {
@@ -495,7 +556,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
         ++cnt;
       }
     }
-    bs_far(s, gx, F, idx, cnt, abort_flag);
+    bs_far(s, F, idx, cnt, abort_flag);
   }
   __syncthreads();
   if (threadIdx.x < ns) {

@@ -82,7 +82,8 @@ struct HostBSweep {
   std::vector<double> mvals;
   std::vector<int32_t> fw;           // far list: width (multiple of kBsFC; 0 = none)
   std::vector<int64_t> fptr;         // G + 1
-  std::vector<int32_t> fcols;        // rows of the result vector (original ordering; pad: n, x[n] = 0)
+  std::vector<int32_t> fcols;        // rows of the result vector (original ordering); padding entries
+                                     //   (value 0) point at the group's oldest far column
   std::vector<double> fvals;
   std::vector<int32_t> fcptr;        // G + 1: first chunk of the group in fneed
   std::vector<int32_t> fneed;        // per chunk: newest group it depends on (-1: none)

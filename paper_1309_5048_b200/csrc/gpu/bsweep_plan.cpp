@@ -6,6 +6,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -136,6 +137,22 @@ void build_dir(int n, int dir, RowFn rows, HostBSweep& s) {
             fneed[pos / kBsFC] = std::max(fneed[pos / kBsFC], e.first / kBsB);
           }
         }
+      }
+      // far padding gathers a real, already published entry (times 0): the
+      // group's oldest far column, which every lane's first chunk waits for anyway
+      if (wf > 0) {
+        int32_t oldest = INT32_MAX;
+        for (int r = 0; r < kBsB; ++r) {
+          const int p = g * kBsB + r;
+          if (p >= n) break;
+          double d;
+          rows(p, ent, d);
+          if (!ent.empty() && g - ent.front().first / kBsB > kBsR) oldest = std::min(oldest, ent.front().first);
+        }
+        const int32_t pad = dir ? n - 1 - oldest : oldest;
+        for (int lane = 0; lane < 32; ++lane)
+          for (int k = 0; k < wf; ++k)
+            if (fv[bs_f64_at(k, lane)] == 0.0 && fc[bs_i32_at(k, lane)] == n) fc[bs_i32_at(k, lane)] = pad;
       }
       // leading mid chunks that are computable two groups early
       int early = 0;

@@ -96,8 +96,8 @@ struct DBlock {
   // blocked sweeps (bsweep.cuh): remote_cta0 / n_remote name the far-worker CTAs
   int bs, bs_ns;                // 1: blocked sweeps; slot-ring depth
   DBSweep bfwd, bbwd;
-  double* fpsum;                // max(G) * 16 far partial sums
-  unsigned* fflag;              // max(G)
+  uint4* bs_gt;                 // n + 1: tagged copy of the sweep result (far workers gather it)
+  uint4* bs_fps;                // max(G) * 16: tagged far partial sums
 };
 
 struct DevReport {
@@ -847,9 +847,9 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
     // blocked sweeps (bsweep.cuh): results go to global memory (y, then z)
     const int workers = B.n_remote * static_cast<int>(blockDim.x >> 5);
     bsweep<kBsK>(B.bfwd, xf, B.bs_ns, bb, y,
-                 BsFar{B.fpsum, B.fflag, B.gprog, sweep_tag(launch_id, sweep_no), workers}, abort_flag);
+                 BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no), workers}, abort_flag);
     bsweep<kBsK>(B.bbwd, xf, B.bs_ns, y, z,
-                 BsFar{B.fpsum, B.fflag, B.gprog, sweep_tag(launch_id, sweep_no + 1), workers}, abort_flag);
+                 BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no + 1), workers}, abort_flag);
     for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += r[i] * z[i];
     return block_sum(rz, red);
   } else if constexpr (RING) {
@@ -879,13 +879,12 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
 }
 
 // What a remote helper CTA does while the IC CTA runs one IC(0) apply.
-__device__ void ic_apply_remote(const DBlock& B, int rank, unsigned* abort_flag, unsigned launch_id,
-                                unsigned sweep_no) {
+__device__ __noinline__ void ic_apply_remote(const DBlock& B, int rank, unsigned* abort_flag, unsigned launch_id,
+                                             unsigned sweep_no) {
   if (B.bs) {  // far workers of the blocked sweeps: every warp of this CTA
     const int nw = blockDim.x >> 5, W = B.n_remote * nw, wid = rank * nw + (threadIdx.x >> 5);
-    bs_far(B.bfwd, B.y, BsFar{B.fpsum, B.fflag, B.gprog, sweep_tag(launch_id, sweep_no), W}, wid, W, abort_flag);
-    bs_far(B.bbwd, B.z, BsFar{B.fpsum, B.fflag, B.gprog, sweep_tag(launch_id, sweep_no + 1), W}, wid, W,
-           abort_flag);
+    bs_far(B.bfwd, BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no), W}, wid, W, abort_flag);
+    bs_far(B.bbwd, BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no + 1), W}, wid, W, abort_flag);
     return;
   }
   flow_remote(B.ffwd, B.n, B.y,
@@ -1295,8 +1294,9 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
 
 // IC(0) server CTA of block b: answers the workers' apply requests until told
 // to exit. Runs no MINRES code, so the sweep's registers are its own.
+// (not inlined: its register allocation stays separate from the MINRES code's)
 template <int TB, bool RING>
-__device__ void ic_server(const Args& a, int b, double* xs, double* red) {
+__device__ __noinline__ void ic_server(const Args& a, int b, double* xs, double* red) {
   const DBlock& B = a.blk[b];
   if (B.kind != DSGPU_BLOCK_PCG_IC0) return;
   Mailbox* m = a.mbox + b;
@@ -2233,11 +2233,11 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         d.bb = h->alloc<double>(hb.n + 1);
         cudaMemset(d.y, 0, sizeof(double) * (hb.n + 1));
         cudaMemset(d.bb, 0, sizeof(double) * (hb.n + 1));
-        d.fpsum = h->alloc<double>(static_cast<size_t>(G_max) * kBsB);
-        d.fflag = h->alloc<unsigned>(static_cast<size_t>(G_max));
-        d.gprog = h->alloc<unsigned long long>(1);
-        cudaMemset(d.fflag, 0, sizeof(unsigned) * G_max);
-        cudaMemset(d.gprog, 0, sizeof(unsigned long long));
+        // tag 0 is never a sweep's tag (launch ids start at 1): zeroed = "not written"
+        d.bs_gt = h->alloc<uint4>(static_cast<size_t>(hb.n) + 1);
+        d.bs_fps = h->alloc<uint4>(static_cast<size_t>(G_max) * kBsB);
+        cudaMemset(d.bs_gt, 0, sizeof(uint4) * (static_cast<size_t>(hb.n) + 1));
+        cudaMemset(d.bs_fps, 0, sizeof(uint4) * static_cast<size_t>(G_max) * kBsB);
         d.n_remote = h->far_ctas[b];
         d.remote_cta0 = 1 + (b == 1 ? h->far_ctas[0] : 0);  // worker units (Ctx::remote_rank)
       } else if (hb.kind == DSGPU_BLOCK_PCG_IC0) {

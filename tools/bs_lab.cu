@@ -165,34 +165,58 @@ __global__ void lat(unsigned long long* out, double seed) {
 // ---- 3. publish -> observe: CTA 0 stores 16 doubles + fence + release flag;
 // CTA `peer` polls with ld.acquire and reads the data; it answers through its
 // own flag. Round trip / 2 = one publish hop.
+// MODE 0: every lane fences (__threadfence), syncwarp, release flag.
+// MODE 1: syncwarp, then lane 0's st.release alone (cumulative release).
+// MODE 2: no flag: each double travels as two 8-byte {half, tag} words
+//         (LL-style, self-validating); the consumer polls the data itself.
+template <int MODE>
 __global__ void hop(double* data, unsigned* flags, int iters, int peer, unsigned long long* out) {
   if (blockIdx.x != 0 && blockIdx.x != peer) return;
   const bool a = blockIdx.x == 0;
   const int lane = threadIdx.x;
   unsigned* mine = flags + (a ? 0 : 64);
   unsigned* theirs = flags + (a ? 64 : 0);
-  double* dout = data + (a ? 0 : 64);
-  const double* din = data + (a ? 64 : 0);
+  double* dout = data + (a ? 0 : 128);
+  const double* din = data + (a ? 128 : 0);
   double v = lane;
   const long long c0 = clock64();
   for (int k = 1; k <= iters; ++k) {
-    if (a) {
+    auto send = [&]() {
+      if (MODE == 2) {
+        if (lane < 16) {
+          const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+          uint4 w;
+          w.x = static_cast<unsigned>(b);
+          w.y = k;
+          w.z = static_cast<unsigned>(b >> 32);
+          w.w = k;
+          __stcg(reinterpret_cast<uint4*>(dout) + lane, w);
+        }
+        return;
+      }
       if (lane < 16) __stcg(dout + lane, v);
-      __threadfence();
+      if (MODE == 0) __threadfence();
       __syncwarp();
       if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(theirs), "r"(k) : "memory");
-    }
-    unsigned f;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(mine) : "memory");
-    } while (f != static_cast<unsigned>(k));
-    v = __ldcg(din + (lane & 15)) + 1.0;
-    if (!a) {
-      if (lane < 16) __stcg(dout + lane, v);
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(theirs), "r"(k) : "memory");
-    }
+    };
+    auto recv = [&]() {
+      if (MODE == 2) {
+        uint4 w;
+        do {
+          w = __ldcg(reinterpret_cast<const uint4*>(din) + (lane & 15));
+        } while (w.y != static_cast<unsigned>(k) || w.w != static_cast<unsigned>(k));
+        v = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(w.z) << 32) | w.x)) + 1.0;
+        return;
+      }
+      unsigned f;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(mine) : "memory");
+      } while (f != static_cast<unsigned>(k));
+      v = __ldcg(din + (lane & 15)) + 1.0;
+    };
+    if (a) send();
+    recv();
+    if (!a) send();
   }
   if (a && lane == 0) {
     out[0] = clock64() - c0;
@@ -200,7 +224,8 @@ __global__ void hop(double* data, unsigned* flags, int iters, int peer, unsigned
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const bool only_lat = argc > 1;
   unsigned long long* out;
   CK(cudaMalloc(&out, 8192 * 8));
   std::vector<unsigned long long> h(2048);
@@ -210,6 +235,7 @@ int main() {
   CK(cudaMemset(src, 1, big));
   CK(cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   for (int ctas : {1, 2, 8, 32, 148}) {
+    if (only_lat) break;
     for (size_t per : {size_t(4) << 20, size_t(1) << 20}) {  // 4 MiB (x reps) and L2-resident 1 MiB
       const int reps = per == (size_t(1) << 20) ? 16 : 4;
       ldg_stream<<<ctas, 512>>>(reinterpret_cast<const int4*>(src), per, 1, out);  // warm
@@ -233,7 +259,7 @@ int main() {
       }
     }
   }
-  {  // cold (HBM) single-CTA TMA: a fresh 64 MiB region
+  if (!only_lat) {  // cold (HBM) single-CTA TMA: a fresh 64 MiB region
     tma_stream<<<1, 64, 1024 + 8192 * 8>>>(src + (size_t(512) << 20), size_t(64) << 20, 8192, 8, out);
     CK(cudaMemcpy(h.data(), out, 8, cudaMemcpyDeviceToHost));
     printf("TMA bulk stream  1 CTA 64 MiB cold (HBM): %.1f B/clk\n", double(size_t(64) << 20) / h[0]);
@@ -249,15 +275,19 @@ int main() {
          h[0] / N, h[1] / N, h[2] / N, h[3] / N, h[4] / N, h[5] / N);
   double* data;
   unsigned* flags;
-  CK(cudaMalloc(&data, 4096));
+  CK(cudaMalloc(&data, 8192));
   CK(cudaMalloc(&flags, 4096));
-  for (int peer : {1, 2, 74, 147}) {
-    CK(cudaMemset(flags, 0, 4096));
-    hop<<<148, 32>>>(data, flags, 2000, peer, out);
-    CK(cudaMemcpy(h.data(), out, 16, cudaMemcpyDeviceToHost));
-    printf("publish hop (16 doubles + fence + release flag -> acquire poll + read), peer CTA %3d: %.0f cycles one way\n",
-           peer, double(h[0]) / 2000 / 2);
-  }
+  for (int mode = 0; mode < 3; ++mode)
+    for (int peer : {1, 74, 147}) {
+      CK(cudaMemset(flags, 0, 4096));
+      CK(cudaMemset(data, 0, 4096));
+      if (mode == 0) hop<0><<<148, 32>>>(data, flags, 2000, peer, out);
+      if (mode == 1) hop<1><<<148, 32>>>(data, flags, 2000, peer, out);
+      if (mode == 2) hop<2><<<148, 32>>>(data, flags, 2000, peer, out);
+      CK(cudaMemcpy(h.data(), out, 16, cudaMemcpyDeviceToHost));
+      printf("publish hop mode %d (0: all-lane fence + release flag, 1: syncwarp + release flag, 2: {half,tag} words), "
+             "peer CTA %3d: %.0f cycles one way\n", mode, peer, double(h[0]) / 2000 / 2);
+    }
   CK(cudaDeviceSynchronize());
   printf("ok\n");
   return 0;
