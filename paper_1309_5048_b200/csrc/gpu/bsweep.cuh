@@ -40,6 +40,17 @@ __device__ __forceinline__ uint4 bs_pack(double v, unsigned tag) {
   return make_uint4(static_cast<unsigned>(b), tag, static_cast<unsigned>(b >> 32), tag);
 }
 __device__ __forceinline__ bool bs_valid(const uint4& w, unsigned tag) { return w.y == tag && w.w == tag; }
+// Re-read of a tagged unit inside a polling loop: volatile, so the compiler can
+// neither hoist it out of the loop nor merge it with the first read (__ldcg is
+// a plain asm the optimizer treats as a pure function of its address).
+__device__ __forceinline__ uint4 bs_poll(const uint4* p) {
+  uint4 w;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "l"(p)
+               : "memory");
+  return w;
+}
 __device__ __forceinline__ double bs_value(const uint4& w) {
   return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(w.z) << 32) | w.x));
 }
@@ -49,7 +60,9 @@ __device__ __forceinline__ double bs_value(const uint4& w) {
 #ifdef DSGPU_DIAG
 // [0] main cycles, [1] main cycles waiting for c, [2] for slots, [3] for the
 // publisher, [4] groups, [5] co-main cycles waiting for progress, [6] for far
-// sums, [7] co-main cycles, [8] far-worker cycles waiting, [9] far-worker cycles
+// sums, [7] co-main cycles, [8] far-worker cycles waiting, [9] far-worker cycles,
+// [10..13] co-main cycles by stage: prefetch + staging wait, mid lists (incl.
+// waits), T product, hand-off
 __device__ unsigned long long g_bs_dbg[16];
 #define BS_DIAG(...) __VA_ARGS__
 #else
@@ -152,14 +165,14 @@ __device__ void bs_far(const DBSweep& s, BsFar F, int wid, int W, unsigned* abor
         do {
           __nanosleep(ns_sleep);
           ns_sleep = min(2000u, ns_sleep * 2);
-          w0 = __ldcg(gt + ca.x);
-          w1 = __ldcg(gt + ca.y);
-          w2 = __ldcg(gt + ca.z);
-          w3 = __ldcg(gt + ca.w);
-          w4 = __ldcg(gt + cb.x);
-          w5 = __ldcg(gt + cb.y);
-          w6 = __ldcg(gt + cb.z);
-          w7 = __ldcg(gt + cb.w);
+          w0 = bs_poll(gt + ca.x);
+          w1 = bs_poll(gt + ca.y);
+          w2 = bs_poll(gt + ca.z);
+          w3 = bs_poll(gt + ca.w);
+          w4 = bs_poll(gt + cb.x);
+          w5 = bs_poll(gt + cb.y);
+          w6 = bs_poll(gt + cb.z);
+          w7 = bs_poll(gt + cb.w);
         } while (!all_valid() && !sg.expired());
         BS_DIAG(t_wait += clock64() - tw;)
       }
@@ -239,15 +252,17 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     // later groups are applied to y_{g-1} right after the chain.
     BS_DIAG(const long long t0 = clock64(); long long w_c = 0, w_s = 0, w_p = 0;)
     const uint8_t* const ringb = reinterpret_cast<const uint8_t*>(S.ring);
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k <= K; ++k) {
       const int gk = k < G ? k : G - 1;
       wait_eq(S.sready + gk % ns, gk);
     }
     wait_eq(S.aready + 0, 0);
     asm volatile("" ::: "memory");
-    // slot cursors: s1 = slot of group g (+1: g+1, +2: g+2); advanced without a modulo
-    int s1 = 0, s2 = (1 < G ? 1 : 0) % ns, s3 = (2 < G ? 2 : G - 1) % ns;
+    // slot cursors: s1, s2, s3 = slots of groups g, g+1, g+2 (clamped to the
+    // last group), advanced without a modulo
+    int s1 = 0, s2 = (1 < G ? 1 : G - 1) % ns, s3 = (2 < G ? 2 : G - 1) % ns;
     auto slot_at = [&](int sl) { return S.slots + static_cast<size_t>(sl) * kBsSlotBytes; };
+    auto next_slot = [&](int sl) { return sl + 1 == ns ? 0 : sl + 1; };
     double f1[8], f2[8], f3[8];
     ld_block(slot_at(s1), 0, f1);  // F_1 of group 0
     ld_block(slot_at(s2), 1, f2);  // F_2 of group 1
@@ -257,57 +272,62 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     int pd = 0;
     int yoff = (kBsR - 1) * 128 + hf * 64;  // ring bytes of y_{g-1}, this lane's half
     int woff = r * 8;                       // ring bytes of y_g, this lane's row
+    // invariant at the top of step g: the slots of groups <= g+3 have landed
     for (int g = 0; g < G; ++g) {
       const double2* yp = reinterpret_cast<const double2*>(ringb + yoff);
       const double2 y0 = yp[0], y1 = yp[1], y2 = yp[2], y3 = yp[3];
-      // the chain
+      // all products with y_{g-1}: F_1 of g (the chain), F_2 of g+1, F_3 of g+2
       double pa = f1[0] * y0.x, pb = f1[4] * y2.x;
+      double ua = f2[0] * y0.x, ub = f2[4] * y2.x, va = f3[0] * y0.x, vb = f3[4] * y2.x;
       pa = fma(f1[1], y0.y, pa);
       pb = fma(f1[5], y2.y, pb);
-      pa = fma(f1[2], y1.x, pa);
-      pb = fma(f1[6], y3.x, pb);
-      pa = fma(f1[3], y1.y, pa);
-      pb = fma(f1[7], y3.y, pb);
-      double t = (pa + pb) + q0;
-      t += bs_shfl_xor16(t);
-      const double y = c - t;
-      if (hf == 0) *reinterpret_cast<double*>(const_cast<uint8_t*>(ringb) + woff) = y;
-      // F_2 of group g+1 and F_3 of group g+2 on y_{g-1} (fills the chain's bubbles)
-      double ua = f2[0] * y0.x, ub = f2[4] * y2.x, va = f3[0] * y0.x, vb = f3[4] * y2.x;
       ua = fma(f2[1], y0.y, ua);
       ub = fma(f2[5], y2.y, ub);
       va = fma(f3[1], y0.y, va);
       vb = fma(f3[5], y2.y, vb);
+      pa = fma(f1[2], y1.x, pa);
+      pb = fma(f1[6], y3.x, pb);
       ua = fma(f2[2], y1.x, ua);
       ub = fma(f2[6], y3.x, ub);
       va = fma(f3[2], y1.x, va);
       vb = fma(f3[6], y3.x, vb);
+      pa = fma(f1[3], y1.y, pa);
+      pb = fma(f1[7], y3.y, pb);
       ua = fma(f2[3], y1.y, ua);
       ub = fma(f2[7], y3.y, ub);
       va = fma(f3[3], y1.y, va);
       vb = fma(f3[7], y3.y, vb);
-      q0 = q1 + (ua + ub);
-      q1 = va + vb;
-      __syncwarp();
-      if (lane == 0) *S.progress = g + 1;
-      // ---- the next step's operands --------------------------------------------
-      const int gn = g + 1 < G ? g + 1 : G - 1;  // clamped: the last steps reload the last slot
-      const int gs = g + K < G ? g + K : G - 1;  // newest group whose slot the next step touches
+      // the next step's coupling rows (their slots have landed: invariant) and the
+      // flags of the step after it, issued under the latency of the chain's tail
       if (g + 1 < G) {
         s1 = s2;
         s2 = s3;
       }
-      if (g + 3 < G) s3 = s3 + 1 == ns ? 0 : s3 + 1;
-      const int fa = S.aready[gn & (kBsRC - 1)];
-      const int fs = S.sready[s3];
-      if (fs != gs) {
-        BS_DIAG(const long long tw = clock64();)
-        wait_eq(S.sready + s3, gs);
-        BS_DIAG(w_s += clock64() - tw;)
-      }
+      if (g + 3 < G) s3 = next_slot(s3);
       ld_block(slot_at(s1), 0, f1);
       ld_block(slot_at(s2), 1, f2);
       ld_block(slot_at(s3), 2, f3);
+      const int gn = g + 1 < G ? g + 1 : G - 1;
+      const int gs = g + K + 1 < G ? g + K + 1 : G - 1;  // newest slot the step after next touches
+      const int s4 = g + K + 1 < G ? next_slot(s3) : s3;
+      const int fa = S.aready[gn & (kBsRC - 1)];
+      const int fs = S.sready[s4];
+      // the chain's tail
+      double t = (pa + pb) + q0;
+      t += bs_shfl_xor16(t);
+      const double y = c - t;
+      if (hf == 0) *reinterpret_cast<double*>(const_cast<uint8_t*>(ringb) + woff) = y;
+      q0 = q1 + (ua + ub);
+      q1 = va + vb;
+      __syncwarp();
+      if (lane == 0) *S.progress = g + 1;
+      yoff = woff - r * 8 + hf * 64;
+      woff = woff + 128 == kBsZero + r * 8 ? r * 8 : woff + 128;
+      if (fs != gs) {
+        BS_DIAG(const long long tw = clock64();)
+        wait_eq(S.sready + s4, gs);
+        BS_DIAG(w_s += clock64() - tw;)
+      }
       if (fa != gn) {
         BS_DIAG(const long long tw = clock64();)
         wait_eq(S.aready + (gn & (kBsRC - 1)), gn);
@@ -315,8 +335,6 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       }
       asm volatile("" ::: "memory");
       c = S.cbuf[(gn & (kBsRC - 1)) * kBsB + r];
-      yoff = woff - r * 8 + hf * 64;
-      woff = woff + 128 == kBsZero + r * 8 ? r * 8 : woff + 128;
       if (g + 1 - pd >= kBsR - 2) {  // never lap the publisher on the y ring
         pd = *S.pubdone;
         if (g + 1 - pd >= kBsR - 2) {
@@ -340,7 +358,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     // A three-deep pipeline over this warp's groups h, h + NC, h + 2 NC: list
     // sizes two groups ahead, mid-list staging (cp.async) and the right-hand
     // side one group ahead, so no global-memory latency sits on a group's path.
-    BS_DIAG(const long long t0 = clock64(); long long w_p = 0, w_f = 0;)
+    BS_DIAG(const long long t0 = clock64(); long long w_p = 0, w_f = 0, d_a = 0, d_b = 0, d_c = 0, d_d = 0;)
     const uint8_t* ringb = reinterpret_cast<const uint8_t*>(S.ring);
     uint8_t* const stage0 = S.stage + static_cast<size_t>(cid) * 2 * kBsStageBytes;
     struct Meta {
@@ -383,6 +401,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     double rhs0 = load_rhs(cid);
     int buf = 0;
     for (int h = cid; h < G; h += kBsNC, buf ^= 1) {
+      BS_DIAG(const long long ta = clock64();)
       const Meta m2 = load_meta(h + 2 * kBsNC);
       stage_group(m1, buf ^ 1);
       const double rhs1 = load_rhs(h + kBsNC);
@@ -441,6 +460,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       };
       // this group's staged list has landed (all but the newest commit group)
       asm volatile("cp.async.wait_group 1;" ::: "memory");
+      BS_DIAG(const long long tb = clock64(); d_a += tb - ta;)
       // entries that only need groups <= h-K-3
       wait_progress(h - K - 2);
       chunks(0, ms);
@@ -449,7 +469,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
           BS_DIAG(const long long tw = clock64();)
           SpinGuard sg(abort_flag);
           do {
-            fw0 = __ldcg(fp);
+            fw0 = bs_poll(fp);
           } while (!bs_valid(fw0, F.tag) && !sg.expired());
           BS_DIAG(w_f += clock64() - tw;)
         }
@@ -459,6 +479,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       wait_progress(h - K);
       chunks(ms, mw);
       const double t = acc + bs_shfl_xor16(acc);
+      BS_DIAG(const long long tc = clock64(); d_b += tc - tb;)
       // c = T t: this lane's half of row r; t_m lives in lane m
       const int sl = h % ns;
       if (S.sready[sl] != h) wait_eq(S.sready + sl, h);
@@ -473,6 +494,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       }
       double cv = ca + cb;
       cv += bs_shfl_xor16(cv);
+      BS_DIAG(const long long td = clock64(); d_c += td - tc;)
       wait_progress(h - kBsRC + 1);  // the c ring slot is free
       if (hf == 0) S.cbuf[(h & (kBsRC - 1)) * kBsB + r] = cv;
       __syncwarp();
@@ -483,12 +505,17 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       m0 = m1;
       m1 = m2;
       rhs0 = rhs1;
+      BS_DIAG(d_d += clock64() - td;)
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     BS_DIAG(if (lane == 0) {
       atomicAdd(&g_bs_dbg[5], static_cast<unsigned long long>(w_p));
       atomicAdd(&g_bs_dbg[6], static_cast<unsigned long long>(w_f));
       atomicAdd(&g_bs_dbg[7], static_cast<unsigned long long>(clock64() - t0));
+      atomicAdd(&g_bs_dbg[10], static_cast<unsigned long long>(d_a));
+      atomicAdd(&g_bs_dbg[11], static_cast<unsigned long long>(d_b));
+      atomicAdd(&g_bs_dbg[12], static_cast<unsigned long long>(d_c));
+      atomicAdd(&g_bs_dbg[13], static_cast<unsigned long long>(d_d));
     })
   } else if (warp == prodw) {
     if (lane == 0) {
