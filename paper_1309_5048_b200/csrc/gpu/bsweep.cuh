@@ -62,7 +62,8 @@ __device__ __forceinline__ double bs_value(const uint4& w) {
 // publisher, [4] groups, [5] co-main cycles waiting for progress, [6] for far
 // sums, [7] co-main cycles, [8] far-worker cycles waiting, [9] far-worker cycles,
 // [10..13] co-main cycles by stage: prefetch + staging wait, mid lists (incl.
-// waits), T product, hand-off
+// waits), T product, hand-off, [14] main cycles waiting for q, [15] second-main
+// cycles waiting for y
 __device__ unsigned long long g_bs_dbg[16];
 #define BS_DIAG(...) __VA_ARGS__
 #else
@@ -72,16 +73,22 @@ __device__ unsigned long long g_bs_dbg[16];
 __device__ __forceinline__ double bs_shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ double bs_shfl_xor16(double v) { return __shfl_xor_sync(0xffffffffu, v, 16); }
 
+// Co-main warps: the warps 0, 1, 2, 4, 5, 6, 8, 9, 10 (never 3 mod 4: that SM
+// sub-partition belongs to the main warp).
+__device__ __forceinline__ int bs_comain_warp(int i) { return i + i / 3; }
+
 // Shared-memory workspace of the sweep CTA.
 struct BsSmem {
   double* ring;             // kBsR groups x 16 results, then the zero slot
   double* cbuf;             // kBsRC x 16 (co-main -> main)
+  double* qbuf;             // kBsRQ x 32 lane partials (second main -> main)
   uint8_t* slots;           // ns x kBsSlotBytes
   uint8_t* stage;           // kBsNC x 2 x kBsStageBytes: co-main mid-list staging
   uint64_t* mbar;           // ns
   volatile int* sready;     // ns: group whose blocks have landed in the slot
   int* base_use;            // ns: completed mbarrier phases before this sweep
   volatile int* aready;     // kBsRC: group whose c is staged
+  volatile int* qready;     // kBsRQ: group whose q is staged
   volatile int* progress;   // groups finished by the main warp
   volatile int* pubdone;    // groups copied to global memory by the publisher
   int ns;
@@ -93,6 +100,8 @@ struct BsSmem {
     p += kBsZero + 128;
     cbuf = reinterpret_cast<double*>(p);
     p += kBsRC * kBsB * 8;
+    qbuf = reinterpret_cast<double*>(p);
+    p += kBsRQ * 32 * 8;
     slots = p;
     p += static_cast<size_t>(ns) * kBsSlotBytes;
     stage = p;
@@ -102,7 +111,8 @@ struct BsSmem {
     sready = reinterpret_cast<volatile int*>(p);
     base_use = reinterpret_cast<int*>(p) + ns;
     aready = reinterpret_cast<volatile int*>(p) + 2 * ns;
-    progress = aready + kBsRC;
+    qready = aready + kBsRC;
+    progress = qready + kBsRQ;
     pubdone = progress + 1;
   }
 };
@@ -204,7 +214,7 @@ __device__ void bs_far(const DBSweep& s, BsFar F, int wid, int W, unsigned* abor
 template <int K>
 __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* __restrict__ rhs, double* gx,
                        BsFar F, unsigned* abort_flag) {
-  static_assert(K == 3 && K == kBsK, "the main loop is written for three dense coupling blocks");
+  static_assert(K >= 3 && K <= 8 && K == kBsK, "dense coupling depth (F_1, F_2: main warp; F_3..F_K: second main warp)");
   const DBSweep s = s_in;
   const int G = s.G, n = s.n;
   BsSmem S(smem, ns);
@@ -213,18 +223,19 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
   for (int i = threadIdx.x; i <= kBsR * kBsB; i += blockDim.x) S.ring[i] = 0.0;
   for (int i = threadIdx.x; i < ns; i += blockDim.x) S.sready[i] = -1;
   for (int i = threadIdx.x; i < kBsRC; i += blockDim.x) S.aready[i] = -1;
+  for (int i = threadIdx.x; i < kBsRQ; i += blockDim.x) S.qready[i] = -1;
   if (threadIdx.x == 0) {
     *S.progress = 0;
     *S.pubdone = 0;
   }
   __syncthreads();
   // roles (warp w runs on SM sub-partition w % 4; the main warp keeps its own)
-  const int mainw = nw - 1, pubw = nw - 2, prodw = nw - 8;
+  const int mainw = nw - 1, pubw = nw - 2, prodw = nw - 3, main2w = nw - 6;
   int cid = -1;
   {
-    const int cw[kBsNC] = {0, 1, 2, 4};
+    static_assert(kBsNC <= 9, "co-main warps are taken off the main warp's sub-partition");
     for (int i = 0; i < kBsNC; ++i)
-      if (warp == cw[i]) cid = i;
+      if (warp == bs_comain_warp(i)) cid = i;
   }
   auto orig = [&](int p) { return s.dir ? n - 1 - p : p; };
   // this lane's half row (8 doubles) of dense block `block` of a slot
@@ -244,103 +255,89 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
   };
 
   if (warp == mainw && G > 0) {
-    // ---- main: y_g = c_g - (F_1^g y_{g-1} + F_2^g y_{g-2} + F_3^g y_{g-3}) ------
-    // One step per group. Everything except the first line of a step is kept
-    // off the dependent chain: the coupling rows and c of the NEXT step are
-    // loaded while the chain's latencies pass (straight-line code, no barrier
-    // inside a step except the __syncwarp that publishes y), and F_2 / F_3 of
-    // later groups are applied to y_{g-1} right after the chain.
-    BS_DIAG(const long long t0 = clock64(); long long w_c = 0, w_s = 0, w_p = 0;)
-    const uint8_t* const ringb = reinterpret_cast<const uint8_t*>(S.ring);
-    for (int k = 0; k <= K; ++k) {
-      const int gk = k < G ? k : G - 1;
-      wait_eq(S.sready + gk % ns, gk);
-    }
+    // ---- main: y_g = c_g - q_g - F_1^g y_{g-1} - F_2^g y_{g-2} -----------------------
+    // One step per group; only F_1 y_{g-1} (+ one shuffle) is on the dependent
+    // chain. F_2 of group g+1 is applied to y_{g-1} beside it; the next step's
+    // rows, c, q and flags are loaded under the chain's tail. The slot array has
+    // K + 1 zero groups behind the last one, so no look-ahead index is clamped.
+    BS_DIAG(const long long t0 = clock64(); long long w_c = 0, w_s = 0, w_p = 0, w_q = 0;)
+    uint8_t* const ringb = reinterpret_cast<uint8_t*>(S.ring);
+    for (int k = 0; k <= 2; ++k) wait_eq(S.sready + k % ns, k);
     wait_eq(S.aready + 0, 0);
     asm volatile("" ::: "memory");
-    // slot cursors: s1, s2, s3 = slots of groups g, g+1, g+2 (clamped to the
-    // last group), advanced without a modulo
-    int s1 = 0, s2 = (1 < G ? 1 : G - 1) % ns, s3 = (2 < G ? 2 : G - 1) % ns;
-    auto slot_at = [&](int sl) { return S.slots + static_cast<size_t>(sl) * kBsSlotBytes; };
-    auto next_slot = [&](int sl) { return sl + 1 == ns ? 0 : sl + 1; };
-    double f1[8], f2[8], f3[8];
+    auto slot_at = [&](int slot) { return S.slots + static_cast<size_t>(slot) * kBsSlotBytes; };
+    auto next_slot = [&](int slot) { return slot + 1 == ns ? 0 : slot + 1; };
+    int s1 = 0, s2 = 1 % ns, s3 = 2 % ns;  // slots of groups g, g+1, g+2
+    double f1[8], f2[8];
     ld_block(slot_at(s1), 0, f1);  // F_1 of group 0
     ld_block(slot_at(s2), 1, f2);  // F_2 of group 1
-    ld_block(slot_at(s3), 2, f3);  // F_3 of group 2
-    double c = S.cbuf[r];
-    double q0 = 0.0, q1 = 0.0;  // partial sums of groups g (terms k = 2, 3) and g + 1 (term k = 3)
+    double c = S.cbuf[r], q2 = 0.0, Q0 = 0.0;
     int pd = 0;
     int yoff = (kBsR - 1) * 128 + hf * 64;  // ring bytes of y_{g-1}, this lane's half
     int woff = r * 8;                       // ring bytes of y_g, this lane's row
-    // invariant at the top of step g: the slots of groups <= g+3 have landed
+    // invariant at the top of step g: the slots of groups <= g + 2 have landed
     for (int g = 0; g < G; ++g) {
       const double2* yp = reinterpret_cast<const double2*>(ringb + yoff);
       const double2 y0 = yp[0], y1 = yp[1], y2 = yp[2], y3 = yp[3];
-      // all products with y_{g-1}: F_1 of g (the chain), F_2 of g+1, F_3 of g+2
-      double pa = f1[0] * y0.x, pb = f1[4] * y2.x;
-      double ua = f2[0] * y0.x, ub = f2[4] * y2.x, va = f3[0] * y0.x, vb = f3[4] * y2.x;
+      double pa = f1[0] * y0.x, pb = f1[4] * y2.x, ua = f2[0] * y0.x, ub = f2[4] * y2.x;
       pa = fma(f1[1], y0.y, pa);
       pb = fma(f1[5], y2.y, pb);
       ua = fma(f2[1], y0.y, ua);
       ub = fma(f2[5], y2.y, ub);
-      va = fma(f3[1], y0.y, va);
-      vb = fma(f3[5], y2.y, vb);
       pa = fma(f1[2], y1.x, pa);
       pb = fma(f1[6], y3.x, pb);
       ua = fma(f2[2], y1.x, ua);
       ub = fma(f2[6], y3.x, ub);
-      va = fma(f3[2], y1.x, va);
-      vb = fma(f3[6], y3.x, vb);
       pa = fma(f1[3], y1.y, pa);
       pb = fma(f1[7], y3.y, pb);
       ua = fma(f2[3], y1.y, ua);
       ub = fma(f2[7], y3.y, ub);
-      va = fma(f3[3], y1.y, va);
-      vb = fma(f3[7], y3.y, vb);
-      // the next step's coupling rows (their slots have landed: invariant) and the
-      // flags of the step after it, issued under the latency of the chain's tail
-      if (g + 1 < G) {
-        s1 = s2;
-        s2 = s3;
-      }
-      if (g + 3 < G) s3 = next_slot(s3);
+      // next step's operands (slots g+1, g+2: landed) and the flags behind them
+      s1 = s2;
+      s2 = s3;
+      s3 = next_slot(s3);
       ld_block(slot_at(s1), 0, f1);
       ld_block(slot_at(s2), 1, f2);
-      ld_block(slot_at(s3), 2, f3);
-      const int gn = g + 1 < G ? g + 1 : G - 1;
-      const int gs = g + K + 1 < G ? g + K + 1 : G - 1;  // newest slot the step after next touches
-      const int s4 = g + K + 1 < G ? next_slot(s3) : s3;
+      const int gn = g + 1;
       const int fa = S.aready[gn & (kBsRC - 1)];
-      const int fs = S.sready[s4];
+      const int fq = S.qready[gn & (kBsRQ - 1)];
+      const int fs = S.sready[s3];
       // the chain's tail
-      double t = (pa + pb) + q0;
+      double t = (pa + pb) + (Q0 + q2);
       t += bs_shfl_xor16(t);
       const double y = c - t;
-      if (hf == 0) *reinterpret_cast<double*>(const_cast<uint8_t*>(ringb) + woff) = y;
-      q0 = q1 + (ua + ub);
-      q1 = va + vb;
+      if (hf == 0) *reinterpret_cast<double*>(ringb + woff) = y;
+      Q0 = ua + ub;
       __syncwarp();
-      if (lane == 0) *S.progress = g + 1;
+      if (lane == 0) *S.progress = gn;
       yoff = woff - r * 8 + hf * 64;
       woff = woff + 128 == kBsZero + r * 8 ? r * 8 : woff + 128;
-      if (fs != gs) {
+      if (fs != g + 3) {
         BS_DIAG(const long long tw = clock64();)
-        wait_eq(S.sready + s4, gs);
+        wait_eq(S.sready + s3, g + 3);
         BS_DIAG(w_s += clock64() - tw;)
       }
-      if (fa != gn) {
-        BS_DIAG(const long long tw = clock64();)
-        wait_eq(S.aready + (gn & (kBsRC - 1)), gn);
-        BS_DIAG(w_c += clock64() - tw;)
+      if (gn < G) {
+        if (fa != gn) {
+          BS_DIAG(const long long tw = clock64();)
+          wait_eq(S.aready + (gn & (kBsRC - 1)), gn);
+          BS_DIAG(w_c += clock64() - tw;)
+        }
+        if (gn >= 3 && fq != gn) {
+          BS_DIAG(const long long tw = clock64();)
+          wait_eq(S.qready + (gn & (kBsRQ - 1)), gn);
+          BS_DIAG(w_q += clock64() - tw;)
+        }
+        asm volatile("" ::: "memory");
+        c = S.cbuf[(gn & (kBsRC - 1)) * kBsB + r];
+        q2 = gn >= 3 ? S.qbuf[(gn & (kBsRQ - 1)) * 32 + lane] : 0.0;
       }
-      asm volatile("" ::: "memory");
-      c = S.cbuf[(gn & (kBsRC - 1)) * kBsB + r];
-      if (g + 1 - pd >= kBsR - 2) {  // never lap the publisher on the y ring
+      if (gn - pd >= kBsR - 2) {  // never lap the publisher on the y ring
         pd = *S.pubdone;
-        if (g + 1 - pd >= kBsR - 2) {
+        if (gn - pd >= kBsR - 2) {
           BS_DIAG(const long long tw = clock64();)
           SpinGuard sg(abort_flag);
-          while ((pd = *S.pubdone) < g + 1 - (kBsR - 3))
+          while ((pd = *S.pubdone) < gn - (kBsR - 3))
             if (sg.expired()) break;
           BS_DIAG(w_p += clock64() - tw;)
         }
@@ -352,7 +349,65 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       atomicAdd(&g_bs_dbg[2], static_cast<unsigned long long>(w_s));
       atomicAdd(&g_bs_dbg[3], static_cast<unsigned long long>(w_p));
       atomicAdd(&g_bs_dbg[4], static_cast<unsigned long long>(G));
+      atomicAdd(&g_bs_dbg[14], static_cast<unsigned long long>(w_q));
     })
+  } else if (warp == main2w && G > 3) {
+    // ---- second main: q_t = sum_{k=3..K} F_k^t y_{t-k} --------------------------------
+    // Step j consumes y_j as soon as the main warp has published it: the k = 3 term
+    // completes q_{j+3} (handed to the main warp two steps before it is needed), the
+    // terms k = 4..K go into the running sums of the groups behind it.
+    BS_DIAG(long long w_y = 0;)
+    const uint8_t* const ringb = reinterpret_cast<const uint8_t*>(S.ring);
+    auto slot_at = [&](int slot) { return S.slots + static_cast<size_t>(slot) * kBsSlotBytes; };
+    auto next_slot = [&](int slot) { return slot + 1 == ns ? 0 : slot + 1; };
+    int sl[K - 2];  // slots of groups j+3 .. j+K
+#pragma unroll
+    for (int i = 0; i < K - 2; ++i) sl[i] = (3 + i) % ns;
+    double A[K - 2];
+#pragma unroll
+    for (int i = 0; i < K - 2; ++i) A[i] = 0.0;
+    int prog = 0, yoff = hf * 64;
+    for (int j = 0; j + 3 < G; ++j) {
+      if (S.sready[sl[K - 3]] != j + K) wait_eq(S.sready + sl[K - 3], j + K);
+      if (prog < j + 1) {
+        BS_DIAG(const long long tw = clock64();)
+        SpinGuard sg(abort_flag);
+        while ((prog = *S.progress) < j + 1)
+          if (sg.expired()) break;
+        BS_DIAG(w_y += clock64() - tw;)
+      }
+      asm volatile("" ::: "memory");
+      const double2* yp = reinterpret_cast<const double2*>(ringb + yoff);
+      const double2 y0 = yp[0], y1 = yp[1], y2 = yp[2], y3 = yp[3];
+      double pk[K - 2];
+#pragma unroll
+      for (int i = 0; i < K - 2; ++i) {
+        double fk[8];
+        ld_block(slot_at(sl[i]), 2 + i, fk);  // F_{3+i} of group j+3+i
+        double ua = fk[0] * y0.x, ub = fk[4] * y2.x;
+        ua = fma(fk[1], y0.y, ua);
+        ub = fma(fk[5], y2.y, ub);
+        ua = fma(fk[2], y1.x, ua);
+        ub = fma(fk[6], y3.x, ub);
+        ua = fma(fk[3], y1.y, ua);
+        ub = fma(fk[7], y3.y, ub);
+        pk[i] = ua + ub;
+      }
+      const int t = j + 3;
+      S.qbuf[(t & (kBsRQ - 1)) * 32 + lane] = A[0] + pk[0];
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        S.qready[t & (kBsRQ - 1)] = t;
+      }
+#pragma unroll
+      for (int i = 0; i + 1 < K - 2; ++i) A[i] = A[i + 1] + pk[i + 1];
+      A[K - 3] = 0.0;
+#pragma unroll
+      for (int i = 0; i < K - 2; ++i) sl[i] = next_slot(sl[i]);
+      yoff = yoff + 128 >= kBsZero ? hf * 64 : yoff + 128;
+    }
+    BS_DIAG(if (lane == 0) atomicAdd(&g_bs_dbg[15], static_cast<unsigned long long>(w_y));)
   } else if (cid >= 0) {
     // ---- co-main: c_h = T_h (rhs_h - far_h - mid_h) ---------------------------
     // A three-deep pipeline over this warp's groups h, h + NC, h + 2 NC: list
@@ -418,8 +473,14 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
         if (prog >= need) return;
         BS_DIAG(const long long tw = clock64();)
         SpinGuard sg(abort_flag);
-        while ((prog = *S.progress) < need)
+        // Polling shared memory is not free for the other warps of the SM (every
+        // poll is a load on the shared LSU): only the waiter whose turn is next
+        // spins; the others sleep in proportion to their distance.
+        while ((prog = *S.progress) < need) {
+          const int d = need - prog;
+          if (d > 1) __nanosleep(d > 4 ? 400 : 80 * (d - 1));
           if (sg.expired()) break;
+        }
         asm volatile("" ::: "memory");
         BS_DIAG(w_p += clock64() - tw;)
       };
@@ -520,10 +581,11 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
   } else if (warp == prodw) {
     if (lane == 0) {
       int issued = 0, done = 0, isl = 0, dsl = 0;
+      const int Gs = G + K + 1;  // incl. the zero groups behind the last one
       SpinGuard sg(abort_flag);
-      while (done < G) {
+      while (done < Gs) {
         bool idle = true;
-        if (issued < G && *S.progress >= issued - ns + 1) {
+        if (issued < Gs && *S.progress >= issued - ns + 1) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_expect_tx(S.mbar + isl, kBsSlotBytes);
           bulk_g2s(S.slots + static_cast<size_t>(isl) * kBsSlotBytes,
@@ -541,6 +603,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
           }
         }
         if (idle) {
+          __nanosleep(100);
           if (sg.expired()) break;
         } else {
           sg.t0 = clock64();
@@ -568,16 +631,17 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
         if (lane == 0) *S.pubdone = pnow;
         done = pnow;
         sg.t0 = clock64();
-      } else if (sg.expired()) {
-        break;
+      } else {
+        __nanosleep(200);
+        if (sg.expired()) break;
       }
     }
   } else if (F.workers == 0 && (warp & 3) != (mainw & 3)) {
     // no far-worker CTAs: the spare warps off the main warp's sub-partition
     int idx = 0, cnt = 0;
     for (int w = 0; w < nw; ++w) {
-      bool role = w == mainw || w == pubw || w == prodw;
-      for (int i = 0; i < kBsNC; ++i) role = role || w == (i < 3 ? i : 4);
+      bool role = w == mainw || w == pubw || w == prodw || w == main2w;
+      for (int i = 0; i < kBsNC; ++i) role = role || w == bs_comain_warp(i);
       if (!role && (w & 3) != (mainw & 3)) {
         if (w == warp) idx = cnt;
         ++cnt;
@@ -588,7 +652,7 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
   __syncthreads();
   if (threadIdx.x < ns) {
     const int sl = threadIdx.x;
-    if (G > sl) S.base_use[sl] += (G - 1 - sl) / ns + 1;
+    if (G + K + 1 > sl) S.base_use[sl] += (G + K - sl) / ns + 1;
   }
   __syncthreads();
 }

@@ -17,9 +17,11 @@
 // (32^3: 7,153 groups vs 10,715 levels of 10.7 rows).
 //
 // Roles (one "sweep CTA" per triangular solve, plus far-worker CTAs):
-//   * MAIN warp: y_g = c_g - sum_k F_{g,k} y_{g-k}; lane (r, h) owns row r and
-//     columns 8h..8h+7 of each block (two lanes per row, combined by one
-//     shuffle). y_{g-1} is broadcast through the shared-memory y ring.
+//   * MAIN warp: y_g = c_g - q_g - F_{g,1} y_{g-1} - F_{g,2} y_{g-2}; lane (r, h)
+//     owns row r and columns 8h..8h+7 of each block (two lanes per row, combined
+//     by one shuffle). y_{g-1} is broadcast through the shared-memory y ring.
+//   * SECOND MAIN warp: q_g = sum_{k=3..K} F_{g,k} y_{g-k}, accumulated as the
+//     y's appear (two steps of slack before the main warp needs q_g).
 //   * CO-MAIN warps (kBsNC, round-robin over groups): c_g = T_g (r_g - far_g
 //     - mid_g): the "mid" entries (groups g-R .. g-K-1) are gathered from the y
 //     ring; the "far" partial sums come from the far workers. Each co-main
@@ -52,13 +54,15 @@
 namespace dsgpu {
 
 constexpr int kBsB = 16;     // rows per group
-constexpr int kBsK = 3;      // dense pre-multiplied coupling blocks on the main warp
+constexpr int kBsK = 5;      // dense pre-multiplied coupling blocks: F_1, F_2 on the main warp,
+                             //   F_3..F_K on the second main warp
+constexpr int kBsRQ = 8;     // q ring (second main warp -> main), groups (power of two)
 constexpr int kBsR = 32;     // y ring depth in groups; older entries are "far"
-constexpr int kBsNC = 4;     // co-main warps
-constexpr int kBsRC = 8;     // c ring (co-main -> main), groups
+constexpr int kBsNC = 8;     // co-main warps
+constexpr int kBsRC = 16;    // c ring (co-main -> main), groups (power of two)
 constexpr int kBsMC = 4;     // mid-list chunk (entries per lane)
 constexpr int kBsFC = 8;     // far-list chunk (entries per lane)
-constexpr int kBsStage = 32;  // mid-list entries per lane staged ahead in shared memory (cp.async)
+constexpr int kBsStage = 16;  // mid-list entries per lane staged ahead in shared memory (cp.async)
 constexpr int kBsStageBytes = kBsStage / kBsMC * 3 * 512;  // per buffer: chunks x (int4 + 2 double2) x 32 lanes
 constexpr int kBsBlock = kBsB * kBsB * 8;              // bytes of one dense block
 constexpr int kBsSlotBytes = (kBsK + 1) * kBsBlock;    // F_1..F_K, T
@@ -74,7 +78,8 @@ inline int64_t bs_f64_at(int k, int l) { return (static_cast<int64_t>(k >> 1) * 
 
 struct HostBSweep {
   int n = 0, G = 0, dir = 0;        // dir 0: forward (L), 1: backward (L^T, reversed ordering)
-  std::vector<uint8_t> slots;        // G * kBsSlotBytes
+  std::vector<uint8_t> slots;        // (G + kBsK + 1) * kBsSlotBytes: zero blocks behind the last group, so the
+                                     //   main warps never clamp a look-ahead index
   std::vector<int32_t> mw, ms;       // mid list: width (multiple of kBsMC), leading entries that only
                                      //   need groups <= g-K-3 (multiple of kBsMC)
   std::vector<int64_t> mptr;         // G + 1, element offset of the group's lists (width * 32 each)
@@ -101,11 +106,11 @@ void bsweep_host_apply(const HostBSweep& s, const double* rhs, double* x);
 // Shared memory of the sweep CTA with a slot ring of `ns` slots.
 inline size_t bs_smem_bytes(int ns) {
   return static_cast<size_t>(kBsZero) + 128            // y ring + zero slot
-         + kBsRC * kBsB * 8                             // c ring
+         + kBsRC * kBsB * 8 + kBsRQ * 32 * 8            // c ring, q ring
          + static_cast<size_t>(ns) * kBsSlotBytes       // dense-block slots
          + static_cast<size_t>(kBsNC) * 2 * kBsStageBytes  // co-main mid-list staging (double-buffered)
          + static_cast<size_t>(ns) * 8                  // mbarriers
-         + (2 * ns + kBsRC + 8) * 4 + 128;              // sready, base_use, aready, progress words
+         + (2 * ns + kBsRC + kBsRQ + 8) * 4 + 128;      // sready, base_use, aready, qready, progress words
 }
 
 }  // namespace dsgpu

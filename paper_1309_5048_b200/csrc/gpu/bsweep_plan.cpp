@@ -71,7 +71,7 @@ void build_dir(int n, int dir, RowFn rows, HostBSweep& s) {
   s.fcols.assign(s.fptr[G], n);
   s.fvals.assign(s.fptr[G], 0.0);
   s.fneed.assign(s.fcptr[G], -1);
-  s.slots.assign(static_cast<size_t>(G) * kBsSlotBytes, 0);
+  s.slots.assign(static_cast<size_t>(G + kBsK + 1) * kBsSlotBytes, 0);
   int64_t nd = 0, nm = 0, nf = 0;
   // ---- pass 2: fill ----------------------------------------------------------
 #pragma omp parallel reduction(+ : nd, nm, nf)

@@ -1763,7 +1763,7 @@ struct dsgpu_handle {
   bool ring = false;
   bool pi = false;            // partitioned-inverse IC(0) applies (pi.cuh)
   bool bs = false;            // blocked sweeps (bsweep.cuh): the default IC(0) apply
-  int bs_ns = 12;             // dense-block slot ring depth
+  int bs_ns = kBsK + 3;       // dense-block slot ring depth (minimum: the main warp looks K + 1 groups ahead)
   int far_ctas[2] = {0, 0};   // far-worker CTAs per IC block
   PiPlan pip[2];
   int pi_cbase = 0, pi_cslot = 0;  // chain coefficient prefetch slots (doubles)
@@ -2078,7 +2078,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     if (h->bs) {
       h->tb = 0;  // selects the blocked-sweep kernels (minres_for / ic_for)
       h->ring = true;
-      if (const char* env = std::getenv("DSGPU_BS_SLOTS")) h->bs_ns = std::max(kBsK + 2, std::atoi(env));
+      if (const char* env = std::getenv("DSGPU_BS_SLOTS")) h->bs_ns = std::max(kBsK + 3, std::atoi(env));
     }
     if (!h->exact && !h->pi && !h->bs && nmax > 0) {
       const int merge = std::getenv("DSGPU_MERGE") ? std::atoi(std::getenv("DSGPU_MERGE")) : kDefaultMerge;

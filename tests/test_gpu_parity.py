@@ -82,15 +82,15 @@ def test_ic0_apply_partitioned_inverse_matches_reference(gpu, port, monkeypatch,
 
 
 @pytest.mark.parametrize("knobs", [{}, {"DSGPU_FAR_A": "0", "DSGPU_FAR_Q": "0"}, {"DSGPU_GRID": "5"},
-                                   {"DSGPU_FAR_A": "3", "DSGPU_FAR_Q": "1", "DSGPU_BS_SLOTS": "5"}])
+                                   {"DSGPU_FAR_A": "3", "DSGPU_FAR_Q": "1", "DSGPU_BS_SLOTS": "9"}])
 def test_ic0_apply_blocked_matches_reference(gpu, port, monkeypatch, knobs):
     """The default IC(0) apply: blocked sweeps (bsweep.hpp) -- dense 16x16
     blocks next to the diagonal on the main warp, mid entries on the co-main
     warps, far entries on far-worker CTAs -- against the reference's own
     Ic0Factor::solve output (fixture), the CPU oracle on 2D and 3D factors, and
     through a whole solve. knobs: no far-worker CTAs (the sweep CTA's spare
-    warps do the far lists), a 5-CTA grid, few far CTAs with the smallest slot
-    ring."""
+    warps do the far lists), a 5-CTA grid, few far CTAs with a different slot
+    ring depth."""
     host, solver = gpu
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
