@@ -180,8 +180,8 @@ int dsgpu_info(const dsgpu_handle* h, int64_t* info);
  * factor L (as dsgpu_setup does) and evaluates it on the host in the plan's own
  * arithmetic order, z = (L L^T)^{-1} r. A test hook for the plan's structure
  * and coefficients, never used by a solve. stats8 (nullable): groups, factor
- * entries in dense blocks / in the worker lists (forward, then backward sweep),
- * widest list, padded list entries (forward, backward). */
+ * entries in dense blocks / mid lists / far lists (forward sweep), widest mid
+ * and far list, padded mid and far list entries. */
 int dsgpu_debug_bsweep_host(int n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
                             const double* r, double* z, int64_t* stats8);
 

@@ -1,5 +1,5 @@
 // Device side of the blocked triangular sweep (see bsweep.hpp for the method
-// and the roles).
+// and the roles). Included by solver.cu after its mbarrier / bulk-copy helpers.
 #pragma once
 
 #include "bsweep.hpp"
@@ -10,26 +10,30 @@ namespace dev {
 
 struct DBSweep {
   int n, G, dir;
-  const uint8_t* slots;  // (G + K + 1) x kBsSlotBytes
-  const uint8_t* tblk;   // G x kBsBlock
-  const int32_t* lw;
-  const int64_t* lptr;
-  const int32_t* lcols;
-  const double* lvals;
+  const uint8_t* slots;
+  const uint8_t* tblk;
+  const int32_t *mw, *ms;
+  const int64_t* mptr;
+  const int32_t* mcols;
+  const double* mvals;
+  const int32_t* fw;
+  const int64_t* fptr;
+  const int32_t* fcols;
+  const double* fvals;
+  const int32_t *fcptr, *fneed;
 };
 
-// Global hand-off state of one sweep. Cross-SM hand-offs carry NO fence and NO
-// flag: every double travels as one 16-byte unit {low word, tag, high word,
-// tag} (two self-validating 8-byte halves, like NCCL's LL protocol), and the
-// consumer polls the data itself until both tags are right.
-struct BsLink {
-  const uint4* rt;            // tagged right-hand side (factor ordering), tag rtag
-  unsigned rtag;
-  uint4* gt;                  // tagged result vector (what the workers gather), tag `tag`
-  uint4* ct;                  // [G][16] tagged c of every group (worker -> main warp)
-  unsigned long long* hint;   // (tag << 32) | groups finished: a progress HINT for sleeping workers
-  unsigned tag;               // unique per sweep (launch id | sweep number)
-  int workers;                // worker warps outside the sweep CTA (0: its spare warps)
+// Global hand-off state of one sweep (shared by a block's two sweeps: tags
+// differ). Cross-SM hand-offs carry NO fence and NO flag: every double travels
+// as one 16-byte unit {low word, tag, high word, tag} (two self-validating
+// 8-byte halves, like NCCL's LL protocol), and the consumer polls the data
+// itself until both tags are the sweep's. Measured on B200 (tools/bs_lab.cu):
+// 175 cycles per hop, against 2,260 for data + __threadfence + release flag.
+struct BsFar {
+  uint4* gt;       // [n + 1] tagged copy of the result vector (what the far workers gather)
+  uint4* fps;      // [G][16] tagged far partial sum of every row
+  unsigned tag;    // unique per sweep (launch id | sweep number)
+  int workers;     // far-worker warps outside the sweep CTA (0: its spare warps)
 };
 
 __device__ __forceinline__ uint4 bs_pack(double v, unsigned tag) {
@@ -37,9 +41,6 @@ __device__ __forceinline__ uint4 bs_pack(double v, unsigned tag) {
   return make_uint4(static_cast<unsigned>(b), tag, static_cast<unsigned>(b >> 32), tag);
 }
 __device__ __forceinline__ bool bs_valid(const uint4& w, unsigned tag) { return w.y == tag && w.w == tag; }
-__device__ __forceinline__ double bs_value(const uint4& w) {
-  return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(w.z) << 32) | w.x));
-}
 // Re-read of a tagged unit inside a polling loop: volatile, so the compiler can
 // neither hoist it out of the loop nor merge it with the first read (__ldcg is
 // a plain asm the optimizer treats as a pure function of its address).
@@ -51,19 +52,19 @@ __device__ __forceinline__ uint4 bs_poll(const uint4* p) {
                : "memory");
   return w;
 }
-__device__ __forceinline__ unsigned long long bs_poll64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+__device__ __forceinline__ double bs_value(const uint4& w) {
+  return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(w.z) << 32) | w.x));
 }
 
 // Diagnostics exist only in the -DDSGPU_DIAG build (make diag): the production
 // kernels carry no counters, clocks or atomics on their paths.
 #ifdef DSGPU_DIAG
 // [0] main cycles, [1] main cycles waiting for c, [2] for slots, [3] for the
-// publisher, [4] groups, [5] main cycles waiting for q, [6] second-main cycles
-// waiting for y, [7] second-main cycles, [8] worker cycles waiting for y, [9]
-// worker cycles, [10] worker cycles waiting for the right-hand side
+// publisher, [4] groups, [5] co-main cycles waiting for progress, [6] for far
+// sums, [7] co-main cycles, [8] far-worker cycles waiting, [9] far-worker cycles,
+// [10..13] co-main cycles by stage: prefetch + staging wait, mid lists (incl.
+// waits), T product, hand-off, [14] main cycles waiting for q, [15] second-main
+// cycles waiting for y
 __device__ unsigned long long g_bs_dbg[16];
 #define BS_DIAG(...) __VA_ARGS__
 #else
@@ -73,14 +74,21 @@ __device__ unsigned long long g_bs_dbg[16];
 __device__ __forceinline__ double bs_shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ double bs_shfl_xor16(double v) { return __shfl_xor_sync(0xffffffffu, v, 16); }
 
+// Co-main warps: the warps 0, 1, 2, 4, 5, 6, 8, 9, 10 (never 3 mod 4: that SM
+// sub-partition belongs to the main warp).
+__device__ __forceinline__ int bs_comain_warp(int i) { return i + i / 3; }
+
 // Shared-memory workspace of the sweep CTA.
 struct BsSmem {
-  double* ring;             // kBsR groups x 16 results
+  double* ring;             // kBsR groups x 16 results, then the zero slot
+  double* cbuf;             // kBsRC x 16 (co-main -> main)
   double* qbuf;             // kBsRQ x 32 lane partials (second main -> main)
   uint8_t* slots;           // ns x kBsSlotBytes
+  uint8_t* stage;           // kBsNC x 2 x kBsStageBytes: co-main mid-list staging
   uint64_t* mbar;           // ns
   volatile int* sready;     // ns: group whose blocks have landed in the slot
   int* base_use;            // ns: completed mbarrier phases before this sweep
+  volatile int* aready;     // kBsRC: group whose c is staged
   volatile int* qready;     // kBsRQ: group whose q is staged
   volatile int* progress;   // groups finished by the main warp
   volatile int* pubdone;    // groups copied to global memory by the publisher
@@ -90,16 +98,21 @@ struct BsSmem {
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
     p += (128u - (a & 127u)) & 127u;
     ring = reinterpret_cast<double*>(p);
-    p += kBsR * kBsB * 8;
+    p += kBsZero + 128;
+    cbuf = reinterpret_cast<double*>(p);
+    p += kBsRC * kBsB * 8;
     qbuf = reinterpret_cast<double*>(p);
     p += kBsRQ * 32 * 8;
     slots = p;
     p += static_cast<size_t>(ns) * kBsSlotBytes;
+    stage = p;
+    p += static_cast<size_t>(kBsNC) * 2 * kBsStageBytes;
     mbar = reinterpret_cast<uint64_t*>(p);
     p += static_cast<size_t>(ns) * 8;
     sready = reinterpret_cast<volatile int*>(p);
     base_use = reinterpret_cast<int*>(p) + ns;
-    qready = reinterpret_cast<volatile int*>(p) + 2 * ns;
+    aready = reinterpret_cast<volatile int*>(p) + 2 * ns;
+    qready = aready + kBsRC;
     progress = qready + kBsRQ;
     pubdone = progress + 1;
   }
@@ -118,144 +131,114 @@ __device__ void bs_setup(double* smem, int ns) {
   __syncthreads();
 }
 
-// Workers: c_g = T_g ( r_g - sum of the group's list entries times y ) for the
-// groups g = wid, wid + W, ... The list (every factor entry older than K
-// groups) streams from HBM in chunks of 8 entries per lane; y is gathered from
-// the tagged result vector as the main warp fills it -- a unit that does not
-// carry this sweep's tag yet is read again (lists are oldest-first, so only
-// the last chunk ever waits; the progress hint tells a worker that is far
-// ahead how long it may sleep).
-__device__ void bs_worker(const DBSweep& s, BsLink L, int wid, int W, unsigned* abort_flag) {
-  const int lane = threadIdx.x & 31, r = lane & 15, hf = lane >> 4;
-  const uint4* __restrict__ gt = L.gt;
-  const unsigned tag = L.tag;
-  const int n = s.n;
-  BS_DIAG(long long t_begin = clock64(); long long t_wait = 0, t_rhs = 0;)
+// Far workers: for every group the partial sums of its far entries, gathered
+// from the tagged result vector F.gt as the publisher fills it. A gathered
+// entry that does not carry this sweep's tag yet is simply read again (lists
+// are oldest-first, so only the last chunk of a list ever waits). wid / W: this
+// warp among the far-worker warps.
+__device__ void bs_far(const DBSweep& s, BsFar F, int wid, int W, unsigned* abort_flag) {
+  const int lane = threadIdx.x & 31;
+  const uint4* __restrict__ gt = F.gt;
+  const unsigned tag = F.tag;
+  BS_DIAG(long long t_begin = clock64(); long long t_wait = 0;)
   for (int g = wid; g < s.G; g += W) {
-    const int p = g * kBsB + r;
-    const int o = s.dir ? n - 1 - p : p;
-    // this lane's half row of T_g and its right-hand side: issued first, used last
-    const double2* tp = reinterpret_cast<const double2*>(s.tblk + static_cast<size_t>(g) * kBsBlock) + lane;
-    const double2 t0 = __ldg(tp), t1 = __ldg(tp + 32), t2 = __ldg(tp + 64), t3 = __ldg(tp + 96);
-    uint4 rw = make_uint4(0u, 0u, 0u, 0u);
-    const bool has_rhs = hf == 0 && p < n;
-    if (has_rhs) rw = __ldcg(L.rt + o);
-    const int lw = __ldg(s.lw + g);
+    const int fw = __ldg(s.fw + g);
+    if (fw == 0) continue;
+    const int64_t base = __ldg(s.fptr + g);
+    const int4* cp = reinterpret_cast<const int4*>(s.fcols + base) + lane;
+    const double2* vp = reinterpret_cast<const double2*>(s.fvals + base) + lane;
+    const int nch = fw / kBsFC;
     double acc = 0.0;
-    if (lw > 0) {
-      const int64_t base = __ldg(s.lptr + g);
-      const int4* cp = reinterpret_cast<const int4*>(s.lcols + base) + lane;
-      const double2* vp = reinterpret_cast<const double2*>(s.lvals + base) + lane;
-      const int nch = lw / kBsLC;
-      int4 ca = __ldcs(cp), cb = __ldcs(cp + 32);
-      double2 v0 = __ldcs(vp), v1 = __ldcs(vp + 32), v2 = __ldcs(vp + 64), v3 = __ldcs(vp + 96);
-      for (int c = 0; c < nch; ++c) {
-        // next chunk's lists first: independent of the dependency wait
-        int4 na = ca, nb = cb;
-        double2 n0 = v0, n1 = v1, n2 = v2, n3 = v3;
-        if (c + 1 < nch) {
-          na = __ldcs(cp + (2 * c + 2) * 32);
-          nb = __ldcs(cp + (2 * c + 3) * 32);
-          n0 = __ldcs(vp + (4 * c + 4) * 32);
-          n1 = __ldcs(vp + (4 * c + 5) * 32);
-          n2 = __ldcs(vp + (4 * c + 6) * 32);
-          n3 = __ldcs(vp + (4 * c + 7) * 32);
-        }
-        uint4 w0 = __ldcg(gt + ca.x), w1 = __ldcg(gt + ca.y), w2 = __ldcg(gt + ca.z), w3 = __ldcg(gt + ca.w);
-        uint4 w4 = __ldcg(gt + cb.x), w5 = __ldcg(gt + cb.y), w6 = __ldcg(gt + cb.z), w7 = __ldcg(gt + cb.w);
-        auto all_valid = [&]() {
-          return bs_valid(w0, tag) && bs_valid(w1, tag) && bs_valid(w2, tag) && bs_valid(w3, tag) &&
-                 bs_valid(w4, tag) && bs_valid(w5, tag) && bs_valid(w6, tag) && bs_valid(w7, tag);
-        };
-        if (!all_valid()) {
-          BS_DIAG(const long long tw = clock64();)
-          SpinGuard sg(abort_flag);
-          do {
-            // far ahead of the main warp: sleep by the hint; close: poll the data
-            const unsigned long long hv = bs_poll64(L.hint);
-            w0 = bs_poll(gt + ca.x);
-            w1 = bs_poll(gt + ca.y);
-            w2 = bs_poll(gt + ca.z);
-            w3 = bs_poll(gt + ca.w);
-            w4 = bs_poll(gt + cb.x);
-            w5 = bs_poll(gt + cb.y);
-            w6 = bs_poll(gt + cb.z);
-            w7 = bs_poll(gt + cb.w);
-            const int done = static_cast<unsigned>(hv >> 32) == tag ? static_cast<int>(static_cast<unsigned>(hv)) : -64;
-            const int dist = g - kBsK - done;  // groups the main warp still had to finish
-            if (dist > 6 && !all_valid()) __nanosleep(min(8000, dist * 60));
-          } while (!all_valid() && !sg.expired());
-          BS_DIAG(t_wait += clock64() - tw;)
-        }
-        double p0 = v0.x * bs_value(w0), p1 = v1.x * bs_value(w2), p2 = v2.x * bs_value(w4), p3 = v3.x * bs_value(w6);
-        p0 = fma(v0.y, bs_value(w1), p0);
-        p1 = fma(v1.y, bs_value(w3), p1);
-        p2 = fma(v2.y, bs_value(w5), p2);
-        p3 = fma(v3.y, bs_value(w7), p3);
-        acc += (p0 + p1) + (p2 + p3);
-        ca = na;
-        cb = nb;
-        v0 = n0;
-        v1 = n1;
-        v2 = n2;
-        v3 = n3;
+    int4 ca = __ldcs(cp), cb = __ldcs(cp + 32);
+    double2 v0 = __ldcs(vp), v1 = __ldcs(vp + 32), v2 = __ldcs(vp + 64), v3 = __ldcs(vp + 96);
+    for (int c = 0; c < nch; ++c) {
+      // next chunk's lists first: independent of the dependency wait
+      int4 na = ca, nb = cb;
+      double2 n0 = v0, n1 = v1, n2 = v2, n3 = v3;
+      if (c + 1 < nch) {
+        na = __ldcs(cp + (2 * c + 2) * 32);
+        nb = __ldcs(cp + (2 * c + 3) * 32);
+        n0 = __ldcs(vp + (4 * c + 4) * 32);
+        n1 = __ldcs(vp + (4 * c + 5) * 32);
+        n2 = __ldcs(vp + (4 * c + 6) * 32);
+        n3 = __ldcs(vp + (4 * c + 7) * 32);
       }
-    }
-    double rhs = 0.0;
-    if (has_rhs) {
-      if (!bs_valid(rw, L.rtag)) {
+      uint4 w0 = __ldcg(gt + ca.x), w1 = __ldcg(gt + ca.y), w2 = __ldcg(gt + ca.z), w3 = __ldcg(gt + ca.w);
+      uint4 w4 = __ldcg(gt + cb.x), w5 = __ldcg(gt + cb.y), w6 = __ldcg(gt + cb.z), w7 = __ldcg(gt + cb.w);
+      auto all_valid = [&]() {
+        return bs_valid(w0, tag) && bs_valid(w1, tag) && bs_valid(w2, tag) && bs_valid(w3, tag) &&
+               bs_valid(w4, tag) && bs_valid(w5, tag) && bs_valid(w6, tag) && bs_valid(w7, tag);
+      };
+      if (!all_valid()) {
         BS_DIAG(const long long tw = clock64();)
         SpinGuard sg(abort_flag);
+        unsigned ns_sleep = 100;
         do {
-          rw = bs_poll(L.rt + o);
-        } while (!bs_valid(rw, L.rtag) && !sg.expired());
-        BS_DIAG(t_rhs += clock64() - tw;)
+          __nanosleep(ns_sleep);
+          ns_sleep = min(2000u, ns_sleep * 2);
+          w0 = bs_poll(gt + ca.x);
+          w1 = bs_poll(gt + ca.y);
+          w2 = bs_poll(gt + ca.z);
+          w3 = bs_poll(gt + ca.w);
+          w4 = bs_poll(gt + cb.x);
+          w5 = bs_poll(gt + cb.y);
+          w6 = bs_poll(gt + cb.z);
+          w7 = bs_poll(gt + cb.w);
+        } while (!all_valid() && !sg.expired());
+        BS_DIAG(t_wait += clock64() - tw;)
       }
-      rhs = bs_value(rw);
+      double p0 = v0.x * bs_value(w0), p1 = v1.x * bs_value(w2), p2 = v2.x * bs_value(w4), p3 = v3.x * bs_value(w6);
+      p0 = fma(v0.y, bs_value(w1), p0);
+      p1 = fma(v1.y, bs_value(w3), p1);
+      p2 = fma(v2.y, bs_value(w5), p2);
+      p3 = fma(v3.y, bs_value(w7), p3);
+      acc += (p0 + p1) + (p2 + p3);
+      ca = na;
+      cb = nb;
+      v0 = n0;
+      v1 = n1;
+      v2 = n2;
+      v3 = n3;
     }
-    double t = rhs - acc;
-    t += bs_shfl_xor16(t);
-    // c = T t: this lane's half of row r; t_m lives in lanes m and m + 16
-    const int src = hf * 8;
-    double ca2 = t0.x * bs_shfl(t, src), cb2 = t2.x * bs_shfl(t, src + 4);
-    ca2 = fma(t0.y, bs_shfl(t, src + 1), ca2);
-    cb2 = fma(t2.y, bs_shfl(t, src + 5), cb2);
-    ca2 = fma(t1.x, bs_shfl(t, src + 2), ca2);
-    cb2 = fma(t3.x, bs_shfl(t, src + 6), cb2);
-    ca2 = fma(t1.y, bs_shfl(t, src + 3), ca2);
-    cb2 = fma(t3.y, bs_shfl(t, src + 7), cb2);
-    double cv = ca2 + cb2;
-    cv += bs_shfl_xor16(cv);
-    if (lane < kBsB) __stcg(L.ct + static_cast<int64_t>(g) * kBsB + lane, bs_pack(cv, tag));
+    acc += bs_shfl_xor16(acc);
+    if (lane < kBsB) __stcg(F.fps + static_cast<int64_t>(g) * kBsB + lane, bs_pack(acc, tag));
   }
   BS_DIAG(if (lane == 0) {
     atomicAdd(&g_bs_dbg[8], static_cast<unsigned long long>(t_wait));
     atomicAdd(&g_bs_dbg[9], static_cast<unsigned long long>(clock64() - t_begin));
-    atomicAdd(&g_bs_dbg[10], static_cast<unsigned long long>(t_rhs));
   })
 }
 
-// One blocked sweep by every thread of the sweep CTA. The result goes to L.gt
-// (tagged) and, when gx is not null, to gx (plain, factor ordering). Returns
-// after a CTA barrier with the result complete.
+// One blocked sweep by every thread of the sweep CTA: gx = T^{-1} rhs (both in
+// the factor's ordering). Returns after a CTA barrier with the result complete
+// in global memory (plain in gx, tagged in F.gt).
 template <int K>
-__device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, BsLink L, unsigned* abort_flag) {
+__device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* __restrict__ rhs, double* gx,
+                       BsFar F, unsigned* abort_flag) {
   static_assert(K >= 3 && K <= 8 && K == kBsK, "dense coupling depth (F_1, F_2: main warp; F_3..F_K: second main warp)");
   const DBSweep s = s_in;
   const int G = s.G, n = s.n;
   BsSmem S(smem, ns);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int r = lane & 15, hf = lane >> 4;
-  for (int i = threadIdx.x; i < kBsR * kBsB; i += blockDim.x) S.ring[i] = 0.0;
+  for (int i = threadIdx.x; i <= kBsR * kBsB; i += blockDim.x) S.ring[i] = 0.0;
   for (int i = threadIdx.x; i < ns; i += blockDim.x) S.sready[i] = -1;
+  for (int i = threadIdx.x; i < kBsRC; i += blockDim.x) S.aready[i] = -1;
   for (int i = threadIdx.x; i < kBsRQ; i += blockDim.x) S.qready[i] = -1;
   if (threadIdx.x == 0) {
     *S.progress = 0;
-    *S.pubdone = gx ? 0 : (1 << 30);  // no plain copy wanted: nobody to wait for
+    *S.pubdone = 0;
   }
   __syncthreads();
   // roles (warp w runs on SM sub-partition w % 4; the main warp keeps its own)
   const int mainw = nw - 1, pubw = nw - 2, prodw = nw - 3, main2w = nw - 6;
+  int cid = -1;
+  {
+    static_assert(kBsNC <= 9, "co-main warps are taken off the main warp's sub-partition");
+    for (int i = 0; i < kBsNC; ++i)
+      if (warp == bs_comain_warp(i)) cid = i;
+  }
+  auto orig = [&](int p) { return s.dir ? n - 1 - p : p; };
   // this lane's half row (8 doubles) of dense block `block` of a slot
   auto ld_block = [&](const uint8_t* slot, int block, double* out) {
     const double2* p = reinterpret_cast<const double2*>(slot + block * kBsBlock) + lane;
@@ -271,8 +254,6 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, Bs
     while (*p != want)
       if (sg.expired()) break;
   };
-  auto slot_at = [&](int slot) { return S.slots + static_cast<size_t>(slot) * kBsSlotBytes; };
-  auto next_slot = [&](int slot) { return slot + 1 == ns ? 0 : slot + 1; };
 
   if (warp == mainw && G > 0) {
     // ---- main: y_g = c_g - q_g - F_1^g y_{g-1} - F_2^g y_{g-2} -----------------------
@@ -283,30 +264,20 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, Bs
     BS_DIAG(const long long t0 = clock64(); long long w_c = 0, w_s = 0, w_p = 0, w_q = 0;)
     uint8_t* const ringb = reinterpret_cast<uint8_t*>(S.ring);
     for (int k = 0; k <= 2; ++k) wait_eq(S.sready + k % ns, k);
+    wait_eq(S.aready + 0, 0);
     asm volatile("" ::: "memory");
+    auto slot_at = [&](int slot) { return S.slots + static_cast<size_t>(slot) * kBsSlotBytes; };
+    auto next_slot = [&](int slot) { return slot + 1 == ns ? 0 : slot + 1; };
     int s1 = 0, s2 = 1 % ns, s3 = 2 % ns;  // slots of groups g, g+1, g+2
     double f1[8], f2[8];
     ld_block(slot_at(s1), 0, f1);  // F_1 of group 0
     ld_block(slot_at(s2), 1, f2);  // F_2 of group 1
-    const uint4* cp = L.ct + r;    // c of group g: cp[16 g]
-    uint4 cw = __ldcg(cp);
-    {
-      BS_DIAG(const long long tw = clock64();)
-      SpinGuard sg(abort_flag);
-      while (!bs_valid(cw, L.tag) && !sg.expired()) cw = bs_poll(cp);
-      BS_DIAG(w_c += clock64() - tw;)
-    }
-    double c = bs_value(cw), q2 = 0.0, Q0 = 0.0;
+    double c = S.cbuf[r], q2 = 0.0, Q0 = 0.0;
     int pd = 0;
     int yoff = (kBsR - 1) * 128 + hf * 64;  // ring bytes of y_{g-1}, this lane's half
     int woff = r * 8;                       // ring bytes of y_g, this lane's row
-    int po = s.dir ? n - 1 - r : r, pstep = s.dir ? -kBsB : kBsB;  // this lane's row of the result vector
-    int prow = r;
     // invariant at the top of step g: the slots of groups <= g + 2 have landed
     for (int g = 0; g < G; ++g) {
-      const int gn = g + 1;
-      // c of the next group: the load is issued a whole step before its use
-      if (gn < G) cw = __ldcg(cp + static_cast<int64_t>(gn) * kBsB);
       const double2* yp = reinterpret_cast<const double2*>(ringb + yoff);
       const double2 y0 = yp[0], y1 = yp[1], y2 = yp[2], y3 = yp[3];
       double pa = f1[0] * y0.x, pb = f1[4] * y2.x, ua = f2[0] * y0.x, ub = f2[4] * y2.x;
@@ -328,48 +299,39 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, Bs
       s3 = next_slot(s3);
       ld_block(slot_at(s1), 0, f1);
       ld_block(slot_at(s2), 1, f2);
+      const int gn = g + 1;
+      const int fa = S.aready[gn & (kBsRC - 1)];
       const int fq = S.qready[gn & (kBsRQ - 1)];
       const int fs = S.sready[s3];
       // the chain's tail
       double t = (pa + pb) + (Q0 + q2);
       t += bs_shfl_xor16(t);
       const double y = c - t;
-      if (hf == 0) {
-        *reinterpret_cast<double*>(ringb + woff) = y;
-        if (prow < n) __stcg(L.gt + po, bs_pack(y, L.tag));  // to the workers: no fence, no flag
-      }
+      if (hf == 0) *reinterpret_cast<double*>(ringb + woff) = y;
       Q0 = ua + ub;
       __syncwarp();
-      if (lane == 0) {
-        *S.progress = gn;
-        __stcg(L.hint, (static_cast<unsigned long long>(L.tag) << 32) | static_cast<unsigned>(gn));
-      }
+      if (lane == 0) *S.progress = gn;
       yoff = woff - r * 8 + hf * 64;
-      woff = woff + 128 == kBsR * 128 + r * 8 ? r * 8 : woff + 128;
-      po += pstep;
-      prow += kBsB;
+      woff = woff + 128 == kBsZero + r * 8 ? r * 8 : woff + 128;
       if (fs != g + 3) {
         BS_DIAG(const long long tw = clock64();)
         wait_eq(S.sready + s3, g + 3);
         BS_DIAG(w_s += clock64() - tw;)
       }
       if (gn < G) {
+        if (fa != gn) {
+          BS_DIAG(const long long tw = clock64();)
+          wait_eq(S.aready + (gn & (kBsRC - 1)), gn);
+          BS_DIAG(w_c += clock64() - tw;)
+        }
         if (gn >= 3 && fq != gn) {
           BS_DIAG(const long long tw = clock64();)
           wait_eq(S.qready + (gn & (kBsRQ - 1)), gn);
           BS_DIAG(w_q += clock64() - tw;)
         }
         asm volatile("" ::: "memory");
+        c = S.cbuf[(gn & (kBsRC - 1)) * kBsB + r];
         q2 = gn >= 3 ? S.qbuf[(gn & (kBsRQ - 1)) * 32 + lane] : 0.0;
-        if (!bs_valid(cw, L.tag)) {
-          BS_DIAG(const long long tw = clock64();)
-          SpinGuard sg(abort_flag);
-          do {
-            cw = bs_poll(cp + static_cast<int64_t>(gn) * kBsB);
-          } while (!bs_valid(cw, L.tag) && !sg.expired());
-          BS_DIAG(w_c += clock64() - tw;)
-        }
-        c = bs_value(cw);
       }
       if (gn - pd >= kBsR - 2) {  // never lap the publisher on the y ring
         pd = *S.pubdone;
@@ -388,15 +350,17 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, Bs
       atomicAdd(&g_bs_dbg[2], static_cast<unsigned long long>(w_s));
       atomicAdd(&g_bs_dbg[3], static_cast<unsigned long long>(w_p));
       atomicAdd(&g_bs_dbg[4], static_cast<unsigned long long>(G));
-      atomicAdd(&g_bs_dbg[5], static_cast<unsigned long long>(w_q));
+      atomicAdd(&g_bs_dbg[14], static_cast<unsigned long long>(w_q));
     })
   } else if (warp == main2w && G > 3) {
     // ---- second main: q_t = sum_{k=3..K} F_k^t y_{t-k} --------------------------------
     // Step j consumes y_j as soon as the main warp has published it: the k = 3 term
     // completes q_{j+3} (handed to the main warp two steps before it is needed), the
     // terms k = 4..K go into the running sums of the groups behind it.
-    BS_DIAG(const long long t0 = clock64(); long long w_y = 0;)
+    BS_DIAG(long long w_y = 0;)
     const uint8_t* const ringb = reinterpret_cast<const uint8_t*>(S.ring);
+    auto slot_at = [&](int slot) { return S.slots + static_cast<size_t>(slot) * kBsSlotBytes; };
+    auto next_slot = [&](int slot) { return slot + 1 == ns ? 0 : slot + 1; };
     int sl[K - 2];  // slots of groups j+3 .. j+K
 #pragma unroll
     for (int i = 0; i < K - 2; ++i) sl[i] = (3 + i) % ns;
@@ -442,11 +406,193 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, Bs
       A[K - 3] = 0.0;
 #pragma unroll
       for (int i = 0; i < K - 2; ++i) sl[i] = next_slot(sl[i]);
-      yoff = yoff + 128 >= kBsR * 128 ? hf * 64 : yoff + 128;
+      yoff = yoff + 128 >= kBsZero ? hf * 64 : yoff + 128;
     }
+    BS_DIAG(if (lane == 0) atomicAdd(&g_bs_dbg[15], static_cast<unsigned long long>(w_y));)
+  } else if (cid >= 0) {
+    // ---- co-main: c_h = T_h (rhs_h - far_h - mid_h) ---------------------------
+    // A three-deep pipeline over this warp's groups h, h + NC, h + 2 NC: list
+    // sizes two groups ahead, mid-list staging (cp.async) and the right-hand
+    // side one group ahead, so no global-memory latency sits on a group's path.
+    BS_DIAG(const long long t0 = clock64(); long long w_p = 0, w_f = 0, d_a = 0, d_b = 0, d_c = 0, d_d = 0;)
+    const uint8_t* ringb = reinterpret_cast<const uint8_t*>(S.ring);
+    uint8_t* const stage0 = S.stage + static_cast<size_t>(cid) * 2 * kBsStageBytes;
+    struct Meta {
+      int mw, ms, fw;
+      int64_t mb;
+    };
+    auto load_meta = [&](int h) {
+      Meta m{0, 0, 0, 0};
+      if (h < G) {
+        m.mw = __ldg(s.mw + h);
+        m.ms = __ldg(s.ms + h);
+        m.fw = __ldg(s.fw + h);
+        m.mb = __ldg(s.mptr + h);
+      }
+      return m;
+    };
+    // stage the first min(mw, kBsStage) mid entries of a group (lane-private units)
+    auto stage_group = [&](const Meta& m, int buf) {
+      const int mw = min(m.mw, kBsStage);
+      const int4* cp = reinterpret_cast<const int4*>(s.mcols + m.mb) + lane;
+      const double2* vp = reinterpret_cast<const double2*>(s.mvals + m.mb) + lane;
+      const unsigned dst = smem_u32(stage0 + static_cast<size_t>(buf) * kBsStageBytes) + lane * 16;
+      for (int c = 0; c < mw / kBsMC; ++c) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536), "l"(cp + c * 32) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536 + 512), "l"(vp + 2 * c * 32)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 1536 + 1024),
+                     "l"(vp + (2 * c + 1) * 32)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto load_rhs = [&](int h) {
+      const int p = h * kBsB + r;
+      return (hf == 0 && p < n) ? __ldcg(rhs + orig(p)) : 0.0;
+    };
+    // this lane's half row of T_h, straight from global memory (one group ahead)
+    struct TRow {
+      double2 a, b, c, d;
+    };
+    auto load_t = [&](int h) {
+      TRow t{};
+      if (h < G) {
+        const double2* tp = reinterpret_cast<const double2*>(s.tblk + static_cast<size_t>(h) * kBsBlock) + lane;
+        t.a = __ldg(tp);
+        t.b = __ldg(tp + 32);
+        t.c = __ldg(tp + 64);
+        t.d = __ldg(tp + 96);
+      }
+      return t;
+    };
+    int prog = 0;  // last progress value seen
+    Meta m0 = load_meta(cid), m1 = load_meta(cid + kBsNC);
+    stage_group(m0, 0);
+    double rhs0 = load_rhs(cid);
+    TRow tr0 = load_t(cid);
+    int buf = 0;
+    for (int h = cid; h < G; h += kBsNC, buf ^= 1) {
+      BS_DIAG(const long long ta = clock64();)
+      const Meta m2 = load_meta(h + 2 * kBsNC);
+      stage_group(m1, buf ^ 1);
+      const double rhs1 = load_rhs(h + kBsNC);
+      const TRow tr1 = load_t(h + kBsNC);
+      // the far partial sum of this lane's row: the load is the poll
+      const uint4* fp = F.fps + static_cast<int64_t>(h) * kBsB + r;
+      uint4 fw0 = make_uint4(0u, 0u, 0u, 0u);
+      if (m0.fw > 0 && hf == 0) fw0 = __ldcg(fp);
+      double acc = rhs0;
+      const int mw = m0.mw, ms = m0.ms;
+      const int4* cp = reinterpret_cast<const int4*>(s.mcols + m0.mb) + lane;
+      const double2* vp = reinterpret_cast<const double2*>(s.mvals + m0.mb) + lane;
+      const uint8_t* sbuf = stage0 + static_cast<size_t>(buf) * kBsStageBytes + lane * 16;
+      auto wait_progress = [&](int need) {
+        if (prog >= need) return;
+        BS_DIAG(const long long tw = clock64();)
+        SpinGuard sg(abort_flag);
+        // Polling shared memory is not free for the other warps of the SM (every
+        // poll is a load on the shared LSU): only the waiter whose turn is next
+        // spins; the others sleep in proportion to their distance.
+        while ((prog = *S.progress) < need) {
+          const int d = need - prog;
+          if (d > 1) __nanosleep(d > 4 ? 400 : 80 * (d - 1));
+          if (sg.expired()) break;
+        }
+        asm volatile("" ::: "memory");
+        BS_DIAG(w_p += clock64() - tw;)
+      };
+      auto use = [&](const int4 cc, const double2 va, const double2 vb) {
+        const double x0 = *reinterpret_cast<const double*>(ringb + cc.x);
+        const double x1 = *reinterpret_cast<const double*>(ringb + cc.y);
+        const double x2 = *reinterpret_cast<const double*>(ringb + cc.z);
+        const double x3 = *reinterpret_cast<const double*>(ringb + cc.w);
+        double pa = va.x * x0, pb = vb.x * x2;
+        pa = fma(va.y, x1, pa);
+        pb = fma(vb.y, x3, pb);
+        acc -= pa + pb;
+      };
+      auto chunks = [&](int k0, int k1) {  // mid entries [k0, k1), whole chunks
+        int k = k0;
+        for (; k < k1 && k < kBsStage; k += kBsMC) {  // staged part
+          const uint8_t* q = sbuf + (k / kBsMC) * 1536;
+          use(*reinterpret_cast<const int4*>(q), *reinterpret_cast<const double2*>(q + 512),
+              *reinterpret_cast<const double2*>(q + 1024));
+        }
+        if (k >= k1) return;
+        // lists wider than the staging buffer (the few groups at the ends of the ordering)
+        int4 cc = __ldcs(cp + (k / 4) * 32);
+        double2 va = __ldcs(vp + (k / 2) * 32), vb = __ldcs(vp + (k / 2 + 1) * 32);
+        for (; k < k1; k += kBsMC) {
+          int4 nc = cc;
+          double2 na = va, nb = vb;
+          if (k + kBsMC < k1) {
+            nc = __ldcs(cp + (k / 4 + 1) * 32);
+            na = __ldcs(vp + (k / 2 + 2) * 32);
+            nb = __ldcs(vp + (k / 2 + 3) * 32);
+          }
+          use(cc, va, vb);
+          cc = nc;
+          va = na;
+          vb = nb;
+        }
+      };
+      // this group's staged list has landed (all but the newest commit group)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      BS_DIAG(const long long tb = clock64(); d_a += tb - ta;)
+      // entries that only need groups <= h-K-3
+      wait_progress(h - K - 2);
+      chunks(0, ms);
+      if (m0.fw > 0 && hf == 0) {
+        if (!bs_valid(fw0, F.tag)) {
+          BS_DIAG(const long long tw = clock64();)
+          SpinGuard sg(abort_flag);
+          do {
+            fw0 = bs_poll(fp);
+          } while (!bs_valid(fw0, F.tag) && !sg.expired());
+          BS_DIAG(w_f += clock64() - tw;)
+        }
+        acc -= bs_value(fw0);
+      }
+      // the newest mid entries need group h-K-1
+      wait_progress(h - K);
+      chunks(ms, mw);
+      const double t = acc + bs_shfl_xor16(acc);
+      BS_DIAG(const long long tc = clock64(); d_b += tc - tb;)
+      // c = T t: this lane's half of row r; t_m lives in lane m
+      const int src = hf * 8;
+      double ca = tr0.a.x * bs_shfl(t, src), cb = tr0.c.x * bs_shfl(t, src + 4);
+      ca = fma(tr0.a.y, bs_shfl(t, src + 1), ca);
+      cb = fma(tr0.c.y, bs_shfl(t, src + 5), cb);
+      ca = fma(tr0.b.x, bs_shfl(t, src + 2), ca);
+      cb = fma(tr0.d.x, bs_shfl(t, src + 6), cb);
+      ca = fma(tr0.b.y, bs_shfl(t, src + 3), ca);
+      cb = fma(tr0.d.y, bs_shfl(t, src + 7), cb);
+      double cv = ca + cb;
+      cv += bs_shfl_xor16(cv);
+      BS_DIAG(const long long td = clock64(); d_c += td - tc;)
+      wait_progress(h - kBsRC + 1);  // the c ring slot is free
+      if (hf == 0) S.cbuf[(h & (kBsRC - 1)) * kBsB + r] = cv;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        S.aready[h & (kBsRC - 1)] = h;
+      }
+      m0 = m1;
+      m1 = m2;
+      rhs0 = rhs1;
+      tr0 = tr1;
+      BS_DIAG(d_d += clock64() - td;)
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     BS_DIAG(if (lane == 0) {
-      atomicAdd(&g_bs_dbg[6], static_cast<unsigned long long>(w_y));
+      atomicAdd(&g_bs_dbg[5], static_cast<unsigned long long>(w_p));
+      atomicAdd(&g_bs_dbg[6], static_cast<unsigned long long>(w_f));
       atomicAdd(&g_bs_dbg[7], static_cast<unsigned long long>(clock64() - t0));
+      atomicAdd(&g_bs_dbg[10], static_cast<unsigned long long>(d_a));
+      atomicAdd(&g_bs_dbg[11], static_cast<unsigned long long>(d_b));
+      atomicAdd(&g_bs_dbg[12], static_cast<unsigned long long>(d_c));
+      atomicAdd(&g_bs_dbg[13], static_cast<unsigned long long>(d_d));
     })
   } else if (warp == prodw) {
     if (lane == 0) {
@@ -461,14 +607,14 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, Bs
           bulk_g2s(S.slots + static_cast<size_t>(isl) * kBsSlotBytes,
                    s.slots + static_cast<size_t>(issued) * kBsSlotBytes, kBsSlotBytes, S.mbar + isl);
           ++issued;
-          isl = next_slot(isl);
+          isl = isl + 1 == ns ? 0 : isl + 1;
           idle = false;
         }
         if (done < issued) {
           if (mbar_poll(S.mbar + dsl, (S.base_use[dsl] + done / ns) & 1)) {
             S.sready[dsl] = done;
             ++done;
-            dsl = next_slot(dsl);
+            dsl = dsl + 1 == ns ? 0 : dsl + 1;
             idle = false;
           }
         }
@@ -480,8 +626,8 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, Bs
         }
       }
     }
-  } else if (warp == pubw && gx) {
-    // ---- publisher: y ring -> the plain result vector ---------------------------------
+  } else if (warp == pubw) {
+    // ---- publisher: y ring -> the result vector (plain and tagged) -------------
     int done = 0;
     SpinGuard sg(abort_flag);
     while (done < G) {
@@ -490,26 +636,34 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, double* gx, Bs
         asm volatile("" ::: "memory");
         for (int g = done + hf; g < pnow; g += 2) {
           const int p = g * kBsB + r;
-          if (p < n) __stcg(gx + (s.dir ? n - 1 - p : p), S.ring[(g & (kBsR - 1)) * kBsB + r]);
+          if (p < n) {
+            const double v = S.ring[(g & (kBsR - 1)) * kBsB + r];
+            const int o = orig(p);
+            __stcg(F.gt + o, bs_pack(v, F.tag));
+            __stcg(gx + o, v);
+          }
         }
         __syncwarp();
         if (lane == 0) *S.pubdone = pnow;
         done = pnow;
         sg.t0 = clock64();
       } else {
-        __nanosleep(100);
+        __nanosleep(200);
         if (sg.expired()) break;
       }
     }
-  } else if (L.workers == 0 && warp < nw - 6 && (warp & 3) != (mainw & 3)) {
-    // no worker CTAs (tiny grids): the spare warps off the main warp's sub-partition
+  } else if (F.workers == 0 && (warp & 3) != (mainw & 3)) {
+    // no far-worker CTAs: the spare warps off the main warp's sub-partition
     int idx = 0, cnt = 0;
-    for (int w = 0; w < nw - 6; ++w)
-      if ((w & 3) != (mainw & 3)) {
+    for (int w = 0; w < nw; ++w) {
+      bool role = w == mainw || w == pubw || w == prodw || w == main2w;
+      for (int i = 0; i < kBsNC; ++i) role = role || w == bs_comain_warp(i);
+      if (!role && (w & 3) != (mainw & 3)) {
         if (w == warp) idx = cnt;
         ++cnt;
       }
-    bs_worker(s, L, idx, cnt, abort_flag);
+    }
+    bs_far(s, F, idx, cnt, abort_flag);
   }
   __syncthreads();
   if (threadIdx.x < ns) {

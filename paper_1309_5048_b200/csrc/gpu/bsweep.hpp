@@ -16,35 +16,34 @@
 // warp out of shared memory, instead of one step per dependency level
 // (32^3: 7,153 groups vs 10,715 levels of 10.7 rows).
 //
-// Who does what (measured reasons in DESIGN.md):
-//   * SWEEP CTA (one SM) -- only the dense near-diagonal part, because one SM
-//     moves 128 B/clk through shared memory and every byte it touches costs:
-//       - MAIN warp: y_g = c_g - q_g - F_{g,1} y_{g-1} - F_{g,2} y_{g-2}; lane
-//         (r, h) owns row r and columns 8h..8h+7 of each block (two lanes per
-//         row, one shuffle). Only F_{g,1} y_{g-1} is on the dependent chain.
-//       - SECOND MAIN warp: q_g = sum_{k=3..K} F_{g,k} y_{g-k}, accumulated as
-//         the y's appear (two steps of slack).
-//       - PRODUCER lane: TMA bulk copies of each group's F_1..F_K into a
-//         shared-memory slot ring. PUBLISHER warp: the plain result vector.
-//   * WORKER warps on all the other SMs (one group per warp, round-robin):
-//     c_g = T_g ( r_g - sum_{h < g-K} E_{g,h} y_h ): the whole sparse part of
-//     the factor (97 % of its entries at 32^3), streamed once from HBM as
-//     lane-interleaved lists, y gathered from L2.
-// Every cross-SM hand-off (y to the workers, c to the main warp, the
-// right-hand side) travels as self-validating 16-byte units {low word, tag,
-// high word, tag} -- two 8-byte halves, each carrying the sweep's tag, like
-// NCCL's LL protocol -- polled by the consumer: no fence, no flag. Measured
-// (tools/bs_lab.cu): 175 cycles per hop against 2,260 for data + fence + flag.
-// A worker needs y_{g-K-1} before it can finish c_g, and the main warp needs c_g
-// K steps later: K sets that slack.
+// Roles (one "sweep CTA" per triangular solve, plus far-worker CTAs):
+//   * MAIN warp: y_g = c_g - q_g - F_{g,1} y_{g-1} - F_{g,2} y_{g-2}; lane (r, h)
+//     owns row r and columns 8h..8h+7 of each block (two lanes per row, combined
+//     by one shuffle). y_{g-1} is broadcast through the shared-memory y ring.
+//   * SECOND MAIN warp: q_g = sum_{k=3..K} F_{g,k} y_{g-k}, accumulated as the
+//     y's appear (two steps of slack before the main warp needs q_g).
+//   * CO-MAIN warps (kBsNC, round-robin over groups): c_g = T_g (r_g - far_g
+//     - mid_g): the "mid" entries (groups g-R .. g-K-1) are gathered from the y
+//     ring; the "far" partial sums come from the far workers. Each co-main
+//     stages its NEXT group's mid list in shared memory with cp.async while it
+//     works on the current one, so the lists' HBM latency is off its path.
+//   * PRODUCER lane: TMA bulk copies of each group's dense blocks (F_1..F_K,
+//     T) into a shared-memory slot ring.
+//   * PUBLISHER warp: copies finished groups from the y ring to the result
+//     vector in global memory and publishes the progress counter (fence +
+//     release), so the main warp never touches global memory.
+//   * FAR WORKERS (warps of other CTAs): for each group the partial sums of
+//     the entries older than the ring (col group < g-R), gathered from the
+//     published result vector; they run far ahead of the main warp and stream
+//     ~85 % of the factor at HBM/L2 speed on as many SMs as needed.
 // The backward solve is the same sweep on the reversed ordering (row p of the
 // sweep = row n-1-p of the factor; L^T's rows are L's columns).
 //
 // Arithmetic: T_g and F_{g,k} are formed in long double and rounded once; the
 // sweep itself is fp64. The result is the same operator (L L^T)^{-1} applied
 // with a different association (measured agreement with the reference's
-// Ic0Factor::solve: ~1e-15, see tests/test_gpu_parity.py); the exact
-// column-order sweep stays available behind DSGPU_EXACT=1.
+// Ic0Factor::solve: see tests/test_gpu_parity.py); the exact column-order
+// sweep stays available behind DSGPU_EXACT=1.
 #pragma once
 
 #include <cstdint>
@@ -55,35 +54,46 @@
 namespace dsgpu {
 
 constexpr int kBsB = 16;     // rows per group
-constexpr int kBsK = 6;      // dense pre-multiplied coupling blocks: F_1, F_2 on the main warp,
+constexpr int kBsK = 5;      // dense pre-multiplied coupling blocks: F_1, F_2 on the main warp,
                              //   F_3..F_K on the second main warp
-constexpr int kBsR = 16;     // y ring depth in groups (main -> second main, publisher); power of two
 constexpr int kBsRQ = 8;     // q ring (second main warp -> main), groups (power of two)
-constexpr int kBsLC = 8;     // list chunk (entries per lane)
-constexpr int kBsBlock = kBsB * kBsB * 8;        // bytes of one dense block
-constexpr int kBsSlotBytes = kBsK * kBsBlock;    // F_1..F_K of one group
+constexpr int kBsR = 16;     // y ring depth in groups; older entries are "far"
+constexpr int kBsNC = 8;     // co-main warps
+constexpr int kBsRC = 16;    // c ring (co-main -> main), groups (power of two)
+constexpr int kBsMC = 4;     // mid-list chunk (entries per lane)
+constexpr int kBsFC = 8;     // far-list chunk (entries per lane)
+constexpr int kBsStage = 8;   // mid-list entries per lane staged ahead in shared memory (cp.async)
+constexpr int kBsStageBytes = kBsStage / kBsMC * 3 * 512;  // per buffer: chunks x (int4 + 2 double2) x 32 lanes
+constexpr int kBsBlock = kBsB * kBsB * 8;              // bytes of one dense block
+constexpr int kBsSlotBytes = kBsK * kBsBlock;          // F_1..F_K (T_g travels separately: co-mains load it)
+constexpr int kBsZero = kBsR * kBsB * 8;               // byte offset of the ring's zero slot
 
 // Lane-unit layouts. A dense block: lane l = (row r = l & 15, half h = l >> 4)
 // owns columns 8h..8h+7 as four 16-byte units; unit q of lane l sits at byte
-// ((q * 32) + l) * 16 (conflict-free 128-bit loads). Sparse lists: entry k of
-// lane l at int32 index ((k / 4) * 32 + l) * 4 + k % 4 and double index
-// ((k / 2) * 32 + l) * 2 + k % 2 from the group's base (coalesced 128-bit loads);
-// a row's entries are dealt alternately to its two lanes, oldest first,
-// right-aligned in the group's width.
+// ((q * 32) + l) * 16 (conflict-free 128-bit shared loads). Sparse lists: entry
+// k of lane l at int32 index ((k / 4) * 32 + l) * 4 + k % 4 and double index
+// ((k / 2) * 32 + l) * 2 + k % 2 from the group's base (coalesced 128-bit loads).
 inline int64_t bs_i32_at(int k, int l) { return (static_cast<int64_t>(k >> 2) * 32 + l) * 4 + (k & 3); }
 inline int64_t bs_f64_at(int k, int l) { return (static_cast<int64_t>(k >> 1) * 32 + l) * 2 + (k & 1); }
 
 struct HostBSweep {
   int n = 0, G = 0, dir = 0;        // dir 0: forward (L), 1: backward (L^T, reversed ordering)
-  std::vector<uint8_t> slots;        // (G + kBsK + 1) * kBsSlotBytes: zero groups behind the last one, so
-                                     //   the main warps never clamp a look-ahead index
-  std::vector<uint8_t> tblk;         // G * kBsBlock: T_g = D_g^{-1} (workers)
-  std::vector<int32_t> lw;           // list width of a group (multiple of kBsLC; 0 = none)
-  std::vector<int64_t> lptr;         // G + 1: element offset of the group's lists (width * 32 each)
-  std::vector<int32_t> lcols;        // rows of the result vector (original ordering); padding entries
-                                     //   (value 0) point at the group's oldest column
-  std::vector<double> lvals;
-  int64_t nnz_dense = 0, nnz_list = 0;  // factor entries in dense blocks / in the lists
+  std::vector<uint8_t> slots;        // (G + kBsK + 1) * kBsSlotBytes: zero blocks behind the last group, so the
+                                     //   main warps never clamp a look-ahead index
+  std::vector<uint8_t> tblk;         // G * kBsBlock: T_g = D_g^{-1} (read by the co-mains straight from global memory)
+  std::vector<int32_t> mw, ms;       // mid list: width (multiple of kBsMC), leading entries that only
+                                     //   need groups <= g-K-3 (multiple of kBsMC)
+  std::vector<int64_t> mptr;         // G + 1, element offset of the group's lists (width * 32 each)
+  std::vector<int32_t> mcols;        // byte offsets into the y ring (pad: kBsZero)
+  std::vector<double> mvals;
+  std::vector<int32_t> fw;           // far list: width (multiple of kBsFC; 0 = none)
+  std::vector<int64_t> fptr;         // G + 1
+  std::vector<int32_t> fcols;        // rows of the result vector (original ordering); padding entries
+                                     //   (value 0) point at the group's oldest far column
+  std::vector<double> fvals;
+  std::vector<int32_t> fcptr;        // G + 1: first chunk of the group in fneed
+  std::vector<int32_t> fneed;        // per chunk: newest group it depends on (-1: none)
+  int64_t nnz_dense = 0, nnz_mid = 0, nnz_far = 0;  // factor entries by class (statistics)
 };
 
 // Builds both sweeps of the factor L (lower triangular CSR, columns ascending,
@@ -96,11 +106,12 @@ void bsweep_host_apply(const HostBSweep& s, const double* rhs, double* x);
 
 // Shared memory of the sweep CTA with a slot ring of `ns` slots.
 inline size_t bs_smem_bytes(int ns) {
-  return static_cast<size_t>(kBsR) * kBsB * 8 + 128      // y ring
-         + kBsRQ * 32 * 8                                 // q ring
-         + static_cast<size_t>(ns) * kBsSlotBytes         // dense-block slots
-         + static_cast<size_t>(ns) * 8                    // mbarriers
-         + (2 * ns + kBsRQ + 8) * 4 + 256;                // sready, base_use, qready, progress words
+  return static_cast<size_t>(kBsZero) + 128            // y ring + zero slot
+         + kBsRC * kBsB * 8 + kBsRQ * 32 * 8            // c ring, q ring
+         + static_cast<size_t>(ns) * kBsSlotBytes       // dense-block slots
+         + static_cast<size_t>(kBsNC) * 2 * kBsStageBytes  // co-main mid-list staging (double-buffered)
+         + static_cast<size_t>(ns) * 8                  // mbarriers
+         + (2 * ns + kBsRC + kBsRQ + 8) * 4 + 128;      // sready, base_use, aready, qready, progress words
 }
 
 }  // namespace dsgpu

@@ -28,45 +28,68 @@ void build_dir(int n, int dir, RowFn rows, HostBSweep& s) {
   s.n = n;
   s.G = G;
   s.dir = dir;
-  s.lw.assign(G, 0);
+  s.mw.assign(G, 0);
+  s.ms.assign(G, 0);
+  s.fw.assign(G, 0);
   // ---- pass 1: list widths -------------------------------------------------
 #pragma omp parallel
   {
     std::vector<Ent> ent;
 #pragma omp for schedule(dynamic, 64)
     for (int g = 0; g < G; ++g) {
-      int w = 0;
+      int wm = 0, wf = 0;
       for (int r = 0; r < kBsB; ++r) {
         const int p = g * kBsB + r;
         if (p >= n) break;
         double d;
         rows(p, ent, d);
-        int cnt = 0;
-        for (const Ent& e : ent) cnt += g - e.first / kBsB > kBsK;
-        w = std::max(w, (cnt + 1) / 2);
+        int cm = 0, cf = 0;
+        for (const Ent& e : ent) {
+          const int dg = g - e.first / kBsB;
+          if (dg > kBsR)
+            ++cf;
+          else if (dg > kBsK)
+            ++cm;
+        }
+        wm = std::max(wm, (cm + 1) / 2);
+        wf = std::max(wf, (cf + 1) / 2);
       }
-      s.lw[g] = round_up(w, kBsLC);
+      s.mw[g] = round_up(wm, kBsMC);
+      s.fw[g] = round_up(wf, kBsFC);
     }
   }
-  s.lptr.assign(G + 1, 0);
-  for (int g = 0; g < G; ++g) s.lptr[g + 1] = s.lptr[g] + static_cast<int64_t>(s.lw[g]) * 32;
-  s.lcols.assign(s.lptr[G], -1);
-  s.lvals.assign(s.lptr[G], 0.0);
+  s.mptr.assign(G + 1, 0);
+  s.fptr.assign(G + 1, 0);
+  s.fcptr.assign(G + 1, 0);
+  for (int g = 0; g < G; ++g) {
+    s.mptr[g + 1] = s.mptr[g] + static_cast<int64_t>(s.mw[g]) * 32;
+    s.fptr[g + 1] = s.fptr[g] + static_cast<int64_t>(s.fw[g]) * 32;
+    s.fcptr[g + 1] = s.fcptr[g] + s.fw[g] / kBsFC;
+  }
+  s.mcols.assign(s.mptr[G], kBsZero);
+  s.mvals.assign(s.mptr[G], 0.0);
+  s.fcols.assign(s.fptr[G], n);
+  s.fvals.assign(s.fptr[G], 0.0);
+  s.fneed.assign(s.fcptr[G], -1);
   s.slots.assign(static_cast<size_t>(G + kBsK + 1) * kBsSlotBytes, 0);
   s.tblk.assign(static_cast<size_t>(G) * kBsBlock, 0);
-  int64_t nd = 0, nl = 0;
+  int64_t nd = 0, nm = 0, nf = 0;
   // ---- pass 2: fill ----------------------------------------------------------
-#pragma omp parallel reduction(+ : nd, nl)
+#pragma omp parallel reduction(+ : nd, nm, nf)
   {
-    std::vector<Ent> ent, old;
+    std::vector<Ent> ent, mid, far;
+    std::vector<int> mneed;
 #pragma omp for schedule(dynamic, 64)
     for (int g = 0; g < G; ++g) {
       long double D[kBsB][kBsB] = {};
       long double E[kBsK][kBsB][kBsB] = {};
-      const int w = s.lw[g];
-      int32_t* lc = s.lcols.data() + s.lptr[g];
-      double* lv = s.lvals.data() + s.lptr[g];
-      int32_t oldest = INT32_MAX;
+      const int wm = s.mw[g], wf = s.fw[g];
+      int32_t* mc = s.mcols.data() + s.mptr[g];
+      double* mv = s.mvals.data() + s.mptr[g];
+      int32_t* fc = s.fcols.data() + s.fptr[g];
+      double* fv = s.fvals.data() + s.fptr[g];
+      int32_t* fneed = s.fneed.data() + s.fcptr[g];
+      mneed.assign(wm / kBsMC, -1);
       for (int r = 0; r < kBsB; ++r) {
         const int p = g * kBsB + r;
         if (p >= n) {
@@ -76,40 +99,66 @@ void build_dir(int n, int dir, RowFn rows, HostBSweep& s) {
         double d;
         rows(p, ent, d);
         D[r][r] = d;
-        old.clear();
+        mid.clear();
+        far.clear();
         for (const Ent& e : ent) {
           const int gq = e.first / kBsB, c = e.first % kBsB, dg = g - gq;
           if (dg == 0)
             D[r][c] = e.second;
           else if (dg <= kBsK)
             E[dg - 1][r][c] = e.second;
+          else if (dg <= kBsR)
+            mid.push_back(e);
           else
-            old.push_back(e);
+            far.push_back(e);
         }
-        nd += static_cast<int64_t>(ent.size()) - static_cast<int64_t>(old.size());
-        nl += static_cast<int64_t>(old.size());
-        if (!old.empty()) oldest = std::min(oldest, old.front().first);
+        nd += static_cast<int64_t>(ent.size()) - static_cast<int64_t>(mid.size() + far.size());
+        nm += static_cast<int64_t>(mid.size());
+        nf += static_cast<int64_t>(far.size());
         // a row's list is dealt alternately to its two lanes (r, r + 16), each
         // lane's entries oldest first and RIGHT-aligned in the group's width,
-        // so the newest dependencies of all lanes share the last chunk
+        // so the newest dependencies of all lanes share the last chunks
         for (int h = 0; h < 2; ++h) {
           const int lane = r + 16 * h;
-          const int len = (static_cast<int>(old.size()) + 1 - h) / 2;
-          for (int k = 0; k < len; ++k) {
-            const Ent& e = old[2 * k + h];
-            const int pos = w - len + k;
-            lc[bs_i32_at(pos, lane)] = dir ? n - 1 - e.first : e.first;
-            lv[bs_f64_at(pos, lane)] = e.second;
+          const int lm = (static_cast<int>(mid.size()) + 1 - h) / 2;
+          for (int k = 0; k < lm; ++k) {
+            const Ent& e = mid[2 * k + h];
+            const int pos = wm - lm + k;
+            const int gq = e.first / kBsB, c = e.first % kBsB;
+            mc[bs_i32_at(pos, lane)] = ((gq % kBsR) * kBsB + c) * 8;
+            mv[bs_f64_at(pos, lane)] = e.second;
+            mneed[pos / kBsMC] = std::max(mneed[pos / kBsMC], gq);
+          }
+          const int lf = (static_cast<int>(far.size()) + 1 - h) / 2;
+          for (int k = 0; k < lf; ++k) {
+            const Ent& e = far[2 * k + h];
+            const int pos = wf - lf + k;
+            fc[bs_i32_at(pos, lane)] = dir ? n - 1 - e.first : e.first;
+            fv[bs_f64_at(pos, lane)] = e.second;
+            fneed[pos / kBsFC] = std::max(fneed[pos / kBsFC], e.first / kBsB);
           }
         }
       }
-      // padding gathers a real, already published entry (times 0): the group's
-      // oldest column, which the first chunk waits for anyway
-      if (w > 0) {
+      // far padding gathers a real, already published entry (times 0): the
+      // group's oldest far column, which every lane's first chunk waits for anyway
+      if (wf > 0) {
+        int32_t oldest = INT32_MAX;
+        for (int r = 0; r < kBsB; ++r) {
+          const int p = g * kBsB + r;
+          if (p >= n) break;
+          double d;
+          rows(p, ent, d);
+          if (!ent.empty() && g - ent.front().first / kBsB > kBsR) oldest = std::min(oldest, ent.front().first);
+        }
         const int32_t pad = dir ? n - 1 - oldest : oldest;
-        for (int64_t k = 0; k < static_cast<int64_t>(w) * 32; ++k)
-          if (lc[k] < 0) lc[k] = pad;
+        for (int lane = 0; lane < 32; ++lane)
+          for (int k = 0; k < wf; ++k)
+            if (fv[bs_f64_at(k, lane)] == 0.0 && fc[bs_i32_at(k, lane)] == n) fc[bs_i32_at(k, lane)] = pad;
       }
+      // leading mid chunks that are computable two groups early
+      int early = 0;
+      while (early < wm / kBsMC && mneed[early] <= g - kBsK - 3) ++early;
+      s.ms[g] = early * kBsMC;
       // T = D^{-1} (forward substitution, long double), F_k = T E_k
       long double T[kBsB][kBsB] = {};
       for (int c = 0; c < kBsB; ++c)
@@ -118,26 +167,28 @@ void build_dir(int n, int dir, RowFn rows, HostBSweep& s) {
           for (int m = c; m < r; ++m) acc -= D[r][m] * T[m][c];
           T[r][c] = acc / D[r][r];
         }
-      auto put = [&](uint8_t* base, int r, int c, long double v) {
+      uint8_t* slot = s.slots.data() + static_cast<size_t>(g) * kBsSlotBytes;
+      uint8_t* tb = s.tblk.data() + static_cast<size_t>(g) * kBsBlock;
+      auto put = [&](int block, int r, int c, long double v) {  // block kBsK: T (its own array)
         const int lane = r + 16 * (c >> 3), q = (c & 7) >> 1;
         const double dv = static_cast<double>(v);
+        uint8_t* base = block == kBsK ? tb : slot + static_cast<size_t>(block) * kBsBlock;
         std::memcpy(base + ((q * 32) + lane) * 16 + (c & 1) * 8, &dv, 8);
       };
-      uint8_t* slot = s.slots.data() + static_cast<size_t>(g) * kBsSlotBytes;
       for (int k = 0; k < kBsK; ++k)
         for (int r = 0; r < kBsB; ++r)
           for (int c = 0; c < kBsB; ++c) {
             long double acc = 0.0L;
             for (int m = 0; m <= r; ++m) acc += T[r][m] * E[k][m][c];
-            put(slot + static_cast<size_t>(k) * kBsBlock, r, c, acc);
+            put(k, r, c, acc);
           }
-      uint8_t* tb = s.tblk.data() + static_cast<size_t>(g) * kBsBlock;
       for (int r = 0; r < kBsB; ++r)
-        for (int c = 0; c < kBsB; ++c) put(tb, r, c, T[r][c]);
+        for (int c = 0; c < kBsB; ++c) put(kBsK, r, c, T[r][c]);
     }
   }
   s.nnz_dense = nd;
-  s.nnz_list = nl;
+  s.nnz_mid = nm;
+  s.nnz_far = nf;
 }
 
 }  // namespace
@@ -222,9 +273,12 @@ void bsweep_host_apply(const HostBSweep& s, const double* rhs, double* x) {
   const int n = s.n;
   auto orig = [&](int p) { return s.dir ? n - 1 - p : p; };
   std::vector<double> y(static_cast<size_t>(s.G + 1) * kBsB, 0.0);  // sweep order
-  auto blk = [&](const uint8_t* base, int r, int c) {
+  auto blk = [&](int g, int block, int r, int c) {
     const int lane = r + 16 * (c >> 3), q = (c & 7) >> 1;
     double v;
+    const uint8_t* base = block == kBsK ? s.tblk.data() + static_cast<size_t>(g) * kBsBlock
+                                        : s.slots.data() + static_cast<size_t>(g) * kBsSlotBytes +
+                                              static_cast<size_t>(block) * kBsBlock;
     std::memcpy(&v, base + ((q * 32) + lane) * 16 + (c & 1) * 8, 8);
     return v;
   };
@@ -235,22 +289,29 @@ void bsweep_host_apply(const HostBSweep& s, const double* rhs, double* x) {
       double part[2];
       for (int h = 0; h < 2; ++h) {
         const int lane = r + 16 * h;
-        double acc = 0.0;
-        for (int k = 0; k < s.lw[g]; ++k)
-          acc += s.lvals[s.lptr[g] + bs_f64_at(k, lane)] * x[s.lcols[s.lptr[g] + bs_i32_at(k, lane)]];
+        double acc = (h == 0 && p < n) ? rhs[orig(p)] : 0.0;
+        for (int k = 0; k < s.fw[g]; ++k) {
+          const int32_t c = s.fcols[s.fptr[g] + bs_i32_at(k, lane)];
+          if (c < n) acc -= s.fvals[s.fptr[g] + bs_f64_at(k, lane)] * x[c];
+        }
+        for (int k = 0; k < s.mw[g]; ++k) {
+          const int32_t off = s.mcols[s.mptr[g] + bs_i32_at(k, lane)];
+          if (off == kBsZero) continue;
+          const int slot = off / 8 / kBsB, c = off / 8 % kBsB;
+          int back = ((g - slot) % kBsR + kBsR) % kBsR;
+          if (back == 0) back = kBsR;
+          acc -= s.mvals[s.mptr[g] + bs_f64_at(k, lane)] * y[static_cast<size_t>(g - back) * kBsB + c];
+        }
         part[h] = acc;
       }
-      t[r] = (p < n ? rhs[orig(p)] : 0.0) - (part[0] + part[1]);
+      t[r] = part[0] + part[1];
     }
-    const uint8_t* slot = s.slots.data() + static_cast<size_t>(g) * kBsSlotBytes;
-    const uint8_t* tb = s.tblk.data() + static_cast<size_t>(g) * kBsBlock;
     for (int r = 0; r < kBsB; ++r) {
       double c = 0.0;
-      for (int m = 0; m < kBsB; ++m) c += blk(tb, r, m) * t[m];
+      for (int m = 0; m < kBsB; ++m) c += blk(g, kBsK, r, m) * t[m];
       double acc = 0.0;
       for (int k = 1; k <= kBsK && k <= g; ++k)
-        for (int m = 0; m < kBsB; ++m)
-          acc += blk(slot + static_cast<size_t>(k - 1) * kBsBlock, r, m) * y[static_cast<size_t>(g - k) * kBsB + m];
+        for (int m = 0; m < kBsB; ++m) acc += blk(g, k - 1, r, m) * y[static_cast<size_t>(g - k) * kBsB + m];
       const double v = c - acc;
       y[static_cast<size_t>(g) * kBsB + r] = v;
       const int p = g * kBsB + r;
@@ -264,8 +325,8 @@ void bsweep_host_apply(const HostBSweep& s, const double* rhs, double* x) {
 // Test hook (no device involved): the blocked-sweep PLAN of the factor L
 // evaluated on the host, z = (L L^T)^{-1} r, so the plan's structure and
 // coefficients can be checked against the plain substitution without a GPU.
-// stats8: G, factor entries in dense blocks / in the worker lists of the
-// forward and backward sweep, widest list, padded list entries (forward, backward).
+// stats8: G, factor entries in dense blocks / mid lists / far lists of the
+// forward sweep, widest mid list, widest far list, padded mid, padded far entries.
 extern "C" int dsgpu_debug_bsweep_host(int n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
                                        const double* r, double* z, int64_t* stats8) {
   try {
@@ -279,12 +340,12 @@ extern "C" int dsgpu_debug_bsweep_host(int n, const int64_t* row_ptr, const int3
     if (stats8) {
       stats8[0] = f.G;
       stats8[1] = f.nnz_dense;
-      stats8[2] = f.nnz_list;
-      stats8[3] = b.nnz_dense;
-      stats8[4] = b.nnz_list;
-      stats8[5] = *std::max_element(f.lw.begin(), f.lw.end());
-      stats8[6] = f.lptr.back();
-      stats8[7] = b.lptr.back();
+      stats8[2] = f.nnz_mid;
+      stats8[3] = f.nnz_far;
+      stats8[4] = *std::max_element(f.mw.begin(), f.mw.end());
+      stats8[5] = *std::max_element(f.fw.begin(), f.fw.end());
+      stats8[6] = f.mptr.back();
+      stats8[7] = f.fptr.back();
     }
     return DSGPU_OK;
   } catch (const std::exception&) {

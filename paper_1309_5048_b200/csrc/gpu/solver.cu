@@ -96,9 +96,8 @@ struct DBlock {
   // blocked sweeps (bsweep.cuh): remote_cta0 / n_remote name the far-worker CTAs
   int bs, bs_ns;                // 1: blocked sweeps; slot-ring depth
   DBSweep bfwd, bbwd;
-  uint4 *bs_bt, *bs_gy, *bs_gz; // n each: tagged right-hand side, forward result, backward result
-  uint4* bs_ct;                 // max(G) * 16: tagged c of every group (worker -> main warp)
-  unsigned long long* bs_hint;  // progress hint of the running sweep
+  uint4* bs_gt;                 // n + 1: tagged copy of the sweep result (far workers gather it)
+  uint4* bs_fps;                // max(G) * 16: tagged far partial sums
 };
 
 struct DevReport {
@@ -841,23 +840,16 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
   }
   // staged sweeps: materialize the right-hand side once (it may update r)
   double* bb = B.bb;
-  if constexpr (TB != 0) {
-    for (int i = threadIdx.x; i < B.n; i += blockDim.x) bb[i] = rhs(i);
-    __syncthreads();
-  }
+  for (int i = threadIdx.x; i < B.n; i += blockDim.x) bb[i] = rhs(i);
+  __syncthreads();
   double* y = B.y;
   if constexpr (TB == 0) {
-    // blocked sweeps (bsweep.cuh): the right-hand side and the forward result
-    // travel tagged; only z is also written plain
-    (void)bb;
-    (void)y;
-    const unsigned tag_f = sweep_tag(launch_id, sweep_no), tag_b = sweep_tag(launch_id, sweep_no + 1);
-    for (int i = threadIdx.x; i < B.n; i += blockDim.x) __stcg(B.bs_bt + i, bs_pack(rhs(i), tag_f));
+    // blocked sweeps (bsweep.cuh): results go to global memory (y, then z)
     const int workers = B.n_remote * static_cast<int>(blockDim.x >> 5);
-    bsweep<kBsK>(B.bfwd, xf, B.bs_ns, nullptr,
-                 BsLink{B.bs_bt, tag_f, B.bs_gy, B.bs_ct, B.bs_hint, tag_f, workers}, abort_flag);
-    bsweep<kBsK>(B.bbwd, xf, B.bs_ns, z, BsLink{B.bs_gy, tag_f, B.bs_gz, B.bs_ct, B.bs_hint, tag_b, workers},
-                 abort_flag);
+    bsweep<kBsK>(B.bfwd, xf, B.bs_ns, bb, y,
+                 BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no), workers}, abort_flag);
+    bsweep<kBsK>(B.bbwd, xf, B.bs_ns, y, z,
+                 BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no + 1), workers}, abort_flag);
     for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += r[i] * z[i];
     return block_sum(rz, red);
   } else if constexpr (RING) {
@@ -889,11 +881,10 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
 // What a remote helper CTA does while the IC CTA runs one IC(0) apply.
 __device__ __noinline__ void ic_apply_remote(const DBlock& B, int rank, unsigned* abort_flag, unsigned launch_id,
                                              unsigned sweep_no) {
-  if (B.bs) {  // workers of the blocked sweeps: every warp of this CTA
+  if (B.bs) {  // far workers of the blocked sweeps: every warp of this CTA
     const int nw = blockDim.x >> 5, W = B.n_remote * nw, wid = rank * nw + (threadIdx.x >> 5);
-    const unsigned tag_f = sweep_tag(launch_id, sweep_no), tag_b = sweep_tag(launch_id, sweep_no + 1);
-    bs_worker(B.bfwd, BsLink{B.bs_bt, tag_f, B.bs_gy, B.bs_ct, B.bs_hint, tag_f, W}, wid, W, abort_flag);
-    bs_worker(B.bbwd, BsLink{B.bs_gy, tag_f, B.bs_gz, B.bs_ct, B.bs_hint, tag_b, W}, wid, W, abort_flag);
+    bs_far(B.bfwd, BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no), W}, wid, W, abort_flag);
+    bs_far(B.bbwd, BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no + 1), W}, wid, W, abort_flag);
     return;
   }
   flow_remote(B.ffwd, B.n, B.y,
@@ -1773,7 +1764,7 @@ struct dsgpu_handle {
   bool pi = false;            // partitioned-inverse IC(0) applies (pi.cuh)
   bool bs = false;            // blocked sweeps (bsweep.cuh): the default IC(0) apply
   int bs_ns = 12;             // dense-block slot ring depth (minimum K + 3: the second main warp looks K groups ahead)
-  int far_ctas[2] = {0, 0};   // blocked-sweep worker CTAs per IC block
+  int far_ctas[2] = {0, 0};   // far-worker CTAs per IC block
   PiPlan pip[2];
   int pi_cbase = 0, pi_cslot = 0;  // chain coefficient prefetch slots (doubles)
   int pi_steps = 0;           // dependent chain steps per IC(0) apply (both sweeps)
@@ -1864,15 +1855,24 @@ DBSweep upload_bsweep(dsgpu_handle* h, HostBSweep& s) {
   d.dir = s.dir;
   d.slots = h->upload(s.slots);
   d.tblk = h->upload(s.tblk);
-  d.lw = h->upload(s.lw);
-  d.lptr = h->upload(s.lptr);
-  d.lcols = h->upload(s.lcols);
-  d.lvals = h->upload(s.lvals);
-  // the device copy is the plan from here on (96^3: 11 GB of lists per sweep)
+  d.mw = h->upload(s.mw);
+  d.ms = h->upload(s.ms);
+  d.mptr = h->upload(s.mptr);
+  d.mcols = h->upload(s.mcols);
+  d.mvals = h->upload(s.mvals);
+  d.fw = h->upload(s.fw);
+  d.fptr = h->upload(s.fptr);
+  d.fcols = h->upload(s.fcols);
+  d.fvals = h->upload(s.fvals);
+  d.fcptr = h->upload(s.fcptr);
+  d.fneed = h->upload(s.fneed);
+  // the device copy is the plan from here on (96^3: 13 GB of lists per sweep)
   std::vector<uint8_t>().swap(s.slots);
   std::vector<uint8_t>().swap(s.tblk);
-  std::vector<int32_t>().swap(s.lcols);
-  std::vector<double>().swap(s.lvals);
+  std::vector<int32_t>().swap(s.mcols);
+  std::vector<double>().swap(s.mvals);
+  std::vector<int32_t>().swap(s.fcols);
+  std::vector<double>().swap(s.fvals);
   return d;
 }
 
@@ -2136,14 +2136,14 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     if (h->ring && !h->bs) G = std::min(wmax, std::max(G, 1 + 2 * h->remote_max));  // room for remote helpers
     if (const char* env = std::getenv("DSGPU_GRID")) G = std::max(2, std::min(wmax, std::atoi(env)));
     if (h->bs) {
-      // worker CTAs of the blocked sweeps (bs_worker: the sparse part of the
-      // factor): workers 1.. of the grid (worker 0 posts the requests), split
-      // between the blocks
-      int want[2] = {96, 24};
+      // far-worker CTAs of the blocked sweeps: workers 1.. of the grid (worker 0
+      // posts the requests), split between the blocks; a block without far
+      // entries (everything within the y ring) needs none
+      int want[2] = {32, 8};
       if (const char* env = std::getenv("DSGPU_FAR_A")) want[0] = std::max(0, std::atoi(env));
       if (const char* env = std::getenv("DSGPU_FAR_Q")) want[1] = std::max(0, std::atoi(env));
       for (int b = 0; b < 2; ++b)
-        if (P.blk[b].kind != DSGPU_BLOCK_PCG_IC0) want[b] = 0;
+        if (P.blk[b].kind != DSGPU_BLOCK_PCG_IC0 || P.blk[b].bfwd.nnz_far + P.blk[b].bbwd.nnz_far == 0) want[b] = 0;
       if (!std::getenv("DSGPU_GRID")) G = std::min(wmax, std::max(G, 1 + want[0] + want[1]));
       while (want[0] + want[1] > G - 1) {  // small grids: shrink the larger share first
         int& w = want[0] >= want[1] ? want[0] : want[1];
@@ -2236,17 +2236,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         cudaMemset(d.y, 0, sizeof(double) * (hb.n + 1));
         cudaMemset(d.bb, 0, sizeof(double) * (hb.n + 1));
         // tag 0 is never a sweep's tag (launch ids start at 1): zeroed = "not written"
-        const size_t nn = static_cast<size_t>(hb.n) + 1;
-        d.bs_bt = h->alloc<uint4>(nn);
-        d.bs_gy = h->alloc<uint4>(nn);
-        d.bs_gz = h->alloc<uint4>(nn);
-        d.bs_ct = h->alloc<uint4>(static_cast<size_t>(G_max) * kBsB);
-        d.bs_hint = h->alloc<unsigned long long>(1);
-        cudaMemset(d.bs_bt, 0, sizeof(uint4) * nn);
-        cudaMemset(d.bs_gy, 0, sizeof(uint4) * nn);
-        cudaMemset(d.bs_gz, 0, sizeof(uint4) * nn);
-        cudaMemset(d.bs_ct, 0, sizeof(uint4) * static_cast<size_t>(G_max) * kBsB);
-        cudaMemset(d.bs_hint, 0, sizeof(unsigned long long));
+        d.bs_gt = h->alloc<uint4>(static_cast<size_t>(hb.n) + 1);
+        d.bs_fps = h->alloc<uint4>(static_cast<size_t>(G_max) * kBsB);
+        cudaMemset(d.bs_gt, 0, sizeof(uint4) * (static_cast<size_t>(hb.n) + 1));
+        cudaMemset(d.bs_fps, 0, sizeof(uint4) * static_cast<size_t>(G_max) * kBsB);
         d.n_remote = h->far_ctas[b];
         d.remote_cta0 = 1 + (b == 1 ? h->far_ctas[0] : 0);  // worker units (Ctx::remote_rank)
       } else if (hb.kind == DSGPU_BLOCK_PCG_IC0) {
