@@ -1763,7 +1763,7 @@ struct dsgpu_handle {
   bool ring = false;
   bool pi = false;            // partitioned-inverse IC(0) applies (pi.cuh)
   bool bs = false;            // blocked sweeps (bsweep.cuh): the default IC(0) apply
-  int bs_ns = 12;             // dense-block slot ring depth (minimum K + 3: the second main warp looks K groups ahead)
+  int bs_ns = 10;             // dense-block slot ring depth (minimum K + 3: the second main warp looks K groups ahead)
   int far_ctas[2] = {0, 0};   // far-worker CTAs per IC block
   PiPlan pip[2];
   int pi_cbase = 0, pi_cslot = 0;  // chain coefficient prefetch slots (doubles)
