@@ -51,18 +51,32 @@
 
 #include "dsgpu.h"
 
+// Tuning constants (overridable at build time for A/B runs: make EXTRA_DEFS=-DDSGPU_BS_K=4 ...)
+#ifndef DSGPU_BS_K
+#define DSGPU_BS_K 5
+#endif
+#ifndef DSGPU_BS_R
+#define DSGPU_BS_R 32
+#endif
+#ifndef DSGPU_BS_NC
+#define DSGPU_BS_NC 8
+#endif
+#ifndef DSGPU_BS_STAGE
+#define DSGPU_BS_STAGE 16
+#endif
+
 namespace dsgpu {
 
 constexpr int kBsB = 16;     // rows per group
-constexpr int kBsK = 5;      // dense pre-multiplied coupling blocks: F_1, F_2 on the main warp,
+constexpr int kBsK = DSGPU_BS_K;      // dense pre-multiplied coupling blocks: F_1, F_2 on the main warp,
                              //   F_3..F_K on the second main warp
 constexpr int kBsRQ = 8;     // q ring (second main warp -> main), groups (power of two)
-constexpr int kBsR = 32;     // y ring depth in groups; older entries are "far"
-constexpr int kBsNC = 8;     // co-main warps
+constexpr int kBsR = DSGPU_BS_R;     // y ring depth in groups; older entries are "far"
+constexpr int kBsNC = DSGPU_BS_NC;     // co-main warps
 constexpr int kBsRC = 16;    // c ring (co-main -> main), groups (power of two)
 constexpr int kBsMC = 4;     // mid-list chunk (entries per lane)
 constexpr int kBsFC = 8;     // far-list chunk (entries per lane)
-constexpr int kBsStage = 16;  // mid-list entries per lane staged ahead in shared memory (cp.async)
+constexpr int kBsStage = DSGPU_BS_STAGE;  // mid-list entries per lane staged ahead in shared memory (cp.async)
 constexpr int kBsStageBytes = kBsStage / kBsMC * 3 * 512;  // per buffer: chunks x (int4 + 2 double2) x 32 lanes
 constexpr int kBsBlock = kBsB * kBsB * 8;              // bytes of one dense block
 constexpr int kBsSlotBytes = kBsK * kBsBlock;          // F_1..F_K (T_g travels separately: co-mains load it)

@@ -1762,8 +1762,9 @@ struct dsgpu_handle {
   bool exact = false;
   bool ring = false;
   bool pi = false;            // partitioned-inverse IC(0) applies (pi.cuh)
-  bool bs = false;            // blocked sweeps (bsweep.cuh): the default IC(0) apply
-  int bs_ns = 10;             // dense-block slot ring depth (minimum K + 3: the second main warp looks K groups ahead)
+  bool bs = false;            // blocked sweeps (bsweep.cuh)
+  bool force_pi = false;      // the early model chose the partitioned inverse
+  int bs_ns = kBsK + 3;       // dense-block slot ring depth (minimum K + 3: the second main warp looks K groups ahead)
   int far_ctas[2] = {0, 0};   // far-worker CTAs per IC block
   PiPlan pip[2];
   int pi_cbase = 0, pi_cslot = 0;  // chain coefficient prefetch slots (doubles)
@@ -1920,7 +1921,7 @@ DSweep upload_sweep(dsgpu_handle* h, const HostSweep& s) {
 // staged); not C4/C5 (3D, lower bandwidth 23k+: tens of GB of block inverses;
 // C4 PI 14 ms per apply vs 14.5 ms staged, staged solve 1.4x faster).
 bool choose_pi(dsgpu_handle* h, const HostPlan& P, size_t smem_budget) {
-  bool force = false;
+  bool force = h->force_pi;
   if (const char* env = std::getenv("DSGPU_PI")) {
     if (std::atoi(env) == 0) return false;
     force = true;
@@ -1968,6 +1969,53 @@ bool choose_pi(dsgpu_handle* h, const HostPlan& P, size_t smem_budget) {
   if (!found) return false;
   const double t_staged = 0.6e-6 * staged_levels;
   return force || best < 0.7 * t_staged;
+}
+
+// Early mode choice (before the plan exists, on the caller's factor arrays):
+// modelled time of one partitioned-inverse apply against one blocked-sweep
+// apply. The partitioned inverse wins where the factor's bandwidth is small
+// (2D systems: its block inverses are tens of MB and its chain a few dozen
+// steps); the blocked sweeps win where the inverses would be GBs (3D).
+//   t_pi = 8 n_coef / 3.9 TB/s + 2 us x steps    (as in choose_pi)
+//   t_bs = 0.35 us x 2 ceil(n / 16)              (measured: 0.28-0.39 us per 16-row group)
+bool prefers_partitioned_inverse(const dsgpu_csr* fac[2], const int kinds[2], size_t smem_budget) {
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  int bw[2] = {0, 0};
+  double t_bs = 0.0;
+  for (int b = 0; b < 2; ++b) {
+    if (kinds[b] != DSGPU_BLOCK_PCG_IC0 || !fac[b]) continue;
+    bw[b] = pi_bandwidth(fac[b]->n_rows, fac[b]->row_ptr, fac[b]->cols);
+    t_bs = std::max(t_bs, 0.35e-6 * 2.0 * ((fac[b]->n_rows + kBsB - 1) / kBsB));
+  }
+  double best = -1.0;
+  for (const double mult : {0.5, 1.0, 1.5}) {
+    PiPlan pp[2];
+    int nb0 = 0;
+    size_t bytes = 0;
+    bool ok = true;
+    for (int b = 0; b < 2 && ok; ++b) {
+      if (kinds[b] != DSGPU_BLOCK_PCG_IC0 || !fac[b]) continue;
+      const int n = fac[b]->n_rows;
+      int bsz = std::max(1, static_cast<int>(std::ceil(std::max(1, bw[b]) * mult)));
+      if (b == 1 && nb0 > 0) bsz = std::max(bsz, (n + nb0 - 1) / nb0);
+      // the inverses alone are ~ n * bsz doubles: skip the exact plan when that cannot fit
+      if (static_cast<double>(n) * bsz * 8.0 > static_cast<double>(free_b) / 2) {
+        ok = false;
+        break;
+      }
+      pp[b] = pi_plan(n, fac[b]->row_ptr, fac[b]->cols, bsz);
+      if (b == 0) nb0 = pp[0].nb;
+      bytes += sizeof(double) * (static_cast<size_t>(pp[b].n_coef) + 8ull * n);
+    }
+    if (!ok) continue;
+    const size_t smem = sizeof(double) * static_cast<size_t>(pp[0].wmax + pp[1].wmax + 32);
+    if (smem > smem_budget || bytes > free_b / 2) continue;
+    const double t_pi = 8.0 * static_cast<double>(pp[0].n_coef + pp[1].n_coef) / 3.9e12 +
+                        2e-6 * 2 * std::max(pp[0].nb, pp[1].nb);
+    if (best < 0.0 || t_pi < best) best = t_pi;
+  }
+  return best >= 0.0 && best < 0.8 * t_bs;
 }
 
 // Shared memory of the PI kernels: both chain windows, then (when it fits)
@@ -2035,9 +2083,32 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
   // legacy knobs DSGPU_PI / DSGPU_EXACT is set): staged level sweeps or the
   // partitioned inverse by the cost model, or the exact column-order sweeps
   h->exact = std::getenv("DSGPU_EXACT") && std::atoi(std::getenv("DSGPU_EXACT")) != 0;
+  h->force_pi = false;
   {
     const char* sw = std::getenv("DSGPU_SWEEP");
-    h->bs = !h->exact && (sw ? std::string(sw) == "bs" : std::getenv("DSGPU_PI") == nullptr);
+    const bool any_ic0 = top_kind == DSGPU_BLOCK_PCG_IC0 || bottom_kind == DSGPU_BLOCK_PCG_IC0;
+    if (h->exact || !any_ic0) {
+      h->bs = false;
+    } else if (sw) {
+      h->bs = std::string(sw) == "bs";  // "legacy": round-1 cost model (partitioned inverse / staged sweeps)
+    } else if (std::getenv("DSGPU_PI")) {
+      h->bs = false;
+    } else {  // auto: partitioned inverse where its model wins (2D), blocked sweeps otherwise
+      int smem_optin = 0;
+      cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+      const dsgpu_csr* fac[2] = {L_A, L_Q};
+      const int kinds[2] = {top_kind, bottom_kind};
+      bool pi = false;
+      try {
+        if ((top_kind != DSGPU_BLOCK_PCG_IC0 || (L_A && L_A->row_ptr && L_A->cols)) &&
+            (bottom_kind != DSGPU_BLOCK_PCG_IC0 || (L_Q && L_Q->row_ptr && L_Q->cols)))
+          pi = prefers_partitioned_inverse(fac, kinds, static_cast<size_t>(smem_optin) - 2048);
+      } catch (const std::exception&) {
+        pi = false;  // malformed factor: build_plan reports it
+      }
+      h->bs = !pi;
+      h->force_pi = pi;
+    }
   }
   try {
     build_plan(h->plan, A, B, Bt, Q_nu, top_kind, perm_A, L_A, bottom_kind, perm_Q, L_Q,

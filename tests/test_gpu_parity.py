@@ -84,14 +84,15 @@ def test_ic0_apply_partitioned_inverse_matches_reference(gpu, port, monkeypatch,
 @pytest.mark.parametrize("knobs", [{}, {"DSGPU_FAR_A": "0", "DSGPU_FAR_Q": "0"}, {"DSGPU_GRID": "5"},
                                    {"DSGPU_FAR_A": "3", "DSGPU_FAR_Q": "1", "DSGPU_BS_SLOTS": "9"}])
 def test_ic0_apply_blocked_matches_reference(gpu, port, monkeypatch, knobs):
-    """The default IC(0) apply: blocked sweeps (bsweep.hpp) -- dense 16x16
-    blocks next to the diagonal on the main warp, mid entries on the co-main
-    warps, far entries on far-worker CTAs -- against the reference's own
-    Ic0Factor::solve output (fixture), the CPU oracle on 2D and 3D factors, and
-    through a whole solve. knobs: no far-worker CTAs (the sweep CTA's spare
-    warps do the far lists), a 5-CTA grid, few far CTAs with a different slot
-    ring depth."""
+    """Blocked sweeps (bsweep.hpp; the IC(0) apply of the large 3D systems,
+    forced here with DSGPU_SWEEP=bs) -- dense 16x16 blocks next to the diagonal
+    on the two main warps, mid entries on the co-main warps, far entries on
+    far-worker CTAs -- against the reference's own Ic0Factor::solve output
+    (fixture), the CPU oracle on 2D and 3D factors, and through a whole solve.
+    knobs: no far-worker CTAs (the sweep CTA's spare warps do the far lists), a
+    5-CTA grid, few far CTAs with a different slot ring depth."""
     host, solver = gpu
+    monkeypatch.setenv("DSGPU_SWEEP", "bs")
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
     d = load_golden("c1_psi_k2_n8.npz")
@@ -115,6 +116,15 @@ def test_ic0_apply_blocked_matches_reference(gpu, port, monkeypatch, knobs):
         sol = g.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
         check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
         g.close()
+
+
+def test_ic0_mode_policy(gpu):
+    """Setup's choice of the IC(0) apply: the partitioned inverse where its
+    model wins (small-bandwidth 2D factors), the exact sweeps on request."""
+    host, solver = gpu
+    g = solver.GpuStokesSolver(host.assemble("psi-mms", 2, 32), "IC0-PCG(A,Q)")
+    assert g.info()["ic0_mode"] == "partitioned-inverse"
+    g.close()
 
 
 def test_two_handles_of_different_sizes(gpu, port):
@@ -357,6 +367,7 @@ def test_full_size_config_vs_reference(gpu, cfg):
     s = host.assemble(kw["case"], kw["k_prime"], kw["n_elem"], dim=kw["dim"], seed=kw["seed"])
     assert [s.n_u, s.n_p, s.A.nnz, s.B.nnz, s.Q.nnz] == g["sizes"].tolist()
     gs = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    assert gs.info()["ic0_mode"] == ("blocked" if cfg == "c4" else "partitioned-inverse")
     sol = gs.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1,
                                                 max_iter=kw["max_iter"]))
     x = np.concatenate([sol.u, sol.p])
