@@ -213,8 +213,10 @@ __device__ void bs_far(const DBSweep& s, BsFar F, int wid, int W, unsigned* abor
 // the factor's ordering). Returns after a CTA barrier with the result complete
 // in global memory (plain in gx, tagged in F.gt).
 template <int K>
-__device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* __restrict__ rhs, double* gx,
-                       BsFar F, unsigned* abort_flag) {
+// Right-hand side: rt (tagged units carrying rtag, written by the rows' owners --
+// possibly other GPUs -- and polled here) or, when rt is null, the plain vector rhs.
+__device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* __restrict__ rt, unsigned rtag,
+                       const double* __restrict__ rhs, double* gx, BsFar F, unsigned* abort_flag) {
   static_assert(K >= 3 && K <= 8 && K == kBsK, "dense coupling depth (F_1, F_2: main warp; F_3..F_K: second main warp)");
   const DBSweep s = s_in;
   const int G = s.G, n = s.n;
@@ -447,9 +449,23 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    // right-hand side of group h, this lane's row: issued one group ahead; a
+    // tagged unit that has not arrived yet is polled when it is needed
     auto load_rhs = [&](int h) {
       const int p = h * kBsB + r;
-      return (hf == 0 && p < n) ? __ldcg(rhs + orig(p)) : 0.0;
+      uint4 w = make_uint4(0u, rtag, 0u, rtag);  // rows without a right-hand side: 0.0, valid
+      if (hf == 0 && p < n) w = rt ? __ldcg(rt + orig(p)) : bs_pack(__ldcg(rhs + orig(p)), rtag);
+      return w;
+    };
+    auto take_rhs = [&](uint4 w, int h) {
+      if (!bs_valid(w, rtag)) {
+        SpinGuard sg(abort_flag);
+        const uint4* q = rt + orig(h * kBsB + r);
+        do {
+          w = bs_poll(q);
+        } while (!bs_valid(w, rtag) && !sg.expired());
+      }
+      return bs_value(w);
     };
     // this lane's half row of T_h, straight from global memory (one group ahead)
     struct TRow {
@@ -469,20 +485,20 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const double* 
     int prog = 0;  // last progress value seen
     Meta m0 = load_meta(cid), m1 = load_meta(cid + kBsNC);
     stage_group(m0, 0);
-    double rhs0 = load_rhs(cid);
+    uint4 rhs0 = load_rhs(cid);
     TRow tr0 = load_t(cid);
     int buf = 0;
     for (int h = cid; h < G; h += kBsNC, buf ^= 1) {
       BS_DIAG(const long long ta = clock64();)
       const Meta m2 = load_meta(h + 2 * kBsNC);
       stage_group(m1, buf ^ 1);
-      const double rhs1 = load_rhs(h + kBsNC);
+      const uint4 rhs1 = load_rhs(h + kBsNC);
       const TRow tr1 = load_t(h + kBsNC);
       // the far partial sum of this lane's row: the load is the poll
       const uint4* fp = F.fps + static_cast<int64_t>(h) * kBsB + r;
       uint4 fw0 = make_uint4(0u, 0u, 0u, 0u);
       if (m0.fw > 0 && hf == 0) fw0 = __ldcg(fp);
-      double acc = rhs0;
+      double acc = take_rhs(rhs0, h);
       const int mw = m0.mw, ms = m0.ms;
       const int4* cp = reinterpret_cast<const int4*>(s.mcols + m0.mb) + lane;
       const double2* vp = reinterpret_cast<const double2*>(s.mvals + m0.mb) + lane;

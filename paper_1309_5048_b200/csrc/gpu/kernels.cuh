@@ -70,8 +70,13 @@ __device__ __forceinline__ double row_partial(const int32_t* ci, const double* v
   const double2* vp = reinterpret_cast<const double2*>(v) + 2 * sub;
   double a0 = 0.0, a1 = 0.0;
   for (int k = 4 * sub; k < len; k += 4 * L, cp += L, vp += 2 * L) {
+#ifdef DSGPU_SPMV_LDG
+    const int4 c = __ldg(cp);
+    const double2 p = __ldg(vp), q = __ldg(vp + 1);
+#else
     const int4 c = __ldcs(cp);
     const double2 p = __ldcs(vp), q = __ldcs(vp + 1);
+#endif
     a0 = fma(p.x, xf(c.x), a0);
     a1 = fma(p.y, xf(c.y), a1);
     a0 = fma(q.x, xf(c.z), a0);

@@ -33,6 +33,7 @@
 
 #include "dsgpu_internal.hpp"
 #include "kernels.cuh"
+#include "partition.hpp"
 #include "pi.cuh"
 #include "bsweep.cuh"
 
@@ -96,9 +97,45 @@ struct DBlock {
   // blocked sweeps (bsweep.cuh): remote_cta0 / n_remote name the far-worker CTAs
   int bs, bs_ns;                // 1: blocked sweeps; slot-ring depth
   DBSweep bfwd, bbwd;
+  uint4* bs_bt;                 // n: tagged right-hand side, written by the rows' owners (every GPU's workers)
   uint4* bs_gt;                 // n + 1: tagged copy of the sweep result (far workers gather it)
   uint4* bs_fps;                // max(G) * 16: tagged far partial sums
 };
+
+// Multi-GPU state of one rank (partition.hpp). Every rank runs
+// the same persistent kernel on its own rows; all cross-GPU traffic goes through
+// peer memory (the ranks' arenas, mapped into every rank with CUDA IPC):
+//   * halo: before an SpMV the ranks copy the vector entries their rows need
+//     from the owners' vectors (NVLink peer loads);
+//   * dot products: every grid-barrier reduction is followed by an exchange of
+//     the per-GPU sums through peer mailboxes (stores + release flag, summed in
+//     rank order on every GPU: identical values everywhere);
+//   * IC(0): every rank pushes its rows of the block residual, tagged, into
+//     every rank's right-hand-side buffer and all ranks run the whole sweep
+//     (replicated: the preconditioner is the single-GPU one).
+constexpr int kMaxWorld = 8;
+struct MultiGpu {
+  int world, rank;
+  char* arena[kMaxWorld];          // base of every rank's arena in THIS rank's address space
+  const int2* halo_y;              // {K' column, owner}: entries of y this rank's rows read but do not own
+  int n_halo_y;
+  const int2* halo_p[2];           // the same for the block operators (block-local column, owner)
+  int n_halo_p[2];
+  double* xsum;                    // [2][kMaxWorld][NSLOT] mailbox (in the arena)
+  unsigned* xflag;                 // [2][kMaxWorld]
+};
+template <class T>
+__device__ __forceinline__ T* peer_ptr(const MultiGpu& m, T* p, int r) {
+  return reinterpret_cast<T*>(m.arena[r] + (reinterpret_cast<char*>(p) - m.arena[m.rank]));
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 struct DevReport {
   int iterations, converged, status, failed_block, hist_len, pad;
@@ -127,8 +164,9 @@ struct Args {
   const int64_t* k_rp;
   const int32_t* k_ci;
   const double* k_v;
-  const int32_t* row_start;  // G + 1
+  const int32_t *row_lo, *row_hi;  // per worker CTA: its rows [row_lo, row_hi) of K' (within one block)
   int k_lanes;               // lanes per row of the saddle SpMV (row_partial)
+  MultiGpu mg;               // world > 1: the row-partitioned solve across the box's GPUs
   DBlock blk[2];
   const double* f_in;        // n_u, original order
   const int32_t* perm_u;     // block ordering -> original
@@ -823,7 +861,8 @@ __device__ void flow_sweep(const DFlow& s_in, int n, double* smem, const double*
 // CTA sum of r_i z_i in warp 0. rhs(row) yields r_row (and may write it).
 template <int TB, bool RING, class Rhs>
 __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, double* red,
-                           unsigned* abort_flag, unsigned launch_id = 0, unsigned sweep_no = 0) {
+                           unsigned* abort_flag, unsigned launch_id = 0, unsigned sweep_no = 0,
+                           bool rhs_is_local = true) {
   double* z = B.z;
   const double* r = B.r;
   double rz = 0.0;
@@ -844,13 +883,20 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
   __syncthreads();
   double* y = B.y;
   if constexpr (TB == 0) {
-    // blocked sweeps (bsweep.cuh): results go to global memory (y, then z)
+    // blocked sweeps (bsweep.cuh). The tagged right-hand side B.bs_bt was
+    // written by the rows' owners (the worker CTAs of every GPU: precond());
+    // the stand-alone kernel passes rhs_is_local and writes it here.
+    (void)bb;
+    const unsigned tag_f = sweep_tag(launch_id, sweep_no), tag_b = sweep_tag(launch_id, sweep_no + 1);
+    if (rhs_is_local)
+      for (int i = threadIdx.x; i < B.n; i += blockDim.x) __stcg(B.bs_bt + i, bs_pack(rhs(i), tag_f));
     const int workers = B.n_remote * static_cast<int>(blockDim.x >> 5);
-    bsweep<kBsK>(B.bfwd, xf, B.bs_ns, bb, y,
-                 BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no), workers}, abort_flag);
-    bsweep<kBsK>(B.bbwd, xf, B.bs_ns, y, z,
-                 BsFar{B.bs_gt, B.bs_fps, sweep_tag(launch_id, sweep_no + 1), workers}, abort_flag);
-    for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += r[i] * z[i];
+    bsweep<kBsK>(B.bfwd, xf, B.bs_ns, B.bs_bt, tag_f, nullptr, y,
+                 BsFar{B.bs_gt, B.bs_fps, tag_f, workers}, abort_flag);
+    bsweep<kBsK>(B.bbwd, xf, B.bs_ns, nullptr, tag_b, y, z, BsFar{B.bs_gt, B.bs_fps, tag_b, workers}, abort_flag);
+    // <r, z> over the whole block from the tagged right-hand side (complete: the
+    // forward sweep has read every entry of it)
+    for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += bs_value(__ldcg(B.bs_bt + i)) * z[i];
     return block_sum(rz, red);
   } else if constexpr (RING) {
     // results go straight to global memory (y, then z)
@@ -924,8 +970,8 @@ struct Ctx {
   __device__ Ctx(const Args& args, double* red_, double* sums_, double* xs)
       : a(args), cta(blockIdx.x - args.n_srv), G(gridDim.x - args.n_srv), epoch(0), red(red_),
         sums(sums_) {
-    r0 = a.row_start[cta];
-    r1 = a.row_start[cta + 1];
+    r0 = a.row_lo[cta];
+    r1 = a.row_hi[cta];
     xf = xs;
     xb = xs + a.smem_half;
     abort_flag = a.bar + 64;
@@ -966,7 +1012,71 @@ struct Ctx {
     }
     __syncthreads();
     ++epoch;
+    if (ok && a.mg.world > 1) return cross_gpu_reduce(mask);
     return ok;
+  }
+  // After the local reduction: exchange the per-GPU sums through the peers'
+  // mailboxes and add them in rank order (every CTA of every GPU gets the same
+  // values). Mailboxes are double-buffered by epoch parity; the epoch word
+  // carries the launch id, so nothing has to be reset between launches.
+  __device__ bool cross_gpu_reduce(unsigned mask) {
+    const MultiGpu& m = a.mg;
+    const unsigned ep = (a.launch_id << 20) | (epoch & 0xFFFFFu);
+    const int par = static_cast<int>(epoch & 1u);
+    if (cta == 0) {
+      if (threadIdx.x < NSLOT)
+        for (int r = 0; r < m.world; ++r)
+          if (r != m.rank)
+            *reinterpret_cast<volatile double*>(peer_ptr(m, m.xsum, r) + (par * kMaxWorld + m.rank) * NSLOT + threadIdx.x) =
+                sums[threadIdx.x];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int r = 0; r < m.world; ++r)
+          if (r != m.rank) st_release_sys(peer_ptr(m, m.xflag, r) + par * kMaxWorld + m.rank, ep);
+      }
+    }
+    __shared__ int xok_sh;
+    if (threadIdx.x == 0) {
+      int ok = 1;
+      const long long t0 = clock64();
+      const unsigned long long w0 = wall_ns();
+      for (int r = 0; r < m.world && ok; ++r) {
+        if (r == m.rank) continue;
+        while (ld_acquire_sys(m.xflag + par * kMaxWorld + r) != ep) {
+          if (*reinterpret_cast<volatile unsigned*>(abort_flag) ||
+              (clock64() - t0 > kSpinTimeoutCycles && wall_ns() - w0 > g_spin_timeout_ns)) {
+            atomicCAS(abort_flag, 0u, kAbortTimeout);
+            ok = 0;
+            break;
+          }
+        }
+      }
+      xok_sh = ok;
+    }
+    __syncthreads();
+    double total = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool mine = warp < NSLOT && ((mask >> warp) & 1u) && lane == 0;
+    if (mine)
+      for (int r = 0; r < m.world; ++r)
+        total += r == m.rank ? sums[warp]
+                             : *reinterpret_cast<volatile double*>(m.xsum + (par * kMaxWorld + r) * NSLOT + warp);
+    __syncthreads();
+    if (mine) sums[warp] = total;
+    __syncthreads();
+    return xok_sh != 0;
+  }
+  // Halo: copy the entries of vector v (length-n K' indexing, or block-local)
+  // that this rank's rows read but do not own from their owners; then a local
+  // grid barrier so every CTA sees them. Call right after a cross-GPU barrier.
+  __device__ bool gather_halo(double* v, const int2* halo, int count) {
+    const MultiGpu& m = a.mg;
+    for (int k = cta * blockDim.x + threadIdx.x; k < count; k += G * blockDim.x) {
+      const int2 e = halo[k];
+      v[e.x] = *reinterpret_cast<volatile const double*>(peer_ptr(m, v, e.y) + e.x);
+    }
+    return grid_sync(a.bar, a.bar + 32, abort_flag, static_cast<unsigned>(G));
   }
   // post an IC(0) apply of block b to its server (the lead worker thread);
   // every worker counts the request
@@ -1010,6 +1120,13 @@ struct Ctx {
     if (!ok_sh) status = DSGPU_E_CUDA;
     return rz_sh;
   }
+  // one row of block B's residual into every rank's tagged right-hand-side buffer
+  __device__ __forceinline__ void push_rhs(const DBlock& B, int li, double v, unsigned tag) const {
+    const uint4 w = bs_pack(v, tag);
+    __stcg(B.bs_bt + li, w);
+    for (int r = 0; r < a.mg.world; ++r)
+      if (r != a.mg.rank) __stcg(peer_ptr(a.mg, B.bs_bt, r) + li, w);
+  }
   // rows of this CTA inside block b: [lo, hi) in global vector indices
   __device__ void block_rows(int b, int& lo, int& hi) const {
     lo = max(r0, a.blk[b].off);
@@ -1048,6 +1165,25 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
   // here, answered at the next reduction); ring mode: remote helper CTAs.
   // PI blocks: every CTA joins the partitioned-inverse apply; r (and the
   // materialized input) are written after the reduction, by their owners.
+  if constexpr (TB == 0) {
+    // blocked sweeps: every worker CTA (of every GPU) writes its rows of the
+    // block residual r := input -- plain for its own PCG, tagged into every
+    // rank's right-hand-side buffer for the (replicated) sweeps. Tagged units
+    // validate themselves: no barrier between this and the sweep.
+    for (int b = 0; b < 2; ++b) {
+      const DBlock& B = a.blk[b];
+      if (B.kind != DSGPU_BLOCK_PCG_IC0) continue;
+      int lo, hi;
+      C.block_rows(b, lo, hi);
+      const unsigned tag = sweep_tag(a.launch_id, C.sweeps[b]);
+      for (int i = lo + tid; i < hi; i += blockDim.x) {
+        const double ri = in.at(i);
+        if (in.dst) in.dst[i] = ri;
+        B.r[i - B.off] = ri;
+        C.push_rhs(B, i - B.off, ri, tag);
+      }
+    }
+  }
   for (int b = 0; b < 2; ++b)
     if (!PI && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_S1, 0.0, &in);
   for (int b = 0; b < 2; ++b) {
@@ -1145,6 +1281,12 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
   while (active[0] || active[1]) {
     // ---- L1: q = A p_new, p_new = z (+ beta p_old) -----------------------
     double kap_p[2] = {0.0, 0.0};
+    if (a.mg.world > 1 && k > 0) {  // the other ranks' entries of p_old that these rows read
+      for (int b = 0; b < 2; ++b)
+        if (active[b] && a.mg.n_halo_p[b] > 0 &&
+            !C.gather_halo(pp ? a.blk[b].p1 : a.blk[b].p0, a.mg.halo_p[b], a.mg.n_halo_p[b]))
+          return false;
+    }
     {
       const int lane = tid & 31, warp = tid >> 5;
       for (int b = 0; b < 2; ++b) {
@@ -1198,6 +1340,22 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
     }
     // ---- L2: r -= alpha q; z = M^{-1} r; x += alpha p -------------------
     double rho_n[2] = {0.0, 0.0}, zr_n[2] = {0.0, 0.0};
+    if constexpr (TB == 0) {  // r -= alpha q by the rows' owners, tagged for the sweeps (as in S1)
+      for (int b = 0; b < 2; ++b) {
+        const DBlock& B = a.blk[b];
+        if (!active[b] || B.kind != DSGPU_BLOCK_PCG_IC0) continue;
+        int lo, hi;
+        C.block_rows(b, lo, hi);
+        const unsigned tag = sweep_tag(a.launch_id, C.sweeps[b]);
+        const double na = -alpha[b];
+        for (int i = lo + tid; i < hi; i += blockDim.x) {
+          const int li = i - B.off;
+          const double ri = add_rn(B.r[li], mul_rn(na, B.q[li]));
+          B.r[li] = ri;
+          C.push_rhs(B, li, ri, tag);
+        }
+      }
+    }
     for (int b = 0; b < 2; ++b)
       if (!PI && active[b] && a.blk[b].kind == DSGPU_BLOCK_PCG_IC0) C.post(b, IC_OP_L2, alpha[b], nullptr);
     for (int b = 0; b < 2; ++b) {
@@ -1356,7 +1514,7 @@ __device__ __noinline__ void ic_server(const Args& a, int b, double* xs, double*
             r[row] = ri;
             return ri;
           },
-          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no);
+          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no, TB != 0);
     } else {
       double* r = B.r;
       const double* q = B.q;
@@ -1368,7 +1526,7 @@ __device__ __noinline__ void ic_server(const Args& a, int b, double* xs, double*
             r[row] = ri;
             return ri;
           },
-          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no);
+          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no, TB != 0);
     }
     __syncthreads();  // every thread's r, z (and dst) written
     if (threadIdx.x == 0) {
@@ -1497,6 +1655,7 @@ __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_consta
                                        gamma, phi);
         C.put(SL_RES, block_sum(acc_res, red));
       }
+      if (do_spmv && a.mg.world > 1 && !C.gather_halo(y, a.mg.halo_y, a.mg.n_halo_y)) goto finish;
       if (do_spmv) {
         const double s = div_rn(1.0, beta);
         const double c1 = it >= 2 ? div_rn(-beta, oldb) : 0.0;
@@ -1751,7 +1910,6 @@ struct dsgpu_handle {
   Args args{};
   int grid = 0;
   size_t smem = 0;
-  std::vector<int32_t> row_start;
   int64_t levels[4] = {0, 0, 0, 0};
   double* d_f = nullptr;
   double* d_u = nullptr;
@@ -1778,6 +1936,24 @@ struct dsgpu_handle {
     return launch_id;
   }
 
+  // multi-GPU (dsgpu_create_multi): this rank, the world size, and the arena --
+  // ONE allocation holding every buffer another rank reads or writes (the
+  // iterate y, the PCG directions, the tagged right-hand sides, the reduction
+  // mailboxes), exported to the peers as one CUDA IPC handle; the same layout
+  // on every rank, so a peer's copy of a buffer sits at the same offset.
+  int rank = 0, world = 1;
+  char* arena = nullptr;
+  size_t arena_size = 0, arena_used = 0;
+  void* peer_arena[kMaxWorld] = {};
+  bool peers_open = false;
+  template <class T>
+  T* arena_alloc(size_t count) {
+    const size_t bytes = (std::max<size_t>(count, 1) * sizeof(T) + 255) / 256 * 256;
+    if (!arena || arena_used + bytes > arena_size) throw std::runtime_error("arena exhausted");
+    T* p = reinterpret_cast<T*>(arena + arena_used);
+    arena_used += bytes;
+    return p;
+  }
   template <class T>
   T* alloc(size_t count) {
     DevBuf b;
@@ -1795,8 +1971,15 @@ struct dsgpu_handle {
     return d;
   }
   void free_all() {
+    if (peers_open)
+      for (int r = 0; r < world; ++r)
+        if (r != rank && peer_arena[r]) cudaIpcCloseMemHandle(peer_arena[r]);
+    peers_open = false;
+    for (auto& p : peer_arena) p = nullptr;
     for (auto& b : bufs) cudaFree(b.p);
     bufs.clear();
+    arena = nullptr;
+    arena_size = arena_used = 0;
     ready = false;
   }
 };
@@ -2062,6 +2245,48 @@ int dsgpu_create(int device, dsgpu_handle** out) {
   return DSGPU_OK;
 }
 
+int dsgpu_create_multi(int rank, int world, int device, dsgpu_handle** out) {
+  if (!out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world) {
+    g_err = "dsgpu_create_multi: need 0 <= rank < world <= 8";
+    return DSGPU_E_BAD_INPUT;
+  }
+  const int rc = dsgpu_create(device, out);
+  if (rc) return rc;
+  (*out)->rank = rank;
+  (*out)->world = world;
+  return DSGPU_OK;
+}
+
+int dsgpu_multi_ipc_export(dsgpu_handle* h, void* handle64) {
+  if (!h || !h->ready || !handle64) return fail(h, DSGPU_E_BAD_INPUT, "dsgpu_multi_ipc_export: not set up");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+  cudaSetDevice(h->device);
+  cudaIpcMemHandle_t m;
+  const int rc = cuda_check(h, cudaIpcGetMemHandle(&m, h->arena), "cudaIpcGetMemHandle");
+  if (rc) return rc;
+  std::memcpy(handle64, &m, 64);
+  return DSGPU_OK;
+}
+
+int dsgpu_multi_ipc_import(dsgpu_handle* h, const void* handles) {
+  if (!h || !h->ready || !handles) return fail(h, DSGPU_E_BAD_INPUT, "dsgpu_multi_ipc_import: not set up");
+  cudaSetDevice(h->device);
+  h->peer_arena[h->rank] = h->arena;
+  h->args.mg.arena[h->rank] = h->arena;
+  for (int r = 0; r < h->world; ++r) {
+    if (r == h->rank) continue;
+    cudaIpcMemHandle_t m;
+    std::memcpy(&m, static_cast<const char*>(handles) + 64 * r, 64);
+    void* p = nullptr;
+    const int rc = cuda_check(h, cudaIpcOpenMemHandle(&p, m, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    if (rc) return rc;
+    h->peer_arena[r] = p;
+    h->args.mg.arena[r] = static_cast<char*>(p);
+  }
+  h->peers_open = true;
+  return DSGPU_OK;
+}
+
 void dsgpu_destroy(dsgpu_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
@@ -2225,16 +2450,55 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     }
     h->grid = n_srv + G;  // G = worker CTAs below
     // K-row partition balanced by nnz + per-row vector work
-    h->row_start.assign(G + 1, 0);
+    // This rank's rows (partition.hpp: one velocity range and one pressure range,
+    // the whole system when world == 1) and their split over the worker CTAs:
+    // every CTA works inside ONE block, its rows balanced by nonzeros + vector work.
+    RowPartition part;
+    if (h->world > 1) {
+      if (!h->bs)
+        return fail(h, DSGPU_E_UNSUPPORTED, "multi-GPU solves use the blocked sweeps (an IC(0) velocity block)");
+      for (int b = 0; b < 2; ++b)
+        if (P.blk[b].kind == DSGPU_BLOCK_PCG_JACOBI)
+          return fail(h, DSGPU_E_UNSUPPORTED, "multi-GPU solves: Jacobi-PCG blocks are not partitioned");
+      part = partition_rows(P.n, P.n_u, P.k_rp.data(), P.k_ci.data(), P.k_v.data(), P.k_na.data(), h->world);
+    }
+    const int own_u0 = h->world > 1 ? part.rank[h->rank].u0 : 0, own_u1 = h->world > 1 ? part.rank[h->rank].u1 : P.n_u;
+    const int own_p0 = h->world > 1 ? part.rank[h->rank].p0 : 0, own_p1 = h->world > 1 ? part.rank[h->rank].p1 : P.n_p;
+    std::vector<int32_t> row_lo(G, 0), row_hi(G, 0);
     {
-      const double total = static_cast<double>(nnz) + 24.0 * P.n;
-      int c = 1;
-      for (int i = 0; i < P.n && c < G; ++i) {
-        const double done = static_cast<double>(P.k_rp[i + 1]) + 24.0 * (i + 1);
-        while (c < G && done >= total * c / G) h->row_start[c++] = i + 1;
-      }
-      while (c < G) h->row_start[c++] = P.n;
-      h->row_start[G] = P.n;
+      auto cost = [&](int lo, int hi) { return static_cast<double>(P.k_rp[hi] - P.k_rp[lo]) + 24.0 * (hi - lo); };
+      const double cu = cost(own_u0, own_u1), cp = cost(P.n_u + own_p0, P.n_u + own_p1);
+      int Gu = static_cast<int>(std::lround(G * cu / std::max(1.0, cu + cp)));
+      Gu = std::max(own_u1 > own_u0 ? 1 : 0, std::min(Gu, G - (own_p1 > own_p0 ? 1 : 0)));
+      auto split = [&](int lo, int hi, int c0, int c1) {  // rows [lo, hi) over the CTAs [c0, c1)
+        const int nc = c1 - c0;
+        if (nc <= 0) return;
+        const double total = cost(lo, hi);
+        int c = 0, start = lo;
+        for (int i = lo; i < hi && c + 1 < nc; ++i)
+          while (c + 1 < nc && cost(lo, i + 1) >= total * (c + 1) / nc) {
+            row_lo[c0 + c] = start;
+            row_hi[c0 + c] = i + 1;
+            start = i + 1;
+            ++c;
+          }
+        row_lo[c0 + c] = start;
+        row_hi[c0 + c] = hi;
+        for (++c; c < nc; ++c) row_lo[c0 + c] = row_hi[c0 + c] = hi;
+      };
+      split(own_u0, own_u1, 0, Gu);
+      split(P.n_u + own_p0, P.n_u + own_p1, Gu, G);
+    }
+    // the arena: sized for everything sub-allocated from it below
+    {
+      auto up = [](size_t b) { return (b + 255) / 256 * 256 + 256; };
+      size_t bytes = up(sizeof(double) * P.n) + up(sizeof(double) * 2 * kMaxWorld * NSLOT) + up(sizeof(unsigned) * 2 * kMaxWorld);
+      for (int b = 0; b < 2; ++b)
+        bytes += 2 * up(sizeof(double) * P.blk[b].n) + up(sizeof(uint4) * (static_cast<size_t>(P.blk[b].n) + 1));
+      h->arena = reinterpret_cast<char*>(h->alloc<char>(bytes));
+      h->arena_size = bytes;
+      h->arena_used = 0;
+      cudaMemset(h->arena, 0, bytes);
     }
     Args& a = h->args;
     a = Args{};
@@ -2244,13 +2508,18 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     a.k_rp = h->upload(P.k_rp);
     a.k_ci = h->upload(P.k_ci);
     a.k_v = h->upload(P.k_v);
-    a.row_start = h->upload(h->row_start);
-    auto lanes_for = [](double mean_row) { return mean_row >= 96.0 ? 32 : mean_row >= 40.0 ? 16 : 8; };
+    a.row_lo = h->upload(row_lo);
+    a.row_hi = h->upload(row_hi);
+    // lanes per row: 16 (64 entries per pass) measured best from 125 to 512 entries per
+    // row (C3 saddle 71.5 us vs 87.0 with 32 lanes, C4 164.7 vs 172.2: tools/spmv_ab.py)
+    auto lanes_for = [](double mean_row) {
+      if (const char* env = std::getenv("DSGPU_SPMV_LANES")) {
+        const int L = std::atoi(env);
+        if (L == 8 || L == 16 || L == 32) return L;
+      }
+      return mean_row >= 48.0 ? 16 : 8;
+    };
     a.k_lanes = lanes_for(static_cast<double>(P.k_rp[P.n]) / P.n);
-    if (const char* env = std::getenv("DSGPU_SPMV_LANES")) {
-      const int L = std::atoi(env);
-      if (L == 8 || L == 16 || L == 32) a.k_lanes = L;
-    }
     const int32_t* d_na = h->upload(P.k_na);
     for (int b = 0; b < 2; ++b) {
       HostBlock& hb = P.blk[b];
@@ -2307,6 +2576,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         cudaMemset(d.y, 0, sizeof(double) * (hb.n + 1));
         cudaMemset(d.bb, 0, sizeof(double) * (hb.n + 1));
         // tag 0 is never a sweep's tag (launch ids start at 1): zeroed = "not written"
+        d.bs_bt = h->arena_alloc<uint4>(static_cast<size_t>(hb.n) + 1);
         d.bs_gt = h->alloc<uint4>(static_cast<size_t>(hb.n) + 1);
         d.bs_fps = h->alloc<uint4>(static_cast<size_t>(G_max) * kBsB);
         cudaMemset(d.bs_gt, 0, sizeof(uint4) * (static_cast<size_t>(hb.n) + 1));
@@ -2342,8 +2612,8 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       d.z = h->alloc<double>(hb.n + 1);  // z[n] = 0: the padding column of the far lists
       cudaMemset(d.z, 0, sizeof(double) * (hb.n + 1));
       d.q = h->alloc<double>(hb.n);
-      d.p0 = h->alloc<double>(hb.n);
-      d.p1 = h->alloc<double>(hb.n);
+      d.p0 = h->arena_alloc<double>(hb.n);
+      d.p1 = h->arena_alloc<double>(hb.n);
     }
     if (!h->bs) {
       h->levels[0] = P.blk[0].fwd.n_levels;
@@ -2359,7 +2629,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     a.perm_u = h->upload(P.blk[0].perm);
     a.perm_p = h->upload(P.blk[1].perm);
     a.x = h->alloc<double>(P.n);
-    a.y = h->alloc<double>(P.n);
+    a.y = h->arena_alloc<double>(P.n);
     a.v = h->alloc<double>(P.n);
     a.av = h->alloc<double>(P.n);
     a.res = h->alloc<double>(P.n);
@@ -2384,6 +2654,39 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     h->d_u = h->alloc<double>(P.n_u);
     h->d_p = h->alloc<double>(P.n_p);
     for (int i = 0; i < 3; ++i) h->d_tmp[i] = h->alloc<double>(P.n);
+    // multi-GPU state (world == 1: no peers, no halos)
+    MultiGpu& m = a.mg;
+    m = MultiGpu{};
+    m.world = h->world;
+    m.rank = h->rank;
+    m.arena[h->rank] = h->arena;
+    m.xsum = h->arena_alloc<double>(2 * kMaxWorld * NSLOT);
+    m.xflag = h->arena_alloc<unsigned>(2 * kMaxWorld);
+    if (h->world > 1) {
+      const RankPart& R = part.rank[h->rank];
+      std::vector<int2> hy, hp[2];
+      for (int s2 = 0; s2 < h->world; ++s2)
+        for (int k = R.src_ptr[s2]; k < R.src_ptr[s2 + 1]; ++k) {
+          hy.push_back(make_int2(R.halo[k], s2));
+          if (k - R.src_ptr[s2] < R.a_cnt[s2]) hp[0].push_back(make_int2(R.halo[k], s2));  // A' part: velocity columns
+        }
+      if (P.blk[1].kind == DSGPU_BLOCK_PCG_IC0) {  // Q' columns of the own pressure rows
+        const HostBlock& hb = P.blk[1];
+        std::vector<int32_t> cols;
+        for (int i = R.p0; i < R.p1; ++i)
+          for (int64_t k = hb.rp[i]; k < hb.rp[i + 1]; ++k)
+            if (hb.ci[k] < R.p0 || hb.ci[k] >= R.p1) cols.push_back(hb.ci[k]);
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        for (const int32_t c : cols) hp[1].push_back(make_int2(c, part.owner_of(P.n_u + c)));
+      }
+      m.halo_y = h->upload(hy);
+      m.n_halo_y = static_cast<int>(hy.size());
+      for (int b = 0; b < 2; ++b) {
+        m.halo_p[b] = h->upload(hp[b]);
+        m.n_halo_p[b] = static_cast<int>(hp[b].size());
+      }
+    }
   } catch (const std::exception& e) {
     h->free_all();
     return fail(h, DSGPU_E_CUDA, e.what());
