@@ -93,6 +93,26 @@ void dsgpu_default_opts(dsgpu_opts* o);
 int dsgpu_create(int device, dsgpu_handle** out);
 void dsgpu_destroy(dsgpu_handle* h);
 
+/* ---- one solve across the GPUs of one NVLink box ----------
+ * One process per GPU (rank r of `world` <= 8). Every rank calls
+ * dsgpu_create_multi, then dsgpu_setup with the SAME system (each rank keeps
+ * the operator rows it owns -- one contiguous velocity range and one pressure
+ * range, balanced by nonzeros -- and the whole IC(0) plan: the sweeps are
+ * replicated so the preconditioner is the single-GPU one), then exchanges one
+ * 64-byte CUDA IPC handle with the other ranks (dsgpu_multi_ipc_export; the
+ * host layer all-gathers them, e.g. torch.distributed; dsgpu_multi_ipc_import
+ * takes the world x 64 bytes in rank order). After that dsgpu_solve /
+ * dsgpu_solve_device run ONE partitioned solve: all ranks call them together
+ * with the same arguments; SpMV halos are read from the owners' memory over
+ * NVLink, dot products are exchanged through peer mailboxes and summed in rank
+ * order (every rank computes identical scalars), and each rank returns the
+ * entries of u and p it owns (all other entries of u_out / p_out untouched:
+ * sum the ranks' zero-initialized outputs). world == 1 is dsgpu_create.
+ * Blocked-sweep IC(0) velocity block required; Jacobi-PCG blocks unsupported. */
+int dsgpu_create_multi(int rank, int world, int device, dsgpu_handle** out);
+int dsgpu_multi_ipc_export(dsgpu_handle* h, void* handle64);
+int dsgpu_multi_ipc_import(dsgpu_handle* h, const void* handles_world_x_64);
+
 /* Upload the saddle system and the two preconditioner blocks.
  *   A (n_u x n_u), B (n_p x n_u), Bt (n_u x n_p), Q_nu (n_p x n_p): the
  *     StokesSystem blocks (assembly.hpp:31-49), original DOF order.

@@ -879,9 +879,11 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
   }
   // staged sweeps: materialize the right-hand side once (it may update r)
   double* bb = B.bb;
-  for (int i = threadIdx.x; i < B.n; i += blockDim.x) bb[i] = rhs(i);
-  __syncthreads();
   double* y = B.y;
+  if constexpr (TB != 0) {
+    for (int i = threadIdx.x; i < B.n; i += blockDim.x) bb[i] = rhs(i);
+    __syncthreads();
+  }
   if constexpr (TB == 0) {
     // blocked sweeps (bsweep.cuh). The tagged right-hand side B.bs_bt was
     // written by the rows' owners (the worker CTAs of every GPU: precond());

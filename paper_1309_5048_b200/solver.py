@@ -79,6 +79,9 @@ def _lib():
         L.dsgpu_last_error.argtypes = [vp]
         L.dsgpu_create.argtypes = [ip, C.POINTER(vp)]
         L.dsgpu_destroy.argtypes = [vp]
+        L.dsgpu_create_multi.argtypes = [ip, ip, ip, C.POINTER(vp)]
+        L.dsgpu_multi_ipc_export.argtypes = [vp, vp]
+        L.dsgpu_multi_ipc_import.argtypes = [vp, vp]
         L.dsgpu_setup.argtypes = [vp, C.POINTER(_Csr), C.POINTER(_Csr), C.POINTER(_Csr),
                                   C.POINTER(_Csr), ip, vp, C.POINTER(_Csr), ip, vp,
                                   C.POINTER(_Csr), C.POINTER(_Csr)]
@@ -210,7 +213,11 @@ class GpuStokesSolver:
 
     def __init__(self, system: host.StokesSystem, strategy: str = "IC0-PCG(A,Q)",
                  device: int = 0, top: BlockSetup | None = None,
-                 bottom: BlockSetup | None = None):
+                 bottom: BlockSetup | None = None, rank: int = 0, world: int = 1,
+                 process_group=None):
+        """rank / world / process_group: one partitioned solve across the GPUs of
+        one box (one process per GPU, torch.distributed group for the exchange of
+        the CUDA IPC handles and of the owned solution entries); see dsgpu.h."""
         if strategy in UNSUPPORTED:
             raise ValueError(f"strategy {strategy} (exact Cholesky blocks) is not provided on GPU")
         if strategy not in STRATEGIES:
@@ -222,7 +229,9 @@ class GpuStokesSolver:
         self.top = top or prepare_block(system.A, tk)
         self.bottom = bottom or prepare_block(system.Q_nu, bk)
         h = C.c_void_p()
-        rc = self.L.dsgpu_create(device, C.byref(h))
+        self.rank, self.world, self.group = rank, world, process_group
+        rc = (self.L.dsgpu_create_multi(rank, world, device, C.byref(h)) if world > 1
+              else self.L.dsgpu_create(device, C.byref(h)))
         if rc:
             _raise(rc, self.L.dsgpu_last_error(None).decode())
         self.h = h
@@ -240,6 +249,39 @@ class GpuStokesSolver:
             msg = self.L.dsgpu_last_error(h).decode()
             self.close()
             _raise(rc, msg)
+        if world > 1:
+            self._exchange_ipc_handles()
+
+    def _exchange_ipc_handles(self):
+        """All-gather the ranks' arena handles (64 bytes each) and map the peers."""
+        import torch
+        import torch.distributed as dist
+        mine = np.zeros(64, np.uint8)
+        rc = self.L.dsgpu_multi_ipc_export(self.h, mine.ctypes.data)
+        if rc:
+            _raise(rc, self.L.dsgpu_last_error(self.h).decode())
+        t = torch.from_numpy(mine)
+        cuda = dist.get_backend(self.group) == "nccl"
+        if cuda:
+            t = t.cuda()
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(parts, t, group=self.group)
+        allh = np.concatenate([p.cpu().numpy() for p in parts])
+        rc = self.L.dsgpu_multi_ipc_import(self.h, allh.ctypes.data)
+        if rc:
+            _raise(rc, self.L.dsgpu_last_error(self.h).decode())
+
+    def _sum_over_ranks(self, *arrays):
+        """Owned entries -> full vectors (every rank returned zeros elsewhere)."""
+        import torch
+        import torch.distributed as dist
+        cuda = dist.get_backend(self.group) == "nccl"
+        for a in arrays:
+            t = torch.from_numpy(a)
+            tt = t.cuda() if cuda else t
+            dist.all_reduce(tt, group=self.group)
+            if cuda:
+                t.copy_(tt.cpu())
 
     def close(self):
         if getattr(self, "h", None):
@@ -272,6 +314,8 @@ class GpuStokesSolver:
                                 he.ctypes.data if cap else None, cap)
         if rc:
             _raise(rc, self.L.dsgpu_last_error(self.h).decode())
+        if self.world > 1:
+            self._sum_over_ranks(u, p)
         n = min(rep.hist_len, cap)
         r = SolveReport(rep.iterations, bool(rep.converged), hm[:n].copy(), he[:n].copy(),
                         rep.wall_seconds, rep.mean_inner_top, rep.mean_inner_bottom,

@@ -127,6 +127,25 @@ def test_ic0_mode_policy(gpu):
     g.close()
 
 
+def test_multi_gpu_entry_point_world1(gpu, port):
+    """dsgpu_create_multi with world = 1 is the single-GPU solver (the multi-GPU
+    data plane -- per-rank row ranges, owner-written tagged right-hand sides,
+    the arena -- is one code path; with one rank it has no peers and no halos)."""
+    import ctypes as C
+    host, solver = gpu
+    s = host.assemble("psi-mms", 2, 10, dim=3)
+    monkey = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    L = monkey.L
+    h = C.c_void_p()
+    assert L.dsgpu_create_multi(0, 1, 0, C.byref(h)) == 0
+    L.dsgpu_destroy(h)
+    assert L.dsgpu_create_multi(1, 1, 0, C.byref(h)) != 0  # rank out of range
+    assert L.dsgpu_create_multi(0, 9, 0, C.byref(h)) != 0  # more than one box's GPUs
+    sol = monkey.solve(options=solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1))
+    check_parity(sol, reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1), 1e-8)
+    monkey.close()
+
+
 def test_two_handles_of_different_sizes(gpu, port):
     """Distinct handles: a smaller system set up after a larger one must not
     disturb the first handle's launches (shared-memory limits are per kernel
