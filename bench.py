@@ -19,9 +19,12 @@ roofline: dominant kernel = the persistent MINRES kernel; algorithmic bytes
           per SURVEY.md §8(d) with the counted inner iterations
 --impl reference: the unmodified reference (oracle/_ref, built from
           /root/reference/proj/src) on the host CPU, same workload.
-Multi-GPU (--gpus N under torchrun): each rank runs an independent replica of
-the solve (weak scaling), max-over-ranks timing; the row-partitioned data
-plane is described in DESIGN.md.
+Multi-GPU (--gpus N under torchrun, one rank per GPU): the ranks solve ONE
+row-partitioned system together (dsgpu_create_multi: halo gathers and
+reduction mailboxes over NVLink peer memory, replicated sweeps; "strong"
+scaling, max-over-ranks device time; NCCL carries the IPC-handle exchange,
+the timing reduction and the assembly of the owned solution entries in the
+e2e leg). --replicas runs N independent copies instead ("weak").
 """
 from __future__ import annotations
 
@@ -183,11 +186,12 @@ def algorithmic_bytes(info: dict, rep, outer_iters: int) -> float:
             + rep.apps_bottom * (S_ICQ + 48 * n_p) + rep.inner_bottom * (S_Q + S_ICQ + 72 * n_p))
 
 
-def measure(tag, args, world, local, dist, full: bool):
+def measure(tag, args, world, rank, local, dist, full: bool):
     """Device-timed and end-to-end runs of one workload; `full` adds the
     per-kernel microbenchmarks and the roofline of the headline workload."""
     import torch
     from paper_1309_5048_b200 import host, solver
+    partitioned = world > 1 and not args.replicas  # one system across the ranks
 
     W = WORKLOADS[tag]
     t0 = time.perf_counter()
@@ -199,7 +203,12 @@ def measure(tag, args, world, local, dist, full: bool):
     bot = solver.prepare_block(s.Q_nu, bk, ic0_on_gpu=True)
     precond_setup_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    g = solver.GpuStokesSolver(s, W["strategy"], device=local, top=top, bottom=bot)
+    if partitioned:
+        os.environ["DSGPU_SWEEP"] = "bs"  # the multi-GPU data plane runs the replicated blocked sweeps
+        g = solver.GpuStokesSolver(s, W["strategy"], device=local, top=top, bottom=bot, rank=rank,
+                                   world=world, process_group=None)
+    else:
+        g = solver.GpuStokesSolver(s, W["strategy"], device=local, top=top, bottom=bot)
     device_setup_s = time.perf_counter() - t0
     info = g.info()
     opts = [solver.SolverOptions(outer_tol=W["outer"], inner_tol=t,
@@ -229,7 +238,8 @@ def measure(tag, args, world, local, dist, full: bool):
             iters += sum(r.iterations for r in reps)
             launches += sum(r.gpu_launches for r in reps)
             last = reps
-    dev_ms, job_iters = reduce_over_ranks(dist, dev, dev_ms, iters)
+    # partitioned: every rank counts the same iterations of the one solve
+    dev_ms, job_iters = reduce_over_ranks(dist, dev, dev_ms, iters if (not partitioned or rank == 0) else 0)
     if dist:
         dist.barrier()
     # ---- e2e: host buffers through the C ABI (pinned), wall clock ---------
@@ -245,7 +255,8 @@ def measure(tag, args, world, local, dist, full: bool):
             e2e_iters += sol.report.iterations
         torch.cuda.synchronize()
         e2e_s += time.perf_counter() - t1
-    e2e_ms, job_e2e_iters = reduce_over_ranks(dist, dev, e2e_s * 1e3, e2e_iters)
+    e2e_ms, job_e2e_iters = reduce_over_ranks(dist, dev, e2e_s * 1e3,
+                                              e2e_iters if (not partitioned or rank == 0) else 0)
     out = {
         "metric": metric_for(tag),
         "value": job_iters / (dev_ms * 1e-3),
@@ -265,16 +276,20 @@ def measure(tag, args, world, local, dist, full: bool):
                     precond_setup_s + device_setup_s + sum(r.wall_seconds for r in last), 3),
                 "grid_ctas": info["grid_ctas"], "ic0_apply": info["ic0_mode"],
                 "far_ctas": [info["far_ctas_A"], info["far_ctas_Q"]],
-                "l2": "flushed between steps (256 MiB write)", "parallelism": f"replicas x{world}"},
+                "l2": "flushed between steps (256 MiB write)", "parallelism": (f"one system row-partitioned over {world} GPUs" if partitioned
+                                else f"replicas x{world}")},
         "e2e": {"value": job_e2e_iters / (e2e_ms * 1e-3), "unit": "iter/s",
                 "h2d_bytes_per_step": 8 * s.n_u * len(opts),
                 "d2h_bytes_per_step": 8 * (s.n_u + s.n_p) * len(opts)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    out["scaling"] = "strong" if partitioned else "weak"
     if full:
         # ---- roofline of the dominant kernel (the persistent MINRES kernel) ----
         peak, peak_kind = measured_peak()
+        if partitioned:
+            peak *= world  # the one solve streams from every rank's HBM
         bytes_step = sum(algorithmic_bytes(info, r, r.iterations) for r in last)
         kern_ms = sum(r.wall_seconds for r in last) * 1e3
         achieved = bytes_step / (kern_ms * 1e-3) / 1e9
@@ -285,6 +300,8 @@ def measure(tag, args, world, local, dist, full: bool):
                            "algorithmic_bytes_per_step": bytes_step}
         # per-kernel microbenchmarks on device-resident data (same launch path)
         try:
+            if partitioned:
+                raise RuntimeError("stand-alone kernels are timed in the single-GPU run")
             n = info["n_u"] + info["n_p"]
             spmv_ms, spmva_ms = g.time_kernel(0, 50), g.time_kernel(3, 50)
             ic_ms, icq_ms = g.time_kernel(1, 10), g.time_kernel(2, 10)
@@ -321,11 +338,11 @@ def run_ours(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    head = measure(args.workload, args, world, local, dist, full=True)
+    head = measure(args.workload, args, world, rank, local, dist, full=True)
     extra = {}
-    if not args.no_extra and args.workload == DEFAULT_WORKLOAD:
+    if not args.no_extra and args.workload == DEFAULT_WORKLOAD and (world == 1 or args.replicas):
         for tag in EXTRA_WORKLOADS:
-            e = measure(tag, args, world, local, dist, full=False)
+            e = measure(tag, args, world, rank, local, dist, full=False)
             extra[tag] = {k: e[k] for k in ("metric", "value", "unit", "ms_per_step", "config", "run", "e2e")}
     result = None
     if rank == 0:
@@ -334,7 +351,7 @@ def run_ours(args, world, rank, local):
         result = {
             "metric": head["metric"], "value": head["value"], "unit": "iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE forcing / seeded RHS, native assembly; the 2D assembly is "
                     "bit-identical to the reference's, the 3D blocks follow the same rule)",
             "config": head["config"], "run": head["run"], "e2e": head["e2e"],
@@ -449,6 +466,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas (weak scaling) instead of one partitioned solve")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     args = ap.parse_args()
     world, rank, local = dist_env()

@@ -216,6 +216,17 @@ int dsgpu_debug_partition_spmv(int n, int n_u, const int64_t* row_ptr, const int
                                const int32_t* na, int world, int32_t* bounds, int64_t* halo_counts,
                                const double* x, double* y);
 
+/* Multi-rank emulation on ONE GPU (tests of the multi-GPU data plane on a
+ * single-GPU box): `world` handles made by dsgpu_create_multi(r, world, device)
+ * on the same device in this process and set up with the same system (their
+ * grids equal and world x grid <= SM count: DSGPU_GRID) solve it as `world`
+ * ranks inside ONE cooperative launch whose CTAs are split into `world` groups;
+ * group r runs rank r's solve and reaches the other ranks' arenas exactly as it
+ * would reach peer GPUs (halo gathers, reduction mailboxes, pushed residuals).
+ * f / u_out / p_out: host vectors of the whole system; reps: world reports. */
+int dsgpu_debug_emulate_ranks(dsgpu_handle** handles, int world, const double* f, const dsgpu_opts* o,
+                              double* u_out, double* p_out, dsgpu_report* reps);
+
 /* Process-wide sweep diagnostics (summed since the last reset), out32:
  * [0] main-warp cycles, [1] main cycles waiting, [2] groups, [3] abort code,
  * [4] main cycles waiting for static slot data, [5] helper cycles waiting for

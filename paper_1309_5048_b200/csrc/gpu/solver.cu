@@ -969,8 +969,8 @@ struct Ctx {
   int status = DSGPU_OK, failed_block = -1;
 
   // worker CTAs only: cta / G index the workers (blockIdx.x - n_srv)
-  __device__ Ctx(const Args& args, double* red_, double* sums_, double* xs)
-      : a(args), cta(blockIdx.x - args.n_srv), G(gridDim.x - args.n_srv), epoch(0), red(red_),
+  __device__ Ctx(const Args& args, int vblock, int vgrid, double* red_, double* sums_, double* xs)
+      : a(args), cta(vblock - args.n_srv), G(vgrid - args.n_srv), epoch(0), red(red_),
         sums(sums_) {
     r0 = a.row_lo[cta];
     r1 = a.row_hi[cta];
@@ -1558,19 +1558,22 @@ __device__ __forceinline__ double minres_update_row(int i, const double* v, cons
   return rv * rv;
 }
 
+// The whole solve as seen by CTA `vblock` of a grid of `vgrid` CTAs (the real
+// grid for minres_kernel; one rank's share of the grid for the multi-rank
+// emulation kernel below).
 template <int TB, bool RING, bool PI>
-__global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
+__device__ __forceinline__ void minres_body(const Args& a, int vblock, int vgrid) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
   __shared__ double sums[NSLOT];
   if constexpr (!PI) {  // (the PI variant must not even instantiate the sweeps)
-    if (static_cast<int>(blockIdx.x) < a.n_srv) {
-      ic_server<TB, RING>(a, blockIdx.x, xs_dyn, red);
+    if (vblock < a.n_srv) {
+      ic_server<TB, RING>(a, vblock, xs_dyn, red);
       return;
     }
   }
   if (PI) pi_prologue();
-  Ctx C(a, red, sums, xs_dyn);
+  Ctx C(a, vblock, vgrid, red, sums, xs_dyn);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   PHASE_DIAG(const long long t_kernel0 = clock64();)
   const int r0 = C.r0, r1 = C.r1;
@@ -1792,6 +1795,22 @@ finish:
   }
 }
 
+template <int TB, bool RING, bool PI>
+__global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
+  minres_body<TB, RING, PI>(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
+}
+
+// Multi-rank emulation on ONE GPU (tests of the multi-GPU data plane where
+// only one GPU exists): a single cooperative launch whose grid is `world`
+// consecutive groups of `per_rank` CTAs; group r runs rank r's solve with rank
+// r's argument block, and the "peer" arenas are the other groups' arenas in the
+// same address space. All CTAs are co-resident (cooperative launch), so the
+// cross-rank waits make progress exactly as they do across GPUs.
+__global__ void __launch_bounds__(kThreads, 1) minres_emul_kernel(const Args* all, int per_rank) {
+  const int r = static_cast<int>(blockIdx.x) / per_rank;
+  minres_body<0, true, false>(all[r], static_cast<int>(blockIdx.x) % per_rank, per_rank);
+}
+
 // ---- standalone kernels (parity / microbenchmarks) -------------------------
 template <int TB, bool RING>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -1934,8 +1953,18 @@ struct dsgpu_handle {
   int sms = 148;
   unsigned launch_id = 0;     // 1..4095, cycled per launch (sweep tags)
   unsigned next_launch_id() {
-    launch_id = launch_id % 4095u + 1u;
+    launch_id = launch_id % (world > 1 ? 2047u : 4095u) + 1u;
     return launch_id;
+  }
+  // Solves of a multi-GPU handle take their ids from their own counter (upper
+  // half of the 12-bit id space): the ranks' tags and reduction epochs agree as
+  // long as every rank has made the same number of SOLVE calls, whatever
+  // stand-alone kernels each rank ran in between.
+  unsigned solve_id = 0;
+  unsigned next_solve_id() {
+    if (world == 1) return next_launch_id();
+    solve_id = solve_id % 2047u + 1u;
+    return 2048u + solve_id;
   }
 
   // multi-GPU (dsgpu_create_multi): this rank, the world size, and the arena --
@@ -2697,9 +2726,11 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
   return DSGPU_OK;
 }
 
-static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, double* d_u,
-                     double* d_p, dsgpu_report* rep, double* d_hm, double* d_he, int hist_cap) {
-  Args a = h->args;
+// The argument block of one solve launch (and the reset of the launch's
+// barrier / mailbox words on the handle's stream).
+static int solve_args(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, double* d_u, double* d_p,
+                      double* d_hm, double* d_he, int hist_cap, Args& a) {
+  a = h->args;
   a.f_in = d_f;
   a.u_out = d_u;
   a.p_out = d_p;
@@ -2708,8 +2739,6 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   if (!o) o = &def;
   if (!(o->outer_tol > 0.0) || o->max_iter < 0 || o->inner_cap < 1)
     return fail(h, DSGPU_E_BAD_INPUT, "dsgpu_solve: bad options");
-  dsgpu_report rep_local;
-  if (!rep) rep = &rep_local;
   a.outer_tol = o->outer_tol;
   a.inner_tol = o->inner_tol;
   a.max_iter = o->max_iter;
@@ -2718,34 +2747,14 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   a.hist_m = d_hm;
   a.hist_e = d_he;
   a.hist_cap = (d_hm && d_he) ? hist_cap : 0;
-  a.launch_id = h->next_launch_id();
+  a.launch_id = h->next_solve_id();
   int rc = cuda_check(h, cudaMemsetAsync(a.bar, 0, 128 * sizeof(unsigned), h->stream), "memset");
   if (!rc) rc = cuda_check(h, cudaMemsetAsync(a.mbox, 0, 2 * sizeof(Mailbox), h->stream), "memset");
-  if (rc) return rc;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventRecord(e0, h->stream);
-  void* params[] = {&a};
-  rc = cuda_check(h,
-                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_for(h->tb, h->ring, h->pi)), dim3(h->grid),
-                                              dim3(kThreads), params, h->smem, h->stream),
-                  "cooperative launch");
-  cudaEventRecord(e1, h->stream);
-  if (rc) {
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return rc;
-  }
-  DevReport R{};
-  rc = cuda_check(h, cudaMemcpyAsync(&R, h->d_rep, sizeof(R), cudaMemcpyDeviceToHost, h->stream),
-                  "report D2H");
-  if (!rc) rc = cuda_check(h, cudaStreamSynchronize(h->stream), "solve");
-  float ms = 0.0f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (rc) return rc;
+  return rc;
+}
+
+// Device report -> dsgpu_report (+ the error the status stands for).
+static int solve_report(dsgpu_handle* h, const DevReport& R, float ms, dsgpu_report* rep) {
   std::memset(rep, 0, sizeof(*rep));
   rep->iterations = R.iterations;
   rep->converged = R.converged;
@@ -2776,6 +2785,120 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
                     : std::string("preconditioner: ") + (R.failed_block == 1 ? "pressure" : "velocity") +
                           " block produced a negative inner product");
   return DSGPU_OK;
+}
+
+static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, double* d_u,
+                     double* d_p, dsgpu_report* rep, double* d_hm, double* d_he, int hist_cap) {
+  Args a;
+  int rc = solve_args(h, d_f, o, d_u, d_p, d_hm, d_he, hist_cap, a);
+  if (rc) return rc;
+  dsgpu_report rep_local;
+  if (!rep) rep = &rep_local;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, h->stream);
+  void* params[] = {&a};
+  rc = cuda_check(h,
+                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_for(h->tb, h->ring, h->pi)), dim3(h->grid),
+                                              dim3(kThreads), params, h->smem, h->stream),
+                  "cooperative launch");
+  cudaEventRecord(e1, h->stream);
+  if (rc) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  DevReport R{};
+  rc = cuda_check(h, cudaMemcpyAsync(&R, h->d_rep, sizeof(R), cudaMemcpyDeviceToHost, h->stream),
+                  "report D2H");
+  if (!rc) rc = cuda_check(h, cudaStreamSynchronize(h->stream), "solve");
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  return solve_report(h, R, ms, rep);
+}
+
+// Multi-rank emulation (tests; see minres_emul_kernel): `world` handles made by
+// dsgpu_create_multi(r, world, device) on ONE device in this process and set up
+// with the same system solve it as `world` ranks inside a single cooperative
+// launch. f, u_out, p_out are host vectors of the whole system; reps[r] is
+// rank r's report.
+int dsgpu_debug_emulate_ranks(dsgpu_handle** hs, int world, const double* f, const dsgpu_opts* o,
+                              double* u_out, double* p_out, dsgpu_report* reps) {
+  if (!hs || world < 1 || world > kMaxWorld || !f || !u_out || !p_out || !reps) return DSGPU_E_BAD_INPUT;
+  dsgpu_handle* h0 = hs[0];
+  for (int r = 0; r < world; ++r) {
+    dsgpu_handle* h = hs[r];
+    if (!h || !h->ready || h->world != world || h->rank != r || h->device != h0->device || h->grid != h0->grid ||
+        h->tb != 0 || h->pi || !h->ring)
+      return fail(h0, DSGPU_E_BAD_INPUT, "dsgpu_debug_emulate_ranks: handles must be ranks 0..world-1 of one device, "
+                                          "blocked sweeps, equal grids");
+  }
+  cudaSetDevice(h0->device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h0->device);
+  if (world * h0->grid > sms)
+    return fail(h0, DSGPU_E_BAD_INPUT, "dsgpu_debug_emulate_ranks: world x grid exceeds the SM count (set DSGPU_GRID)");
+  const HostPlan& P = h0->plan;
+  std::vector<Args> all(world);
+  size_t smem = 0;
+  for (int r = 0; r < world; ++r) {
+    dsgpu_handle* h = hs[r];
+    for (int q = 0; q < world; ++q) {  // peers: the other handles' arenas, same address space
+      h->peer_arena[q] = hs[q]->arena;
+      h->args.mg.arena[q] = hs[q]->arena;
+    }
+    int rc = cuda_check(h, cudaMemcpyAsync(h->d_f, f, sizeof(double) * P.n_u, cudaMemcpyHostToDevice, h->stream), "f H2D");
+    if (!rc) rc = cuda_check(h, cudaMemsetAsync(h->d_u, 0, sizeof(double) * P.n_u, h->stream), "memset");
+    if (!rc) rc = cuda_check(h, cudaMemsetAsync(h->d_p, 0, sizeof(double) * P.n_p, h->stream), "memset");
+    if (!rc) rc = solve_args(h, h->d_f, o, h->d_u, h->d_p, nullptr, nullptr, 0, all[r]);
+    if (!rc) rc = cuda_check(h, cudaStreamSynchronize(h->stream), "sync");
+    if (rc) return rc;
+    all[r].launch_id = all[0].launch_id;  // one launch: the ranks' tags and epochs must agree
+    smem = std::max(smem, h->smem);
+  }
+  Args* d_all = nullptr;
+  int rc = cuda_check(h0, cudaMalloc(&d_all, sizeof(Args) * world), "cudaMalloc");
+  if (rc) return rc;
+  cudaMemcpy(d_all, all.data(), sizeof(Args) * world, cudaMemcpyHostToDevice);
+  cudaFuncSetAttribute(minres_emul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int per_rank = h0->grid;
+  void* params[] = {&d_all, &per_rank};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, h0->stream);
+  rc = cuda_check(h0,
+                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_emul_kernel), dim3(world * per_rank),
+                                              dim3(kThreads), params, smem, h0->stream),
+                  "cooperative launch (emulated ranks)");
+  cudaEventRecord(e1, h0->stream);
+  if (!rc) rc = cuda_check(h0, cudaStreamSynchronize(h0->stream), "emulated solve");
+  float ms = 0.0f;
+  if (!rc) cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d_all);
+  if (rc) return rc;
+  std::vector<double> u(P.n_u), p(P.n_p);
+  std::fill(u_out, u_out + P.n_u, 0.0);
+  std::fill(p_out, p_out + P.n_p, 0.0);
+  int first_err = DSGPU_OK;
+  for (int r = 0; r < world; ++r) {
+    dsgpu_handle* h = hs[r];
+    DevReport R{};
+    cudaMemcpy(&R, h->d_rep, sizeof(R), cudaMemcpyDeviceToHost);
+    cudaMemcpy(u.data(), h->d_u, sizeof(double) * P.n_u, cudaMemcpyDeviceToHost);
+    cudaMemcpy(p.data(), h->d_p, sizeof(double) * P.n_p, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < P.n_u; ++i) u_out[i] += u[i];  // every row is written by exactly one rank
+    for (int i = 0; i < P.n_p; ++i) p_out[i] += p[i];
+    const int src = solve_report(h, R, ms, reps + r);
+    if (src && !first_err) first_err = src;
+  }
+  return first_err;
 }
 
 int dsgpu_solve_device(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, double* d_u_out,

@@ -82,6 +82,8 @@ def _lib():
         L.dsgpu_create_multi.argtypes = [ip, ip, ip, C.POINTER(vp)]
         L.dsgpu_multi_ipc_export.argtypes = [vp, vp]
         L.dsgpu_multi_ipc_import.argtypes = [vp, vp]
+        L.dsgpu_debug_emulate_ranks.argtypes = [C.POINTER(vp), ip, _dp, C.POINTER(_Opts), _dp, _dp,
+                                                C.POINTER(_Report)]
         L.dsgpu_setup.argtypes = [vp, C.POINTER(_Csr), C.POINTER(_Csr), C.POINTER(_Csr),
                                   C.POINTER(_Csr), ip, vp, C.POINTER(_Csr), ip, vp,
                                   C.POINTER(_Csr), C.POINTER(_Csr)]
@@ -214,7 +216,7 @@ class GpuStokesSolver:
     def __init__(self, system: host.StokesSystem, strategy: str = "IC0-PCG(A,Q)",
                  device: int = 0, top: BlockSetup | None = None,
                  bottom: BlockSetup | None = None, rank: int = 0, world: int = 1,
-                 process_group=None):
+                 process_group=None, exchange: bool = True):
         """rank / world / process_group: one partitioned solve across the GPUs of
         one box (one process per GPU, torch.distributed group for the exchange of
         the CUDA IPC handles and of the owned solution entries); see dsgpu.h."""
@@ -249,7 +251,7 @@ class GpuStokesSolver:
             msg = self.L.dsgpu_last_error(h).decode()
             self.close()
             _raise(rc, msg)
-        if world > 1:
+        if world > 1 and exchange:
             self._exchange_ipc_handles()
 
     def _exchange_ipc_handles(self):
@@ -377,6 +379,38 @@ class GpuStokesSolver:
         d = dict(zip(keys, a.tolist()))
         d["ic0_mode"] = ("exact", "staged", "partitioned-inverse", "blocked")[d["ic0_mode"]]
         return d
+
+
+def emulate_ranks(system: host.StokesSystem, strategy: str, world: int,
+                  options: SolverOptions | None = None, device: int = 0,
+                  top: BlockSetup | None = None, bottom: BlockSetup | None = None):
+    """The multi-GPU solve of `world` ranks emulated on ONE GPU
+    (dsgpu_debug_emulate_ranks: one cooperative launch, one CTA group per rank;
+    set DSGPU_GRID so that world x grid fits the SM count). Returns
+    (StokesSolution of rank 0's report, [SolveReport per rank])."""
+    o = options or SolverOptions()
+    tk, bk = STRATEGIES[strategy]
+    top = top or prepare_block(system.A, tk)
+    bottom = bottom or prepare_block(system.Q_nu, bk)
+    ranks = [GpuStokesSolver(system, strategy, device, top, bottom, rank=r, world=world, exchange=False)
+             for r in range(world)]
+    try:
+        L = ranks[0].L
+        hs = (C.c_void_p * world)(*[g.h for g in ranks])
+        reps = (_Report * world)()
+        u, p = np.zeros(system.n_u), np.zeros(system.n_p)
+        opts = ranks[0]._opts(o)
+        rc = L.dsgpu_debug_emulate_ranks(hs, world, np.ascontiguousarray(system.f, np.float64), C.byref(opts),
+                                         u, p, reps)
+        if rc:
+            _raise(rc, L.dsgpu_last_error(ranks[0].h).decode())
+        out = [SolveReport(r.iterations, bool(r.converged), np.zeros(0), np.zeros(0), r.wall_seconds,
+                           r.mean_inner_top, r.mean_inner_bottom, r.relres_m, r.relres_e, r.inner_top,
+                           r.apps_top, r.inner_bottom, r.apps_bottom, r.gpu_launches) for r in reps]
+        return StokesSolution(u, p, out[0]), out
+    finally:
+        for g in ranks:
+            g.close()
 
 
 def solve_stokes(system: host.StokesSystem, strategy: str,

@@ -146,6 +146,28 @@ def test_multi_gpu_entry_point_world1(gpu, port):
     monkey.close()
 
 
+@pytest.mark.parametrize("world,dim,n", [(2, 2, 16), (3, 2, 24), (4, 3, 8), (2, 3, 12)])
+def test_multi_gpu_data_plane_emulated(gpu, port, monkeypatch, world, dim, n):
+    """The multi-GPU solve (row-partitioned operators, halo gathers, cross-rank
+    reductions, pushed tagged residuals, replicated sweeps) run as `world` ranks
+    inside ONE cooperative launch on one GPU (dsgpu_debug_emulate_ranks): every
+    rank must report the reference's iteration counts and the assembled
+    solution must match the reference like the single-GPU solve does."""
+    host, solver = gpu
+    monkeypatch.setenv("DSGPU_SWEEP", "bs")
+    monkeypatch.setenv("DSGPU_GRID", str(148 // world - 2))   # worker CTAs per rank (+ 2 servers each)
+    monkeypatch.setenv("DSGPU_TIMEOUT_S", "60")
+    s = host.assemble("psi-mms", 2, n, dim=dim)
+    o = solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1)
+    sol, reps = solver.emulate_ranks(s, "IC0-PCG(A,Q)", world, o)
+    ref = reference_solve(port, s, "IC0-PCG(A,Q)", 1e-8, 1e-1)
+    check_parity(sol, ref, 1e-8)
+    for r in reps:
+        assert (r.iterations, r.inner_top, r.inner_bottom) == (reps[0].iterations, reps[0].inner_top,
+                                                               reps[0].inner_bottom)
+        assert r.relres_e == reps[0].relres_e  # identical scalars on every rank
+
+
 def test_two_handles_of_different_sizes(gpu, port):
     """Distinct handles: a smaller system set up after a larger one must not
     disturb the first handle's launches (shared-memory limits are per kernel
