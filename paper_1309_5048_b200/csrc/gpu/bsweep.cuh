@@ -3,6 +3,8 @@
 #pragma once
 
 #include "bsweep.hpp"
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace dsgpu {
@@ -56,6 +58,38 @@ __device__ __forceinline__ double bs_value(const uint4& w) {
   return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(w.z) << 32) | w.x));
 }
 
+// Tag of group g's units inside one sweep (shared-memory hand-offs reuse their
+// slots every kBsRC groups, so the tag names the group as well as the sweep).
+__device__ __forceinline__ unsigned bs_gtag(unsigned sweep_tag, int g) {
+  return ((sweep_tag & 0x3FFFu) << 18) | static_cast<unsigned>(g + 1);
+}
+__device__ __forceinline__ uint4 bs_lds_poll(const uint4* p) {  // volatile 16-byte shared-memory load
+  uint4 w;
+  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "r"(smem_u32(p))
+               : "memory");
+  return w;
+}
+__device__ __forceinline__ void bs_sts_unit(uint4* p, const uint4& w) {
+  asm volatile("st.volatile.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(w.x), "r"(w.y), "r"(w.z),
+               "r"(w.w)
+               : "memory");
+}
+// The same address in the shared memory of CTA `rank` of this cluster (DSMEM).
+__device__ __forceinline__ unsigned bs_peer_addr(const void* p, unsigned rank) {
+  unsigned a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ void bs_st_peer(unsigned addr, const uint4& w) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+               : "memory");
+}
+__device__ __forceinline__ void bs_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // Diagnostics exist only in the -DDSGPU_DIAG build (make diag): the production
 // kernels carry no counters, clocks or atomics on their paths.
 #ifdef DSGPU_DIAG
@@ -81,38 +115,39 @@ __device__ __forceinline__ int bs_comain_warp(int i) { return i + i / 3; }
 // Shared-memory workspace of the sweep CTA.
 struct BsSmem {
   double* ring;             // kBsR groups x 16 results, then the zero slot
-  double* cbuf;             // kBsRC x 16 (co-main -> main)
+  uint4* land;              // kBsRC x 16 tagged units at the SAME offset in every part: c (co-main -> main) in
+                            //   the whole / chain CTA, y (main -> relay) in the list CTA
   double* qbuf;             // kBsRQ x 32 lane partials (second main -> main)
   uint8_t* slots;           // ns x kBsSlotBytes
   uint8_t* stage;           // kBsNC x 2 x kBsStageBytes: co-main mid-list staging
   uint64_t* mbar;           // ns
   volatile int* sready;     // ns: group whose blocks have landed in the slot
   int* base_use;            // ns: completed mbarrier phases before this sweep
-  volatile int* aready;     // kBsRC: group whose c is staged
   volatile int* qready;     // kBsRQ: group whose q is staged
   volatile int* progress;   // groups finished by the main warp
   volatile int* pubdone;    // groups copied to global memory by the publisher
-  int ns;
-  __device__ BsSmem(double* base, int ns_) : ns(ns_) {
+  int ns;                   // slots of THIS part (0 in the list CTA)
+  __device__ BsSmem(double* base, int ns_, int part) : ns(part == kBsLists ? 0 : ns_) {
+    static_assert(kBsRL == kBsRC, "the landing rings share one region");
+    const int nc = part == kBsLists ? kBsNC2 : (part == kBsChain ? 0 : kBsNC);
     uint8_t* p = reinterpret_cast<uint8_t*>(base);
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
     p += (128u - (a & 127u)) & 127u;
     ring = reinterpret_cast<double*>(p);
     p += kBsZero + 128;
-    cbuf = reinterpret_cast<double*>(p);
-    p += kBsRC * kBsB * 8;
+    land = reinterpret_cast<uint4*>(p);
+    p += kBsRC * kBsB * 16;
     qbuf = reinterpret_cast<double*>(p);
     p += kBsRQ * 32 * 8;
     slots = p;
     p += static_cast<size_t>(ns) * kBsSlotBytes;
     stage = p;
-    p += static_cast<size_t>(kBsNC) * 2 * kBsStageBytes;
+    p += static_cast<size_t>(nc) * 2 * kBsStageBytes;
     mbar = reinterpret_cast<uint64_t*>(p);
     p += static_cast<size_t>(ns) * 8;
     sready = reinterpret_cast<volatile int*>(p);
     base_use = reinterpret_cast<int*>(p) + ns;
-    aready = reinterpret_cast<volatile int*>(p) + 2 * ns;
-    qready = aready + kBsRC;
+    qready = reinterpret_cast<volatile int*>(p) + 2 * ns;
     progress = qready + kBsRQ;
     pubdone = progress + 1;
   }
@@ -120,15 +155,17 @@ struct BsSmem {
 
 // Once per kernel launch and sweep CTA: the slot ring's mbarriers are
 // initialized once and only ever advance afterwards.
-__device__ void bs_setup(double* smem, int ns) {
-  BsSmem S(smem, ns);
-  for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+__device__ void bs_setup(double* smem, int ns, int part) {
+  BsSmem S(smem, ns, part);
+  for (int i = threadIdx.x; i < S.ns; i += blockDim.x) {
     mbar_init(S.mbar + i, 1);
     S.base_use[i] = 0;
   }
+  for (int i = threadIdx.x; i < kBsRC * kBsB; i += blockDim.x) S.land[i] = make_uint4(0u, 0u, 0u, 0u);  // tag 0: never valid
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  if (part != kBsWhole) bs_cluster_sync();  // the peer's landing ring is clean before anything is sent to it
 }
 
 // Far workers: for every group the partial sums of its far entries, gathered
@@ -209,23 +246,72 @@ __device__ void bs_far(const DBSweep& s, BsFar F, int wid, int W, unsigned* abor
   })
 }
 
+// The main warp's waits, out of line (see the step in bsweep): after step g
+// (g = -1: before the first) make sure that the dense blocks of group g + 3 have
+// landed, that c_{g+1} (tagged unit, re-polled into cw) and q_{g+1} are there and
+// that the publisher is not lapped on the y ring.
+struct BsMainWait {
+  uint4 cw;
+  int pd;
+};
+__device__ __noinline__ BsMainWait bs_main_wait(volatile int* sready_s3, const uint4* land, volatile int* qready,
+                                                volatile int* pubdone, unsigned sweep_tag, int g, int G, int r,
+                                                uint4 cw, int pd, unsigned* abort_flag) {
+  const int gn = g + 1;
+  BsMainWait out{cw, pd};
+  SpinGuard sg(abort_flag);
+  BS_DIAG(long long t0 = clock64(); const bool rec = (threadIdx.x & 31) == 0;)
+  // diag: cycles by what was waited for ([2] slots, [1] c, [14] q, [3] publisher)
+#define BS_WAIT_MARK(slot)                                                               \
+  BS_DIAG({                                                                              \
+    const long long t1 = clock64();                                                      \
+    if (rec) atomicAdd(&g_bs_dbg[slot], static_cast<unsigned long long>(t1 - t0));       \
+    t0 = t1;                                                                             \
+  })
+  if (g >= 0)
+    while (*sready_s3 != g + 3)
+      if (sg.expired()) return out;
+  BS_WAIT_MARK(2)
+  if (gn >= G) return out;
+  const unsigned tg = bs_gtag(sweep_tag, gn);
+  const uint4* q = land + (gn & (kBsRC - 1)) * kBsB + r;
+  while (!bs_valid(out.cw, tg)) {
+    if (sg.expired()) return out;
+    out.cw = bs_lds_poll(q);
+  }
+  BS_WAIT_MARK(1)
+  if (gn >= 3)
+    while (*(qready + (gn & (kBsRQ - 1))) != gn)
+      if (sg.expired()) return out;
+  BS_WAIT_MARK(14)
+  if (gn - out.pd >= kBsR - 2)
+    while ((out.pd = *pubdone) < gn - (kBsR - 3))
+      if (sg.expired()) return out;
+  BS_WAIT_MARK(3)
+#undef BS_WAIT_MARK
+  return out;
+}
+
 // One blocked sweep by every thread of the sweep CTA: gx = T^{-1} rhs (both in
 // the factor's ordering). Returns after a CTA barrier with the result complete
 // in global memory (plain in gx, tagged in F.gt).
 template <int K>
 // Right-hand side: rt (tagged units carrying rtag, written by the rows' owners --
 // possibly other GPUs -- and polled here) or, when rt is null, the plain vector rhs.
-__device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* __restrict__ rt, unsigned rtag,
-                       const double* __restrict__ rhs, double* gx, BsFar F, unsigned* abort_flag) {
+__device__ void bsweep(const DBSweep& s_in, double* smem, int ns_in, const uint4* __restrict__ rt, unsigned rtag,
+                       const double* __restrict__ rhs, double* gx, BsFar F, unsigned* abort_flag,
+                       int part = kBsWhole) {
   static_assert(K >= 3 && K <= 8 && K == kBsK, "dense coupling depth (F_1, F_2: main warp; F_3..F_K: second main warp)");
   const DBSweep s = s_in;
   const int G = s.G, n = s.n;
-  BsSmem S(smem, ns);
+  BsSmem S(smem, ns_in, part);
+  const int ns = S.ns;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int r = lane & 15, hf = lane >> 4;
+  // the partner CTA's landing ring (same offset in its shared memory)
+  const unsigned peer_land = part == kBsWhole ? 0u : bs_peer_addr(S.land, part == kBsChain ? 1u : 0u);
   for (int i = threadIdx.x; i <= kBsR * kBsB; i += blockDim.x) S.ring[i] = 0.0;
   for (int i = threadIdx.x; i < ns; i += blockDim.x) S.sready[i] = -1;
-  for (int i = threadIdx.x; i < kBsRC; i += blockDim.x) S.aready[i] = -1;
   for (int i = threadIdx.x; i < kBsRQ; i += blockDim.x) S.qready[i] = -1;
   if (threadIdx.x == 0) {
     *S.progress = 0;
@@ -233,9 +319,16 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* _
   }
   __syncthreads();
   // roles (warp w runs on SM sub-partition w % 4; the main warp keeps its own)
-  const int mainw = nw - 1, pubw = nw - 2, prodw = nw - 3, main2w = nw - 6;
+  const bool chain = part != kBsLists, lists = part != kBsChain;
+  const int mainw = chain ? nw - 1 : -1, pubw = chain ? nw - 2 : -1, prodw = chain ? nw - 3 : -1,
+            main2w = chain ? nw - 6 : -1;
+  const int NCv = part == kBsLists ? kBsNC2 : kBsNC;  // co-main warps of this CTA (round-robin stride)
+  const int relayw = part == kBsLists ? kBsNC2 : -1;
   int cid = -1;
-  {
+  if (part == kBsLists) {
+    static_assert(kBsNC2 <= 14, "list CTA: co-mains, one relay warp, spare warps");
+    if (warp < kBsNC2) cid = warp;
+  } else if (part == kBsWhole) {
     static_assert(kBsNC <= 9, "co-main warps are taken off the main warp's sub-partition");
     for (int i = 0; i < kBsNC; ++i)
       if (warp == bs_comain_warp(i)) cid = i;
@@ -266,7 +359,13 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* _
     BS_DIAG(const long long t0 = clock64(); long long w_c = 0, w_s = 0, w_p = 0, w_q = 0;)
     uint8_t* const ringb = reinterpret_cast<uint8_t*>(S.ring);
     for (int k = 0; k <= 2; ++k) wait_eq(S.sready + k % ns, k);
-    wait_eq(S.aready + 0, 0);
+    // c_g arrives as a tagged unit in the landing ring (from this CTA's co-mains or
+    // the list CTA's): the load is the poll. The step below is straight-line
+    // code: everything it may have to wait for is tested by ONE predicate, and
+    // the waiting itself lives out of line (bs_main_wait) -- with a single warp
+    // on its sub-partition every taken branch costs an instruction-fetch
+    // bubble (ncu: 32 % of the step was no_inst / branch_resolving when each
+    // wait had its own inline block).
     asm volatile("" ::: "memory");
     auto slot_at = [&](int slot) { return S.slots + static_cast<size_t>(slot) * kBsSlotBytes; };
     auto next_slot = [&](int slot) { return slot + 1 == ns ? 0 : slot + 1; };
@@ -274,78 +373,79 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* _
     double f1[8], f2[8];
     ld_block(slot_at(s1), 0, f1);  // F_1 of group 0
     ld_block(slot_at(s2), 1, f2);  // F_2 of group 1
-    double c = S.cbuf[r], q2 = 0.0, Q0 = 0.0;
     int pd = 0;
+    double c, q2 = 0.0, Q0 = 0.0;
+    {
+      uint4 cw0 = bs_lds_poll(S.land + r);
+      const BsMainWait mw = bs_main_wait(S.sready + s3, S.land, S.qready, S.pubdone, F.tag, -1, G, r, cw0, pd, abort_flag);
+      c = bs_value(mw.cw);
+    }
     int yoff = (kBsR - 1) * 128 + hf * 64;  // ring bytes of y_{g-1}, this lane's half
     int woff = r * 8;                       // ring bytes of y_g, this lane's row
     // invariant at the top of step g: the slots of groups <= g + 2 have landed
-    for (int g = 0; g < G; ++g) {
+    // One step. (fa, fb) hold F_1 of group g and F_2 of group g+1; the next step's
+    // blocks are loaded into the OTHER register set (na, nb): the loop below is
+    // unrolled by two with the sets swapped, so no loaded value is copied and
+    // nothing on the chain's tail waits for a load.
+    auto step = [&](const int g, const double (&fa)[8], const double (&fb)[8], double (&na)[8], double (&nb)[8]) {
       const double2* yp = reinterpret_cast<const double2*>(ringb + yoff);
       const double2 y0 = yp[0], y1 = yp[1], y2 = yp[2], y3 = yp[3];
-      double pa = f1[0] * y0.x, pb = f1[4] * y2.x, ua = f2[0] * y0.x, ub = f2[4] * y2.x;
-      pa = fma(f1[1], y0.y, pa);
-      pb = fma(f1[5], y2.y, pb);
-      ua = fma(f2[1], y0.y, ua);
-      ub = fma(f2[5], y2.y, ub);
-      pa = fma(f1[2], y1.x, pa);
-      pb = fma(f1[6], y3.x, pb);
-      ua = fma(f2[2], y1.x, ua);
-      ub = fma(f2[6], y3.x, ub);
-      pa = fma(f1[3], y1.y, pa);
-      pb = fma(f1[7], y3.y, pb);
-      ua = fma(f2[3], y1.y, ua);
-      ub = fma(f2[7], y3.y, ub);
+      double pa = fa[0] * y0.x, pb = fa[4] * y2.x, ua = fb[0] * y0.x, ub = fb[4] * y2.x;
+      pa = fma(fa[1], y0.y, pa);
+      pb = fma(fa[5], y2.y, pb);
+      ua = fma(fb[1], y0.y, ua);
+      ub = fma(fb[5], y2.y, ub);
+      pa = fma(fa[2], y1.x, pa);
+      pb = fma(fa[6], y3.x, pb);
+      ua = fma(fb[2], y1.x, ua);
+      ub = fma(fb[6], y3.x, ub);
+      pa = fma(fa[3], y1.y, pa);
+      pb = fma(fa[7], y3.y, pb);
+      ua = fma(fb[3], y1.y, ua);
+      ub = fma(fb[7], y3.y, ub);
       // next step's operands (slots g+1, g+2: landed) and the flags behind them
       s1 = s2;
       s2 = s3;
       s3 = next_slot(s3);
-      ld_block(slot_at(s1), 0, f1);
-      ld_block(slot_at(s2), 1, f2);
+      ld_block(slot_at(s1), 0, na);
+      ld_block(slot_at(s2), 1, nb);
       const int gn = g + 1;
-      const int fa = S.aready[gn & (kBsRC - 1)];
+      uint4 cw = bs_lds_poll(S.land + (gn & (kBsRC - 1)) * kBsB + r);
       const int fq = S.qready[gn & (kBsRQ - 1)];
       const int fs = S.sready[s3];
       // the chain's tail
       double t = (pa + pb) + (Q0 + q2);
       t += bs_shfl_xor16(t);
       const double y = c - t;
-      if (hf == 0) *reinterpret_cast<double*>(ringb + woff) = y;
+      if (hf == 0) {
+        *reinterpret_cast<double*>(ringb + woff) = y;
+        if (part == kBsChain)  // the list CTA's copy, through distributed shared memory
+          bs_st_peer(peer_land + ((g & (kBsRL - 1)) * kBsB + r) * 16, bs_pack(y, bs_gtag(F.tag, g)));
+      }
       Q0 = ua + ub;
       __syncwarp();
       if (lane == 0) *S.progress = gn;
       yoff = woff - r * 8 + hf * 64;
       woff = woff + 128 == kBsZero + r * 8 ? r * 8 : woff + 128;
-      if (fs != g + 3) {
-        BS_DIAG(const long long tw = clock64();)
-        wait_eq(S.sready + s3, g + 3);
-        BS_DIAG(w_s += clock64() - tw;)
+      // anything to wait for? (slot of group g+3, c and q of group g+1, the publisher)
+      const bool slow = (fs != g + 3) | !bs_valid(cw, bs_gtag(F.tag, gn)) | (gn >= 3 && fq != gn) |
+                        (gn - pd >= kBsR - 2) | (gn >= G);
+      if (__builtin_expect(slow, 0)) {
+        const BsMainWait mw = bs_main_wait(S.sready + s3, S.land, S.qready, S.pubdone, F.tag, g, G, r, cw, pd, abort_flag);
+        cw = mw.cw;
+        pd = mw.pd;
       }
-      if (gn < G) {
-        if (fa != gn) {
-          BS_DIAG(const long long tw = clock64();)
-          wait_eq(S.aready + (gn & (kBsRC - 1)), gn);
-          BS_DIAG(w_c += clock64() - tw;)
-        }
-        if (gn >= 3 && fq != gn) {
-          BS_DIAG(const long long tw = clock64();)
-          wait_eq(S.qready + (gn & (kBsRQ - 1)), gn);
-          BS_DIAG(w_q += clock64() - tw;)
-        }
-        asm volatile("" ::: "memory");
-        c = S.cbuf[(gn & (kBsRC - 1)) * kBsB + r];
-        q2 = gn >= 3 ? S.qbuf[(gn & (kBsRQ - 1)) * 32 + lane] : 0.0;
-      }
-      if (gn - pd >= kBsR - 2) {  // never lap the publisher on the y ring
-        pd = *S.pubdone;
-        if (gn - pd >= kBsR - 2) {
-          BS_DIAG(const long long tw = clock64();)
-          SpinGuard sg(abort_flag);
-          while ((pd = *S.pubdone) < gn - (kBsR - 3))
-            if (sg.expired()) break;
-          BS_DIAG(w_p += clock64() - tw;)
-        }
-      }
+      asm volatile("" ::: "memory");
+      c = bs_value(cw);
+      q2 = gn >= 3 ? S.qbuf[(gn & (kBsRQ - 1)) * 32 + lane] : 0.0;
+    };
+    double f1b[8], f2b[8];
+    int g = 0;
+    for (; g + 1 < G; g += 2) {
+      step(g, f1, f2, f1b, f2b);
+      step(g + 1, f1b, f2b, f1, f2);
     }
+    if (g < G) step(g, f1, f2, f1b, f2b);
     BS_DIAG(if (lane == 0) {
       atomicAdd(&g_bs_dbg[0], static_cast<unsigned long long>(clock64() - t0));
       atomicAdd(&g_bs_dbg[1], static_cast<unsigned long long>(w_c));
@@ -483,17 +583,17 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* _
       return t;
     };
     int prog = 0;  // last progress value seen
-    Meta m0 = load_meta(cid), m1 = load_meta(cid + kBsNC);
+    Meta m0 = load_meta(cid), m1 = load_meta(cid + NCv);
     stage_group(m0, 0);
     uint4 rhs0 = load_rhs(cid);
     TRow tr0 = load_t(cid);
     int buf = 0;
-    for (int h = cid; h < G; h += kBsNC, buf ^= 1) {
+    for (int h = cid; h < G; h += NCv, buf ^= 1) {
       BS_DIAG(const long long ta = clock64();)
-      const Meta m2 = load_meta(h + 2 * kBsNC);
+      const Meta m2 = load_meta(h + 2 * NCv);
       stage_group(m1, buf ^ 1);
-      const uint4 rhs1 = load_rhs(h + kBsNC);
-      const TRow tr1 = load_t(h + kBsNC);
+      const uint4 rhs1 = load_rhs(h + NCv);
+      const TRow tr1 = load_t(h + NCv);
       // the far partial sum of this lane's row: the load is the poll
       const uint4* fp = F.fps + static_cast<int64_t>(h) * kBsB + r;
       uint4 fw0 = make_uint4(0u, 0u, 0u, 0u);
@@ -512,7 +612,11 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* _
         // spins; the others sleep in proportion to their distance.
         while ((prog = *S.progress) < need) {
           const int d = need - prog;
-          if (d > 1) __nanosleep(d > 4 ? 400 : 80 * (d - 1));
+          if (part == kBsLists) {  // the list CTA's pipe is its own: short naps only when far away
+            if (d > 3) __nanosleep(100);
+          } else if (d > 1) {
+            __nanosleep(d > 4 ? 400 : 80 * (d - 1));
+          }
           if (sg.expired()) break;
         }
         asm volatile("" ::: "memory");
@@ -588,12 +692,15 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* _
       cv += bs_shfl_xor16(cv);
       BS_DIAG(const long long td = clock64(); d_c += td - tc;)
       wait_progress(h - kBsRC + 1);  // the c ring slot is free
-      if (hf == 0) S.cbuf[(h & (kBsRC - 1)) * kBsB + r] = cv;
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        S.aready[h & (kBsRC - 1)] = h;
+      if (hf == 0) {  // one self-validating unit: no flag, no fence
+        const uint4 u = bs_pack(cv, bs_gtag(F.tag, h));
+        const int at = (h & (kBsRC - 1)) * kBsB + r;
+        if (part == kBsLists)
+          bs_st_peer(peer_land + at * 16, u);
+        else
+          bs_sts_unit(S.land + at, u);
       }
+
       m0 = m1;
       m1 = m2;
       rhs0 = rhs1;
@@ -668,13 +775,47 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns, const uint4* _
         if (sg.expired()) break;
       }
     }
-  } else if (F.workers == 0 && (warp & 3) != (mainw & 3)) {
-    // no far-worker CTAs: the spare warps off the main warp's sub-partition
+  } else if (warp == relayw) {
+    // ---- relay (list CTA): the chain CTA's results, landed as tagged units through
+    // DSMEM, into this CTA's y ring; `progress` is what the co-mains here wait on.
+    // It cannot be lapped: the main warp needs c_g, c_g needs progress >= g - K here.
+    SpinGuard sg(abort_flag);
+    for (int g = 0; g < G; ++g) {
+      const unsigned tg = bs_gtag(F.tag, g);
+      bool ok = true;
+      if (lane < kBsB) {
+        const uint4* q = S.land + (g & (kBsRL - 1)) * kBsB + lane;
+        uint4 w = bs_lds_poll(q);
+        while (!bs_valid(w, tg)) {
+          if (sg.expired()) {
+            ok = false;
+            break;
+          }
+          w = bs_lds_poll(q);
+        }
+        S.ring[(g & (kBsR - 1)) * kBsB + lane] = bs_value(w);
+      }
+      if (!__all_sync(0xffffffffu, ok)) break;  // aborted
+      if (lane == 0) {
+        __threadfence_block();
+        *S.progress = g + 1;
+      }
+      sg.t0 = clock64();
+      sg.w0 = 0;
+    }
+  } else if (lists && F.workers == 0 && (part == kBsLists ? warp > relayw : true)) {
+    // no far-worker CTAs (small grids): the spare warps of this CTA
     int idx = 0, cnt = 0;
     for (int w = 0; w < nw; ++w) {
-      bool role = w == mainw || w == pubw || w == prodw || w == main2w;
-      for (int i = 0; i < kBsNC; ++i) role = role || w == bs_comain_warp(i);
-      if (!role && (w & 3) != (mainw & 3)) {
+      bool spare;
+      if (part == kBsLists) {
+        spare = w > relayw;
+      } else {
+        bool role = w == mainw || w == pubw || w == prodw || w == main2w;
+        for (int i = 0; i < kBsNC; ++i) role = role || w == bs_comain_warp(i);
+        spare = !role;
+      }
+      if (spare) {
         if (w == warp) idx = cnt;
         ++cnt;
       }

@@ -64,6 +64,9 @@
 #ifndef DSGPU_BS_STAGE
 #define DSGPU_BS_STAGE 16
 #endif
+#ifndef DSGPU_BS_NC2
+#define DSGPU_BS_NC2 12
+#endif
 
 namespace dsgpu {
 
@@ -73,7 +76,9 @@ constexpr int kBsK = DSGPU_BS_K;      // dense pre-multiplied coupling blocks: F
 constexpr int kBsRQ = 8;     // q ring (second main warp -> main), groups (power of two)
 constexpr int kBsR = DSGPU_BS_R;     // y ring depth in groups; older entries are "far"
 constexpr int kBsNC = DSGPU_BS_NC;     // co-main warps
+constexpr int kBsNC2 = DSGPU_BS_NC2;  // co-main warps of the list CTA when the sweep runs on a CTA pair
 constexpr int kBsRC = 16;    // c ring (co-main -> main), groups (power of two)
+constexpr int kBsRL = 16;    // y landing ring of the list CTA (chain CTA -> relay warp), groups (power of two)
 constexpr int kBsMC = 4;     // mid-list chunk (entries per lane)
 constexpr int kBsFC = 8;     // far-list chunk (entries per lane)
 constexpr int kBsStage = DSGPU_BS_STAGE;  // mid-list entries per lane staged ahead in shared memory (cp.async)
@@ -118,14 +123,31 @@ void build_bsweeps(const dsgpu_csr& L, HostBSweep& fwd, HostBSweep& bwd);
 // substitution): x = T^{-1} rhs in the sweep's own arithmetic order.
 void bsweep_host_apply(const HostBSweep& s, const double* rhs, double* x);
 
-// Shared memory of the sweep CTA with a slot ring of `ns` slots.
-inline size_t bs_smem_bytes(int ns) {
+// The sweep runs on ONE CTA (part 0: every role) or on a CTA PAIR of a 2-CTA
+// thread-block cluster (part 1, "chain": main, second main, producer, publisher
+// -- the dense blocks; part 2, "lists": the co-mains and a relay warp that
+// receives the chain CTA's results through distributed shared memory), so that
+// the chain's latency-critical shared-memory loads do not queue behind the
+// lists' bulk traffic on one SM's shared-memory pipe.
+enum { kBsWhole = 0, kBsChain = 1, kBsLists = 2 };
+
+// Shared memory of a sweep CTA with a slot ring of `ns` slots (same carve-up as
+// BsSmem in bsweep.cuh; the chain CTA of a pair may use a deeper ring ns1).
+inline size_t bs_smem_bytes_part(int ns, int part) {
+  const int nc = part == kBsLists ? kBsNC2 : (part == kBsChain ? 0 : kBsNC);
+  const int nslot = part == kBsLists ? 0 : ns;
   return static_cast<size_t>(kBsZero) + 128            // y ring + zero slot
-         + kBsRC * kBsB * 8 + kBsRQ * 32 * 8            // c ring, q ring
-         + static_cast<size_t>(ns) * kBsSlotBytes       // dense-block slots
-         + static_cast<size_t>(kBsNC) * 2 * kBsStageBytes  // co-main mid-list staging (double-buffered)
-         + static_cast<size_t>(ns) * 8                  // mbarriers
-         + (2 * ns + kBsRC + kBsRQ + 8) * 4 + 128;      // sready, base_use, aready, qready, progress words
+         + kBsRC * kBsB * 16                            // c ring / y landing ring (tagged 16-byte units)
+         + kBsRQ * 32 * 8                               // q ring
+         + static_cast<size_t>(nslot) * kBsSlotBytes    // dense-block slots
+         + static_cast<size_t>(nc) * 2 * kBsStageBytes  // co-main mid-list staging (double-buffered)
+         + static_cast<size_t>(nslot) * 8               // mbarriers
+         + (2 * nslot + kBsRQ + 8) * 4 + 128;           // sready, base_use, qready, progress words
+}
+inline size_t bs_smem_bytes(int ns) { return bs_smem_bytes_part(ns, kBsWhole); }
+inline size_t bs_smem_bytes_pair(int ns) {
+  return bs_smem_bytes_part(ns, kBsChain) > bs_smem_bytes_part(ns, kBsLists) ? bs_smem_bytes_part(ns, kBsChain)
+                                                                              : bs_smem_bytes_part(ns, kBsLists);
 }
 
 }  // namespace dsgpu

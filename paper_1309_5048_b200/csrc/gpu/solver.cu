@@ -190,7 +190,8 @@ struct Args {
   DevReport* rep;
   int smem_half;  // doubles per dataflow array (largest IC block)
   unsigned launch_id;  // distinguishes the sweep tags of successive launches
-  int n_srv;           // CTAs [0, n_srv) are IC(0) servers (CTA b serves block b)
+  int n_srv;           // CTAs [0, n_srv) are IC(0) servers (CTA b serves block b; with bs_pair CTAs 2b, 2b + 1)
+  int bs_pair;         // blocked sweeps on CTA pairs (2-CTA clusters: chain + lists, bsweep.hpp)
   Mailbox* mbox;       // [2]
 };
 
@@ -862,7 +863,7 @@ __device__ void flow_sweep(const DFlow& s_in, int n, double* smem, const double*
 template <int TB, bool RING, class Rhs>
 __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, double* red,
                            unsigned* abort_flag, unsigned launch_id = 0, unsigned sweep_no = 0,
-                           bool rhs_is_local = true) {
+                           bool rhs_is_local = true, int part = kBsWhole) {
   double* z = B.z;
   const double* r = B.r;
   double rz = 0.0;
@@ -894,8 +895,10 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
       for (int i = threadIdx.x; i < B.n; i += blockDim.x) __stcg(B.bs_bt + i, bs_pack(rhs(i), tag_f));
     const int workers = B.n_remote * static_cast<int>(blockDim.x >> 5);
     bsweep<kBsK>(B.bfwd, xf, B.bs_ns, B.bs_bt, tag_f, nullptr, y,
-                 BsFar{B.bs_gt, B.bs_fps, tag_f, workers}, abort_flag);
-    bsweep<kBsK>(B.bbwd, xf, B.bs_ns, nullptr, tag_b, y, z, BsFar{B.bs_gt, B.bs_fps, tag_b, workers}, abort_flag);
+                 BsFar{B.bs_gt, B.bs_fps, tag_f, workers}, abort_flag, part);
+    bsweep<kBsK>(B.bbwd, xf, B.bs_ns, nullptr, tag_b, y, z, BsFar{B.bs_gt, B.bs_fps, tag_b, workers}, abort_flag,
+                 part);
+    if (part == kBsLists) return 0.0;  // the chain CTA answers
     // <r, z> over the whole block from the tagged right-hand side (complete: the
     // forward sweep has read every entry of it)
     for (int i = threadIdx.x; i < B.n; i += blockDim.x) rz += bs_value(__ldcg(B.bs_bt + i)) * z[i];
@@ -1456,7 +1459,10 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
 // to exit. Runs no MINRES code, so the sweep's registers are its own.
 // (not inlined: its register allocation stays separate from the MINRES code's)
 template <int TB, bool RING>
-__device__ __noinline__ void ic_server(const Args& a, int b, double* xs, double* red) {
+__device__ __noinline__ void ic_server(const Args& a, int vblock, double* xs, double* red) {
+  // bs_pair: server CTAs 2b (chain) and 2b + 1 (lists) are one 2-CTA cluster serving block b
+  const int b = (TB == 0 && a.bs_pair) ? vblock >> 1 : vblock;
+  const int part = (TB == 0 && a.bs_pair) ? (vblock & 1 ? kBsLists : kBsChain) : kBsWhole;
   const DBlock& B = a.blk[b];
   if (B.kind != DSGPU_BLOCK_PCG_IC0) return;
   Mailbox* m = a.mbox + b;
@@ -1467,7 +1473,7 @@ __device__ __noinline__ void ic_server(const Args& a, int b, double* xs, double*
   __shared__ const double* src1_sh;
   __shared__ double* dst_sh;
   if constexpr (TB == 0) {
-    if (!B.exact) bs_setup(xs, B.bs_ns);
+    if (!B.exact) bs_setup(xs, B.bs_ns, part);
   } else {
     if (!B.exact) flow_setup<TB>(xs, B.n, B.ffwd.ring);
   }
@@ -1516,7 +1522,7 @@ __device__ __noinline__ void ic_server(const Args& a, int b, double* xs, double*
             r[row] = ri;
             return ri;
           },
-          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no, TB != 0);
+          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no, TB != 0, part);
     } else {
       double* r = B.r;
       const double* q = B.q;
@@ -1528,15 +1534,18 @@ __device__ __noinline__ void ic_server(const Args& a, int b, double* xs, double*
             r[row] = ri;
             return ri;
           },
-          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no, TB != 0);
+          xs, xs + a.smem_half, red, abort_flag, a.launch_id, sweep_no, TB != 0, part);
     }
     __syncthreads();  // every thread's r, z (and dst) written
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && part != kBsLists) {
       m->rz = rz;
       __threadfence();
       st_release(&m->done, seq);
       PHASE_DIAG(atomicAdd(&g_phase_dbg[b == 0 ? 1 : 5], static_cast<unsigned long long>(clock64() - ti0));)
     }
+  }
+  if constexpr (TB == 0) {
+    if (part != kBsWhole && !B.exact) bs_cluster_sync();  // neither CTA leaves while the other may still store into it
   }
 }
 
@@ -1825,7 +1834,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;
   }
   if constexpr (TB == 0) {
-    if (!B.exact) bs_setup(xs_dyn, B.bs_ns);
+    if (!B.exact) bs_setup(xs_dyn, B.bs_ns, kBsWhole);
   } else {
     if (!B.exact) flow_setup<TB>(xs_dyn, B.n, B.ffwd.ring);
   }
@@ -1944,6 +1953,7 @@ struct dsgpu_handle {
   bool bs = false;            // blocked sweeps (bsweep.cuh)
   bool force_pi = false;      // the early model chose the partitioned inverse
   int bs_ns = kBsK + 3;       // dense-block slot ring depth (minimum K + 3: the second main warp looks K groups ahead)
+  bool bs_pair = false;       // the solve's IC(0) servers are CTA pairs (2-CTA clusters; DSGPU_BS_PAIR=0: single CTAs)
   int far_ctas[2] = {0, 0};   // far-worker CTAs per IC block
   PiPlan pip[2];
   int pi_cbase = 0, pi_cslot = 0;  // chain coefficient prefetch slots (doubles)
@@ -2408,6 +2418,12 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       h->tb = 0;  // selects the blocked-sweep kernels (minres_for / ic_for)
       h->ring = true;
       if (const char* env = std::getenv("DSGPU_BS_SLOTS")) h->bs_ns = std::max(kBsK + 3, std::atoi(env));
+      // CTA pairs need groups that fit the 18-bit group tag, the column-order
+      // ("exact") sweep off, and -- for now -- a single-GPU handle
+      h->bs_pair = !h->exact && h->world == 1;
+      for (int b = 0; b < 2; ++b)
+        if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0 && (P.blk[b].n + kBsB - 1) / kBsB >= (1 << 18) - 2) h->bs_pair = false;
+      if (const char* env = std::getenv("DSGPU_BS_PAIR")) h->bs_pair = h->bs_pair && std::atoi(env) != 0;
     }
     if (!h->exact && !h->pi && !h->bs && nmax > 0) {
       const int merge = std::getenv("DSGPU_MERGE") ? std::atoi(std::getenv("DSGPU_MERGE")) : kDefaultMerge;
@@ -2427,7 +2443,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     h->smem = h->exact ? static_cast<size_t>(2) * nmax * sizeof(double)
                        : FlowSmem::bytes(nmax, SlotLayout(h->tb).bytes);
     if (h->pi) h->smem = pi_smem(h, static_cast<size_t>(smem_optin_pi) - 2048);
-    if (h->bs) h->smem = bs_smem_bytes(h->bs_ns);
+    if (h->bs) h->smem = std::max(bs_smem_bytes(h->bs_ns), h->bs_pair ? bs_smem_bytes_pair(h->bs_ns) : size_t(0));
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const size_t static_smem = 1024;
@@ -2454,8 +2470,12 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     // grid: IC(0) server CTAs (one per block, CTA b serves block b) + worker
     // CTAs, one per SM, fewer for tiny systems (barrier cost grows with CTAs)
     const int64_t nnz = P.nnz_k;
+    if (!h->bs) h->bs_pair = false;
     const int n_srv =
-        (!h->pi && (P.blk[0].kind == DSGPU_BLOCK_PCG_IC0 || P.blk[1].kind == DSGPU_BLOCK_PCG_IC0)) ? 2 : 0;
+        (!h->pi && (P.blk[0].kind == DSGPU_BLOCK_PCG_IC0 || P.blk[1].kind == DSGPU_BLOCK_PCG_IC0))
+            ? (h->bs_pair ? 4 : 2)
+            : 0;
+    if (n_srv == 0) h->bs_pair = false;
     const int wmax = sms - n_srv;
     int G = static_cast<int>(std::min<int64_t>(wmax, std::max<int64_t>(2, (nnz + 16383) / 16384)));
     G = std::max(G, 2);
@@ -2479,6 +2499,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
       h->far_ctas[0] = want[0];
       h->far_ctas[1] = want[1];
     }
+    if (h->bs_pair && (G & 1)) G += (G < wmax) ? 1 : -1;  // 2-CTA clusters: an even grid
     h->grid = n_srv + G;  // G = worker CTAs below
     // K-row partition balanced by nnz + per-row vector work
     // This rank's rows (partition.hpp: one velocity range and one pressure range,
@@ -2676,6 +2697,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     a.partial = h->alloc<double>(static_cast<size_t>(2) * NSLOT * G);
     a.bar = h->alloc<unsigned>(128);
     a.n_srv = n_srv;
+    a.bs_pair = h->bs_pair ? 1 : 0;
     a.mbox = h->alloc<Mailbox>(2);
     rc = cuda_check(h, cudaMemset(a.bar, 0, 128 * sizeof(unsigned)), "cudaMemset");
     if (rc) return rc;
@@ -2787,6 +2809,28 @@ static int solve_report(dsgpu_handle* h, const DevReport& R, float ms, dsgpu_rep
   return DSGPU_OK;
 }
 
+// Cooperative launch of a persistent solve kernel; `pair`: as 2-CTA thread-block
+// clusters (the IC(0) server pairs exchange data through distributed shared memory).
+static cudaError_t launch_solve_kernel(const void* fn, int grid, void** params, size_t smem, cudaStream_t stream,
+                                       bool pair) {
+  if (!pair) return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), params, smem, stream);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelExC(&cfg, fn, params);
+}
+
 static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, double* d_u,
                      double* d_p, dsgpu_report* rep, double* d_hm, double* d_he, int hist_cap) {
   Args a;
@@ -2800,8 +2844,8 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   cudaEventRecord(e0, h->stream);
   void* params[] = {&a};
   rc = cuda_check(h,
-                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_for(h->tb, h->ring, h->pi)), dim3(h->grid),
-                                              dim3(kThreads), params, h->smem, h->stream),
+                  launch_solve_kernel(reinterpret_cast<const void*>(minres_for(h->tb, h->ring, h->pi)), h->grid, params,
+                                      h->smem, h->stream, h->bs_pair),
                   "cooperative launch");
   cudaEventRecord(e1, h->stream);
   if (rc) {

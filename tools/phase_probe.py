@@ -48,7 +48,12 @@ def main():
                                  main_wait_publisher=round(bs[3] / G, 1),
                                  comain_cycles_per_group=round(bs[7] / G, 1),
                                  comain_wait_progress=round(bs[5] / G, 1), comain_wait_far=round(bs[6] / G, 1),
-                                 far_worker_wait_frac=round(bs[8] / max(1.0, float(bs[9])), 4))
+                                 far_worker_wait_frac=round(bs[8] / max(1.0, float(bs[9])), 4),
+                                 main_wait_q=round(bs[14] / G, 1), main2_wait_y=round(bs[15] / G, 1),
+                                 comain_stage_cycles=dict(prefetch_and_staging_wait=round(bs[10] / G, 1),
+                                                          mid_lists_incl_waits=round(bs[11] / G, 1),
+                                                          t_product=round(bs[12] / G, 1),
+                                                          hand_off=round(bs[13] / G, 1)))
         print(json.dumps(out), flush=True)
         g.close()
 
