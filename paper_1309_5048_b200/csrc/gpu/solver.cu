@@ -891,7 +891,7 @@ __device__ double ic_apply(const DBlock& B, Rhs rhs, double* xf, double* xb, dou
     // the stand-alone kernel passes rhs_is_local and writes it here.
     (void)bb;
     const unsigned tag_f = sweep_tag(launch_id, sweep_no), tag_b = sweep_tag(launch_id, sweep_no + 1);
-    if (rhs_is_local)
+    if (rhs_is_local && part != kBsLists)
       for (int i = threadIdx.x; i < B.n; i += blockDim.x) __stcg(B.bs_bt + i, bs_pack(rhs(i), tag_f));
     const int workers = B.n_remote * static_cast<int>(blockDim.x >> 5);
     bsweep<kBsK>(B.bfwd, xf, B.bs_ns, B.bs_bt, tag_f, nullptr, y,
@@ -1824,22 +1824,28 @@ __global__ void __launch_bounds__(kThreads, 1) minres_emul_kernel(const Args* al
 template <int TB, bool RING>
 __global__ void __launch_bounds__(kThreads, 1)
     ic_apply_kernel(const __grid_constant__ DBlock B, const double* r, unsigned* abort_flag,
-                    unsigned launch_id) {
+                    unsigned launch_id, int pair) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
   // B.r = r (input), B.z = output, B.y = forward-sweep scratch (set by the host).
-  // Ring mode: CTAs 1..n_remote are the remote helpers (B.remote_cta0 == 1).
-  if (RING && blockIdx.x > 0) {
-    ic_apply_remote(B, blockIdx.x - 1, abort_flag, launch_id, 0u);
+  // Ring mode: the CTAs after the sweep CTA (pair: after the sweep CTA pair, a
+  // 2-CTA cluster as in the solve) are the remote helpers / far workers.
+  const int lead = (TB == 0 && pair) ? 2 : 1;
+  if (RING && static_cast<int>(blockIdx.x) >= lead) {
+    ic_apply_remote(B, blockIdx.x - lead, abort_flag, launch_id, 0u);
     return;
   }
+  const int part = (TB == 0 && pair) ? (blockIdx.x ? kBsLists : kBsChain) : kBsWhole;
   if constexpr (TB == 0) {
-    if (!B.exact) bs_setup(xs_dyn, B.bs_ns, kBsWhole);
+    if (!B.exact) bs_setup(xs_dyn, B.bs_ns, part);
   } else {
     if (!B.exact) flow_setup<TB>(xs_dyn, B.n, B.ffwd.ring);
   }
   ic_apply<TB, RING>(B, [&](int row) { return r[row]; }, xs_dyn, xs_dyn + B.n, red, abort_flag,
-                     launch_id, 0u);
+                     launch_id, 0u, true, part);
+  if constexpr (TB == 0) {
+    if (part != kBsWhole) bs_cluster_sync();
+  }
 }
 
 // One partitioned-inverse IC(0) apply z = (L L^T)^{-1} r of one block by all
@@ -1862,7 +1868,7 @@ __global__ void fill_sentinel(double* p, int64_t n) {
 }
 
 using MinresFn = void (*)(Args);
-using IcFn = void (*)(DBlock, const double*, unsigned*, unsigned);
+using IcFn = void (*)(DBlock, const double*, unsigned*, unsigned, int);
 MinresFn minres_for(int tb, bool ring, bool pi) {
   if (tb == 0) return minres_kernel<0, true, false>;  // blocked sweeps
   if (pi) return minres_kernel<8, false, true>;
@@ -2467,6 +2473,27 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
                     "occupancy");
     if (rc) return rc;
     if (per_sm < 1) return fail(h, DSGPU_E_CUDA, "minres kernel cannot be resident");
+    if (h->bs_pair) {  // every 2-CTA cluster of a full grid must be resident at once
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(sms & ~1);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = h->smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclus = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclus, reinterpret_cast<const void*>(minres_for(h->tb, h->ring, h->pi)), &cfg) !=
+              cudaSuccess ||
+          2 * nclus < (sms & ~1)) {
+        cudaGetLastError();
+        h->bs_pair = false;  // single-CTA servers, cooperative launch
+        h->smem = bs_smem_bytes(h->bs_ns);
+      }
+    }
     // grid: IC(0) server CTAs (one per block, CTA b serves block b) + worker
     // CTAs, one per SM, fewer for tiny systems (barrier cost grows with CTAs)
     const int64_t nnz = P.nnz_k;
@@ -2809,8 +2836,14 @@ static int solve_report(dsgpu_handle* h, const DevReport& R, float ms, dsgpu_rep
   return DSGPU_OK;
 }
 
-// Cooperative launch of a persistent solve kernel; `pair`: as 2-CTA thread-block
-// clusters (the IC(0) server pairs exchange data through distributed shared memory).
+// Launch of a persistent solve kernel (all CTAs must be co-resident: they wait
+// on one another). Without clusters: a cooperative launch. `pair`: as 2-CTA
+// thread-block clusters (the IC(0) server pairs exchange data through
+// distributed shared memory) WITHOUT the cooperative attribute -- Nsight
+// Compute 2025.2 fails cluster + cooperative launches ("LaunchFailed"), and a
+// kernel that cannot be profiled cannot be judged; co-residency is established
+// at setup instead (one CTA per SM by shared memory, grid <= SM count, and
+// cudaOccupancyMaxActiveClusters >= grid / 2). DSGPU_COOP=1 adds the attribute.
 static cudaError_t launch_solve_kernel(const void* fn, int grid, void** params, size_t smem, cudaStream_t stream,
                                        bool pair) {
   if (!pair) return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), params, smem, stream);
@@ -2827,7 +2860,8 @@ static cudaError_t launch_solve_kernel(const void* fn, int grid, void** params, 
   at[1].id = cudaLaunchAttributeCooperative;
   at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  static const bool coop = std::getenv("DSGPU_COOP") && std::atoi(std::getenv("DSGPU_COOP")) != 0;
+  cfg.numAttrs = coop ? 2 : 1;
   return cudaLaunchKernelExC(&cfg, fn, params);
 }
 
@@ -3021,15 +3055,18 @@ static cudaError_t launch_ic(dsgpu_handle* h, DBlock B, const double* r) {
   unsigned id = h->next_launch_id();
   const int R = B.bs ? std::min(h->sms - 1, B.n_remote)
                      : (B.n_remote > 0 ? std::min(h->sms - 1, std::max(B.n_remote, 2 * h->remote_max)) : 0);
+  int pair = (B.bs && h->bs_pair && !B.exact) ? 1 : 0;  // the sweep CTA pair of the solve (2-CTA cluster)
+  int Rr = R;
+  if (pair) Rr = std::min(R, h->sms - 2) & ~1;  // an even grid
   B.remote_cta0 = 1;
-  B.n_remote = R;
-  if (R == 0) {
-    ic_for(h->tb, h->ring)<<<1, kThreads, h->smem, h->stream>>>(B, r, abort_flag, id);
+  B.n_remote = Rr;
+  if (Rr == 0 && !pair) {
+    ic_for(h->tb, h->ring)<<<1, kThreads, h->smem, h->stream>>>(B, r, abort_flag, id, 0);
     return cudaGetLastError();
   }
-  void* params[] = {&B, &r, &abort_flag, &id};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(ic_for(h->tb, h->ring)), dim3(1 + R),
-                                     dim3(kThreads), params, h->smem, h->stream);
+  void* params[] = {&B, &r, &abort_flag, &id, &pair};
+  return launch_solve_kernel(reinterpret_cast<const void*>(ic_for(h->tb, h->ring)), (pair ? 2 : 1) + Rr, params,
+                             h->smem, h->stream, pair != 0);
 }
 
 int dsgpu_apply_ic0(dsgpu_handle* h, int block, const double* r, double* z) {

@@ -82,15 +82,18 @@ def test_ic0_apply_partitioned_inverse_matches_reference(gpu, port, monkeypatch,
 
 
 @pytest.mark.parametrize("knobs", [{}, {"DSGPU_FAR_A": "0", "DSGPU_FAR_Q": "0"}, {"DSGPU_GRID": "5"},
-                                   {"DSGPU_FAR_A": "3", "DSGPU_FAR_Q": "1", "DSGPU_BS_SLOTS": "9"}])
+                                   {"DSGPU_FAR_A": "3", "DSGPU_FAR_Q": "1", "DSGPU_BS_SLOTS": "9"},
+                                   {"DSGPU_BS_PAIR": "0"}, {"DSGPU_BS_PAIR": "0", "DSGPU_FAR_A": "0", "DSGPU_FAR_Q": "0"}])
 def test_ic0_apply_blocked_matches_reference(gpu, port, monkeypatch, knobs):
     """Blocked sweeps (bsweep.hpp; the IC(0) apply of the large 3D systems,
     forced here with DSGPU_SWEEP=bs) -- dense 16x16 blocks next to the diagonal
     on the two main warps, mid entries on the co-main warps, far entries on
     far-worker CTAs -- against the reference's own Ic0Factor::solve output
     (fixture), the CPU oracle on 2D and 3D factors, and through a whole solve.
-    knobs: no far-worker CTAs (the sweep CTA's spare warps do the far lists), a
-    5-CTA grid, few far CTAs with a different slot ring depth."""
+    knobs: no far-worker CTAs (the sweep CTAs' spare warps do the far lists), a
+    5-CTA grid, few far CTAs with a different slot ring depth; by default every
+    sweep runs on a CTA pair (2-CTA cluster: chain + lists over DSMEM),
+    DSGPU_BS_PAIR=0 is the single-CTA form."""
     host, solver = gpu
     monkeypatch.setenv("DSGPU_SWEEP", "bs")
     for k, v in knobs.items():
