@@ -2449,7 +2449,10 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     h->smem = h->exact ? static_cast<size_t>(2) * nmax * sizeof(double)
                        : FlowSmem::bytes(nmax, SlotLayout(h->tb).bytes);
     if (h->pi) h->smem = pi_smem(h, static_cast<size_t>(smem_optin_pi) - 2048);
-    if (h->bs) h->smem = std::max(bs_smem_bytes(h->bs_ns), h->bs_pair ? bs_smem_bytes_pair(h->bs_ns) : size_t(0));
+    // CTA pairs need less shared memory per CTA than the single-CTA sweep (no slot
+    // ring in the list CTA, no list staging in the chain CTA): the smaller
+    // carve-out leaves the SpMV CTAs of the same kernel more L1
+    if (h->bs) h->smem = h->bs_pair && !std::getenv("DSGPU_BS_SMEM_WHOLE") ? bs_smem_bytes_pair(h->bs_ns) : bs_smem_bytes(h->bs_ns);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const size_t static_smem = 1024;
