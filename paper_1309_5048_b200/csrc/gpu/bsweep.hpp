@@ -53,7 +53,7 @@
 
 // Tuning constants (overridable at build time for A/B runs: make EXTRA_DEFS=-DDSGPU_BS_K=4 ...)
 #ifndef DSGPU_BS_K
-#define DSGPU_BS_K 5
+#define DSGPU_BS_K 6
 #endif
 #ifndef DSGPU_BS_R
 #define DSGPU_BS_R 32

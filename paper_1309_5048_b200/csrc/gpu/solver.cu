@@ -2423,13 +2423,15 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     if (h->bs) {
       h->tb = 0;  // selects the blocked-sweep kernels (minres_for / ic_for)
       h->ring = true;
-      if (const char* env = std::getenv("DSGPU_BS_SLOTS")) h->bs_ns = std::max(kBsK + 3, std::atoi(env));
-      // CTA pairs need groups that fit the 18-bit group tag, the column-order
-      // ("exact") sweep off, and -- for now -- a single-GPU handle
-      h->bs_pair = !h->exact && h->world == 1;
+      // CTA pairs need groups that fit the 18-bit group tag and the column-order
+      // ("exact") sweep off
+      h->bs_pair = !h->exact;
       for (int b = 0; b < 2; ++b)
         if (P.blk[b].kind == DSGPU_BLOCK_PCG_IC0 && (P.blk[b].n + kBsB - 1) / kBsB >= (1 << 18) - 2) h->bs_pair = false;
       if (const char* env = std::getenv("DSGPU_BS_PAIR")) h->bs_pair = h->bs_pair && std::atoi(env) != 0;
+      // slot ring: K + 3 at least; the chain CTA of a pair has room for 12 (C4: 1.24 -> 1.17 s)
+      h->bs_ns = h->bs_pair ? std::max(kBsK + 3, 12) : kBsK + 3;
+      if (const char* env = std::getenv("DSGPU_BS_SLOTS")) h->bs_ns = std::max(kBsK + 3, std::atoi(env));
     }
     if (!h->exact && !h->pi && !h->bs && nmax > 0) {
       const int merge = std::getenv("DSGPU_MERGE") ? std::atoi(std::getenv("DSGPU_MERGE")) : kDefaultMerge;
@@ -2452,7 +2454,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     // CTA pairs need less shared memory per CTA than the single-CTA sweep (no slot
     // ring in the list CTA, no list staging in the chain CTA): the smaller
     // carve-out leaves the SpMV CTAs of the same kernel more L1
-    if (h->bs) h->smem = h->bs_pair && !std::getenv("DSGPU_BS_SMEM_WHOLE") ? bs_smem_bytes_pair(h->bs_ns) : bs_smem_bytes(h->bs_ns);
+    if (h->bs) h->smem = h->bs_pair ? bs_smem_bytes_pair(h->bs_ns) : bs_smem_bytes(h->bs_ns);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const size_t static_smem = 1024;
@@ -2494,6 +2496,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
           2 * nclus < (sms & ~1)) {
         cudaGetLastError();
         h->bs_pair = false;  // single-CTA servers, cooperative launch
+        h->bs_ns = kBsK + 3;
         h->smem = bs_smem_bytes(h->bs_ns);
       }
     }
@@ -2914,7 +2917,7 @@ int dsgpu_debug_emulate_ranks(dsgpu_handle** hs, int world, const double* f, con
   for (int r = 0; r < world; ++r) {
     dsgpu_handle* h = hs[r];
     if (!h || !h->ready || h->world != world || h->rank != r || h->device != h0->device || h->grid != h0->grid ||
-        h->tb != 0 || h->pi || !h->ring)
+        h->tb != 0 || h->pi || !h->ring || h->bs_pair != h0->bs_pair)
       return fail(h0, DSGPU_E_BAD_INPUT, "dsgpu_debug_emulate_ranks: handles must be ranks 0..world-1 of one device, "
                                           "blocked sweeps, equal grids");
   }
@@ -2952,10 +2955,11 @@ int dsgpu_debug_emulate_ranks(dsgpu_handle** hs, int world, const double* f, con
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, h0->stream);
+  // (with CTA pairs every rank's share of the grid is even, so the 2-CTA clusters never straddle two ranks)
   rc = cuda_check(h0,
-                  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(minres_emul_kernel), dim3(world * per_rank),
-                                              dim3(kThreads), params, smem, h0->stream),
-                  "cooperative launch (emulated ranks)");
+                  launch_solve_kernel(reinterpret_cast<const void*>(minres_emul_kernel), world * per_rank, params, smem,
+                                      h0->stream, h0->bs_pair),
+                  "launch (emulated ranks)");
   cudaEventRecord(e1, h0->stream);
   if (!rc) rc = cuda_check(h0, cudaStreamSynchronize(h0->stream), "emulated solve");
   float ms = 0.0f;

@@ -82,7 +82,7 @@ def test_ic0_apply_partitioned_inverse_matches_reference(gpu, port, monkeypatch,
 
 
 @pytest.mark.parametrize("knobs", [{}, {"DSGPU_FAR_A": "0", "DSGPU_FAR_Q": "0"}, {"DSGPU_GRID": "5"},
-                                   {"DSGPU_FAR_A": "3", "DSGPU_FAR_Q": "1", "DSGPU_BS_SLOTS": "9"},
+                                   {"DSGPU_FAR_A": "3", "DSGPU_FAR_Q": "1", "DSGPU_BS_SLOTS": "10"},
                                    {"DSGPU_BS_PAIR": "0"}, {"DSGPU_BS_PAIR": "0", "DSGPU_FAR_A": "0", "DSGPU_FAR_Q": "0"}])
 def test_ic0_apply_blocked_matches_reference(gpu, port, monkeypatch, knobs):
     """Blocked sweeps (bsweep.hpp; the IC(0) apply of the large 3D systems,
@@ -158,7 +158,7 @@ def test_multi_gpu_data_plane_emulated(gpu, port, monkeypatch, world, dim, n):
     solution must match the reference like the single-GPU solve does."""
     host, solver = gpu
     monkeypatch.setenv("DSGPU_SWEEP", "bs")
-    monkeypatch.setenv("DSGPU_GRID", str(148 // world - 2))   # worker CTAs per rank (+ 2 servers each)
+    monkeypatch.setenv("DSGPU_GRID", str((148 // world - 4) & ~1))   # worker CTAs per rank (+ 2 server CTA pairs each)
     monkeypatch.setenv("DSGPU_TIMEOUT_S", "60")
     s = host.assemble("psi-mms", 2, n, dim=dim)
     o = solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1)
