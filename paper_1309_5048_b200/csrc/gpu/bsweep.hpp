@@ -16,7 +16,11 @@
 // warp out of shared memory, instead of one step per dependency level
 // (32^3: 7,153 groups vs 10,715 levels of 10.7 rows).
 //
-// Roles (one "sweep CTA" per triangular solve, plus far-worker CTAs):
+// Roles (per triangular solve one "sweep CTA", or -- the production form -- a
+// CTA PAIR of a 2-CTA cluster: a chain CTA with the main / second main /
+// producer / publisher warps and a list CTA with the co-mains and a relay warp,
+// exchanging y_g and c_g as tagged units through distributed shared memory;
+// plus far-worker CTAs):
 //   * MAIN warp: y_g = c_g - q_g - F_{g,1} y_{g-1} - F_{g,2} y_{g-2}; lane (r, h)
 //     owns row r and columns 8h..8h+7 of each block (two lanes per row, combined
 //     by one shuffle). y_{g-1} is broadcast through the shared-memory y ring.
@@ -27,11 +31,11 @@
 //     ring; the "far" partial sums come from the far workers. Each co-main
 //     stages its NEXT group's mid list in shared memory with cp.async while it
 //     works on the current one, so the lists' HBM latency is off its path.
-//   * PRODUCER lane: TMA bulk copies of each group's dense blocks (F_1..F_K,
-//     T) into a shared-memory slot ring.
+//   * PRODUCER lane: TMA bulk copies of each group's dense blocks (F_1..F_K)
+//     into a shared-memory slot ring.
 //   * PUBLISHER warp: copies finished groups from the y ring to the result
-//     vector in global memory and publishes the progress counter (fence +
-//     release), so the main warp never touches global memory.
+//     vector in global memory (plain, and as tagged units for the far workers),
+//     so the main warp never touches global memory.
 //   * FAR WORKERS (warps of other CTAs): for each group the partial sums of
 //     the entries older than the ring (col group < g-R), gathered from the
 //     published result vector; they run far ahead of the main warp and stream

@@ -337,7 +337,11 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
     if (e == b || l_cols[e - 1] != i)
       return fail(DSGPU_E_BAD_INPUT, "ic0: structurally missing diagonal at row " + std::to_string(i));
     int lv = 0;
-    for (int64_t k = b; k < e - 1; ++k) lv = std::max(lv, level[l_cols[k]] + 1);
+    for (int64_t k = b; k < e - 1; ++k) {
+      if (l_cols[k] < 0 || l_cols[k] >= i)
+        return fail(DSGPU_E_BAD_INPUT, "ic0: row " + std::to_string(i) + " has a column outside [0, row)");
+      lv = std::max(lv, level[l_cols[k]] + 1);
+    }
     level[i] = lv;
     nlev = std::max(nlev, lv + 1);
     maxlen = std::max(maxlen, static_cast<int>(e - b));
@@ -354,7 +358,12 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   int64_t cap_w = std::min<int64_t>(2368, (8ll << 30) / (4ll * std::max(n, 1)));
   if (const char* env = std::getenv("DSGPU_IC0_MAX_WARPS")) cap_w = std::min<int64_t>(cap_w, std::atoll(env));
   const int maxw_flow = static_cast<int>(std::max<int64_t>(kWarpsPerBlock, cap_w / kWarpsPerBlock * kWarpsPerBlock));
-  maxw = std::max(maxw, maxw_flow);
+  // the barrier-free dataflow kernel by default; DSGPU_IC0_FLOW=0: level-scheduled launches.
+  // Column-position maps: one per warp of the dataflow grid, or one per row of the
+  // widest level for the level schedule -- never both (the widest level of a large
+  // 3D block would ask for tens of GB the dataflow kernel never touches).
+  const bool flow = !(std::getenv("DSGPU_IC0_FLOW") && std::atoi(std::getenv("DSGPU_IC0_FLOW")) == 0);
+  maxw = flow ? maxw_flow : maxw;
   std::vector<int32_t> order(n);
   {
     std::vector<int64_t> fill(lstart.begin(), lstart.end() - 1);
@@ -408,8 +417,6 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   cudaMemsetAsync(d_pos, 0xFF, sizeof(int) * static_cast<size_t>(maxw) * n, st);  // all -1
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  // the barrier-free dataflow kernel by default; DSGPU_IC0_FLOW=0: level-scheduled launches
-  const bool flow = !(std::getenv("DSGPU_IC0_FLOW") && std::atoi(std::getenv("DSGPU_IC0_FLOW")) == 0);
   int flow_grid = 0;
   int* d_done = nullptr;
   int* d_abort = nullptr;
@@ -429,9 +436,14 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
     cudaMemsetAsync(d_abort, 0, sizeof(int), st);
   }
   cudaEventRecord(e0, st);
-  if (flow)
-    ic0_flow_kernel<<<flow_grid, kWarpsPerBlock * 32, smem, st>>>(n, d_rp, d_ci, d_v, maxlen, d_pos, d_done, d_bad,
-                                                                  d_abort);
+  cudaError_t le = cudaSuccess;
+  if (flow) {
+    // its warps wait on one another's rows: a cooperative launch (every CTA co-resident)
+    int n_arg = n, maxlen_arg = maxlen;
+    void* params[] = {&n_arg, &d_rp, &d_ci, &d_v, &maxlen_arg, &d_pos, &d_done, &d_bad, &d_abort};
+    le = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(ic0_flow_kernel), dim3(flow_grid),
+                                     dim3(kWarpsPerBlock * 32), params, smem, st);
+  }
   for (int l = 0; !flow && l < nlev; ++l) {
     const int cnt = static_cast<int>(lstart[l + 1] - lstart[l]);
     const int grid = (cnt + kWarpsPerBlock - 1) / kWarpsPerBlock;
@@ -443,7 +455,8 @@ int dsgpu_ic0_factor(int device, int n, const int64_t* row_ptr, const int32_t* c
   if (flow) cudaMemcpyAsync(&aborted, d_abort, sizeof(int), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(l_vals, d_v, sizeof(double) * nnz, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st);
-  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (le != cudaSuccess) e = le;
   float ms = 0.0f;
   if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
   cudaFree(d_done);

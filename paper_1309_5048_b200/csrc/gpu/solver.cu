@@ -2691,7 +2691,7 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
         cudaMemset(d.gprog, 0, sizeof(unsigned long long));
         const int R = std::min(h->remote_max, (G - 1) / 2);
         d.n_remote = R > 0 ? R : 0;
-        d.remote_cta0 = n_srv + 1 + b * d.n_remote;  // workers, after the lead worker
+        d.remote_cta0 = 1 + b * d.n_remote;  // worker units (Ctx::remote_rank), after the lead worker
       }
       d.r = h->alloc<double>(hb.n);
       d.z = h->alloc<double>(hb.n + 1);  // z[n] = 0: the padding column of the far lists
