@@ -61,7 +61,7 @@ __device__ __forceinline__ double bs_value(const uint4& w) {
 // Tag of group g's units inside one sweep (shared-memory hand-offs reuse their
 // slots every kBsRC groups, so the tag names the group as well as the sweep).
 __device__ __forceinline__ unsigned bs_gtag(unsigned sweep_tag, int g) {
-  return ((sweep_tag & 0x3FFFu) << 18) | static_cast<unsigned>(g + 1);
+  return ((sweep_tag & 0x3FFFu) << 18) + static_cast<unsigned>(g + 1);  // linear in g: the main warp just increments it
 }
 __device__ __forceinline__ uint4 bs_lds_poll(const uint4* p) {  // volatile 16-byte shared-memory load
   uint4 w;
@@ -81,6 +81,17 @@ __device__ __forceinline__ unsigned bs_peer_addr(const void* p, unsigned rank) {
   unsigned a;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
   return a;
+}
+// ... as a 64-bit generic pointer (computed once: a st.shared::cluster through a
+// 32-bit address makes the compiler rebuild the generic address -- S2R SR_SWINHI,
+// ~50 cycles -- at every store)
+__device__ __forceinline__ unsigned long long bs_peer_generic(const void* p, unsigned rank) {
+  unsigned long long g;
+  asm volatile("cvta.shared::cluster.u64 %0, %1;" : "=l"(g) : "l"(static_cast<unsigned long long>(bs_peer_addr(p, rank))));
+  return g;
+}
+__device__ __forceinline__ void bs_st_generic(unsigned long long addr, const uint4& w) {
+  asm volatile("st.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w) : "memory");
 }
 __device__ __forceinline__ void bs_st_peer(unsigned addr, const uint4& w) {
   asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
@@ -369,10 +380,31 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns_in, const uint4
     asm volatile("" ::: "memory");
     auto slot_at = [&](int slot) { return S.slots + static_cast<size_t>(slot) * kBsSlotBytes; };
     auto next_slot = [&](int slot) { return slot + 1 == ns ? 0 : slot + 1; };
-    int s1 = 0, s2 = 1 % ns, s3 = 2 % ns;  // slots of groups g, g+1, g+2
+    int s3 = 2 % ns;  // slot of group g+2; o1, o2: byte offsets of the slots of groups g, g+1
+    int o1 = 0, o2 = (1 % ns) * kBsSlotBytes, o3 = (2 % ns) * kBsSlotBytes;
+    const int oend = ns * kBsSlotBytes;
+    const uint8_t* const slot_l = S.slots + lane * 16;  // this lane's unit inside every block
+    // this lane's half row (4 units, 512 bytes apart) of one block
+    auto ld_row = [&](const uint8_t* p, double* out) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 t = *reinterpret_cast<const double2*>(p + q * 512);
+        out[2 * q] = t.x;
+        out[2 * q + 1] = t.y;
+      }
+    };
+    (void)slot_at;
+    (void)next_slot;
     double f1[8], f2[8];
-    ld_block(slot_at(s1), 0, f1);  // F_1 of group 0
-    ld_block(slot_at(s2), 1, f2);  // F_2 of group 1
+    ld_row(slot_l + o1, f1);             // F_1 of group 0
+    ld_row(slot_l + o2 + kBsBlock, f2);  // F_2 of group 1
+    // running addresses and tags of the step: the c unit of group g+1, the tag of
+    // group g, the partner's y landing unit of group g
+    int coff = (1 & (kBsRC - 1)) * kBsB * 16 + r * 16;
+    unsigned tg = bs_gtag(F.tag, 0);
+    const uint8_t* const landb = reinterpret_cast<const uint8_t*>(S.land);
+    const unsigned long long peer_y = part == kBsChain ? bs_peer_generic(S.land, 1u) + r * 16 : 0ull;
+    int poff = 0;
     int pd = 0;
     double c, q2 = 0.0, Q0 = 0.0;
     {
@@ -404,13 +436,14 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns_in, const uint4
       ua = fma(fb[3], y1.y, ua);
       ub = fma(fb[7], y3.y, ub);
       // next step's operands (slots g+1, g+2: landed) and the flags behind them
-      s1 = s2;
-      s2 = s3;
-      s3 = next_slot(s3);
-      ld_block(slot_at(s1), 0, na);
-      ld_block(slot_at(s2), 1, nb);
+      o1 = o2;
+      o2 = o3;
+      o3 = o3 + kBsSlotBytes == oend ? 0 : o3 + kBsSlotBytes;
+      s3 = s3 + 1 == ns ? 0 : s3 + 1;
+      ld_row(slot_l + o1, na);
+      ld_row(slot_l + o2 + kBsBlock, nb);
       const int gn = g + 1;
-      uint4 cw = bs_lds_poll(S.land + (gn & (kBsRC - 1)) * kBsB + r);
+      uint4 cw = bs_lds_poll(reinterpret_cast<const uint4*>(landb + coff));
       const int fq = S.qready[gn & (kBsRQ - 1)];
       const int fs = S.sready[s3];
       // the chain's tail
@@ -420,15 +453,18 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns_in, const uint4
       if (hf == 0) {
         *reinterpret_cast<double*>(ringb + woff) = y;
         if (part == kBsChain)  // the list CTA's copy, through distributed shared memory
-          bs_st_peer(peer_land + ((g & (kBsRL - 1)) * kBsB + r) * 16, bs_pack(y, bs_gtag(F.tag, g)));
+          bs_st_generic(peer_y + poff, bs_pack(y, tg));
       }
+      poff = (poff + kBsB * 16) & (kBsRL * kBsB * 16 - 1);
+      coff = (coff + kBsB * 16) & (kBsRC * kBsB * 16 - 1);
+      tg += 1u;  // = bs_gtag(F.tag, g + 1)
       Q0 = ua + ub;
       __syncwarp();
       if (lane == 0) *S.progress = gn;
       yoff = woff - r * 8 + hf * 64;
       woff = woff + 128 == kBsZero + r * 8 ? r * 8 : woff + 128;
       // anything to wait for? (slot of group g+3, c and q of group g+1, the publisher)
-      const bool slow = (fs != g + 3) | !bs_valid(cw, bs_gtag(F.tag, gn)) | (gn >= 3 && fq != gn) |
+      const bool slow = (fs != g + 3) | !bs_valid(cw, tg) | (gn >= 3 && fq != gn) |
                         (gn - pd >= kBsR - 2) | (gn >= G);
       if (__builtin_expect(slow, 0)) {
         const BsMainWait mw = bs_main_wait(S.sready + s3, S.land, S.qready, S.pubdone, F.tag, g, G, r, cw, pd, abort_flag);

@@ -149,19 +149,22 @@ Csr permute_symmetric(const Csr& a, const std::vector<int32_t>& perm) {
   b.v.resize(a.v.size());
 #pragma omp parallel
   {
-    std::vector<std::pair<int32_t, double>> row;
+    // one 64-bit key per entry: (new column << 32) | position in the old row --
+    // sorting plain integers is ~2x faster than sorting (column, value) pairs
+    std::vector<uint64_t> key;
 #pragma omp for schedule(dynamic, 256)
     for (int r = 0; r < n; ++r) {
       const int old = perm[r];
-      row.clear();
-      for (int64_t k = a.rp[old]; k < a.rp[old + 1]; ++k) row.emplace_back(inv[a.ci[k]], a.v[k]);
-      std::sort(row.begin(), row.end(),
-                [](const auto& x, const auto& y) { return x.first < y.first; });
+      const int64_t k0 = a.rp[old], len = a.rp[old + 1] - k0;
+      key.resize(static_cast<size_t>(len));
+      for (int64_t k = 0; k < len; ++k)
+        key[k] = (static_cast<uint64_t>(static_cast<uint32_t>(inv[a.ci[k0 + k]])) << 32) | static_cast<uint32_t>(k);
+      std::sort(key.begin(), key.end());
       int64_t at = b.rp[r];
-      for (const auto& e : row) {
-        b.ci[at] = e.first;
+      for (int64_t k = 0; k < len; ++k) {
+        b.ci[at] = static_cast<int32_t>(key[k] >> 32);
         double sum = 0.0;  // csr_from_triplets sums from 0.0
-        sum += e.second;
+        sum += a.v[k0 + static_cast<uint32_t>(key[k])];
         b.v[at++] = sum;
       }
     }
