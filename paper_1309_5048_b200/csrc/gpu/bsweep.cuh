@@ -443,12 +443,14 @@ __device__ void bsweep(const DBSweep& s_in, double* smem, int ns_in, const uint4
       ld_row(slot_l + o1, na);
       ld_row(slot_l + o2 + kBsBlock, nb);
       const int gn = g + 1;
-      uint4 cw = bs_lds_poll(reinterpret_cast<const uint4*>(landb + coff));
-      const int fq = S.qready[gn & (kBsRQ - 1)];
-      const int fs = S.sready[s3];
       // the chain's tail
       double t = (pa + pb) + (Q0 + q2);
       t += bs_shfl_xor16(t);
+      // the flags and c of the next step, as late as their latency allows (issued
+      // under the shuffle): a c that lands during the tail is still seen
+      uint4 cw = bs_lds_poll(reinterpret_cast<const uint4*>(landb + coff));
+      const int fq = S.qready[gn & (kBsRQ - 1)];
+      const int fs = S.sready[s3];
       const double y = c - t;
       if (hf == 0) {
         *reinterpret_cast<double*>(ringb + woff) = y;
