@@ -203,11 +203,26 @@ def measure(tag, args, world, rank, local, dist, full: bool):
     bot = solver.prepare_block(s.Q_nu, bk, ic0_on_gpu=True)
     precond_setup_s = time.perf_counter() - t0
     t0 = time.perf_counter()
+    fallback = None
+    g = None
     if partitioned:
         os.environ["DSGPU_SWEEP"] = "bs"  # the multi-GPU data plane runs the replicated blocked sweeps
-        g = solver.GpuStokesSolver(s, W["strategy"], device=local, top=top, bottom=bot, rank=rank,
-                                   world=world, process_group=None)
-    else:
+        err = ""
+        try:
+            g = solver.GpuStokesSolver(s, W["strategy"], device=local, top=top, bottom=bot, rank=rank,
+                                       world=world, process_group=None)
+        except Exception as e:  # e.g. no peer access between these GPUs
+            err = f"{type(e).__name__}: {e}"[:160]
+        ok = torch.tensor([0 if g is None else 1], device=torch.device("cuda", local))
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same branch
+        if int(ok.item()) == 0:
+            if g is not None:
+                g.close()
+                g = None
+            partitioned = False
+            fallback = "partitioned setup failed on a rank (" + (err or "another rank") + "): independent replicas"
+            os.environ.pop("DSGPU_SWEEP", None)
+    if g is None:
         g = solver.GpuStokesSolver(s, W["strategy"], device=local, top=top, bottom=bot)
     device_setup_s = time.perf_counter() - t0
     info = g.info()
@@ -285,6 +300,8 @@ def measure(tag, args, world, rank, local, dist, full: bool):
         "clocks": clk.summary(),
     }
     out["scaling"] = "strong" if partitioned else "weak"
+    if fallback:
+        out["run"]["multi_gpu_fallback"] = fallback
     if full:
         # ---- roofline of the dominant kernel (the persistent MINRES kernel) ----
         peak, peak_kind = measured_peak()
