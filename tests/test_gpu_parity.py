@@ -334,6 +334,28 @@ def test_bit_deterministic(gpu):
     assert np.array_equal(a.report.euclid_history, b.report.euclid_history)
 
 
+def test_blocked_sweeps_bitwise_reproducible(gpu, monkeypatch):
+    """The blocked sweeps fix the order of every sum (dense blocks, mid lists,
+    far partial sums per worker), so repeated solves -- on one handle and on a
+    fresh one -- must agree BIT FOR BIT; a lost hand-off or a race between the
+    chain CTA, the list CTA and the far workers would show as a differing bit
+    (tools/soak.py is the long form: 20 C4 solves, 6 at 48^3)."""
+    host, solver = gpu
+    monkeypatch.setenv("DSGPU_SWEEP", "bs")
+    s = host.assemble("random", 2, 14, dim=3, seed=42)
+    o = solver.SolverOptions(outer_tol=1e-6, inner_tol=1e-1)
+    ref = None
+    for _ in range(2):
+        g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+        assert g.info()["ic0_mode"] == "blocked"
+        for _ in range(4):
+            sol = g.solve(options=o)
+            x = np.concatenate([sol.u, sol.p])
+            ref = x if ref is None else ref
+            assert np.array_equal(ref, x)
+        g.close()
+
+
 def test_max_iter_and_errors(gpu):
     host, solver = gpu
     s = host.assemble("psi-mms", 2, 8)
