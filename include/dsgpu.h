@@ -137,6 +137,13 @@ int dsgpu_solve(dsgpu_handle* h, const double* f, const dsgpu_opts* opts, double
                 double* p_out, dsgpu_report* rep, double* hist_m, double* hist_e,
                 int32_t hist_cap);
 
+/* Initial guess of the NEXT solve on this handle (MinresOptions::x0,
+ * solvers.hpp:34, solvers.cpp:35-42: x = x0, r1 = b - K x0, relative residuals
+ * against ||b - K x0||): host vectors u0 (n_u), p0 (n_p) in the original
+ * ordering, copied at once; the solve after it consumes the guess, later solves
+ * start from 0 again. NULL, NULL cancels. Single-GPU handles. */
+int dsgpu_set_initial_guess(dsgpu_handle* h, const double* u0, const double* p0);
+
 /* Same, DEVICE buffers (cudaMalloc'd by the caller), on the handle's stream;
  * histories stay device-side and are not returned. Synchronizes at the end. */
 int dsgpu_solve_device(dsgpu_handle* h, const double* d_f, const dsgpu_opts* opts,

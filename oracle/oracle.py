@@ -343,6 +343,26 @@ class RefPrecond:
                     euclid_history=he[:n])
 
 
+def ref_minres_x0(pre: "RefPrecond", x0: np.ndarray, outer_tol: float, max_iter: int = 20000,
+                  euclid: bool = True):
+    """The reference's minres with MinresOptions::x0 on pre.system (no pressure filter)."""
+    s = pre.system
+    n = s.n_u + s.n_p
+    x = np.zeros(n)
+    rep = np.zeros(3)
+    he = np.zeros(max_iter + 1)
+    err = C.create_string_buffer(512)
+    fn = s.lib.L.ref_minres_x0
+    fn.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, C.c_int,
+                   C.c_char_p, C.c_int]
+    rc = fn(C.c_void_p(s.h), C.c_void_p(pre.h), np.ascontiguousarray(x0, np.float64), outer_tol, max_iter,
+            int(euclid), x, rep, he, max_iter + 1, err, 512)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    k = min(int(rep[2]), max_iter + 1)
+    return dict(x=x, iterations=int(rep[0]), converged=bool(rep[1]), euclid_history=he[:k])
+
+
 class _OrCsr(C.Structure):
     _fields_ = [("n_rows", C.c_int), ("n_cols", C.c_int), ("rp", C.c_void_p),
                 ("ci", C.c_void_p), ("v", C.c_void_p)]

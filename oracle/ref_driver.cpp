@@ -357,6 +357,36 @@ int ref_solve_with(ref_system* s, ref_precond* h, double outer_tol, double inner
   });
 }
 
+// MINRES from an initial guess: the reference's own minres (solvers.cpp:24-123) with
+// MinresOptions::x0 (solvers.hpp:34) on the saddle operator and a kept
+// preconditioner, exactly as solve_stokes sets it up (precond.cpp:245-258) --
+// solve_stokes itself never passes x0, and its zero-mean pressure filter is not
+// applied here. x0 / x: [u; p] in the original ordering.
+int ref_minres_x0(ref_system* s, ref_precond* h, const double* x0, double outer_tol, int max_iter,
+                  int stop_euclid, double* x, double* report3, double* hist_e, int hist_cap, char* err,
+                  int errlen) {
+  return guarded(err, errlen, [&] {
+    const int n = s->sys.n_u() + s->sys.n_p();
+    std::vector<double> b(n, 0.0), guess(x0, x0 + n);
+    for (int i = 0; i < s->sys.n_u(); ++i) b[i] = s->sys.f[i];
+    MinresOptions mopt;
+    mopt.tol = outer_tol;
+    mopt.max_iter = max_iter;
+    mopt.stop = stop_euclid ? MinresStop::euclidean : MinresStop::preconditioned;
+    mopt.x0 = &guess;
+    SolveReport rep;
+    LinearOperator op = [&](const double* in, double* out) { s->sys.apply(in, out); };
+    const std::vector<double> sol = minres(op, b, h->p.as_operator(), mopt, rep);
+    std::memcpy(x, sol.data(), sizeof(double) * n);
+    report3[0] = rep.iterations;
+    report3[1] = rep.converged ? 1.0 : 0.0;
+    const int len = static_cast<int>(rep.euclid_history.size());
+    report3[2] = len;
+    for (int i = 0; i < len && i < hist_cap; ++i)
+      if (hist_e) hist_e[i] = rep.euclid_history[i];
+  });
+}
+
 // ---- solver-layer primitives -------------------------------------------
 
 void ref_spmv(int n_rows, int n_cols, const int64_t* rp, const int32_t* ci, const double* v,

@@ -169,6 +169,8 @@ struct Args {
   MultiGpu mg;               // world > 1: the row-partitioned solve across the box's GPUs
   DBlock blk[2];
   const double* f_in;        // n_u, original order
+  const double* u0_in;       // initial guess (MinresOptions::x0, solvers.hpp:34), original order; null: x0 = 0
+  const double* p0_in;
   const int32_t* perm_u;     // block ordering -> original
   const int32_t* perm_p;
   double* u_out;             // n_u, original order
@@ -1591,18 +1593,43 @@ __device__ __forceinline__ void minres_body(const Args& a, int vblock, int vgrid
   double relres_m = 1.0, relres_e = 1.0;
   const bool writer = (C.cta == 0 && tid == 0);
 
-  // ---- P0: b = [f'; 0]; res = b; x = w* = aw* = 0; ||b||^2 --------------
+  // ---- P0: b = [f'; 0]; x = x0 (or 0); r1 = res = b - K x0; w* = aw* = 0; ||res||^2
+  // (solvers.cpp:29-42)
   double* bvec = a.rbuf[0];
   {
+    const bool warm = a.u0_in != nullptr;
     double acc = 0.0;
     for (int i = r0 + tid; i < r1; i += blockDim.x) {
       const double bi = i < a.n_u ? a.f_in[a.perm_u[i]] : 0.0;
       bvec[i] = bi;
       a.res[i] = bi;
-      a.x[i] = 0.0;
+      a.x[i] = warm ? (i < a.n_u ? a.u0_in[a.perm_u[i]] : a.p0_in[a.perm_p[i - a.n_u]]) : 0.0;
       a.w[0][i] = a.w[1][i] = a.w[2][i] = 0.0;
       a.aw[0][i] = a.aw[1][i] = a.aw[2][i] = 0.0;
-      acc += bi * bi;
+      if (!warm) acc += bi * bi;
+    }
+    if (warm) {  // r1 = b - K x0 once every CTA's part of x0 is in place
+      if (!C.sync_reduce(0u)) goto finish;
+      const int L = a.k_lanes, sub = lane & (L - 1), ng = kWarps * (32 / L);
+      const int gid = warp * (32 / L) + lane / L;
+      const double* x0v = a.x;
+      for (int base = r0; base < r1; base += ng) {
+        const int i = base + gid;
+        const bool ok = i < r1;
+        double kx = 0.0;
+        if (ok) {
+          const int64_t ks = a.k_rp[i];
+          kx = row_partial(a.k_ci + ks, a.k_v + ks, static_cast<int>(a.k_rp[i + 1] - ks), sub, L,
+                           [&](int j) { return x0v[j]; });
+        }
+        kx = group_sum(kx, L);
+        if (ok && sub == 0) {
+          const double ri = sub_rn(bvec[i], kx);
+          bvec[i] = ri;
+          a.res[i] = ri;
+          acc += ri * ri;
+        }
+      }
     }
     C.put(SL_BB, block_sum(acc, red));
     if (PI)  // both partitioned-inverse buffer sets start out "not yet computed"
@@ -1959,6 +1986,8 @@ struct dsgpu_handle {
   bool bs = false;            // blocked sweeps (bsweep.cuh)
   bool force_pi = false;      // the early model chose the partitioned inverse
   int bs_ns = kBsK + 3;       // dense-block slot ring depth (minimum K + 3: the second main warp looks K groups ahead)
+  double *d_u0 = nullptr, *d_p0 = nullptr;  // initial guess of the next solve (dsgpu_set_initial_guess)
+  bool warm = false;
   bool bs_pair = false;       // the solve's IC(0) servers are CTA pairs (2-CTA clusters; DSGPU_BS_PAIR=0: single CTAs)
   int far_ctas[2] = {0, 0};   // far-worker CTAs per IC block
   PiPlan pip[2];
@@ -2025,6 +2054,8 @@ struct dsgpu_handle {
     for (auto& p : peer_arena) p = nullptr;
     for (auto& b : bufs) cudaFree(b.p);
     bufs.clear();
+    d_u0 = d_p0 = nullptr;
+    warm = false;
     arena = nullptr;
     arena_size = arena_used = 0;
     ready = false;
@@ -2787,6 +2818,9 @@ static int solve_args(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, d
                       double* d_hm, double* d_he, int hist_cap, Args& a) {
   a = h->args;
   a.f_in = d_f;
+  a.u0_in = h->warm ? h->d_u0 : nullptr;  // one solve only
+  a.p0_in = h->warm ? h->d_p0 : nullptr;
+  h->warm = false;
   a.u_out = d_u;
   a.p_out = d_p;
   dsgpu_opts def;
@@ -2984,6 +3018,31 @@ int dsgpu_debug_emulate_ranks(dsgpu_handle** hs, int world, const double* f, con
     if (src && !first_err) first_err = src;
   }
   return first_err;
+}
+
+int dsgpu_set_initial_guess(dsgpu_handle* h, const double* u0, const double* p0) {
+  if (!h || !h->ready) return fail(h, DSGPU_E_BAD_INPUT, "dsgpu_set_initial_guess: not set up");
+  if (!u0 || !p0) {  // back to x0 = 0
+    h->warm = false;
+    return DSGPU_OK;
+  }
+  if (h->world > 1) return fail(h, DSGPU_E_UNSUPPORTED, "dsgpu_set_initial_guess: single-GPU handles only");
+  cudaSetDevice(h->device);
+  const HostPlan& P = h->plan;
+  try {
+    if (!h->d_u0) {
+      h->d_u0 = h->alloc<double>(P.n_u);
+      h->d_p0 = h->alloc<double>(P.n_p);
+    }
+  } catch (const std::exception& e) {
+    return fail(h, DSGPU_E_CUDA, e.what());
+  }
+  int rc = cuda_check(h, cudaMemcpyAsync(h->d_u0, u0, sizeof(double) * P.n_u, cudaMemcpyHostToDevice, h->stream), "x0 H2D");
+  if (!rc) rc = cuda_check(h, cudaMemcpyAsync(h->d_p0, p0, sizeof(double) * P.n_p, cudaMemcpyHostToDevice, h->stream), "x0 H2D");
+  if (!rc) rc = cuda_check(h, cudaStreamSynchronize(h->stream), "x0 H2D");
+  if (rc) return rc;
+  h->warm = true;
+  return DSGPU_OK;
 }
 
 int dsgpu_solve_device(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, double* d_u_out,

@@ -89,6 +89,7 @@ def _lib():
                                   C.POINTER(_Csr), C.POINTER(_Csr)]
         L.dsgpu_solve.argtypes = [vp, _dp, C.POINTER(_Opts), _dp, _dp, C.POINTER(_Report), vp, vp,
                                   C.c_int32]
+        L.dsgpu_set_initial_guess.argtypes = [vp, vp, vp]
         L.dsgpu_solve_device.argtypes = [vp, vp, C.POINTER(_Opts), vp, vp, C.POINTER(_Report)]
         L.dsgpu_apply_saddle.argtypes = [vp, _dp, _dp]
         L.dsgpu_apply_ic0.argtypes = [vp, ip, _dp, _dp]
@@ -300,9 +301,17 @@ class GpuStokesSolver:
         return _Opts(o.outer_tol, o.inner_tol, o.max_iter, o.stop, o.inner_cap)
 
     def solve(self, f: np.ndarray | None = None, options: SolverOptions | None = None,
-              history: bool = True) -> StokesSolution:
+              history: bool = True, x0: tuple[np.ndarray, np.ndarray] | None = None) -> StokesSolution:
+        """x0 = (u0, p0): MINRES initial guess (MinresOptions::x0, solvers.hpp:34)."""
         o = options or SolverOptions()
         s = self.system
+        if x0 is not None:
+            u0 = np.ascontiguousarray(x0[0], np.float64)
+            p0 = np.ascontiguousarray(x0[1], np.float64)
+            assert u0.shape == (s.n_u,) and p0.shape == (s.n_p,)
+            rc = self.L.dsgpu_set_initial_guess(self.h, u0.ctypes.data, p0.ctypes.data)
+            if rc:
+                _raise(rc, self.L.dsgpu_last_error(self.h).decode())
         f = np.ascontiguousarray(s.f if f is None else f, np.float64)
         u = np.zeros(s.n_u)
         p = np.zeros(s.n_p)

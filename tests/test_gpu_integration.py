@@ -48,3 +48,37 @@ def test_shim_matches_reference_solve(ref, shim, case, k, n, strategy, inner):
     assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
     assert abs(int(rep[0]) - r["iterations"]) <= 2 and rep[1] == 1.0
     assert abs(rep[2] - r["mean_inner_top"]) < 0.2
+
+
+def test_initial_guess_matches_reference_minres(ref):
+    """MinresOptions::x0 (solvers.hpp:34, solvers.cpp:35-42) through
+    dsgpu_set_initial_guess: the GPU solve started from a perturbed solution
+    against the reference's own minres started from the same vector on the same
+    system and preconditioner (no zero-mean filter on either side: that is
+    solve_stokes's, not minres's). The guess is consumed by one solve."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle.oracle import RefPrecond, ref_minres_x0
+    from paper_1309_5048_b200 import host, solver
+    rs = ref.assemble("psi-mms", 2, 16, seed=0)
+    pre = RefPrecond(rs, "IC0-PCG(A,Q)", 1e-1)
+    s = host.assemble("psi-mms", 2, 16)
+    s.has_constant_pressure_kernel = False
+    g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
+    o = solver.SolverOptions(outer_tol=1e-8, inner_tol=1e-1)
+    cold = g.solve(options=o)
+    rng = np.random.default_rng(3)
+    x0 = np.concatenate([cold.u, cold.p]) * (1.0 + 1e-3 * rng.standard_normal(s.size))
+    r = ref_minres_x0(pre, x0, 1e-8)
+    warm = g.solve(options=o, x0=(x0[:s.n_u], x0[s.n_u:]))
+    x = np.concatenate([warm.u, warm.p])
+    assert np.linalg.norm(x - r["x"]) <= 1e-8 * np.linalg.norm(r["x"])
+    assert abs(warm.report.iterations - r["iterations"]) <= 2 and warm.report.converged == r["converged"]
+    he, hr = warm.report.euclid_history, r["euclid_history"]
+    m = min(len(he), len(hr))
+    assert m > 1 and np.all(np.abs(he[:m] - hr[:m]) <= 1e-6 * np.maximum(hr[:m], 1e-12))
+    again = g.solve(options=o)  # the guess was for one solve only
+    assert again.report.iterations == cold.report.iterations
+    assert np.array_equal(again.u, cold.u)
+    g.close()
