@@ -1569,10 +1569,39 @@ __device__ __forceinline__ double minres_update_row(int i, const double* v, cons
   return rv * rv;
 }
 
+// Warm start (MinresOptions::x0): r1 = res = b - K x0 for the rows [r0, r1) of this
+// CTA; returns the thread's share of ||r1||^2. Out of line: it runs once per
+// solve and must not cost the solve loop a register.
+__device__ __noinline__ double warm_residual(const Args& a, int r0, int r1, double* bvec) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int L = a.k_lanes, sub = lane & (L - 1), ng = kWarps * (32 / L);
+  const int gid = warp * (32 / L) + lane / L;
+  const double* x0v = a.x;
+  double acc = 0.0;
+  for (int base = r0; base < r1; base += ng) {
+    const int i = base + gid;
+    const bool ok = i < r1;
+    double kx = 0.0;
+    if (ok) {
+      const int64_t ks = a.k_rp[i];
+      kx = row_partial(a.k_ci + ks, a.k_v + ks, static_cast<int>(a.k_rp[i + 1] - ks), sub, L,
+                       [&](int j) { return x0v[j]; });
+    }
+    kx = group_sum(kx, L);
+    if (ok && sub == 0) {
+      const double ri = sub_rn(bvec[i], kx);
+      bvec[i] = ri;
+      a.res[i] = ri;
+      acc += ri * ri;
+    }
+  }
+  return acc;
+}
+
 // The whole solve as seen by CTA `vblock` of a grid of `vgrid` CTAs (the real
 // grid for minres_kernel; one rank's share of the grid for the multi-rank
 // emulation kernel below).
-template <int TB, bool RING, bool PI>
+template <int TB, bool RING, bool PI, bool WARM = false>
 __device__ __forceinline__ void minres_body(const Args& a, int vblock, int vgrid) {
   extern __shared__ double xs_dyn[];
   __shared__ double red[32];
@@ -1597,7 +1626,9 @@ __device__ __forceinline__ void minres_body(const Args& a, int vblock, int vgrid
   // (solvers.cpp:29-42)
   double* bvec = a.rbuf[0];
   {
-    const bool warm = a.u0_in != nullptr;
+    // (a separate instantiation: the cold kernel's code -- and its register
+    // allocation -- carry no trace of the warm start)
+    constexpr bool warm = WARM;
     double acc = 0.0;
     for (int i = r0 + tid; i < r1; i += blockDim.x) {
       const double bi = i < a.n_u ? a.f_in[a.perm_u[i]] : 0.0;
@@ -1608,28 +1639,9 @@ __device__ __forceinline__ void minres_body(const Args& a, int vblock, int vgrid
       a.aw[0][i] = a.aw[1][i] = a.aw[2][i] = 0.0;
       if (!warm) acc += bi * bi;
     }
-    if (warm) {  // r1 = b - K x0 once every CTA's part of x0 is in place
+    if constexpr (warm) {  // r1 = b - K x0 once every CTA's part of x0 is in place
       if (!C.sync_reduce(0u)) goto finish;
-      const int L = a.k_lanes, sub = lane & (L - 1), ng = kWarps * (32 / L);
-      const int gid = warp * (32 / L) + lane / L;
-      const double* x0v = a.x;
-      for (int base = r0; base < r1; base += ng) {
-        const int i = base + gid;
-        const bool ok = i < r1;
-        double kx = 0.0;
-        if (ok) {
-          const int64_t ks = a.k_rp[i];
-          kx = row_partial(a.k_ci + ks, a.k_v + ks, static_cast<int>(a.k_rp[i + 1] - ks), sub, L,
-                           [&](int j) { return x0v[j]; });
-        }
-        kx = group_sum(kx, L);
-        if (ok && sub == 0) {
-          const double ri = sub_rn(bvec[i], kx);
-          bvec[i] = ri;
-          a.res[i] = ri;
-          acc += ri * ri;
-        }
-      }
+      acc = warm_residual(a, r0, r1, bvec);
     }
     C.put(SL_BB, block_sum(acc, red));
     if (PI)  // both partitioned-inverse buffer sets start out "not yet computed"
@@ -1831,9 +1843,9 @@ finish:
   }
 }
 
-template <int TB, bool RING, bool PI>
+template <int TB, bool RING, bool PI, bool WARM = false>
 __global__ void __launch_bounds__(kThreads, 1) minres_kernel(const __grid_constant__ Args a) {
-  minres_body<TB, RING, PI>(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
+  minres_body<TB, RING, PI, WARM>(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
 }
 
 // Multi-rank emulation on ONE GPU (tests of the multi-GPU data plane where
@@ -1896,7 +1908,14 @@ __global__ void fill_sentinel(double* p, int64_t n) {
 
 using MinresFn = void (*)(Args);
 using IcFn = void (*)(DBlock, const double*, unsigned*, unsigned, int);
-MinresFn minres_for(int tb, bool ring, bool pi) {
+// warm: the instantiation that starts from an initial guess (blocked sweeps and
+// partitioned inverse only -- the modes the policy selects; nullptr otherwise)
+MinresFn minres_for(int tb, bool ring, bool pi, bool warm = false) {
+  if (warm) {
+    if (tb == 0) return minres_kernel<0, true, false, true>;
+    if (pi) return minres_kernel<8, false, true, true>;
+    return nullptr;
+  }
   if (tb == 0) return minres_kernel<0, true, false>;  // blocked sweeps
   if (pi) return minres_kernel<8, false, true>;
   if (ring) return tb <= 8 ? minres_kernel<8, true, false> : minres_kernel<16, true, false>;
@@ -2917,10 +2936,19 @@ static int run_solve(dsgpu_handle* h, const double* d_f, const dsgpu_opts* o, do
   cudaEventCreate(&e1);
   cudaEventRecord(e0, h->stream);
   void* params[] = {&a};
-  rc = cuda_check(h,
-                  launch_solve_kernel(reinterpret_cast<const void*>(minres_for(h->tb, h->ring, h->pi)), h->grid, params,
-                                      h->smem, h->stream, h->bs_pair),
-                  "cooperative launch");
+  const bool warm = a.u0_in != nullptr;
+  const void* fn = reinterpret_cast<const void*>(minres_for(h->tb, h->ring, h->pi, warm));
+  if (warm) {  // the warm-start instantiation: its shared-memory limit is raised on first use
+    if (!fn) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      return fail(h, DSGPU_E_UNSUPPORTED, "initial guess: blocked-sweep and partitioned-inverse modes only");
+    }
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+    raise_smem_limit(fn, optin);
+  }
+  rc = cuda_check(h, launch_solve_kernel(fn, h->grid, params, h->smem, h->stream, h->bs_pair), "cooperative launch");
   cudaEventRecord(e1, h->stream);
   if (rc) {
     cudaEventDestroy(e0);
