@@ -259,6 +259,14 @@ int dsgpu_debug_bs_counters(int reset, int64_t* out16);
  * wait, CTA0 IC(0) apply, CTA2 grid-barrier wait, barriers, CTA0 kernel,
  * CTA1 IC(0) apply, 0, 0. */
 int dsgpu_debug_phases(int reset, int64_t* out8);
+/* SpMV phases inside the persistent kernel as worker CTA 0 times them (cycles;
+ * -DDSGPU_DIAG build only). Outer saddle SpMV (the reference's
+ * StokesSystem::apply inside minres, solvers.cpp:66): out8[0] cycles over its own
+ * rows, [1] phases, [2] stored entries of its rows, [3] cycles through the
+ * phase's grid barrier. Inner A-block SpMV (pcg, solvers.cpp:139): [4] own
+ * cycles, [5] phases, [6] stored entries of its rows, [7] cycles through the
+ * barrier (the pressure block's SpMV included). */
+int dsgpu_debug_spmv_phases(int reset, int64_t* out8);
 /* Partitioned-inverse IC(0) apply timeline: arm != 0 arms the recorder (CTA 0
  * and the last CTA record %globaltimer at every phase boundary of their next
  * apply); arm == 0 reads it: out1024[s*512] = marks recorded by slot s,

@@ -90,6 +90,82 @@ __device__ __forceinline__ double group_sum(double v, int L) {
   return v;
 }
 
+// Row loop of the SpMV phases INSIDE the persistent kernel, software-pipelined.
+// A persistent CTA is alone on its SM (16 warps), so with one 48-byte trip per
+// lane in flight the phase is latency-bound (measured in the diag build:
+// 25 GB/s per CTA, 3.5 TB/s over the grid, against 6.2 TB/s for spmv_kernel
+// at full occupancy). Here every lane issues the NEXT trip of its row -- or,
+// on the row's last trip, the first trip of its next row -- before the
+// current trip's gathers, and reads the next row's extent one row ahead: two
+// trips per lane in flight and no row-pointer latency on the path. The
+// per-lane order of the products is that of row_partial, so the results are
+// bit-identical to it.
+//   info(i, s, len): first stored entry and entry count of row i (lo <= i < hi)
+//   xf(j): the gathered operand; done(i, ok, sum): called by every lane after
+//   the row group's shuffle sum (ok: the lane's row exists)
+struct SpmvTrip {
+  int4 c;
+  double2 p, q;
+};
+__device__ __forceinline__ SpmvTrip spmv_trip(const int32_t* ci, const double* v, int64_t at) {
+  SpmvTrip t;
+  const double2* vp = reinterpret_cast<const double2*>(v + at);
+  t.c = __ldcs(reinterpret_cast<const int4*>(ci + at));
+  t.p = __ldcs(vp);
+  t.q = __ldcs(vp + 1);
+  return t;
+}
+template <class Info, class X, class Done>
+__device__ __forceinline__ void spmv_rows(int lo, int hi, int L, const int32_t* ci, const double* v, Info info,
+                                          X xf, Done done) {
+  const int lane = threadIdx.x & 31, sub = lane & (L - 1), per = 32 / L;
+  const int ng = static_cast<int>(blockDim.x >> 5) * per;
+  int i = lo + static_cast<int>(threadIdx.x >> 5) * per + lane / L;
+  bool ok = i < hi;
+  int64_t s = 0;
+  int len = 0;
+  if (ok) info(i, s, len);
+  bool have = ok && 4 * sub < len;
+  SpmvTrip t = {};
+  if (have) t = spmv_trip(ci, v, s + 4 * sub);
+  for (int base = lo; base < hi; base += ng) {
+    const int in = i + ng;
+    const bool okn = in < hi;
+    int64_t sn = 0;
+    int lenn = 0;
+    if (okn) info(in, sn, lenn);
+    const bool first_n = okn && 4 * sub < lenn;
+    double a0 = 0.0, a1 = 0.0;
+    bool ahead = false;  // the next row's first trip is already in flight
+    int k = 4 * sub;
+    while (have) {
+      const int kn = k + 4 * L;
+      const bool more = kn < len;
+      SpmvTrip n = {};
+      if (more) {
+        n = spmv_trip(ci, v, s + kn);
+      } else {
+        if (first_n) n = spmv_trip(ci, v, sn + 4 * sub);
+        ahead = true;
+      }
+      a0 = fma(t.p.x, xf(t.c.x), a0);
+      a1 = fma(t.p.y, xf(t.c.y), a1);
+      a0 = fma(t.q.x, xf(t.c.z), a0);
+      a1 = fma(t.q.y, xf(t.c.w), a1);
+      t = n;
+      k = kn;
+      have = more;
+    }
+    if (!ahead && first_n) t = spmv_trip(ci, v, sn + 4 * sub);
+    done(i, ok, group_sum(a0 + a1, L));
+    i = in;
+    ok = okn;
+    s = sn;
+    len = lenn;
+    have = first_n;
+  }
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

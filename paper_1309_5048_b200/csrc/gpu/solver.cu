@@ -332,6 +332,12 @@ __device__ int g_nowait = 0;
 // [1] CTA0 cycles in IC(0) applies, [2] CTA2 cycles in grid barriers,
 // [3] barriers, [4] CTA0 kernel cycles, [5] CTA1 cycles in IC(0) applies
 __device__ unsigned long long g_phase_dbg[8];
+// SpMV phases of the persistent kernel as worker CTA 0 sees them (diag build):
+// M1 (outer saddle SpMV): [0] cycles of its own rows, [1] phases, [2] stored
+// entries of its rows, [3] cycles through the phase's grid barrier; L1 (inner
+// A-block SpMV): [4] own cycles, [5] phases, [6] stored entries of its rows,
+// [7] cycles through the barrier (the pressure block's SpMV included)
+__device__ unsigned long long g_spmv_dbg[8];
 #ifdef DSGPU_DIAG
 #define PHASE_DIAG(...) __VA_ARGS__
 #else
@@ -1294,6 +1300,7 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
             !C.gather_halo(pp ? a.blk[b].p1 : a.blk[b].p0, a.mg.halo_p[b], a.mg.n_halo_p[b]))
           return false;
     }
+    PHASE_DIAG(const long long tl1 = clock64();)
     {
       const int lane = tid & 31, warp = tid >> 5;
       for (int b = 0; b < 2; ++b) {
@@ -1301,40 +1308,44 @@ __device__ bool precond(Ctx& C, const Input& in, double* zout, double zr[2],
         const DBlock& B = a.blk[b];
         int lo, hi;
         C.block_rows(b, lo, hi);
+        PHASE_DIAG(const long long tb1 = clock64();)
         const double* z = B.z;
         const double* po = pp ? B.p1 : B.p0;
         double* pn = pp ? B.p0 : B.p1;
         const double bt = beta[b];
         const bool first = k == 0;
         double acc_k = 0.0;
-        const int L = B.lanes, sub = lane & (L - 1), ng = kWarps * (32 / L);
-        const int gid = warp * (32 / L) + lane / L;
-        for (int base = lo; base < hi; base += ng) {
-          const int i = base + gid;
-          const bool ok = i < hi;
-          const int li = i - B.off;
-          double acc = 0.0;
-          if (ok) {
-            const int64_t s = B.rp[li];
-            const int len = B.na ? B.na[li] : static_cast<int>(B.rp[li + 1] - s);
-            acc = row_partial(B.ci + s, B.v + s, len, sub, L, [&](int j) {
-              return first ? z[j] : add_rn(z[j], mul_rn(bt, po[j]));
+        const int sub = lane & (B.lanes - 1);
+        spmv_rows(
+            lo, hi, B.lanes, B.ci, B.v,
+            [&](int i, int64_t& s, int& len) {
+              const int li = i - B.off;
+              s = B.rp[li];
+              len = B.na ? B.na[li] : static_cast<int>(B.rp[li + 1] - s);
+            },
+            [&](int j) { return first ? z[j] : add_rn(z[j], mul_rn(bt, po[j])); },
+            [&](int i, bool ok, double acc) {
+              if (ok && sub == 0) {
+                const int li = i - B.off;
+                const double pi = first ? z[li] : add_rn(z[li], mul_rn(bt, po[li]));
+                pn[li] = pi;
+                B.q[li] = acc;
+                acc_k += pi * acc;
+              }
             });
-          }
-          acc = group_sum(acc, L);
-          if (ok && sub == 0) {
-            const double pi = first ? z[li] : add_rn(z[li], mul_rn(bt, po[li]));
-            pn[li] = pi;
-            B.q[li] = acc;
-            acc_k += pi * acc;
-          }
-        }
         kap_p[b] = block_sum(acc_k, C.red);
+        PHASE_DIAG(if (b == 0 && C.cta == 0 && tid == 0 && hi > lo) {
+          atomicAdd(&g_spmv_dbg[4], static_cast<unsigned long long>(clock64() - tb1));
+          atomicAdd(&g_spmv_dbg[5], 1ull);
+          g_spmv_dbg[6] = static_cast<unsigned long long>(B.rp[hi - B.off] - B.rp[lo - B.off]);
+        })
       }
     }
     C.put(SL_KAP0, kap_p[0]);
     C.put(SL_KAP1, kap_p[1]);
     if (!C.sync_reduce((1u << SL_KAP0) | (1u << SL_KAP1))) return false;
+    PHASE_DIAG(if (active[0] && C.cta == 0 && tid == 0)
+                 atomicAdd(&g_spmv_dbg[7], static_cast<unsigned long long>(clock64() - tl1));)
     for (int b = 0; b < 2; ++b) {
       if (!active[b]) continue;
       const double kap = C.sums[SL_KAP0 + b];
@@ -1689,6 +1700,7 @@ __device__ __forceinline__ void minres_body(const Args& a, int vblock, int vgrid
     int wi = 0;  // w[wi] = current w; rotation per reference swaps
     bool pending = false;
     bool do_spmv = true;
+    PHASE_DIAG(long long tm1 = 0;)
     for (int it = 1;; ++it) {
       // ---- M1: finish iteration it-1 (vector recurrences) + SpMV of it --
       double acc_res = 0.0, acc_alpha = 0.0;
@@ -1714,8 +1726,11 @@ __device__ __forceinline__ void minres_body(const Args& a, int vblock, int vgrid
         const double c1 = it >= 2 ? div_rn(-beta, oldb) : 0.0;
         for (int i = r0 + tid; i < r1; i += blockDim.x) a.v[i] = mul_rn(s, y[i]);
         __syncthreads();  // old av consumed above before the new av is written
+        // (one trip per lane in flight: the pipelined spmv_rows of the inner SpMV measured
+        // slower here -- C3 152 -> 181 us, C4 294 -> 302 us per phase, profiles/r02_phases_spmv.md)
         const int L = a.k_lanes, sub = lane & (L - 1), ng = kWarps * (32 / L);
         const int gid = warp * (32 / L) + lane / L;
+        PHASE_DIAG(tm1 = clock64();)
         for (int base = r0; base < r1; base += ng) {
           const int i = base + gid;
           const bool ok = i < r1;
@@ -1734,9 +1749,15 @@ __device__ __forceinline__ void minres_body(const Args& a, int vblock, int vgrid
           }
         }
         C.put(SL_ALPHA, block_sum(acc_alpha, red));
+        PHASE_DIAG(if (writer) {
+          atomicAdd(&g_spmv_dbg[0], static_cast<unsigned long long>(clock64() - tm1));
+          atomicAdd(&g_spmv_dbg[1], 1ull);
+          g_spmv_dbg[2] = static_cast<unsigned long long>(a.k_rp[r1] - a.k_rp[r0]);
+        })
       }
       if (!C.sync_reduce((pending ? (1u << SL_RES) : 0u) | (do_spmv ? (1u << SL_ALPHA) : 0u)))
         goto finish;
+      PHASE_DIAG(if (writer && do_spmv) atomicAdd(&g_spmv_dbg[3], static_cast<unsigned long long>(clock64() - tm1));)
       if (pending) {
         // stop test of iteration it-1 (solvers.cpp:102-117)
         relres_e = rnorm0 > 0.0 ? div_rn(sqrt_rn(sums[SL_RES]), rnorm0) : 0.0;
@@ -3334,6 +3355,17 @@ int dsgpu_debug_phases(int reset, int64_t* out8) {
   if (reset) {
     const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_phase_dbg, z, sizeof(z));
+  }
+  return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
+}
+
+int dsgpu_debug_spmv_phases(int reset, int64_t* out8) {
+  unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyFromSymbol(v, g_spmv_dbg, sizeof(v));
+  for (int i = 0; i < 8; ++i) out8[i] = static_cast<int64_t>(v[i]);
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_spmv_dbg, z, sizeof(z));
   }
   return cudaGetLastError() == cudaSuccess ? DSGPU_OK : DSGPU_E_CUDA;
 }

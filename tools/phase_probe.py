@@ -27,13 +27,15 @@ def main():
         g = solver.GpuStokesSolver(s, "IC0-PCG(A,Q)")
         o = solver.SolverOptions(outer_tol=c["outer"], inner_tol=c["inner"], max_iter=c.get("max_iter", 20000))
         g.solve(options=o)  # warm-up
-        ph, bs = np.zeros(8, np.int64), np.zeros(16, np.int64)
+        ph, bs, sp = np.zeros(8, np.int64), np.zeros(16, np.int64), np.zeros(8, np.int64)
         vp = C.c_void_p
         g.L.dsgpu_debug_phases(1, ph.ctypes.data_as(vp))
         g.L.dsgpu_debug_bs_counters(1, bs.ctypes.data_as(vp))
+        g.L.dsgpu_debug_spmv_phases(1, sp.ctypes.data_as(vp))
         sol = g.solve(options=o)
         g.L.dsgpu_debug_phases(1, ph.ctypes.data_as(vp))
         g.L.dsgpu_debug_bs_counters(1, bs.ctypes.data_as(vp))
+        g.L.dsgpu_debug_spmv_phases(1, sp.ctypes.data_as(vp))
         r = sol.report
         k = float(ph[4]) or 1.0
         out = dict(cfg=tag, ic0_mode=g.info()["ic0_mode"], iterations=r.iterations, kernel_ms=round(r.wall_seconds * 1e3, 2),
@@ -41,6 +43,19 @@ def main():
                    kernel_cycles=int(ph[4]), grid_barriers=int(ph[3]),
                    frac_cta0_barrier_wait=round(ph[0] / k, 4), frac_cta2_barrier_wait=round(ph[2] / k, 4),
                    frac_server_A_busy=round(ph[1] / k, 4), frac_server_Q_busy=round(ph[5] / k, 4))
+        # SpMV phases inside the persistent kernel (worker CTA 0's clock; 12 bytes per stored
+        # entry = int32 column + f64 value; cycles -> ns through kernel_ms / kernel_cycles)
+        info = g.info()
+        ns = r.wall_seconds * 1e9 / k
+        for name, j, nnz in (("saddle_spmv_M1", 0, info["nnz_K"]), ("A_spmv_L1", 4, info["nnz_A"])):
+            if sp[j + 1]:
+                own = sp[j] / sp[j + 1] * ns
+                thru = sp[j + 3] / sp[j + 1] * ns
+                out[name] = dict(phases=int(sp[j + 1]), cta0_entries=int(sp[j + 2]), cta0_own_us=round(own / 1e3, 2),
+                                 cta0_GBps=round(sp[j + 2] * 12 / own, 2),
+                                 ctas_sharing_rows=round(nnz / max(1, int(sp[j + 2])), 1),
+                                 GBps_own=round(nnz * 12 / own, 1),
+                                 through_barrier_us=round(thru / 1e3, 2), GBps_through_barrier=round(nnz * 12 / thru, 1))
         if bs[4]:
             G = float(bs[4])
             out["bsweep"] = dict(groups=int(bs[4]), main_cycles_per_group=round(bs[0] / G, 1),
