@@ -2666,14 +2666,17 @@ int dsgpu_setup(dsgpu_handle* h, const dsgpu_csr* A, const dsgpu_csr* B, const d
     a.k_v = h->upload(P.k_v);
     a.row_lo = h->upload(row_lo);
     a.row_hi = h->upload(row_hi);
-    // lanes per row: 16 (64 entries per pass) measured best from 125 to 512 entries per
-    // row (C3 saddle 71.5 us vs 87.0 with 32 lanes, C4 164.7 vs 172.2: tools/spmv_ab.py)
+    // lanes per row: 16 (64 entries per pass) for the long 3D rows (C4, ~500 entries: saddle
+    // 164.7 us vs 172.2 with 8 or 32 lanes, tools/spmv_ab.py); 8 below 256 entries per row
+    // (2D): equal in the stand-alone kernel (C3 72.0 vs 71.5 us) but faster inside the
+    // persistent kernel, where 16 warps per SM want more rows in flight (C3 saddle phase
+    // 153 -> 120 us, inner A phase 116 -> 96 us; profiles/r02_phases_spmv.md)
     auto lanes_for = [](double mean_row) {
       if (const char* env = std::getenv("DSGPU_SPMV_LANES")) {
         const int L = std::atoi(env);
         if (L == 8 || L == 16 || L == 32) return L;
       }
-      return mean_row >= 48.0 ? 16 : 8;
+      return mean_row >= 256.0 ? 16 : 8;
     };
     a.k_lanes = lanes_for(static_cast<double>(P.k_rp[P.n]) / P.n);
     const int32_t* d_na = h->upload(P.k_na);
